@@ -1,0 +1,139 @@
+/*
+ * pcgs.h — C ABI of the B200-native prior-preconditioned CG sampler path.
+ *
+ * This is the drop-in boundary for the β-draw hot path of the reference
+ * package `priorcg` (arXiv 1810.12437).  The reference is pure Python; its
+ * plug-in seam is duck typing (`pcg_solve(phi, ...)` accepts any operator with
+ * `.apply`, reference pkg/src/priorcg/cg.py:105-113), so every entry point below
+ * replaces one numpy routine of the reference and is bound from Python with
+ * ctypes.  All vectors use the reference's column layout:
+ * the dense intercept (when present) is coordinate 0, the shrunk block follows
+ * (pkg/src/priorcg/sparse.py:314-341, `hstack_dense_columns`).
+ *
+ * Conventions
+ *  - Every function returns PCGS_OK (0) or a negative PCGS_E* code;
+ *    pcgs_last_error() returns a thread-local message for the last failure.
+ *  - Pointers are DEVICE pointers unless the parameter name ends in `_h`.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  No entry
+ *    point synchronises the stream except pcgs_design_create.
+ *  - A design handle is immutable after create: it may be used concurrently
+ *    from several host threads on distinct streams (the reference's concurrency
+ *    model: pure kernels over immutable data).
+ */
+#ifndef PCGS_H
+#define PCGS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCGS_OK 0
+#define PCGS_EINVAL (-1)   /* bad argument (maps to ValueError)            */
+#define PCGS_ECUDA (-2)    /* CUDA runtime error                            */
+#define PCGS_ENOMEM (-3)   /* device or host allocation failed              */
+#define PCGS_EUNSUP (-4)   /* configuration not supported by this build     */
+
+/* PCG termination codes written to result[1] by pcgs_pcg (device int32). */
+#define PCGS_CONVERGED 0   /* CGReport.termination == "converged"           */
+#define PCGS_MAX_ITER 1    /* CGReport.termination == "max_iter"            */
+#define PCGS_NOT_PD (-1)   /* NotPositiveDefiniteError, cg.py:157-160       */
+#define PCGS_NONFINITE (-2)/* NumericBreakdownError(k), cg.py:141-142,172   */
+
+typedef struct pcgs_design* pcgs_design_t;
+typedef void* pcgs_stream_t; /* cudaStream_t */
+
+int pcgs_version(void);
+const char* pcgs_last_error(void);
+
+/* Build the pattern-only store of a binary design and upload it to `device`.
+ * Replaces the CSR container SparseDesignMatrix (sparse.py:46-117) for 0/1
+ * designs: values are implicit ones, indices are re-encoded as uint16
+ * slab-local offsets (CSR over column slabs, CSC over row slabs).
+ *   n, p          rows and SHRUNK columns (the intercept is not counted in p)
+ *   row_ptr_h     int64[n+1], host; col_idx_h int32[nnz], host, columns of the
+ *                 shrunk block only, strictly increasing within a row
+ *   intercept     1 if the design carries the dense all-ones column in front
+ *                 (hstack_dense_columns, sparse.py:314-341), else 0
+ *   slab_max      0 = automatic (largest slab that fits shared memory); a small
+ *                 value forces many slabs (used by the tests)
+ * Synchronous.  Returns PCGS_EINVAL for malformed CSR (sparse.py:94-117). */
+int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h,
+                       const int32_t* col_idx_h, int intercept, int slab_max,
+                       int device, pcgs_design_t* out);
+int pcgs_design_destroy(pcgs_design_t d);
+/* info_h[16]: n, p, p_total, nnz, csr_slabs, csc_slabs, csr_vectors,
+ * csc_vectors, csr_bundles, csc_bundles, csc_pieces, grid, device,
+ * index_bytes (both directions), reserved, reserved */
+int pcgs_design_info(pcgs_design_t d, int64_t* info_h);
+
+/* out[n] = X v, v[p_total].  Replaces SparseDesignMatrix.matvec
+ * (sparse.py:178-193) for the unstandardised binary design. */
+int pcgs_matvec(pcgs_design_t d, const double* v, double* out, pcgs_stream_t stream);
+
+/* out[p_total] = X' w, w[n].  Replaces SparseDesignMatrix.matvec_t
+ * (sparse.py:195-203). */
+int pcgs_matvec_t(pcgs_design_t d, const double* w, double* out, pcgs_stream_t stream);
+
+/* out = X' (omega ⊙ X v) + prior_diag ⊙ v.  Replaces PrecisionOperator.apply
+ * (sampler.py:53-58). */
+int pcgs_phi_apply(pcgs_design_t d, const double* omega, const double* prior_diag,
+                   const double* v, double* out, pcgs_stream_t stream);
+
+/* out[p_total] = X' (omega) + prior_diag: the diagonal of Phi for a binary
+ * design (gram_diagonal, sparse.py:235-246, plus the prior; the Jacobi
+ * preconditioner's M of precond.py:105-117). */
+int pcgs_phi_diagonal(pcgs_design_t d, const double* omega, const double* prior_diag,
+                      double* out, pcgs_stream_t stream);
+
+/* Randomised right-hand side (generate_rhs, sampler.py:94-107, with the linear
+ * term of GaussianTarget.from_pseudo_outcome, sampler.py:86-91):
+ *   b = X'(kappa + sqrt(omega) ⊙ eta) + sqrt(prior_diag) ⊙ delta
+ * kappa may be NULL (zero); `linear` (p_total, may be NULL) is added as the
+ * target's precomputed linear term.
+ * eta[n] / delta[p_total] are taken from the given device arrays when non-NULL
+ * (host-noise injection: the reference's stream order, eta then delta), else
+ * drawn on device from Philox4x32-10 keyed by (seed, stream_id). */
+int pcgs_rhs(pcgs_design_t d, const double* kappa, const double* omega,
+             const double* prior_diag, const double* linear, const double* eta,
+             const double* delta, uint64_t seed, uint64_t stream_id, double* b,
+             pcgs_stream_t stream);
+
+/* Prior-preconditioned CG on Phi = X'ΩX + diag(prior_diag), the whole loop on
+ * device in one persistent cooperative kernel (pcg_solve, cg.py:105-192).
+ *   minv[p_total]   diagonal of M^-1 (Preconditioner.inv_diagonal)
+ *   scale[p_total]  termination metric scale s (cg.py:89-102)
+ *   x               in: x0, out: solution
+ *   trace[max_iter+1], alphas[max_iter], betas[max_iter]: device outputs
+ *   result[4] (device int32): iterations, termination code, failing
+ *   iteration, operator applications.  Nothing is synchronised. */
+int pcgs_pcg(pcgs_design_t d, const double* omega, const double* prior_diag,
+             const double* minv, const double* scale, const double* b, double* x,
+             int32_t max_iter, double rtol, double* trace, double* alphas,
+             double* betas, int32_t* result, pcgs_stream_t stream);
+
+/* Generic-operator PCG (pcg_solve with a duck-typed operator, cg.py:105-113):
+ * the same loop, vector algebra on device, Phi supplied by a callback
+ * fn(ctx, v, out) on device buffers of length p (returns 0 on success).
+ * trace_h/alphas_h/betas_h/result_h are HOST arrays; synchronises every
+ * iteration (desk-scale path, used by the reference's operator tests). */
+typedef int (*pcgs_apply_fn)(void* ctx, const double* v, double* out);
+int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv,
+                const double* scale, const double* b, double* x, int32_t max_iter,
+                double rtol, double* trace_h, double* alphas_h, double* betas_h,
+                int32_t* result_h, pcgs_stream_t stream);
+
+/* Synchronous copy helper for operator callbacks: kind 0 host->device,
+ * 1 device->host, 2 device->device. */
+int pcgs_copy(void* dst, const void* src, int64_t bytes, int kind);
+
+/* omega[i] ~ PG(1, z[i]) (pg_draw_batch, polya_gamma.py:39-84), Philox keyed
+ * by (seed, stream_id), one thread per draw. */
+int pcgs_pg_draw(const double* z, int64_t n, uint64_t seed, uint64_t stream_id,
+                 double* omega, pcgs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCGS_H */

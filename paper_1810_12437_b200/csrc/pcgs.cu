@@ -1,0 +1,910 @@
+// pcgs: B200-native kernels and C ABI for the prior-preconditioned CG sampler
+// hot path (reference: pkg/src/priorcg/{sparse,sampler,cg,polya_gamma}.py).
+//
+// Kernel inventory:
+//   k_csr_*      X v over column slabs         (sparse.py:178-193)
+//   k_csc_*      X' w over row slabs           (sparse.py:195-203)
+//   k_assemble   per-column piece sums + diagonal terms
+//   k_pcg        the whole PCG solve, one persistent cooperative kernel
+//                (cg.py:105-192, operator sampler.py:53-58)
+//   k_pg         Polya-Gamma PG(1, z) draws    (polya_gamma.py:39-147)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "device.cuh"
+#include "pcgs.h"
+
+namespace cg = cooperative_groups;
+using namespace pcgs;
+
+// =====================================================================
+// error plumbing
+// =====================================================================
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CUDA_TRY(x)                                                                  \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(PCGS_ECUDA, std::string(#x " failed: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+// =====================================================================
+// design handle
+// =====================================================================
+struct pcgs_design {
+  DesignDev dev;
+  int device;
+  int64_t info[16];
+  std::vector<void*> allocs;
+};
+
+template <class T>
+static int upload(pcgs_design* D, const std::vector<T>& h, const T** out) {
+  if (h.empty()) {
+    *out = nullptr;
+    return PCGS_OK;
+  }
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, h.size() * sizeof(T)));
+  D->allocs.push_back(p);
+  CUDA_TRY(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  *out = (const T*)p;
+  return PCGS_OK;
+}
+
+static int upload_pass(pcgs_design* D, const PassHost& H, PassDev& P) {
+  int rc;
+  const uint16_t* idx;
+  if ((rc = upload(D, H.idx, &idx))) return rc;
+  P.vec = (const uint4*)idx;
+  const Bundle* b;
+  if ((rc = upload(D, H.bundles, &b))) return rc;
+  P.bundle = (const int4*)b;
+  const Task* t;
+  if ((rc = upload(D, H.tasks, &t))) return rc;
+  P.task = (const int4*)t;
+  if ((rc = upload(D, H.cta_task_ptr, &P.cta_task_ptr))) return rc;
+  if ((rc = upload(D, H.warp_split, &P.warp_split))) return rc;
+  std::vector<long long> lo(H.slab_lo.begin(), H.slab_lo.end());
+  if ((rc = upload(D, lo, &P.slab_lo))) return rc;
+  if ((rc = upload(D, H.piece_ptr, &P.piece_ptr))) return rc;
+  P.nslab = H.nslab;
+  P.nseg = H.nseg;
+  return PCGS_OK;
+}
+
+// scratch buffers for one call, stream-ordered
+struct Scratch {
+  cudaStream_t s;
+  std::vector<void*> bufs;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  ~Scratch() {
+    for (void* b : bufs) cudaFreeAsync(b, s);
+  }
+  template <class T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    if (cudaMallocAsync(&p, count * sizeof(T), s) != cudaSuccess) return nullptr;
+    bufs.push_back(p);
+    return (T*)p;
+  }
+};
+
+// =====================================================================
+// fills and epilogues
+// =====================================================================
+struct FillVecRef {  // CSR slab of a reference-layout p_total vector
+  const double* v;
+  int icpt;
+  long long lo;
+  __device__ double operator()(int j) const { return __ldcg(v + icpt + lo + j); }
+  __device__ void operator()(double* sv, long long l, int len) {
+    lo = l;
+    fill_smem(sv, len, *this);
+  }
+};
+
+struct FillVecN {  // CSC slab of an n-vector (optionally scaled elementwise)
+  const double* w;
+  const double* scale;  // may be null
+  long long lo;
+  __device__ double operator()(int j) const {
+    double x = __ldcg(w + lo + j);
+    return scale ? x * __ldg(scale + lo + j) : x;
+  }
+  __device__ void operator()(double* sv, long long l, int len) {
+    lo = l;
+    fill_smem(sv, len, *this);
+  }
+};
+
+struct FillRhs {  // u_i = kappa_i + sqrt(omega_i) * eta_i
+  const double* kappa;
+  const double* omega;
+  const double* eta;  // null: Philox
+  unsigned long long seed, stream;
+  long long lo;
+  __device__ double operator()(int j) const {
+    const long long i = lo + j;
+    double e;
+    if (eta) {
+      e = __ldg(eta + i);
+    } else {
+      Philox R(seed, stream, (unsigned)i);
+      e = R.normal();
+    }
+    return (kappa ? __ldg(kappa + i) : 0.0) + sqrt(__ldg(omega + i)) * e;
+  }
+  __device__ void operator()(double* sv, long long l, int len) {
+    lo = l;
+    fill_smem(sv, len, *this);
+  }
+};
+
+struct EpiStore {  // out[seg] = s
+  double* out;
+  __device__ void emit(long long seg, double s) { out[seg] = s; }
+};
+
+struct EpiZ {  // matvec, single column slab: out[i] = v0 + s
+  double* out;
+  double v0;
+  __device__ void emit(long long seg, double s) { out[seg] = v0 + s; }
+};
+
+struct EpiW {  // Phi apply, single column slab: w_i = omega_i (v0 + s); acc += w_i z_i
+  double* w;
+  const double* omega;
+  double v0;
+  double acc;
+  __device__ void emit(long long seg, double s) {
+    const double z = v0 + s;
+    const double wi = __ldg(omega + seg) * z;
+    w[seg] = wi;
+    acc += wi * z;
+  }
+};
+
+struct EpiCsr {  // runtime choice: multi column slab -> partial store, else EpiW
+  double* out;
+  const double* omega;
+  double v0;
+  double acc;
+  bool multi;
+  __device__ void emit(long long seg, double s) {
+    if (multi) {
+      out[seg] = s;
+    } else {
+      const double z = v0 + s;
+      const double wi = __ldg(omega + seg) * z;
+      out[seg] = wi;
+      acc += wi * z;
+    }
+  }
+};
+
+// =====================================================================
+// standalone kernels (one pass each; launched with the plan's G CTAs)
+// =====================================================================
+__global__ void __launch_bounds__(kThreads, 1) k_csr_matvec(DesignDev D, const double* v, double* out) {
+  extern __shared__ __align__(128) double sv[];
+  FillVecRef f{v, D.icpt, 0};
+  const double v0 = D.icpt ? __ldg(v) : 0.0;
+  if (D.csr.nslab == 1) {
+    EpiZ e{out, v0};
+    run_pass(D.csr, sv, f, e);
+  } else {
+    EpiStore e{out};  // out is the (nslab x n) partial buffer
+    run_pass(D.csr, sv, f, e);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_csr_phi(DesignDev D, const double* v, const double* omega, double* w) {
+  extern __shared__ __align__(128) double sv[];
+  FillVecRef f{v, D.icpt, 0};
+  const double v0 = D.icpt ? __ldg(v) : 0.0;
+  if (D.csr.nslab == 1) {
+    EpiW e{w, omega, v0, 0.0};
+    run_pass(D.csr, sv, f, e);
+  } else {
+    EpiStore e{w};
+    run_pass(D.csr, sv, f, e);
+  }
+}
+
+// multi column slab: z_i = v0 + sum_s part[s*n+i]; out = scale ? scale*z : z
+__global__ void k_rows_combine(DesignDev D, const double* part, const double* v, const double* scale, double* out) {
+  const double v0 = D.icpt ? __ldg(v) : 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < D.n; i += (long long)gridDim.x * blockDim.x) {
+    double z = 0.0;
+    for (int s = 0; s < D.csr.nslab; ++s) z += part[(long long)s * D.n + i];
+    z += v0;
+    out[i] = scale ? __ldg(scale + i) * z : z;
+  }
+}
+
+template <class Fill>
+__global__ void __launch_bounds__(kThreads, 1) k_csc(DesignDev D, Fill f, double* pieces) {
+  extern __shared__ __align__(128) double sv[];
+  EpiStore e{pieces};
+  run_pass(D.csc, sv, f, e);
+}
+
+// out[ref(j)] = column_sum(j) + diag_j * v[ref(j)]  (diag/v may be null)
+//               + sqrt(diag_j) * delta_j           (mode 2: RHS noise)
+__global__ void k_assemble(DesignDev D, const double* pieces, const double* diag, const double* v,
+                           const double* delta, unsigned long long seed, unsigned long long stream, int mode,
+                           double* out, const double* linear = nullptr) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < D.pt; j += (long long)gridDim.x * blockDim.x) {
+    const long long r = ref_index(j, D.p, D.icpt);
+    double s = column_sum(D.csc, pieces, D.pt, j);
+    if (mode == 1) {
+      s += __ldg(diag + r) * __ldg(v + r);
+    } else if (mode == 2) {
+      if (linear) s = __ldg(linear + r) + s;
+      double e;
+      if (delta) {
+        e = __ldg(delta + r);
+      } else {
+        Philox R(seed, stream, (unsigned)r);
+        e = R.normal();
+      }
+      s += sqrt(__ldg(diag + r)) * e;
+    } else if (mode == 3) {
+      s += __ldg(diag + r);
+    }
+    out[r] = s;
+  }
+}
+
+// =====================================================================
+// persistent PCG kernel
+// =====================================================================
+struct PcgArgs {
+  DesignDev D;
+  const double* omega;  // n
+  const double* diag;   // prior precision, reference layout
+  const double* minv;   // reference layout
+  const double* scale;  // reference layout
+  const double* b;      // reference layout
+  double* x;            // in x0 / out solution, reference layout
+  int max_iter;
+  double rtol;
+  double* trace;
+  double* alphas;
+  double* betas;
+  int* result;
+  // scratch
+  double* w;       // n (+pad)
+  double* zpart;   // nslab_csr * n (multi column slab only)
+  double* pieces;  // csc nseg
+  double* zv;      // p_total internal layout: minv * r
+  double* dvg;     // 2 * p_total internal layout: search directions
+  double* part;    // 4 * G partial sums: dAd, rms, rz, spare
+};
+
+struct FillDir {  // search direction: first ? a : a + beta * b   (internal layout)
+  const double* a;
+  const double* b;
+  double beta;
+  int first;
+  long long lo;
+  __device__ double operator()(int j) const {
+    const double aj = __ldcg(a + lo + j);
+    return first ? aj : fma(beta, __ldcg(b + lo + j), aj);
+  }
+  __device__ void operator()(double* sv, long long l, int len) {
+    lo = l;
+    fill_smem(sv, len, *this);
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(128) double sv[];
+  __shared__ double red[64];
+  const DesignDev& D = A.D;
+  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
+  const long long pt = D.pt, p = D.p, n = D.n;
+  const int icpt = D.icpt;
+  const bool multi = D.csr.nslab > 1;
+
+  // ---- own slice of the p_total coordinates, kept in registers ----
+  const long long chunk = (pt + G - 1) / G;
+  const long long j = c * chunk + tid;
+  const bool own = tid < chunk && j < pt;
+  const long long rj = own ? ref_index(j, p, icpt) : 0;
+  double xj = 0, rjv = 0, dj = 0, mj = 0, sj = 0, Dj = 0, bj = 0, zj = 0;
+  if (own) {
+    xj = A.x[rj];
+    mj = __ldg(A.minv + rj);
+    sj = __ldg(A.scale + rj);
+    Dj = __ldg(A.diag + rj);
+    bj = __ldg(A.b + rj);
+  }
+  double* part_dAd = A.part;
+  double* part_rms = A.part + G;
+  double* part_rz = A.part + 2 * G;
+
+  double rz = 0.0;
+  int status = PCGS_MAX_ITER, iterations = 0, fail_iter = -1, applies = 0;
+  if (own) A.dvg[pt + j] = xj;
+  grid.sync();
+
+  for (int a = 0;; ++a) {
+    double beta = 0.0, vj;
+    // ---------------- convergence test of iteration a-1 ----------------
+    if (a > 0) {
+      double s_rms = reduce_partials(part_rms, G);
+      double s_rz = reduce_partials(part_rz, G);
+      const double rms = sqrt(s_rms / (double)pt);
+      if (c == 0 && tid == 0) A.trace[a - 1] = rms;
+      const int k = a - 1;  // iterations completed
+      if (rms <= A.rtol) {
+        status = PCGS_CONVERGED;
+        iterations = k;
+        break;
+      }
+      if (!isfinite(rms)) {
+        status = PCGS_NONFINITE;
+        iterations = k;
+        fail_iter = k;
+        break;
+      }
+      if (a >= 2) {
+        beta = s_rz / rz;
+        if (c == 0 && tid == 0) A.betas[a - 2] = beta;
+      }
+      rz = s_rz;
+      if (k >= A.max_iter) {
+        status = PCGS_MAX_ITER;
+        iterations = k;
+        break;
+      }
+      // new direction (own slice in registers, full vector into smem below)
+      if (own) {
+        dj = a == 1 ? zj : fma(beta, dj, zj);
+        A.dvg[(a & 1) * pt + j] = dj;
+      }
+      vj = dj;
+    } else {
+      vj = xj;
+    }
+
+    // ---------------- phase A: CSR pass, w = omega (X v) ----------------
+    double acc_dAd = own ? Dj * vj * vj : 0.0;
+    // a == 0: v = x0 (staged into dvg[1] by the owners before the loop)
+    const double* fa = a == 0 ? A.dvg + pt : A.zv;
+    const double* fb = A.dvg + ((a - 1) & 1) * pt;
+    const bool first = a <= 1;
+    const double v0 = icpt ? (first ? __ldcg(fa + p) : fma(beta, __ldcg(fb + p), __ldcg(fa + p))) : 0.0;
+    {
+      FillDir f{fa, fb, beta, first, 0};
+      EpiCsr e{multi ? A.zpart : A.w, A.omega, v0, 0.0, multi};
+      run_pass(D.csr, sv, f, e);
+      if (a > 0) acc_dAd += e.acc;
+    }
+    if (multi) {
+      grid.sync();
+      for (long long i = (long long)c * kThreads + tid; i < n; i += (long long)G * kThreads) {
+        double z = 0.0;
+        for (int s = 0; s < D.csr.nslab; ++s) z += __ldcg(A.zpart + (long long)s * n + i);
+        z += v0;
+        const double wi = __ldg(A.omega + i) * z;
+        A.w[i] = wi;
+        acc_dAd += wi * z;
+      }
+    }
+    {
+      double t = block_sum(acc_dAd, red);
+      if (tid == 0) part_dAd[c] = t;
+    }
+    grid.sync();
+
+    // ---------------- phase B: CSC pass, pieces of X' w ----------------
+    {
+      FillVecN f{A.w, nullptr, 0};
+      EpiStore e{A.pieces};
+      run_pass(D.csc, sv, f, e);
+    }
+    grid.sync();
+    ++applies;
+
+    // ---------------- phase C: assemble, step, residual ----------------
+    double alpha = 0.0;
+    if (a > 0) {
+      const double dAd = reduce_partials(part_dAd, G);
+      if (!(dAd > 0.0)) {
+        status = PCGS_NOT_PD;
+        iterations = a;
+        fail_iter = a;
+        break;
+      }
+      alpha = rz / dAd;
+      if (c == 0 && tid == 0) A.alphas[a - 1] = alpha;
+    }
+    double t_rms = 0.0, t_rz = 0.0;
+    if (own) {
+      const double Ad = column_sum(D.csc, A.pieces, pt, j) + Dj * vj;
+      if (a == 0) {
+        rjv = bj - Ad;
+      } else {
+        xj = fma(alpha, dj, xj);
+        rjv = fma(-alpha, Ad, rjv);
+      }
+      zj = mj * rjv;
+      A.zv[j] = zj;
+      const double tj = sj * rjv;
+      t_rms = tj * tj;
+      t_rz = rjv * zj;
+    }
+    block_sum2(t_rms, t_rz, red);
+    if (tid == 0) {
+      part_rms[c] = t_rms;
+      part_rz[c] = t_rz;
+    }
+    grid.sync();
+  }
+
+  if (own) A.x[rj] = xj;
+  if (c == 0 && tid == 0) {
+    A.result[0] = iterations;
+    A.result[1] = status;
+    A.result[2] = fail_iter;
+    A.result[3] = applies;
+  }
+}
+
+// =====================================================================
+// Polya-Gamma PG(1, z) (restates polya_gamma.py:39-147 per thread)
+// =====================================================================
+__device__ __forceinline__ double log_ndtr(double x) {
+  if (x < -1.0) return log(0.5 * erfcx(-x * M_SQRT1_2)) - 0.5 * x * x;
+  return log1p(-0.5 * erfc(x * M_SQRT1_2));
+}
+__device__ __forceinline__ double logaddexp(double a, double b) {
+  const double m = fmax(a, b);
+  return m + log1p(exp(-fabs(a - b)));
+}
+
+__device__ bool pg_series_accept(double x, Philox& R) {
+  const double T = 0.64;
+  const double u = R.uniform();
+  const bool inside = x <= T;
+  double partial = 1.0;
+  for (int k = 1; k < 1000; ++k) {
+    const double coef = 2.0 * k + 1.0;
+    const double term = inside ? coef * exp(-2.0 * k * (k + 1.0) / x)
+                               : coef * exp(-0.5 * k * (k + 1.0) * M_PI * M_PI * x);
+    if (k & 1) {
+      partial -= term;
+      if (u <= partial) return true;
+    } else {
+      partial += term;
+      if (!(u < partial)) return false;
+    }
+  }
+  return false;
+}
+
+__device__ double pg_trunc_ig(double h, Philox& R) {
+  const double T = 0.64;
+  if (h < 1.0 / T) {
+    for (;;) {
+      const double e1 = R.exponential(), e2 = R.exponential();
+      if (e1 * e1 <= 2.0 * e2 / T) {
+        const double q = 1.0 + T * e1;
+        const double x = T / (q * q);
+        if (R.uniform() <= exp(-0.5 * h * h * x)) return x;
+      }
+    }
+  }
+  const double mu = 1.0 / h;
+  for (;;) {
+    const double nrm = R.normal();
+    const double y = nrm * nrm;
+    double x = mu + 0.5 * mu * mu * y - 0.5 * mu * sqrt(4.0 * mu * y + (mu * y) * (mu * y));
+    x = fmax(x, 1e-300);
+    if (R.uniform() > mu / (mu + x)) x = mu * mu / x;
+    if (x <= T) return x;
+  }
+}
+
+__device__ double pg_draw1(double z, Philox& R) {
+  const double T = 0.64, SQT = 0.8;
+  const double h = 0.5 * fabs(z);
+  const double K = M_PI * M_PI / 8.0 + 0.5 * h * h;
+  const double log_right = log(M_PI / (2.0 * K)) - K * T;
+  const double log_left = M_LN2 + logaddexp(-h + log_ndtr((T * h - 1.0) / SQT), h + log_ndtr(-(T * h + 1.0) / SQT));
+  const double prob_right = 1.0 / (1.0 + exp(-(log_right - log_left)));
+  for (;;) {
+    double x;
+    if (R.uniform() < prob_right) x = T + R.exponential() / K;
+    else x = pg_trunc_ig(h, R);
+    if (pg_series_accept(x, R)) return 0.25 * x;
+  }
+}
+
+__global__ void k_pg(const double* z, long long n, unsigned long long seed, unsigned long long stream, double* omega) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    Philox R(seed, stream, (unsigned)i);
+    omega[i] = pg_draw1(z[i], R);
+  }
+}
+
+// =====================================================================
+// C ABI
+// =====================================================================
+extern "C" {
+
+int pcgs_version(void) { return 1; }
+const char* pcgs_last_error(void) { return g_err.c_str(); }
+
+static size_t smem_bytes(const DesignDev& D) { return (size_t)D.smem_doubles * sizeof(double); }
+
+static int set_smem_attrs(const DesignDev& D) {
+  const int bytes = (int)smem_bytes(D);
+  CUDA_TRY(cudaFuncSetAttribute(k_csr_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(cudaFuncSetAttribute(k_csr_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(cudaFuncSetAttribute(k_csc<FillVecN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(cudaFuncSetAttribute(k_csc<FillRhs>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  return PCGS_OK;
+}
+
+int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int32_t* col_idx_h, int intercept,
+                       int slab_max, int device, pcgs_design_t* out) {
+  if (!out || !row_ptr_h || (!col_idx_h && row_ptr_h[n] > 0)) return fail(PCGS_EINVAL, "null argument");
+  *out = nullptr;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  const int G = prop.multiProcessorCount;
+  DesignHost H;
+  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H);
+  if (!err.empty()) return fail(PCGS_EINVAL, err);
+  if ((H.p_total + G - 1) / G > kThreads) return fail(PCGS_EUNSUP, "p_total too large for the persistent PCG slice");
+  pcgs_design* D = new pcgs_design();
+  D->device = device;
+  DesignDev& dd = D->dev;
+  dd.n = n;
+  dd.p = p;
+  dd.pt = H.p_total;
+  dd.icpt = H.intercept;
+  dd.G = G;
+  int64_t maxlen = 0;
+  for (const PassHost* P : {&H.csr, &H.csc})
+    for (int q = 0; q < P->nslab; ++q) maxlen = std::max<int64_t>(maxlen, P->slab_lo[q + 1] - P->slab_lo[q]);
+  dd.smem_doubles = (int)((maxlen + 1 + 15) / 16 * 16);
+  int rc;
+  if ((rc = upload_pass(D, H.csr, dd.csr)) || (rc = upload_pass(D, H.csc, dd.csc))) {
+    pcgs_design_destroy(D);
+    return rc;
+  }
+  if ((rc = set_smem_attrs(dd))) {
+    pcgs_design_destroy(D);
+    return rc;
+  }
+  // make freed stream-ordered scratch stay cached in the pool
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  int64_t* I = D->info;
+  memset(I, 0, sizeof(D->info));
+  I[0] = n;
+  I[1] = p;
+  I[2] = H.p_total;
+  I[3] = H.nnz;
+  I[4] = H.csr.nslab;
+  I[5] = H.csc.nslab;
+  I[6] = (int64_t)(H.csr.idx.size() / kVecIdx);
+  I[7] = (int64_t)(H.csc.idx.size() / kVecIdx);
+  I[8] = (int64_t)H.csr.bundles.size();
+  I[9] = (int64_t)H.csc.bundles.size();
+  I[10] = H.csc.nseg;
+  I[11] = G;
+  I[12] = device;
+  I[13] = (int64_t)(H.csr.idx.size() + H.csc.idx.size()) * 2;
+  I[14] = H.slab_max;
+  *out = D;
+  return PCGS_OK;
+}
+
+int pcgs_design_destroy(pcgs_design_t d) {
+  if (!d) return PCGS_OK;
+  cudaSetDevice(d->device);
+  for (void* p : d->allocs) cudaFree(p);
+  delete d;
+  return PCGS_OK;
+}
+
+int pcgs_design_info(pcgs_design_t d, int64_t* info_h) {
+  if (!d || !info_h) return fail(PCGS_EINVAL, "null argument");
+  memcpy(info_h, d->info, sizeof(d->info));
+  return PCGS_OK;
+}
+
+static int launch_csr(pcgs_design_t d, bool phi, const double* v, const double* omega, double* out, cudaStream_t s,
+                      Scratch& S) {
+  const DesignDev& D = d->dev;
+  const size_t sm = smem_bytes(D);
+  if (D.csr.nslab == 1) {
+    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, out);
+    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, out);
+  } else {
+    double* part = S.get<double>((size_t)D.csr.nslab * D.n);
+    if (!part) return fail(PCGS_ENOMEM, "scratch allocation failed");
+    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, part);
+    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, part);
+    k_rows_combine<<<D.G * 4, 256, 0, s>>>(D, part, v, phi ? omega : nullptr, out);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+int pcgs_matvec(pcgs_design_t d, const double* v, double* out, pcgs_stream_t stream) {
+  if (!d || !v || !out) return fail(PCGS_EINVAL, "null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch S(s);
+  return launch_csr(d, false, v, nullptr, out, s, S);
+}
+
+int pcgs_matvec_t(pcgs_design_t d, const double* w, double* out, pcgs_stream_t stream) {
+  if (!d || !w || !out) return fail(PCGS_EINVAL, "null argument");
+  const DesignDev& D = d->dev;
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch S(s);
+  double* pieces = S.get<double>(D.csc.nseg);
+  if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  FillVecN f{w, nullptr, 0};
+  k_csc<FillVecN><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, nullptr, nullptr, nullptr, 0, 0, 0, out);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+int pcgs_phi_apply(pcgs_design_t d, const double* omega, const double* prior_diag, const double* v, double* out,
+                   pcgs_stream_t stream) {
+  if (!d || !omega || !prior_diag || !v || !out) return fail(PCGS_EINVAL, "null argument");
+  const DesignDev& D = d->dev;
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch S(s);
+  double* w = S.get<double>(D.n + 2);
+  double* pieces = S.get<double>(D.csc.nseg);
+  if (!w || !pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  int rc = launch_csr(d, true, v, omega, w, s, S);
+  if (rc) return rc;
+  FillVecN f{w, nullptr, 0};
+  k_csc<FillVecN><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, v, nullptr, 0, 0, 1, out);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+int pcgs_phi_diagonal(pcgs_design_t d, const double* omega, const double* prior_diag, double* out,
+                      pcgs_stream_t stream) {
+  if (!d || !omega || !prior_diag || !out) return fail(PCGS_EINVAL, "null argument");
+  const DesignDev& D = d->dev;
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch S(s);
+  double* pieces = S.get<double>(D.csc.nseg);
+  if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  FillVecN f{omega, nullptr, 0};
+  k_csc<FillVecN><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, nullptr, 0, 0, 3, out);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+int pcgs_rhs(pcgs_design_t d, const double* kappa, const double* omega, const double* prior_diag,
+             const double* linear, const double* eta, const double* delta, uint64_t seed, uint64_t stream_id,
+             double* b, pcgs_stream_t stream) {
+  if (!d || !omega || !prior_diag || !b) return fail(PCGS_EINVAL, "null argument");
+  const DesignDev& D = d->dev;
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch S(s);
+  double* pieces = S.get<double>(D.csc.nseg);
+  if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  FillRhs f{kappa, omega, eta, seed, kStreamEta ^ stream_id, 0};
+  k_csc<FillRhs><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, delta, seed,
+                                                       kStreamDelta ^ stream_id, 2, b, linear);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+int pcgs_pcg(pcgs_design_t d, const double* omega, const double* prior_diag, const double* minv, const double* scale,
+             const double* b, double* x, int32_t max_iter, double rtol, double* trace, double* alphas, double* betas,
+             int32_t* result, pcgs_stream_t stream) {
+  if (!d || !omega || !prior_diag || !minv || !scale || !b || !x || !trace || !alphas || !betas || !result)
+    return fail(PCGS_EINVAL, "null argument");
+  if (max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
+  const DesignDev& D = d->dev;
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch S(s);
+  PcgArgs A;
+  A.D = D;
+  A.omega = omega;
+  A.diag = prior_diag;
+  A.minv = minv;
+  A.scale = scale;
+  A.b = b;
+  A.x = x;
+  A.max_iter = max_iter;
+  A.rtol = rtol;
+  A.trace = trace;
+  A.alphas = alphas;
+  A.betas = betas;
+  A.result = result;
+  A.w = S.get<double>(D.n + 2);
+  A.zpart = D.csr.nslab > 1 ? S.get<double>((size_t)D.csr.nslab * D.n) : nullptr;
+  A.pieces = S.get<double>(D.csc.nseg);
+  A.zv = S.get<double>(D.pt + 2);
+  A.dvg = S.get<double>(2 * D.pt + 2);
+  A.part = S.get<double>(4 * (size_t)D.G);
+  if (!A.w || !A.pieces || !A.zv || !A.dvg || !A.part || (D.csr.nslab > 1 && !A.zpart))
+    return fail(PCGS_ENOMEM, "scratch allocation failed");
+  void* args[] = {&A};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_pcg, D.G, kThreads, args, smem_bytes(D), s));
+  return PCGS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Generic-operator PCG: the reference loop (cg.py:105-192) with the vector
+// algebra on device and the operator supplied as a callback (any duck-typed
+// `phi`, cg.py:110-113).  Desk-scale: one CTA per vector kernel, host reads
+// the three scalars of every iteration exactly as the reference does.
+// ---------------------------------------------------------------------------
+__device__ double block_sum_1024(double v, double* red) { return block_sum(v, red); }
+
+// mode 0: r = b - Ad, x kept; sums (s r)^2
+// mode 1: z = minv r, d = z;   sums r.z
+// mode 2: sums d.Ad
+// mode 3: x += a d, r -= a Ad, z = minv r; sums (s r)^2, r.z
+// mode 4: d = z + beta d
+__global__ void __launch_bounds__(kThreads) k_opvec(int mode, long long p, double a, const double* b,
+                                                    const double* minv, const double* scale, double* x,
+                                                    double* r, double* z, double* d, const double* Ad,
+                                                    double* out2) {
+  __shared__ double red[64];
+  double s0 = 0.0, s1 = 0.0;
+  for (long long i = threadIdx.x; i < p; i += blockDim.x) {
+    if (mode == 0) {
+      const double ri = b[i] - Ad[i];
+      r[i] = ri;
+      const double t = scale[i] * ri;
+      s0 += t * t;
+    } else if (mode == 1) {
+      const double zi = minv[i] * r[i];
+      z[i] = zi;
+      d[i] = zi;
+      s1 += r[i] * zi;
+    } else if (mode == 2) {
+      s0 += d[i] * Ad[i];
+    } else if (mode == 3) {
+      x[i] = fma(a, d[i], x[i]);
+      const double ri = fma(-a, Ad[i], r[i]);
+      r[i] = ri;
+      const double zi = minv[i] * ri;
+      z[i] = zi;
+      const double t = scale[i] * ri;
+      s0 += t * t;
+      s1 += ri * zi;
+    } else {
+      d[i] = fma(a, d[i], z[i]);
+    }
+  }
+  block_sum2(s0, s1, red);
+  if (threadIdx.x == 0 && out2) {
+    out2[0] = s0;
+    out2[1] = s1;
+  }
+}
+
+int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, const double* scale, const double* b,
+                double* x, int32_t max_iter, double rtol, double* trace_h, double* alphas_h, double* betas_h,
+                int32_t* result_h, pcgs_stream_t stream) {
+  if (!fn || p < 1 || !minv || !scale || !b || !x || !trace_h || !alphas_h || !betas_h || !result_h)
+    return fail(PCGS_EINVAL, "null argument");
+  if (max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch S(s);
+  double* r = S.get<double>(p);
+  double* z = S.get<double>(p);
+  double* dv = S.get<double>(p);
+  double* Ad = S.get<double>(p);
+  double* sc = S.get<double>(2);
+  if (!r || !z || !dv || !Ad || !sc) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  double h2[2];
+  auto run = [&](int mode, double a, double* outp) -> int {
+    k_opvec<<<1, kThreads, 0, s>>>(mode, p, a, b, minv, scale, x, r, z, dv, Ad, outp);
+    CUDA_TRY(cudaGetLastError());
+    if (outp) {
+      CUDA_TRY(cudaMemcpyAsync(h2, outp, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    return PCGS_OK;
+  };
+  auto apply = [&](const double* v) -> int {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    int rc = fn(ctx, v, Ad);
+    if (rc) return fail(PCGS_ECUDA, "operator callback failed");
+    return PCGS_OK;
+  };
+  int rc;
+  int applies = 0, k = 0;
+  result_h[2] = -1;
+  if ((rc = apply(x))) return rc;
+  ++applies;
+  if ((rc = run(0, 0.0, sc))) return rc;
+  double rms = std::sqrt(h2[0] / (double)p);
+  trace_h[0] = rms;
+  auto finish = [&](int status, int fail_iter) {
+    result_h[0] = k;
+    result_h[1] = status;
+    result_h[2] = fail_iter;
+    result_h[3] = applies;
+    return PCGS_OK;
+  };
+  if (!std::isfinite(rms)) return finish(PCGS_NONFINITE, 0);
+  if (!(rms > rtol)) return finish(PCGS_CONVERGED, -1);
+  if ((rc = run(1, 0.0, sc))) return rc;
+  double rz = h2[1];
+  while (k < max_iter) {
+    ++k;
+    if ((rc = apply(dv))) return rc;
+    ++applies;
+    if ((rc = run(2, 0.0, sc))) return rc;
+    const double dAd = h2[0];
+    if (!(dAd > 0)) return finish(PCGS_NOT_PD, k);
+    const double alpha = rz / dAd;
+    alphas_h[k - 1] = alpha;
+    if ((rc = run(3, alpha, sc))) return rc;
+    rms = std::sqrt(h2[0] / (double)p);
+    trace_h[k] = rms;
+    if (rms <= rtol) return finish(PCGS_CONVERGED, -1);
+    if (!std::isfinite(rms)) return finish(PCGS_NONFINITE, k);
+    const double beta = h2[1] / rz;
+    betas_h[k - 1] = beta;
+    rz = h2[1];
+    if ((rc = run(4, beta, nullptr))) return rc;
+  }
+  return finish(PCGS_MAX_ITER, -1);
+}
+
+int pcgs_copy(void* dst, const void* src, int64_t bytes, int kind) {
+  if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(PCGS_EINVAL, "null argument");
+  if (bytes == 0) return PCGS_OK;
+  const cudaMemcpyKind k = kind == 0 ? cudaMemcpyHostToDevice : kind == 1 ? cudaMemcpyDeviceToHost
+                                                                          : cudaMemcpyDeviceToDevice;
+  CUDA_TRY(cudaMemcpy(dst, src, (size_t)bytes, k));
+  return PCGS_OK;
+}
+
+int pcgs_pg_draw(const double* z, int64_t n, uint64_t seed, uint64_t stream_id, double* omega,
+                 pcgs_stream_t stream) {
+  if (n < 0 || (n > 0 && (!z || !omega))) return fail(PCGS_EINVAL, "null argument");
+  if (n == 0) return PCGS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
+  k_pg<<<blocks, 128, 0, s>>>(z, n, seed, kStreamPG ^ stream_id, omega);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+}  // extern "C"

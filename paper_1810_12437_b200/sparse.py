@@ -1,0 +1,399 @@
+"""Binary sparse designs on the B200: the drop-in for priorcg.sparse.
+
+`SparseDesignMatrix` keeps the reference constructor and attribute contract
+(pkg/src/priorcg/sparse.py:46-117): host CSR arrays, standardisation vectors,
+call counters, `matvec` / `matvec_t`.  The kernels run on the GPU through the
+pattern-only store of libpcgs (include/pcgs.h: pcgs_design_create): values
+are implicit ones, a leading dense all-ones column (the intercept that
+`hstack_dense_columns` prepends, sparse.py:314-341) is stripped into a dense
+term, and the remaining pattern is re-encoded as uint16 slab-local indices.
+
+`SparseDesignMatrix.from_pattern` builds the same object straight from a
+shrunk-block pattern plus an intercept flag without materialising the
+reference's float64 `values` (8 B/nnz), which is what paper-scale designs use.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+DEFAULT_DENSE_CAP = 5000
+
+
+class DimensionCapError(RuntimeError):
+    """Dense operation requested above the dimension cap; use the CG path."""
+
+
+class NotPositiveDefiniteError(RuntimeError):
+    """A matrix that must be positive definite is not (sparse.py:31)."""
+
+
+class ZeroVarianceColumnError(ValueError):
+    """Standardization hit a constant column that was not excluded."""
+
+
+def _finite_f64(x, name):
+    arr = np.ascontiguousarray(x, dtype=np.float64)
+    if not np.all(np.isfinite(arr)):
+        raise ValueError(f"{name} contains non-finite entries")
+    return arr
+
+
+def _check_csr(n, p, row_ptr, col_idx, nvals):
+    """The reference's CSR invariants (sparse.py:94-117)."""
+    if row_ptr.shape != (n + 1,):
+        raise ValueError("row_ptr must have length n_rows + 1")
+    if row_ptr[0] != 0 or row_ptr[-1] != nvals:
+        raise ValueError("row_ptr endpoints must be 0 and nnz")
+    if np.any(np.diff(row_ptr) < 0):
+        raise ValueError("row_ptr must be nondecreasing")
+    if len(col_idx) != nvals:
+        raise ValueError("col_idx and values must have equal length")
+    if col_idx.size:
+        if col_idx.min() < 0 or col_idx.max() >= p:
+            raise ValueError("col_idx entry out of range")
+        d = np.diff(col_idx)
+        if d.size:
+            bad = d <= 0
+            inner = row_ptr[1:-1]
+            inner = inner[(inner > 0) & (inner < len(col_idx))] - 1
+            bad[inner] = False
+            if np.any(bad):
+                raise ValueError("col_idx must be strictly increasing within each row")
+
+
+class DesignStore:
+    """Owner of one libpcgs design handle on one CUDA device."""
+
+    def __init__(self, n, p, row_ptr, col_idx, intercept, device=None, slab_max=0):
+        L = _lib.lib()
+        self.device = _lib.cuda_device(device)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _lib.check(L.pcgs_design_create(int(n), int(p), rp.ctypes.data, ci.ctypes.data,
+                                        int(bool(intercept)), int(slab_max),
+                                        int(self.device.index), ctypes.byref(h)))
+        self._h = h
+        info = np.zeros(16, dtype=np.int64)
+        _lib.check(L.pcgs_design_info(h, info.ctypes.data))
+        self.info = info
+        self.n, self.p, self.p_total, self.nnz = (int(v) for v in info[:4])
+        self.intercept = bool(intercept)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def describe(self) -> dict:
+        keys = ["n", "p", "p_total", "nnz", "csr_slabs", "csc_slabs", "csr_vectors",
+                "csc_vectors", "csr_bundles", "csc_bundles", "csc_pieces", "grid", "device",
+                "index_bytes", "slab_max"]
+        return {k: int(v) for k, v in zip(keys, self.info)}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().pcgs_design_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
+
+    # ---- device primitives (tensors in, tensors out) ----
+    def _stream(self):
+        return _lib.stream_ptr(self.device)
+
+    def matvec(self, v, out=None):
+        t = _lib.torch()
+        out = t.empty(self.n, dtype=t.float64, device=self.device) if out is None else out
+        _lib.check(_lib.lib().pcgs_matvec(self._h, _lib.ptr(v), _lib.ptr(out), self._stream()))
+        return out
+
+    def matvec_t(self, w, out=None):
+        t = _lib.torch()
+        out = t.empty(self.p_total, dtype=t.float64, device=self.device) if out is None else out
+        _lib.check(_lib.lib().pcgs_matvec_t(self._h, _lib.ptr(w), _lib.ptr(out), self._stream()))
+        return out
+
+    def phi_apply(self, omega, diag, v, out=None):
+        t = _lib.torch()
+        out = t.empty(self.p_total, dtype=t.float64, device=self.device) if out is None else out
+        _lib.check(_lib.lib().pcgs_phi_apply(self._h, _lib.ptr(omega), _lib.ptr(diag), _lib.ptr(v),
+                                             _lib.ptr(out), self._stream()))
+        return out
+
+    def phi_diagonal(self, omega, diag, out=None):
+        t = _lib.torch()
+        out = t.empty(self.p_total, dtype=t.float64, device=self.device) if out is None else out
+        _lib.check(_lib.lib().pcgs_phi_diagonal(self._h, _lib.ptr(omega), _lib.ptr(diag),
+                                                _lib.ptr(out), self._stream()))
+        return out
+
+
+class SparseDesignMatrix:
+    """CSR design whose products run on the GPU (drop-in for sparse.py:46).
+
+    Parameters are the reference's.  Device products require a binary design
+    (every stored value 1.0) and identity standardisation; anything else raises
+    NotImplementedError at the first device call rather than silently falling
+    back to the CPU.
+    """
+
+    def __init__(self, n_rows, n_cols, row_ptr, col_idx, values,
+                 col_means=None, col_scales=None):
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self._row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self._col_idx = np.ascontiguousarray(col_idx, dtype=np.int64)
+        self._values = _finite_f64(values, "values")
+        self._pattern = None  # (shrunk row_ptr, shrunk col_idx int32, intercept)
+        self.col_means = _finite_f64(np.zeros(self.n_cols) if col_means is None else col_means,
+                                     "col_means")
+        self.col_scales = _finite_f64(np.ones(self.n_cols) if col_scales is None else col_scales,
+                                      "col_scales")
+        self.constant_columns = np.zeros(0, dtype=np.int64)
+        self.matvec_calls = 0
+        self.matvec_t_calls = 0
+        self.weighted_gram_calls = 0
+        self._stores = {}
+        self.slab_max = 0
+        _check_csr(self.n_rows, self.n_cols, self._row_ptr, self._col_idx, len(self._values))
+        if self.col_means.shape != (self.n_cols,) or self.col_scales.shape != (self.n_cols,):
+            raise ValueError("col_means/col_scales must have length n_cols")
+        if np.any(self.col_scales <= 0):
+            raise ValueError("col_scales must be strictly positive")
+
+    # ------------------------------------------------------------ constructors
+    @classmethod
+    def from_dense(cls, dense):
+        dense = np.asarray(dense, dtype=np.float64)
+        if dense.ndim != 2:
+            raise ValueError("expected a 2-d array")
+        n, p = dense.shape
+        mask = dense != 0.0
+        row_ptr = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(mask.sum(axis=1), out=row_ptr[1:])
+        rows, cols = np.nonzero(mask)
+        return cls(n, p, row_ptr, cols.astype(np.int64), dense[rows, cols])
+
+    @classmethod
+    def from_coo(cls, n_rows, n_cols, rows, cols, vals):
+        import scipy.sparse
+        coo = scipy.sparse.coo_matrix(
+            (np.asarray(vals, dtype=np.float64),
+             (np.asarray(rows, dtype=np.int64), np.asarray(cols, dtype=np.int64))),
+            shape=(n_rows, n_cols))
+        csr = coo.tocsr()
+        csr.sum_duplicates()
+        csr.sort_indices()
+        return cls(n_rows, n_cols, csr.indptr, csr.indices, csr.data)
+
+    @classmethod
+    def from_pattern(cls, n_rows, n_shrunk, row_ptr, col_idx, intercept=True, check=True):
+        """Binary design from the shrunk-block pattern (+ optional dense intercept).
+
+        The reference-layout arrays (`row_ptr`, `col_idx`, `values`, with the
+        intercept as column 0) are materialised lazily on first access.
+        """
+        self = cls.__new__(cls)
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_shrunk) + (1 if intercept else 0)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        if check:
+            _check_csr(self.n_rows, int(n_shrunk), rp, ci, int(rp[-1]) if rp.size else 0)
+        self._row_ptr = self._col_idx = self._values = None
+        self._pattern = (rp, ci, bool(intercept))
+        self.col_means = np.zeros(self.n_cols)
+        self.col_scales = np.ones(self.n_cols)
+        self.constant_columns = np.zeros(0, dtype=np.int64)
+        self.matvec_calls = self.matvec_t_calls = self.weighted_gram_calls = 0
+        self._stores = {}
+        self.slab_max = 0
+        return self
+
+    # ------------------------------------------------------------ reference-layout arrays
+    def _materialise(self):
+        rp, ci, icpt = self._pattern
+        n = self.n_rows
+        if not icpt:
+            self._row_ptr = rp.copy()
+            self._col_idx = ci.astype(np.int64)
+        else:
+            self._row_ptr = rp + np.arange(n + 1, dtype=np.int64)
+            counts = np.diff(rp)
+            col = np.empty(len(ci) + n, dtype=np.int64)
+            first = self._row_ptr[:-1]
+            col[first] = 0
+            mask = np.ones(len(col), dtype=bool)
+            mask[first] = False
+            col[mask] = ci.astype(np.int64) + 1
+            self._col_idx = col
+            del counts
+        self._values = np.ones(len(self._col_idx))
+
+    @property
+    def row_ptr(self):
+        if self._row_ptr is None:
+            self._materialise()
+        return self._row_ptr
+
+    @property
+    def col_idx(self):
+        if self._col_idx is None:
+            self._materialise()
+        return self._col_idx
+
+    @property
+    def values(self):
+        if self._values is None:
+            self._materialise()
+        return self._values
+
+    @property
+    def nnz(self):
+        if self._pattern is not None:
+            rp, _, icpt = self._pattern
+            return int(rp[-1]) + (self.n_rows if icpt else 0)
+        return len(self._values)
+
+    # ------------------------------------------------------------ pattern + device store
+    def pattern(self):
+        """(shrunk row_ptr int64, shrunk col_idx int32, intercept flag)."""
+        if self._pattern is not None:
+            return self._pattern
+        if not np.all(self._values == 1.0):
+            raise NotImplementedError(
+                "the B200 store is pattern-only: every stored value must be 1.0 (binary design)")
+        if np.any(self.col_means != 0.0) or np.any(self.col_scales != 1.0):
+            raise NotImplementedError("implicit standardisation is not supported on device yet")
+        rp, ci, n = self._row_ptr, self._col_idx, self.n_rows
+        counts = np.diff(rp)
+        icpt = False
+        if self.n_cols >= 1 and n > 0 and np.all(counts >= 1):
+            icpt = bool(np.all(ci[rp[:-1]] == 0))
+        if icpt:
+            keep = np.ones(len(ci), dtype=bool)
+            keep[rp[:-1]] = False
+            sci = (ci[keep] - 1).astype(np.int32)
+            srp = rp - np.arange(n + 1, dtype=np.int64)
+        else:
+            sci = ci.astype(np.int32)
+            srp = rp.copy()
+        self._pattern = (srp, sci, icpt)
+        return self._pattern
+
+    @property
+    def has_intercept(self):
+        return self.pattern()[2]
+
+    def device_store(self, device=None) -> DesignStore:
+        dev = _lib.cuda_device(device)
+        st = self._stores.get(dev.index)
+        if st is None:
+            if np.any(self.col_means != 0.0) or np.any(self.col_scales != 1.0):
+                raise NotImplementedError("implicit standardisation is not supported on device yet")
+            rp, ci, icpt = self.pattern()
+            st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0), rp, ci, icpt,
+                             device=dev, slab_max=self.slab_max)
+            self._stores[dev.index] = st
+        return st
+
+    # ------------------------------------------------------------ kernels
+    def matvec(self, v):
+        """X v (sparse.py:178-193), on the GPU; numpy in -> numpy out, tensor in -> tensor out."""
+        as_tensor = _lib.is_tensor(v)
+        if not as_tensor:
+            v = np.asarray(v, dtype=np.float64)
+        if tuple(v.shape) != (self.n_cols,):
+            raise ValueError("matvec: vector length must equal n_cols")
+        self.matvec_calls += 1
+        st = self.device_store(v.device if as_tensor and v.is_cuda else None)
+        out = st.matvec(_lib.to_device(v, st.device))
+        return out if as_tensor else out.cpu().numpy()
+
+    def matvec_t(self, w):
+        """X' w (sparse.py:195-203), on the GPU."""
+        as_tensor = _lib.is_tensor(w)
+        if not as_tensor:
+            w = np.asarray(w, dtype=np.float64)
+        if tuple(w.shape) != (self.n_rows,):
+            raise ValueError("matvec_t: vector length must equal n_rows")
+        self.matvec_t_calls += 1
+        st = self.device_store(w.device if as_tensor and w.is_cuda else None)
+        out = st.matvec_t(_lib.to_device(w, st.device))
+        return out if as_tensor else out.cpu().numpy()
+
+    def gram_diagonal(self, omega):
+        """diag(X' diag(omega) X) (sparse.py:235-246): for a binary design, X' omega."""
+        as_tensor = _lib.is_tensor(omega)
+        if not as_tensor:
+            omega = np.asarray(omega, dtype=np.float64)
+        if tuple(omega.shape) != (self.n_rows,):
+            raise ValueError("gram_diagonal: omega length must equal n_rows")
+        st = self.device_store(omega.device if as_tensor and omega.is_cuda else None)
+        t = _lib.torch()
+        zero = t.zeros(st.p_total, dtype=t.float64, device=st.device)
+        out = st.phi_diagonal(_lib.to_device(omega, st.device), zero)
+        return out if as_tensor else out.cpu().numpy()
+
+    # ------------------------------------------------------------ host views (tests)
+    def to_dense_raw(self, dense_cap=DEFAULT_DENSE_CAP):
+        _check_cap(self.n_cols, dense_cap, "to_dense_raw")
+        out = np.zeros((self.n_rows, self.n_cols))
+        rows = np.repeat(np.arange(self.n_rows), np.diff(self.row_ptr))
+        out[rows, self.col_idx] = self.values
+        return out
+
+    def to_dense(self, dense_cap=DEFAULT_DENSE_CAP):
+        raw = self.to_dense_raw(dense_cap=dense_cap)
+        return (raw - self.col_means) / self.col_scales
+
+
+def hstack_dense_columns(cols, X):
+    """Prepend dense columns (sparse.py:314-341).
+
+    A single all-ones column in front of a pattern-only design without an
+    intercept becomes the store's dense intercept (no CSR copy); any other
+    block is materialised in the reference layout.
+    """
+    cols = np.atleast_2d(np.asarray(cols, dtype=np.float64))
+    if cols.shape[0] == 1 and X.n_rows != 1:
+        cols = cols.T
+    if cols.shape[0] != X.n_rows:
+        raise ValueError("column block row count must match the design")
+    q = cols.shape[1]
+    if q == 0:
+        return X
+    if (q == 1 and np.all(cols == 1.0) and X._pattern is not None and not X._pattern[2]):
+        rp, ci, _ = X._pattern
+        return SparseDesignMatrix.from_pattern(X.n_rows, X.n_cols, rp, ci, intercept=True,
+                                               check=False)
+    n = X.n_rows
+    row_ptr = X.row_ptr + q * np.arange(n + 1, dtype=np.int64)
+    counts = np.diff(X.row_ptr)
+    total = X.nnz + n * q
+    col_idx = np.empty(total, dtype=np.int64)
+    values = np.empty(total)
+    dense_pos = (row_ptr[:-1][:, None] + np.arange(q, dtype=np.int64)).ravel()
+    col_idx[dense_pos] = np.tile(np.arange(q, dtype=np.int64), n)
+    values[dense_pos] = cols.ravel()
+    rows = np.repeat(np.arange(n, dtype=np.int64), counts)
+    orig = np.arange(X.nnz, dtype=np.int64) + q * (rows + 1)
+    col_idx[orig] = X.col_idx + q
+    values[orig] = X.values
+    means = np.concatenate([np.zeros(q), X.col_means])
+    scales = np.concatenate([np.ones(q), X.col_scales])
+    return SparseDesignMatrix(n, X.n_cols + q, row_ptr, col_idx, values,
+                              col_means=means, col_scales=scales)
+
+
+def _check_cap(dim, dense_cap, what):
+    if dense_cap is not None and dim > dense_cap:
+        raise DimensionCapError(
+            f"{what}: dimension {dim} exceeds the dense cap {dense_cap}; "
+            "use the matrix-free CG path or raise the cap explicitly")
