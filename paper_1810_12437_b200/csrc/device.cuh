@@ -10,10 +10,10 @@ namespace pcgs {
 
 struct PassDev {
   const uint4* vec;          // uint16 index vectors (8 per uint4)
-  const int4* bundle;        // Bundle {vec_off, seg0, mask, nvec|long}
-  const int4* task;          // Task {slab, b0, b1, split}
+  const uint2* blocks;       // BlockDesc {first_id, mask} per 32-vector block
+  const uint4* warps;        // WarpRange {v0, nvec, blk0, pad}
+  const int2* task;          // Task {slab, warp0}
   const int* cta_task_ptr;   // G+1
-  const int* warp_split;     // kWarps+1 per task
   const long long* slab_lo;  // nslab+1
   const int* piece_ptr;      // CSC: nslab*(p_total+1)
   int nslab;
@@ -108,83 +108,145 @@ __device__ __forceinline__ void fill_smem(double* sv, int len, F& f) {
   __syncthreads();
 }
 
+// Bulk (TMA engine) copy of a 16-byte aligned global slab into shared memory,
+// completion tracked by an mbarrier; an odd tail element is copied by a thread.
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+struct BulkFill {
+  unsigned long long* mbar;  // in shared memory, initialised by bulk_init
+  unsigned phase;
+};
+
+__device__ __forceinline__ void bulk_init(BulkFill& B, unsigned long long* mbar) {
+  B.mbar = mbar;
+  B.phase = 0;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(smem_addr(mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double* src, int len) {
+  const int n2 = len & ~1;
+  if (threadIdx.x == 0) {
+    const unsigned bytes = (unsigned)n2 * 8u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(B.mbar)), "r"(bytes)
+                 : "memory");
+    const unsigned CH = 32768;
+    for (unsigned off = 0; off < bytes; off += CH) {
+      const unsigned sz = bytes - off < CH ? bytes - off : CH;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr((char*)sv + off)),
+          "l"((const char*)src + off), "r"(sz), "r"(smem_addr(B.mbar))
+          : "memory");
+    }
+  }
+  if ((len & 1) && threadIdx.x == 32) sv[len - 1] = __ldcg(src + len - 1);
+  asm volatile(
+      "{\n.reg .pred P;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n}" ::"r"(smem_addr(B.mbar)),
+      "r"(B.phase)
+      : "memory");
+  B.phase ^= 1u;
+  if (threadIdx.x == 0) sv[len] = 0.0;
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------ passes
+// ---------------------------------------------------------------------------
+// Flat per-warp stream: block k of a warp range is vectors [32k, 32k+32), one
+// per lane.  Index loads run kRing blocks ahead in a register ring; the block
+// descriptors (start mask + first segment id) drive a segmented reduction whose
+// open segment is carried across blocks in a per-lane accumulator.
+// ---------------------------------------------------------------------------
+constexpr int kRing = 4;
+
 template <class Epi>
-__device__ __forceinline__ void seg_emit(int4 D, double s, int lane, Epi& epi) {
-  const unsigned mask = (unsigned)D.z;
-  const int nv = D.w;
-  const unsigned le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-  const int rank = __popc(mask & le) - 1;
-  const unsigned after = mask & ~le;
-  int end = after ? (__ffs(after) - 2) : (nv - 1);
-  if (lane >= nv) end = lane;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    double t = __shfl_down_sync(0xffffffffu, s, o);
-    if (lane + o <= end) s += t;
+__device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, double& acc, unsigned& open_id,
+                                             bool& have_open, Epi& epi) {
+  const unsigned M = dsc.y;
+  if (M == 0u) {
+    acc += s;
+    return;
   }
-  if (lane < nv && ((mask >> lane) & 1u)) epi.emit((long long)(unsigned)D.y + rank, s);
+  const int f = __ffs(M) - 1;
+  const int Lh = 31 - __clz(M);
+  // close the open segment: its lanes < f plus every lane's carried partial
+  {
+    const double c = warp_sum(acc + (lane < f ? s : 0.0));
+    if (have_open && lane == 0) epi.emit((long long)open_id, c);
+  }
+  // segments that start and end inside this block: starts in [f, Lh)
+  if (f != Lh) {
+    double x = (lane >= f && lane < Lh) ? s : 0.0;
+    const unsigned le = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+    const unsigned after = M & ~le;
+    const int end = after ? (__ffs(after) - 2) : 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_down_sync(0xffffffffu, x, o);
+      if (lane + o <= end) x += t;
+    }
+    if (((M >> lane) & 1u) && lane < Lh) epi.emit((long long)(dsc.x + __popc(M & (le >> 1))), x);
+  }
+  acc = lane >= Lh ? s : 0.0;
+  open_id = dsc.x + __popc(M) - 1;
+  have_open = true;
 }
 
 template <class Epi>
-__device__ __forceinline__ void process_long(const PassDev& P, int4 D, const double* sv, int lane, Epi& epi) {
-  const int nv = D.w & 0x7fffffff;
-  const uint4* base = P.vec + (unsigned)D.x;
-  double s = 0.0;
-  for (int b0 = 0; b0 < nv; b0 += 128) {
-    uint4 q[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int v = b0 + u * 32 + lane;
-      if (v < nv) q[u] = ldg_stream(base + v);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int v = b0 + u * 32 + lane;
-      if (v < nv) s += gather8(q[u], sv);
-    }
-  }
-  s = warp_sum(s);
-  if (lane == 0) epi.emit((long long)(unsigned)D.y, s);
-}
-
-template <class Epi>
-__device__ __forceinline__ void process_bundles(const PassDev& P, int4 T, const double* sv, Epi& epi) {
+__device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const double* sv, Epi& epi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int b = P.warp_split[T.w + warp];
-  const int b1 = P.warp_split[T.w + warp + 1];
-  while (b < b1) {
-    const int nb = min(4, b1 - b);
-    int4 d = make_int4(0, 0, 0, 0);
-    if (lane < nb) d = __ldg(P.bundle + b + lane);
-    int4 D[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      D[u].x = __shfl_sync(0xffffffffu, d.x, u);
-      D[u].y = __shfl_sync(0xffffffffu, d.y, u);
-      D[u].z = __shfl_sync(0xffffffffu, d.z, u);
-      D[u].w = __shfl_sync(0xffffffffu, d.w, u);
+  const uint4 R = __ldg(P.warps + warp0 + warp);
+  const int nvec = (int)R.y;
+  if (nvec == 0) return;
+  const int nb = (nvec + 31) >> 5;
+  const uint4* base = P.vec + R.x;
+  const uint2* bd = P.blocks + R.z;
+  // L2 prefetch of the whole range (TMA engine; no registers or scoreboards)
+  if (lane == 0) {
+    const char* p0 = (const char*)base;
+    const unsigned bytes = (unsigned)nvec * 16u;
+    for (unsigned off = 0; off < bytes; off += 16384u) {
+      const unsigned sz = bytes - off < 16384u ? bytes - off : 16384u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0 + off), "r"(sz) : "memory");
     }
-    if (D[0].w < 0) {  // long bundle (flag in the sign bit)
-      process_long(P, D[0], sv, lane, epi);
-      b += 1;
-      continue;
+    const unsigned long long d0 = (unsigned long long)bd & ~15ull;
+    const unsigned long long d1 = ((unsigned long long)(bd + nb) + 15ull) & ~15ull;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d0), "r"((unsigned)(d1 - d0)) : "memory");
+  }
+  double acc = 0.0;
+  unsigned open_id = 0;
+  bool have_open = false;
+  // batches of kRing blocks: all loads of a batch issued together, then consumed
+  for (int k0 = 0; k0 < nb; k0 += kRing) {
+    uint4 q[kRing];
+    uint2 dl = lane < kRing && k0 + lane < nb ? __ldg(bd + k0 + lane) : make_uint2(0u, 0u);
+#pragma unroll
+    for (int u = 0; u < kRing; ++u) {
+      const int v = (k0 + u) * 32 + lane;
+      if (v < nvec) q[u] = ldg_stream(base + v);
     }
-    int m = 1;
-    while (m < nb && D[m].w >= 0) ++m;
-    uint4 q[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (u < m && lane < D[u].w) q[u] = ldg_stream(P.vec + (unsigned)D[u].x + lane);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (u < m) {
-        double s = lane < D[u].w ? gather8(q[u], sv) : 0.0;
-        seg_emit(D[u], s, lane, epi);
+    for (int u = 0; u < kRing; ++u) {
+      const int k = k0 + u;
+      if (k < nb) {
+        uint2 dsc;
+        dsc.x = __shfl_sync(0xffffffffu, dl.x, u);
+        dsc.y = __shfl_sync(0xffffffffu, dl.y, u);
+        const int v = k * 32 + lane;
+        const double s = v < nvec ? gather8(q[u], sv) : 0.0;
+        block_reduce(dsc, s, lane, acc, open_id, have_open, epi);
       }
     }
-    b += m;
   }
+  const double c = warp_sum(acc);
+  if (have_open && lane == 0) epi.emit((long long)open_id, c);
 }
 
 // Runs every task of this CTA: fill the slab vector into shared memory, then
@@ -194,11 +256,11 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
   const int c = blockIdx.x;
   const int t0 = P.cta_task_ptr[c], t1 = P.cta_task_ptr[c + 1];
   for (int t = t0; t < t1; ++t) {
-    const int4 T = __ldg(P.task + t);
+    const int2 T = __ldg(P.task + t);
     const long long lo = P.slab_lo[T.x], hi = P.slab_lo[T.x + 1];
     __syncthreads();
     fill(sv, lo, (int)(hi - lo));
-    process_bundles(P, T, sv, epi);
+    process_warp(P, T.y, sv, epi);
   }
 }
 

@@ -69,14 +69,16 @@ static int upload_pass(pcgs_design* D, const PassHost& H, PassDev& P) {
   const uint16_t* idx;
   if ((rc = upload(D, H.idx, &idx))) return rc;
   P.vec = (const uint4*)idx;
-  const Bundle* b;
-  if ((rc = upload(D, H.bundles, &b))) return rc;
-  P.bundle = (const int4*)b;
+  const BlockDesc* b;
+  if ((rc = upload(D, H.blocks, &b))) return rc;
+  P.blocks = (const uint2*)b;
+  const WarpRange* w;
+  if ((rc = upload(D, H.warps, &w))) return rc;
+  P.warps = (const uint4*)w;
   const Task* t;
   if ((rc = upload(D, H.tasks, &t))) return rc;
-  P.task = (const int4*)t;
+  P.task = (const int2*)t;
   if ((rc = upload(D, H.cta_task_ptr, &P.cta_task_ptr))) return rc;
-  if ((rc = upload(D, H.warp_split, &P.warp_split))) return rc;
   std::vector<long long> lo(H.slab_lo.begin(), H.slab_lo.end());
   if ((rc = upload(D, lo, &P.slab_lo))) return rc;
   if ((rc = upload(D, H.piece_ptr, &P.piece_ptr))) return rc;
@@ -117,18 +119,10 @@ struct FillVecRef {  // CSR slab of a reference-layout p_total vector
   }
 };
 
-struct FillVecN {  // CSC slab of an n-vector (optionally scaled elementwise)
+struct FillVecN {  // CSC slab of an n-vector: TMA bulk copy
   const double* w;
-  const double* scale;  // may be null
-  long long lo;
-  __device__ double operator()(int j) const {
-    double x = __ldcg(w + lo + j);
-    return scale ? x * __ldg(scale + lo + j) : x;
-  }
-  __device__ void operator()(double* sv, long long l, int len) {
-    lo = l;
-    fill_smem(sv, len, *this);
-  }
+  BulkFill* bf;
+  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, w + l, len); }
 };
 
 struct FillRhs {  // u_i = kappa_i + sqrt(omega_i) * eta_i
@@ -243,6 +237,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_csc(DesignDev D, Fill f, double
   run_pass(D.csc, sv, f, e);
 }
 
+__global__ void __launch_bounds__(kThreads, 1) k_csc_vec(DesignDev D, const double* w, double* pieces) {
+  extern __shared__ __align__(128) double sv[];
+  __shared__ unsigned long long mbar;
+  BulkFill bf;
+  bulk_init(bf, &mbar);
+  FillVecN f{w, &bf};
+  EpiStore e{pieces};
+  run_pass(D.csc, sv, f, e);
+}
+
 // out[ref(j)] = column_sum(j) + diag_j * v[ref(j)]  (diag/v may be null)
 //               + sqrt(diag_j) * delta_j           (mode 2: RHS noise)
 __global__ void k_assemble(DesignDev D, const double* pieces, const double* diag, const double* v,
@@ -316,6 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[64];
+  __shared__ unsigned long long mbar;
+  BulkFill bf;
+  bulk_init(bf, &mbar);
   const DesignDev& D = A.D;
   const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
   const long long pt = D.pt, p = D.p, n = D.n;
@@ -416,7 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
 
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
     {
-      FillVecN f{A.w, nullptr, 0};
+      FillVecN f{A.w, &bf};
       EpiStore e{A.pieces};
       run_pass(D.csc, sv, f, e);
     }
@@ -559,7 +566,7 @@ static int set_smem_attrs(const DesignDev& D) {
   const int bytes = (int)smem_bytes(D);
   CUDA_TRY(cudaFuncSetAttribute(k_csr_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(cudaFuncSetAttribute(k_csr_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CUDA_TRY(cudaFuncSetAttribute(k_csc<FillVecN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(cudaFuncSetAttribute(k_csc_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(cudaFuncSetAttribute(k_csc<FillRhs>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   return PCGS_OK;
@@ -614,13 +621,15 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int
   I[5] = H.csc.nslab;
   I[6] = (int64_t)(H.csr.idx.size() / kVecIdx);
   I[7] = (int64_t)(H.csc.idx.size() / kVecIdx);
-  I[8] = (int64_t)H.csr.bundles.size();
-  I[9] = (int64_t)H.csc.bundles.size();
+  I[8] = (int64_t)H.csr.blocks.size();
+  I[9] = (int64_t)H.csc.blocks.size();
   I[10] = H.csc.nseg;
   I[11] = G;
   I[12] = device;
   I[13] = (int64_t)(H.csr.idx.size() + H.csc.idx.size()) * 2;
   I[14] = H.slab_max;
+  I[15] = (H.csr.lds_conflict_excess + H.csc.lds_conflict_excess) * 1000000 /
+          std::max<int64_t>(1, H.csr.lds_groups + H.csc.lds_groups);
   *out = D;
   return PCGS_OK;
 }
@@ -671,8 +680,7 @@ int pcgs_matvec_t(pcgs_design_t d, const double* w, double* out, pcgs_stream_t s
   Scratch S(s);
   double* pieces = S.get<double>(D.csc.nseg);
   if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
-  FillVecN f{w, nullptr, 0};
-  k_csc<FillVecN><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, w, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, nullptr, nullptr, nullptr, 0, 0, 0, out);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
@@ -689,8 +697,7 @@ int pcgs_phi_apply(pcgs_design_t d, const double* omega, const double* prior_dia
   if (!w || !pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
   int rc = launch_csr(d, true, v, omega, w, s, S);
   if (rc) return rc;
-  FillVecN f{w, nullptr, 0};
-  k_csc<FillVecN><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, w, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, v, nullptr, 0, 0, 1, out);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
@@ -704,8 +711,7 @@ int pcgs_phi_diagonal(pcgs_design_t d, const double* omega, const double* prior_
   Scratch S(s);
   double* pieces = S.get<double>(D.csc.nseg);
   if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
-  FillVecN f{omega, nullptr, 0};
-  k_csc<FillVecN><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, omega, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, nullptr, 0, 0, 3, out);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;

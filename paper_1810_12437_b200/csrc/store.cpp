@@ -15,7 +15,7 @@ namespace pcgs {
 
 namespace {
 
-constexpr int64_t kPieceMaxVec = 256;  // CSC pieces: at most 8 warp iterations
+constexpr int64_t kPieceMaxVec = 256;  // CSC pieces: at most 256 vectors (load balance)
 
 std::vector<int64_t> make_slabs(int64_t len, int64_t slab_max) {
   std::vector<int64_t> lo;
@@ -24,188 +24,191 @@ std::vector<int64_t> make_slabs(int64_t len, int64_t slab_max) {
   per = (per + 15) / 16 * 16;  // keep slab starts 128-byte aligned in doubles
   if (per > slab_max) per = slab_max;
   for (int64_t s = 0; s <= ns; ++s) lo.push_back(std::min<int64_t>(s * per, std::max<int64_t>(len, 0)));
-  // drop empty trailing slabs (possible after rounding)
   while (lo.size() > 2 && lo[lo.size() - 2] == lo.back()) lo.pop_back();
   return lo;
 }
 
-// Writes segments of one slab into a pass, packing them into bundles and
-// permuting indices for bank balance.
-class Emitter {
- public:
-  Emitter(PassHost& P, uint16_t sentinel) : P_(P), sent_(sentinel) {}
-  ~Emitter() { flush(); }
-
-  void add(uint32_t seg, const uint16_t* d, int64_t len) {
-    int64_t nv = len == 0 ? 1 : (len + kVecIdx - 1) / kVecIdx;
-    if (!pend_.empty() && (seg != last_seg_ + 1 || pend_vec_ + nv > 32)) flush();
-    last_seg_ = seg;
-    if (nv > 32) {
-      flush();
-      emit_long(seg, d, len, nv);
-      return;
-    }
-    pend_.push_back({seg, std::vector<uint16_t>(d, d + len), (int)nv});
-    pend_vec_ += (int)nv;
-    if (pend_vec_ == 32) flush();
-  }
-
-  void flush() {
-    if (pend_.empty()) return;
-    const uint32_t off = (uint32_t)(P_.idx.size() / kVecIdx);
-    const int nvec = pend_vec_;
-    P_.idx.resize(P_.idx.size() + (size_t)nvec * kVecIdx, sent_);
-    uint16_t* out = P_.idx.data() + (size_t)off * kVecIdx;
-    uint32_t mask = 0;
-    int lane = 0;
-    // counts[slot][half][bank pair]
-    std::array<std::array<std::array<uint16_t, 16>, 2>, 8> cnt{};
-    for (auto& s : pend_) {
-      mask |= 1u << lane;
-      // deal the segment's indices round-robin over its lanes, bank-sorted,
-      // so each lane gets a spread of banks
-      std::vector<uint16_t>& v = s.idx;
-      std::stable_sort(v.begin(), v.end(), [](uint16_t a, uint16_t b) { return (a & 15) < (b & 15); });
-      std::vector<std::vector<uint16_t>> per(s.nv);
-      for (size_t t = 0; t < v.size(); ++t) per[t % s.nv].push_back(v[t]);
-      for (int q = 0; q < s.nv; ++q, ++lane) {
-        const int h = lane >> 4;
-        bool used[8] = {false, false, false, false, false, false, false, false};
-        for (uint16_t ix : per[q]) {
-          const int b = ix & 15;
-          int best = -1;
-          for (int k = 0; k < 8; ++k)
-            if (!used[k] && (best < 0 || cnt[k][h][b] < cnt[best][h][b])) best = k;
-          used[best] = true;
-          cnt[best][h][b]++;
-          out[lane * kVecIdx + best] = ix;
-        }
-      }
-    }
-    Bundle B{off, pend_.front().seg, mask, (uint32_t)nvec};
-    P_.bundles.push_back(B);
-    pend_.clear();
-    pend_vec_ = 0;
-  }
-
- private:
-  struct Pend {
-    uint32_t seg;
-    std::vector<uint16_t> idx;
-    int nv;
-  };
-
-  void emit_long(uint32_t seg, const uint16_t* d, int64_t len, int64_t nv) {
-    const uint32_t off = (uint32_t)(P_.idx.size() / kVecIdx);
-    P_.idx.resize(P_.idx.size() + (size_t)nv * kVecIdx, sent_);
-    uint16_t* out = P_.idx.data() + (size_t)off * kVecIdx;
-    std::array<std::vector<uint16_t>, 16> bucket;
-    for (int64_t t = 0; t < len; ++t) bucket[d[t] & 15].push_back(d[t]);
-    int64_t remaining = len;
-    const int64_t iters = (nv + 31) / 32;
-    std::array<int, 16> order;
-    for (int64_t it = 0; it < iters && remaining > 0; ++it) {
-      for (int k = 0; k < kVecIdx && remaining > 0; ++k) {
-        for (int h = 0; h < 2 && remaining > 0; ++h) {
-          // lanes of this half-warp group that own a vector
-          int64_t v0 = it * 32 + h * 16;
-          int m = (int)std::max<int64_t>(0, std::min<int64_t>(16, nv - v0));
-          if (m == 0) continue;
-          std::iota(order.begin(), order.end(), 0);
-          std::sort(order.begin(), order.end(),
-                    [&](int a, int b) { return bucket[a].size() > bucket[b].size(); });
-          int take = (int)std::min<int64_t>(m, remaining);
-          for (int q = 0; q < take; ++q) {
-            int b = order[q % 16];
-            if (bucket[b].empty()) {  // fewer non-empty buckets than lanes: reuse the largest
-              for (int r = 0; r < 16; ++r)
-                if (!bucket[order[r]].empty()) { b = order[r]; break; }
-            }
-            out[(v0 + q) * kVecIdx + k] = bucket[b].back();
-            bucket[b].pop_back();
-            --remaining;
-          }
-        }
-      }
-    }
-    Bundle B{off, seg, 0u, (uint32_t)nv | kLongFlag};
-    P_.bundles.push_back(B);
-  }
-
-  PassHost& P_;
-  uint16_t sent_;
-  std::vector<Pend> pend_;
-  int pend_vec_ = 0;
-  uint32_t last_seg_ = 0xffffffffu;
+struct Seg {
+  uint32_t id;
+  uint64_t off;  // into the slab buffer
+  uint32_t len;  // real indices
+  uint32_t nv;   // vectors (>= 1)
 };
 
-inline int64_t bundle_weight(const Bundle& b) { return (int64_t)(b.nvec & ~kLongFlag) + 2; }
+struct SlabSegs {
+  std::vector<uint16_t> buf;
+  std::vector<Seg> segs;
+  uint16_t sentinel = 0;
+  void add(uint32_t id, const uint16_t* d, uint32_t len) {
+    Seg s{id, buf.size(), len, len == 0 ? 1u : (len + kVecIdx - 1) / kVecIdx};
+    buf.insert(buf.end(), d, d + len);
+    segs.push_back(s);
+  }
+};
 
-// Static CTA/warp plan (deterministic: every output is produced by exactly one
-// warp and every partial sum is reduced in a fixed order).
-void plan_pass(PassHost& P, const std::vector<int64_t>& slab_b, int G) {
-  const int ns = P.nslab;
-  std::vector<int64_t> pre(P.bundles.size() + 1, 0);
-  for (size_t b = 0; b < P.bundles.size(); ++b) pre[b + 1] = pre[b] + bundle_weight(P.bundles[b]);
-  auto cut = [&](int64_t b0, int64_t b1, int parts, std::vector<int32_t>& outv) {
-    // boundaries of `parts` ranges over [b0, b1) with balanced weight
-    const int64_t w0 = pre[b0], W = pre[b1] - pre[b0];
-    outv.push_back((int32_t)b0);
-    for (int q = 1; q < parts; ++q) {
-      int64_t target = w0 + (W * q + parts - 1) / parts;
-      int64_t b = std::lower_bound(pre.begin() + b0, pre.begin() + b1 + 1, target) - pre.begin();
-      b = std::max<int64_t>(b, outv.back());
-      b = std::min<int64_t>(b, b1);
-      outv.push_back((int32_t)b);
+// Indices of one segment still to be placed, bucketed by shared-memory bank pair.
+struct Pool {
+  std::array<std::vector<uint16_t>, 16> b;
+  uint32_t remaining = 0;
+  void load(const uint16_t* d, uint32_t len) {
+    for (auto& v : b) v.clear();
+    for (uint32_t t = 0; t < len; ++t) b[d[t] & 15].push_back(d[t]);
+    remaining = len;
+  }
+  // an index whose bank pair is not in `used` (largest bucket first); -1 when empty
+  int pick(uint32_t used, bool& conflict) {
+    conflict = false;
+    if (remaining == 0) return -1;
+    int best = -1;
+    size_t bs = 0;
+    for (int k = 0; k < 16; ++k)
+      if (!((used >> k) & 1u) && b[k].size() > bs) { best = k; bs = b[k].size(); }
+    if (best < 0) {
+      conflict = true;
+      for (int k = 0; k < 16; ++k)
+        if (b[k].size() > bs) { best = k; bs = b[k].size(); }
     }
-    outv.push_back((int32_t)b1);
-  };
-  P.tasks.clear();
-  P.warp_split.clear();
+    const int v = b[best].back();
+    b[best].pop_back();
+    --remaining;
+    return v;
+  }
+};
+
+// Appends one warp range (segments [s0, s1) of slab S) to the pass.
+void emit_warp(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std::vector<Pool>& pools) {
+  WarpRange R{};
+  R.v0 = (uint32_t)(P.idx.size() / kVecIdx);
+  R.blk0 = (uint32_t)P.blocks.size();
+  uint64_t nvec = 0;
+  for (size_t s = s0; s < s1; ++s) nvec += S.segs[s].nv;
+  R.nvec = (uint32_t)nvec;
+  P.warps.push_back(R);
+  if (nvec == 0) return;
+  P.idx.resize(P.idx.size() + nvec * kVecIdx, S.sentinel);
+  uint16_t* out = P.idx.data() + (size_t)R.v0 * kVecIdx;
+  const uint64_t nb = (nvec + 31) / 32;
+  // per-lane segment for the current block; pools keyed by lane-segment slot
+  size_t seg = s0;
+  uint32_t in_seg = 0;  // vectors of `seg` already laid out
+  int lane_seg[32];
+  int lane_pool[32];
+  int next_pool = 0;
+  int seg_pool = -1;
+  for (uint64_t k = 0; k < nb; ++k) {
+    uint32_t mask = 0;
+    uint32_t first_id = 0;
+    bool have_first = false;
+    // assign lanes
+    for (int l = 0; l < 32; ++l) {
+      const uint64_t v = k * 32 + l;
+      if (v >= nvec) { lane_seg[l] = -1; lane_pool[l] = -1; continue; }
+      while (in_seg >= S.segs[seg].nv) { ++seg; in_seg = 0; seg_pool = -1; }
+      if (in_seg == 0) {
+        mask |= 1u << l;
+        if (!have_first) { first_id = S.segs[seg].id; have_first = true; }
+      }
+      if (seg_pool < 0) {
+        seg_pool = next_pool;
+        next_pool = (next_pool + 1) % (int)pools.size();
+        pools[seg_pool].load(S.buf.data() + S.segs[seg].off, S.segs[seg].len);
+      }
+      lane_seg[l] = (int)seg;
+      lane_pool[l] = seg_pool;
+      ++in_seg;
+    }
+    P.blocks.push_back(BlockDesc{first_id, mask});
+    // bank-balanced placement: group = (slot, half-warp)
+    for (int slot = 0; slot < kVecIdx; ++slot) {
+      for (int h = 0; h < 2; ++h) {
+        uint32_t used = 0;
+        bool any = false;
+        for (int l = h * 16; l < h * 16 + 16; ++l) {
+          if (lane_seg[l] < 0) continue;
+          any = true;
+          bool conflict;
+          const int ix = pools[lane_pool[l]].pick(used, conflict);
+          if (ix < 0) continue;  // pad: sentinel already in place (broadcast)
+          used |= 1u << (ix & 15);
+          P.lds_conflict_excess += conflict;
+          out[(k * 32 + l) * kVecIdx + slot] = (uint16_t)ix;
+        }
+        P.lds_groups += any;
+      }
+    }
+  }
+}
+
+// Balanced cut of segments [a, b) into `parts` ranges by vector count.
+void cut(const std::vector<uint64_t>& pre, size_t a, size_t b, int parts, std::vector<size_t>& outv) {
+  outv.clear();
+  outv.push_back(a);
+  const uint64_t w0 = pre[a], W = pre[b] - pre[a];
+  for (int q = 1; q < parts; ++q) {
+    const uint64_t target = w0 + (W * q + parts / 2) / parts;
+    size_t s = std::lower_bound(pre.begin() + a, pre.begin() + b + 1, target) - pre.begin();
+    // choose the closer of s-1 / s
+    if (s > a && s <= b && target - pre[s - 1] < pre[s] - target) --s;
+    s = std::max(s, outv.back());
+    s = std::min(s, b);
+    outv.push_back(s);
+  }
+  outv.push_back(b);
+}
+
+void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G) {
+  const int ns = (int)slabs.size();
   P.cta_task_ptr.assign(G + 1, 0);
-  auto add_task = [&](int slab, int32_t b0, int32_t b1) {
-    Task t{slab, b0, b1, (int32_t)P.warp_split.size()};
-    std::vector<int32_t> ws;
-    cut(b0, b1, kWarps, ws);
-    P.warp_split.insert(P.warp_split.end(), ws.begin(), ws.end());
+  std::vector<Pool> pools(40);
+  std::vector<std::vector<uint64_t>> pre(ns);
+  std::vector<uint64_t> sw(ns);
+  uint64_t W = 0;
+  for (int s = 0; s < ns; ++s) {
+    auto& pr = pre[s];
+    pr.assign(slabs[s].segs.size() + 1, 0);
+    for (size_t q = 0; q < slabs[s].segs.size(); ++q) pr[q + 1] = pr[q] + slabs[s].segs[q].nv;
+    sw[s] = pr.back();
+    W += sw[s];
+  }
+  auto emit_task = [&](int s, size_t a, size_t b) {
+    Task t{s, (int32_t)P.warps.size()};
+    std::vector<size_t> wc;
+    cut(pre[s], a, b, kWarps, wc);
+    for (int w = 0; w < kWarps; ++w) emit_warp(P, slabs[s], wc[w], wc[w + 1], pools);
     P.tasks.push_back(t);
   };
   if (ns <= G) {
-    // proportional CTA allocation per slab (largest remainder, at least one each)
-    std::vector<int64_t> sw(ns);
-    int64_t W = 0;
-    for (int s = 0; s < ns; ++s) { sw[s] = pre[slab_b[s + 1]] - pre[slab_b[s]] + 1; W += sw[s]; }
     std::vector<int> cnt(ns, 1);
     int left = G - ns;
     std::vector<std::pair<double, int>> rem;
     for (int s = 0; s < ns; ++s) {
-      double ideal = (double)sw[s] / (double)W * G - 1.0;
-      int add = std::max(0, (int)ideal);
-      add = std::min(add, left);
+      const double ideal = W ? (double)sw[s] / (double)W * G - 1.0 : 0.0;
+      int add = std::min(std::max(0, (int)ideal), left);
       cnt[s] += add;
       left -= add;
       rem.push_back({ideal - add, s});
     }
-    std::sort(rem.begin(), rem.end(), [](auto& a, auto& b) { return a.first > b.first; });
+    std::sort(rem.begin(), rem.end(), [](auto& x, auto& y) { return x.first > y.first; });
     for (size_t q = 0; left > 0; q = (q + 1) % rem.size(), --left) cnt[rem[q].second]++;
     int c = 0;
     for (int s = 0; s < ns; ++s) {
-      std::vector<int32_t> cb;
-      cut(slab_b[s], slab_b[s + 1], cnt[s], cb);
+      std::vector<size_t> cb;
+      cut(pre[s], 0, slabs[s].segs.size(), cnt[s], cb);
       for (int q = 0; q < cnt[s]; ++q, ++c) {
         P.cta_task_ptr[c] = (int32_t)P.tasks.size();
-        add_task(s, cb[q], cb[q + 1]);
+        emit_task(s, cb[q], cb[q + 1]);
         P.cta_task_ptr[c + 1] = (int32_t)P.tasks.size();
       }
+      std::vector<uint16_t>().swap(slabs[s].buf);
     }
   } else {
-    std::vector<int32_t> cb;
-    cut(0, (int64_t)P.bundles.size(), G, cb);
+    // more slabs than CTAs: contiguous groups of slabs per CTA
     for (int c = 0; c < G; ++c) {
       P.cta_task_ptr[c] = (int32_t)P.tasks.size();
-      for (int s = 0; s < ns; ++s) {
-        int64_t a = std::max<int64_t>(cb[c], slab_b[s]), b = std::min<int64_t>(cb[c + 1], slab_b[s + 1]);
-        if (a < b) add_task(s, (int32_t)a, (int32_t)b);
+      const int a = (int)((int64_t)ns * c / G), b = (int)((int64_t)ns * (c + 1) / G);
+      for (int s = a; s < b; ++s) {
+        emit_task(s, 0, slabs[s].segs.size());
+        std::vector<uint16_t>().swap(slabs[s].buf);
       }
       P.cta_task_ptr[c + 1] = (int32_t)P.tasks.size();
     }
@@ -246,23 +249,21 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
     P.nslab = (int)P.slab_lo.size() - 1;
     P.nseg = (int64_t)P.nslab * n;
     std::vector<int64_t> cursor(row_ptr, row_ptr + n);
-    std::vector<int64_t> slab_b(P.nslab + 1, 0);
-    std::vector<uint16_t> buf;
+    std::vector<SlabSegs> slabs(P.nslab);
+    std::vector<uint16_t> tmp;
     for (int s = 0; s < P.nslab; ++s) {
-      slab_b[s] = (int64_t)P.bundles.size();
       const int64_t lo = P.slab_lo[s], hi = P.slab_lo[s + 1];
-      Emitter E(P, (uint16_t)(hi - lo));
+      SlabSegs& S = slabs[s];
+      S.sentinel = (uint16_t)(hi - lo);
       for (int64_t i = 0; i < n; ++i) {
-        buf.clear();
+        tmp.clear();
         int64_t k = cursor[i];
-        while (k < row_ptr[i + 1] && col_idx[k] < hi) buf.push_back((uint16_t)(col_idx[k++] - lo));
+        while (k < row_ptr[i + 1] && col_idx[k] < hi) tmp.push_back((uint16_t)(col_idx[k++] - lo));
         cursor[i] = k;
-        E.add((uint32_t)(s * n + i), buf.data(), (int64_t)buf.size());
+        S.add((uint32_t)(s * n + i), tmp.data(), (uint32_t)tmp.size());
       }
-      E.flush();
     }
-    slab_b[P.nslab] = (int64_t)P.bundles.size();
-    plan_pass(P, slab_b, G);
+    plan_and_emit(P, slabs, G);
   }
 
   // ------------- CSC pass: segments = pieces of (row slab, column) -------------
@@ -282,35 +283,33 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
     P.nslab = (int)P.slab_lo.size() - 1;
     P.piece_ptr.assign((size_t)P.nslab * (pt + 1), 0);
     std::vector<int64_t> cursor(col_ptr.begin(), col_ptr.end() - 1);
-    std::vector<int64_t> slab_b(P.nslab + 1, 0);
-    std::vector<uint16_t> buf;
+    std::vector<SlabSegs> slabs(P.nslab);
+    std::vector<uint16_t> tmp;
     uint32_t piece = 0;
     for (int s = 0; s < P.nslab; ++s) {
-      slab_b[s] = (int64_t)P.bundles.size();
       const int64_t lo = P.slab_lo[s], hi = P.slab_lo[s + 1];
-      Emitter E(P, (uint16_t)(hi - lo));
+      SlabSegs& S = slabs[s];
+      S.sentinel = (uint16_t)(hi - lo);
       for (int64_t j = 0; j < pt; ++j) {
         P.piece_ptr[(size_t)s * (pt + 1) + j] = (int32_t)piece;
-        buf.clear();
+        tmp.clear();
         if (j < p) {
           int64_t k = cursor[j];
-          while (k < col_ptr[j + 1] && row_idx[k] < hi) buf.push_back((uint16_t)(row_idx[k++] - lo));
+          while (k < col_ptr[j + 1] && row_idx[k] < hi) tmp.push_back((uint16_t)(row_idx[k++] - lo));
           cursor[j] = k;
         } else {
-          for (int64_t i = lo; i < hi; ++i) buf.push_back((uint16_t)(i - lo));
+          for (int64_t i = lo; i < hi; ++i) tmp.push_back((uint16_t)(i - lo));
         }
-        const int64_t len = (int64_t)buf.size();
+        const int64_t len = (int64_t)tmp.size();
         for (int64_t a = 0; a < len; a += kPieceMaxVec * kVecIdx) {
-          int64_t m = std::min<int64_t>(kPieceMaxVec * kVecIdx, len - a);
-          E.add(piece++, buf.data() + a, m);
+          const int64_t m = std::min<int64_t>(kPieceMaxVec * kVecIdx, len - a);
+          S.add(piece++, tmp.data() + a, (uint32_t)m);
         }
       }
       P.piece_ptr[(size_t)s * (pt + 1) + pt] = (int32_t)piece;
-      E.flush();
     }
-    slab_b[P.nslab] = (int64_t)P.bundles.size();
     P.nseg = piece;
-    plan_pass(P, slab_b, G);
+    plan_and_emit(P, slabs, G);
   }
   return "";
 }

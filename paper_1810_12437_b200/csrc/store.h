@@ -1,18 +1,21 @@
 // Pattern-only tiled store for a binary design (host side of the pcgs library).
 //
-// Layout (both directions share it; see DESIGN.md §3):
+// Layout (both directions share it; DESIGN.md §3):
 //   * the gathered vector is cut into SLABS that fit one CTA's shared memory
 //     (CSR: column slabs of v; CSC: row slabs of w = ω⊙Xv);
 //   * every output SEGMENT (CSR: a row within a column slab; CSC: a piece of
 //     a column within a row slab) is a run of uint16 slab-local indices padded
 //     to a multiple of 8 with the slab's SENTINEL index (which points at a
-//     zero in shared memory), so one 16-byte vector never straddles segments;
-//   * segments are packed into BUNDLES of one warp's work: either up to 32
-//     short segments (one 16-byte vector per lane) or one long segment that
-//     the warp walks 32 vectors at a time;
+//     zero in shared memory), so a 16-byte vector never straddles segments;
+//   * the segments of a slab are cut into WARP RANGES (contiguous, balanced by
+//     vector count, cut only at segment boundaries).  A warp streams its range
+//     32 vectors (one per lane) at a time; every 32-vector BLOCK carries a
+//     descriptor {id of the first segment starting in it, 32-bit start mask},
+//     so the kernel's loads never depend on segment structure and can be
+//     prefetched many blocks ahead;
 //   * inside a segment the index order is free (the sum is order-independent
-//     in exact arithmetic), so the builder permutes indices so that each
-//     16-lane half-warp LDS.64 touches 16 distinct shared-memory bank pairs.
+//     in exact arithmetic), so the builder places indices so that each 16-lane
+//     half-warp LDS.64 of a block touches distinct shared-memory bank pairs.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -20,36 +23,39 @@
 
 namespace pcgs {
 
-constexpr int kWarps = 16;            // warps per CTA of the pass kernels
-constexpr int kThreads = kWarps * 32; // 512
-constexpr int kVecIdx = 8;            // uint16 indices per 16-byte vector
-constexpr uint32_t kLongFlag = 0x80000000u;
+constexpr int kWarps = 32;             // warps per CTA of the pass kernels
+constexpr int kThreads = kWarps * 32;  // 1024
+constexpr int kVecIdx = 8;             // uint16 indices per 16-byte vector
 
-struct Bundle {      // 16 bytes, device-readable as int4
-  uint32_t vec_off;  // first vector (units of 8 indices) in the pass stream
-  uint32_t seg0;     // first output segment id
-  uint32_t mask;     // multi: bit l set when lane l starts a new segment
-  uint32_t nvec;     // number of vectors; kLongFlag set for a long bundle
+struct WarpRange {    // 16 bytes, device-readable as uint4
+  uint32_t v0;        // first vector of the range in the pass stream
+  uint32_t nvec;      // vectors in the range
+  uint32_t blk0;      // first block descriptor
+  uint32_t pad;
 };
 
-struct Task {        // one (slab, bundle range) assignment of a CTA
+struct BlockDesc {    // 8 bytes, device-readable as uint2
+  uint32_t first_id;  // id of the segment starting at the lowest set mask bit
+  uint32_t mask;      // bit l: vector (32k + l) starts a segment
+};
+
+struct Task {         // one (slab, 16 warp ranges) assignment of a CTA
   int32_t slab;
-  int32_t b0, b1;    // bundle range [b0, b1)
-  int32_t split;     // offset into warp_split (kWarps + 1 entries)
+  int32_t warp0;      // first of kWarps consecutive WarpRange entries
 };
 
 struct PassHost {
   int nslab = 0;
-  std::vector<int64_t> slab_lo;      // nslab+1 boundaries in gathered-vector coords
-  std::vector<uint16_t> idx;         // nvec * 8 indices
-  std::vector<Bundle> bundles;
-  int64_t nseg = 0;                  // number of output segments
-  // CTA plan
-  std::vector<int32_t> cta_task_ptr; // G+1
+  std::vector<int64_t> slab_lo;        // nslab+1 boundaries in gathered-vector coords
+  std::vector<uint16_t> idx;           // nvec * 8 indices
+  std::vector<BlockDesc> blocks;
+  std::vector<WarpRange> warps;
   std::vector<Task> tasks;
-  std::vector<int32_t> warp_split;   // per task: kWarps+1 bundle boundaries
-  // CSC only: piece pointer, slab-major: piece_ptr[s*(ncols+1) + j]
-  std::vector<int32_t> piece_ptr;
+  std::vector<int32_t> cta_task_ptr;   // G+1
+  int64_t nseg = 0;                    // number of output segments
+  std::vector<int32_t> piece_ptr;      // CSC: slab-major piece_ptr[s*(ncols+1) + j]
+  // statistics
+  int64_t lds_groups = 0, lds_conflict_excess = 0;
 };
 
 struct DesignHost {
