@@ -128,6 +128,14 @@ int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv,
  * 1 device->host, 2 device->device. */
 int pcgs_copy(void* dst, const void* src, int64_t bytes, int kind);
 
+/* Debug: device buffer (>= 256 uint64) receiving CTA-0 phase timestamps
+ * (globaltimer ns; 4 per operator application) of subsequent pcgs_pcg calls;
+ * NULL disables. */
+int pcgs_debug_profile(void* buf);
+/* Debug/tuning switches: key 0 = direction fill mode of pcgs_pcg (1: owners
+ * publish + grid sync + TMA copy, 0: computed fill). */
+int pcgs_debug_option(int key, int value);
+
 /* omega[i] ~ PG(1, z[i]) (pg_draw_batch, polya_gamma.py:39-84), Philox keyed
  * by (seed, stream_id), one thread per draw. */
 int pcgs_pg_draw(const double* z, int64_t n, uint64_t seed, uint64_t stream_id,

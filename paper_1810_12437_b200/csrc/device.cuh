@@ -69,12 +69,24 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
   b = warp_sum(rb);
 }
 
-// Every CTA reduces the same G partials in the same order (bitwise identical).
-__device__ __forceinline__ double reduce_partials(const double* part, int G) {
+// Cross-CTA partial sums: CTA c's value lives alone in a 128-byte line
+// (part[c * kPartStride]) so that the G readers of the G lines spread over L2
+// slices.  Every CTA reduces the same G partials in the same order (bitwise
+// identical everywhere); only warp 0 loads them, the result is broadcast
+// through shared memory.  Must be called by the whole CTA.
+constexpr int kPartStride = 16;
+
+__device__ __forceinline__ double reduce_partials(const double* part, int G, double* bcast) {
   const int lane = threadIdx.x & 31;
-  double s = 0.0;
-  for (int q = lane; q < G; q += 32) s += __ldcg(part + q);
-  return warp_sum(s);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (int q = lane; q < G; q += 32) s += __ldcg(part + (long long)q * kPartStride);
+    s = warp_sum(s);
+    if (lane == 0) *bcast = s;
+  }
+  __syncthreads();
+  return *bcast;
 }
 
 __device__ __forceinline__ double gather8(uint4 q, const double* sv) {
@@ -164,7 +176,7 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
 // descriptors (start mask + first segment id) drive a segmented reduction whose
 // open segment is carried across blocks in a per-lane accumulator.
 // ---------------------------------------------------------------------------
-constexpr int kRing = 4;
+constexpr int kRing = 8;
 
 template <class Epi>
 __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, double& acc, unsigned& open_id,
@@ -251,6 +263,8 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 
 // Runs every task of this CTA: fill the slab vector into shared memory, then
 // walk the warp's bundle range.  `fill(sv, lo, len)` must end with a barrier.
+// Not inlined: inside the persistent PCG kernel the caller's live state is
+// saved once per pass and the streaming loop gets the whole register budget.
 template <class Fill, class Epi>
 __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi) {
   const int c = blockIdx.x;

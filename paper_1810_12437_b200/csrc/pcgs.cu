@@ -28,6 +28,8 @@ using namespace pcgs;
 // error plumbing
 // =====================================================================
 static thread_local std::string g_err;
+static unsigned long long* g_prof = nullptr;  // debug: phase timestamps of the next pcgs_pcg
+static int g_tma_dir = 1;
 
 static int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -298,7 +300,15 @@ struct PcgArgs {
   double* zv;      // p_total internal layout: minv * r
   double* dvg;     // 2 * p_total internal layout: search directions
   double* part;    // 4 * G partial sums: dAd, rms, rz, spare
+  unsigned long long* prof;  // optional: CTA-0 phase timestamps (ns), 4 per apply
+  int tma_dir;     // 1: owners publish the direction, grid sync, TMA fill
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct FillDir {  // search direction: first ? a : a + beta * b   (internal layout)
   const double* a;
@@ -316,10 +326,83 @@ struct FillDir {  // search direction: first ? a : a + beta * b   (internal layo
   }
 };
 
+struct FillBulk {  // TMA copy of an internal-layout vector slab
+  const double* src;
+  BulkFill* bf;
+  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, src + l, len); }
+};
+
+// Shared-memory layout of k_pcg: [slab vector | own-slice state | piece pointers]
+struct OwnState {
+  double *x, *r, *d, *m, *s, *D, *b, *z;
+  int* pp;  // nslab_csc x (chunk + 1) piece pointers of the owned columns
+};
+
+__device__ __forceinline__ OwnState own_state(double* sv, int slab_doubles, int chunk, int nslab) {
+  OwnState o;
+  double* base = sv + slab_doubles;
+  o.x = base;
+  o.r = base + chunk;
+  o.d = base + 2 * chunk;
+  o.m = base + 3 * chunk;
+  o.s = base + 4 * chunk;
+  o.D = base + 5 * chunk;
+  o.b = base + 6 * chunk;
+  o.z = base + 7 * chunk;
+  o.pp = (int*)(base + 8 * chunk);
+  (void)nslab;
+  return o;
+}
+
+size_t pcg_smem_bytes(const DesignDev& D) {
+  const long long chunk = (D.pt + D.G - 1) / D.G;
+  return (size_t)D.smem_doubles * 8 + (size_t)chunk * 8 * 8 + (size_t)D.csc.nslab * (chunk + 1) * 4 + 16;
+}
+
+// Stages the pieces of the CTA's owned columns (contiguous per slab) into the
+// idle slab area of shared memory in one coalesced round; returns false when
+// they do not fit (then owned_column_sum reads global memory).
+__device__ __forceinline__ bool stage_pieces(const OwnState& o, const double* pieces, int nslab, int chunk,
+                                             double* stage, int cap) {
+  int total = 0;
+  for (int s = 0; s < nslab; ++s) total += o.pp[s * (chunk + 1) + chunk] - o.pp[s * (chunk + 1)];
+  if (total > cap) return false;
+  int off = 0;
+  for (int s = 0; s < nslab; ++s) {
+    const int q0 = o.pp[s * (chunk + 1)], len = o.pp[s * (chunk + 1) + chunk] - q0;
+#pragma unroll 4
+    for (int q = threadIdx.x; q < len; q += kThreads) stage[off + q] = __ldcg(pieces + q0 + q);
+    off += len;
+  }
+  __syncthreads();
+  return true;
+}
+
+// Sum of the pieces of owned column t, slab-major then piece order (fixed).
+__device__ __forceinline__ double owned_column_sum(const OwnState& o, const double* pieces, int nslab, int chunk,
+                                                   int t, const double* stage, bool staged) {
+  double total = 0.0;
+  int off = 0;
+  for (int s = 0; s < nslab; ++s) {
+    const int* pp = o.pp + s * (chunk + 1);
+    const int q0 = pp[t], q1 = pp[t + 1];
+    double ts = 0.0;
+    if (staged) {
+      for (int q = q0; q < q1; ++q) ts += stage[off + q - pp[0]];
+      off += pp[chunk] - pp[0];
+    } else {
+      for (int q = q0; q < q1; ++q) ts += __ldcg(pieces + q);
+    }
+    total += ts;
+  }
+  return total;
+}
+
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[64];
+  __shared__ double bc[4];
   __shared__ unsigned long long mbar;
   BulkFill bf;
   bulk_init(bf, &mbar);
@@ -328,35 +411,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
   const long long pt = D.pt, p = D.p, n = D.n;
   const int icpt = D.icpt;
   const bool multi = D.csr.nslab > 1;
+  const int S = D.csc.nslab;
+  const long long dvs = (pt + 15) / 16 * 16;  // 128-byte aligned stride of the two direction buffers
 
-  // ---- own slice of the p_total coordinates, kept in registers ----
-  const long long chunk = (pt + G - 1) / G;
-  const long long j = c * chunk + tid;
-  const bool own = tid < chunk && j < pt;
-  const long long rj = own ? ref_index(j, p, icpt) : 0;
-  double xj = 0, rjv = 0, dj = 0, mj = 0, sj = 0, Dj = 0, bj = 0, zj = 0;
-  if (own) {
-    xj = A.x[rj];
-    mj = __ldg(A.minv + rj);
-    sj = __ldg(A.scale + rj);
-    Dj = __ldg(A.diag + rj);
-    bj = __ldg(A.b + rj);
+  // ---- own slice of the p_total coordinates, kept in shared memory ----
+  const int chunk = (int)((pt + G - 1) / G);
+  const long long j0 = (long long)c * chunk;
+  const OwnState o = own_state(sv, D.smem_doubles, chunk, S);
+  for (int t = tid; t < chunk; t += kThreads) {
+    const long long j = j0 + t;
+    double xv = 0, m = 0, sc = 0, dg = 0, bv = 0;
+    if (j < pt) {
+      const long long rj = ref_index(j, p, icpt);
+      xv = A.x[rj];
+      m = __ldg(A.minv + rj);
+      sc = __ldg(A.scale + rj);
+      dg = __ldg(A.diag + rj);
+      bv = __ldg(A.b + rj);
+      A.dvg[dvs + j] = xv;  // v = x0 for the first application
+    }
+    o.x[t] = xv;
+    o.r[t] = 0.0;
+    o.d[t] = xv;
+    o.m[t] = m;
+    o.s[t] = sc;
+    o.D[t] = dg;
+    o.b[t] = bv;
+    o.z[t] = 0.0;
+  }
+  for (int t = tid; t < S * (chunk + 1); t += kThreads) {
+    const int s = t / (chunk + 1), q = t % (chunk + 1);
+    const long long j = min(j0 + q, pt);
+    o.pp[t] = D.csc.piece_ptr[(long long)s * (pt + 1) + j];
   }
   double* part_dAd = A.part;
-  double* part_rms = A.part + G;
-  double* part_rz = A.part + 2 * G;
+  double* part_rms = A.part + 1;
+  double* part_rz = A.part + 2;
 
   double rz = 0.0;
   int status = PCGS_MAX_ITER, iterations = 0, fail_iter = -1, applies = 0;
-  if (own) A.dvg[pt + j] = xj;
   grid.sync();
 
   for (int a = 0;; ++a) {
-    double beta = 0.0, vj;
+    double beta = 0.0;
+    const bool prof = A.prof && c == 0 && tid == 0 && a < 64;
     // ---------------- convergence test of iteration a-1 ----------------
     if (a > 0) {
-      double s_rms = reduce_partials(part_rms, G);
-      double s_rz = reduce_partials(part_rz, G);
+      const double s_rms = reduce_partials(part_rms, G, bc);
+      const double s_rz = reduce_partials(part_rz, G, bc + 1);
       const double rms = sqrt(s_rms / (double)pt);
       if (c == 0 && tid == 0) A.trace[a - 1] = rms;
       const int k = a - 1;  // iterations completed
@@ -381,28 +483,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
         iterations = k;
         break;
       }
-      // new direction (own slice in registers, full vector into smem below)
-      if (own) {
-        dj = a == 1 ? zj : fma(beta, dj, zj);
-        A.dvg[(a & 1) * pt + j] = dj;
+      // new direction d = z + beta d on the owned slice
+      for (int t = tid; t < chunk; t += kThreads) {
+        const double dn = a == 1 ? o.z[t] : fma(beta, o.d[t], o.z[t]);
+        o.d[t] = dn;
+        if (j0 + t < pt) A.dvg[(a & 1) * dvs + j0 + t] = dn;
       }
-      vj = dj;
-    } else {
-      vj = xj;
+      if (A.tma_dir) grid.sync();
     }
+    if (prof) A.prof[4 * a + 0] = gtimer();
 
     // ---------------- phase A: CSR pass, w = omega (X v) ----------------
-    double acc_dAd = own ? Dj * vj * vj : 0.0;
-    // a == 0: v = x0 (staged into dvg[1] by the owners before the loop)
-    const double* fa = a == 0 ? A.dvg + pt : A.zv;
-    const double* fb = A.dvg + ((a - 1) & 1) * pt;
-    const bool first = a <= 1;
-    const double v0 = icpt ? (first ? __ldcg(fa + p) : fma(beta, __ldcg(fb + p), __ldcg(fa + p))) : 0.0;
+    double acc_dAd = 0.0;
+    for (int t = tid; t < chunk; t += kThreads) acc_dAd += o.D[t] * o.d[t] * o.d[t];
+    const double* vcur = A.dvg + (a == 0 ? dvs : (a & 1) * dvs);
+    double v0 = 0.0;
     {
-      FillDir f{fa, fb, beta, first, 0};
-      EpiCsr e{multi ? A.zpart : A.w, A.omega, v0, 0.0, multi};
-      run_pass(D.csr, sv, f, e);
-      if (a > 0) acc_dAd += e.acc;
+      EpiCsr e{multi ? A.zpart : A.w, A.omega, 0.0, 0.0, multi};
+      if (a == 0 || A.tma_dir) {
+        if (tid == 0) bc[2] = icpt ? __ldcg(vcur + p) : 0.0;
+        __syncthreads();
+        v0 = bc[2];
+        e.v0 = v0;
+        FillBulk f{vcur, &bf};
+        run_pass(D.csr, sv, f, e);
+      } else {
+        const double* zvp = A.zv;
+        const double* old = A.dvg + ((a - 1) & 1) * dvs;
+        if (tid == 0) bc[2] = icpt ? (a == 1 ? __ldcg(zvp + p) : fma(beta, __ldcg(old + p), __ldcg(zvp + p))) : 0.0;
+        __syncthreads();
+        v0 = bc[2];
+        e.v0 = v0;
+        FillDir f{zvp, old, beta, a == 1, 0};
+        run_pass(D.csr, sv, f, e);
+      }
+      acc_dAd += e.acc;
     }
     if (multi) {
       grid.sync();
@@ -416,9 +531,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       }
     }
     {
-      double t = block_sum(acc_dAd, red);
-      if (tid == 0) part_dAd[c] = t;
+      const double t = block_sum(acc_dAd, red);
+      if (tid == 0) part_dAd[c * kPartStride] = t;
     }
+    if (prof) A.prof[4 * a + 1] = gtimer();
     grid.sync();
 
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
@@ -427,13 +543,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       EpiStore e{A.pieces};
       run_pass(D.csc, sv, f, e);
     }
+    if (prof) A.prof[4 * a + 2] = gtimer();
     grid.sync();
     ++applies;
+    if (prof) A.prof[4 * a + 3] = gtimer();
 
     // ---------------- phase C: assemble, step, residual ----------------
     double alpha = 0.0;
     if (a > 0) {
-      const double dAd = reduce_partials(part_dAd, G);
+      const double dAd = reduce_partials(part_dAd, G, bc);
       if (!(dAd > 0.0)) {
         status = PCGS_NOT_PD;
         iterations = a;
@@ -444,29 +562,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       if (c == 0 && tid == 0) A.alphas[a - 1] = alpha;
     }
     double t_rms = 0.0, t_rz = 0.0;
-    if (own) {
-      const double Ad = column_sum(D.csc, A.pieces, pt, j) + Dj * vj;
+    const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, D.smem_doubles);
+    for (int t = tid; t < chunk; t += kThreads) {
+      if (j0 + t >= pt) continue;
+      const double Ad = owned_column_sum(o, A.pieces, S, chunk, t, sv, staged) + o.D[t] * o.d[t];
+      double rv;
       if (a == 0) {
-        rjv = bj - Ad;
+        rv = o.b[t] - Ad;
       } else {
-        xj = fma(alpha, dj, xj);
-        rjv = fma(-alpha, Ad, rjv);
+        o.x[t] = fma(alpha, o.d[t], o.x[t]);
+        rv = fma(-alpha, Ad, o.r[t]);
       }
-      zj = mj * rjv;
-      A.zv[j] = zj;
-      const double tj = sj * rjv;
-      t_rms = tj * tj;
-      t_rz = rjv * zj;
+      o.r[t] = rv;
+      const double zn = o.m[t] * rv;
+      o.z[t] = zn;
+      if (!A.tma_dir) A.zv[j0 + t] = zn;
+      const double tj = o.s[t] * rv;
+      t_rms += tj * tj;
+      t_rz += rv * zn;
     }
     block_sum2(t_rms, t_rz, red);
     if (tid == 0) {
-      part_rms[c] = t_rms;
-      part_rz[c] = t_rz;
+      part_rms[c * kPartStride] = t_rms;
+      part_rz[c * kPartStride] = t_rz;
     }
     grid.sync();
   }
 
-  if (own) A.x[rj] = xj;
+  for (int t = tid; t < chunk; t += kThreads)
+    if (j0 + t < pt) A.x[ref_index(j0 + t, p, icpt)] = o.x[t];
   if (c == 0 && tid == 0) {
     A.result[0] = iterations;
     A.result[1] = status;
@@ -568,7 +692,7 @@ static int set_smem_attrs(const DesignDev& D) {
   CUDA_TRY(cudaFuncSetAttribute(k_csr_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(cudaFuncSetAttribute(k_csc_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
   CUDA_TRY(cudaFuncSetAttribute(k_csc<FillRhs>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CUDA_TRY(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_TRY(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem_bytes(D)));
   return PCGS_OK;
 }
 
@@ -761,12 +885,14 @@ int pcgs_pcg(pcgs_design_t d, const double* omega, const double* prior_diag, con
   A.zpart = D.csr.nslab > 1 ? S.get<double>((size_t)D.csr.nslab * D.n) : nullptr;
   A.pieces = S.get<double>(D.csc.nseg);
   A.zv = S.get<double>(D.pt + 2);
-  A.dvg = S.get<double>(2 * D.pt + 2);
-  A.part = S.get<double>(4 * (size_t)D.G);
+  A.dvg = S.get<double>(2 * ((D.pt + 15) / 16 * 16) + 16);
+  A.part = S.get<double>((size_t)kPartStride * D.G);
+  A.prof = g_prof;
+  A.tma_dir = g_tma_dir;
   if (!A.w || !A.pieces || !A.zv || !A.dvg || !A.part || (D.csr.nslab > 1 && !A.zpart))
     return fail(PCGS_ENOMEM, "scratch allocation failed");
   void* args[] = {&A};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_pcg, D.G, kThreads, args, smem_bytes(D), s));
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_pcg, D.G, kThreads, args, pcg_smem_bytes(D), s));
   return PCGS_OK;
 }
 
@@ -891,6 +1017,16 @@ int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, cons
     if ((rc = run(4, beta, nullptr))) return rc;
   }
   return finish(PCGS_MAX_ITER, -1);
+}
+
+int pcgs_debug_profile(void* buf) {
+  g_prof = (unsigned long long*)buf;
+  return PCGS_OK;
+}
+
+int pcgs_debug_option(int key, int value) {
+  if (key == 0) g_tma_dir = value;
+  return PCGS_OK;
 }
 
 int pcgs_copy(void* dst, const void* src, int64_t bytes, int kind) {

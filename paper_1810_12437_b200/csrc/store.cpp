@@ -232,7 +232,7 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
         return "col_idx must be strictly increasing within each row";
     }
   }
-  const int64_t hard_max = 28672 - 16;  // doubles of shared memory per slab (+ sentinel)
+  const int64_t hard_max = 22528 - 16;  // doubles per slab (+ sentinel): 176 KB, leaves room for PCG state
   int64_t smax = slab_max > 0 ? std::min<int64_t>(slab_max, hard_max) : hard_max;
   if (smax < 16) smax = 16;
   D.n = n;

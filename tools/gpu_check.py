@@ -124,6 +124,28 @@ def check_config2(run_oracle=False):
     phi = pk.PrecisionOperator(X, om, d)
     bt = torch.tensor(b, device=dev)
     mt, stt = torch.tensor(minv, device=dev), torch.tensor(scale, device=dev)
+    from paper_1810_12437_b200 import _lib
+    for mode in (0, 1):
+        _lib.lib().pcgs_debug_option(0, mode)
+        prof = torch.zeros(256, dtype=torch.int64, device=dev)
+        _lib.lib().pcgs_debug_profile(prof.data_ptr())
+        pk.cg.pcg_solve_device(phi, bt, mt, stt, rtol=1e-6)
+        torch.cuda.synchronize()
+        _lib.lib().pcgs_debug_profile(None)
+        pr = prof.cpu().numpy().reshape(-1, 4).astype(np.float64)
+        print(f"  tma_dir={mode}")
+        for a in (0, 1, 2, 10, 20):
+            t0 = pr[a, 0]
+            nxt = pr[a + 1, 0]
+            print(f"  apply {a}: A {(pr[a,1]-t0)/1e3:.1f}  syncA+B {(pr[a,2]-pr[a,1])/1e3:.1f}"
+                  f"  syncB {(pr[a,3]-pr[a,2])/1e3:.1f}  C+syncC+dir {(nxt-pr[a,3])/1e3:.1f}  total {(nxt-t0)/1e3:.1f} us")
+        res = {}
+
+        def solve():
+            res["o"] = pk.cg.pcg_solve_device(phi, bt, mt, stt, rtol=1e-6)
+        med, mn = timed(solve, reps=5, warm=1)
+        r = res["o"][4].cpu().numpy()
+        print(f"  tma_dir={mode} PCG iters {r[0]} time {med:.2f} ms ({med / max(r[3],1) * 1e3:.1f} us/iter)")
     for rtol in (1e-6, 1e-10):
         res = {}
 
