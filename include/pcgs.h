@@ -63,6 +63,13 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h,
                        const int32_t* col_idx_h, int intercept, int slab_max,
                        int device, pcgs_design_t* out);
 int pcgs_design_destroy(pcgs_design_t d);
+/* Host-only: builds the store for a grid of `grid` CTAs and verifies that both
+ * tiled passes reproduce the input pattern exactly (no GPU needed).
+ * stats_h[8]: csr slabs, csc slabs, csr vectors, csc vectors, csc pieces,
+ * shared-memory load groups, bank-conflicted picks, index bytes. */
+int pcgs_store_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h,
+                        const int32_t* col_idx_h, int intercept, int slab_max,
+                        int grid, int64_t* stats_h);
 /* info_h[16]: n, p, p_total, nnz, csr_slabs, csc_slabs, csr_vectors,
  * csc_vectors, csr_bundles, csc_bundles, csc_pieces, grid, device,
  * index_bytes (both directions), reserved, reserved */
@@ -140,6 +147,52 @@ int pcgs_debug_option(int key, int value);
  * by (seed, stream_id), one thread per draw. */
 int pcgs_pg_draw(const double* z, int64_t n, uint64_t seed, uint64_t stream_id,
                  double* omega, pcgs_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Device Gibbs scan (gibbs_run, gibbs.py:260-379).  All pointers are device
+ * arrays owned by the caller; vectors of length p_total use the reference
+ * layout (unshrunk block first).  One pcgs_gibbs_scan call issues one scan on
+ * `stream` without synchronising: omega -> tau -> lambda -> beta (RHS + PCG)
+ * -> X beta + log density -> Welford statistics and the stored draw.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int prior;          /* 0: bridge alpha = 1 (reference), 1: horseshoe        */
+  int q;              /* leading unshrunk coefficients                       */
+  int precond;        /* 0 prior (augmented), 1 identity, 2 Jacobi          */
+  int fixed_omega, fixed_tau, fixed_lam; /* pinned updates (gibbs.py:321-329) */
+  int max_iter;       /* CG iteration cap                                    */
+  double rtol;        /* CG RMS stopping threshold                           */
+  double a0, b0;      /* bridge: Gamma(a0, b0) prior on tau^-alpha          */
+  double alpha;       /* bridge exponent (local updates need alpha = 1)     */
+  double gamma_scale; /* gamma policy constant c (precond.py:137)           */
+  uint64_t seed;      /* Philox key of the chain                             */
+  const double* y;        /* n outcomes (0/1)                                */
+  const double* kappa;    /* n: y - 1/2                                      */
+  const double* usd_prec; /* q prior precisions of the unshrunk block (0 flat) */
+  const double* usd_sd;   /* q prior sds (inf = flat), gamma cold start       */
+  double* beta;       /* p_total: current draw (in: previous draw)           */
+  double* z;          /* n: X beta                                           */
+  double* omega;      /* n                                                   */
+  double* lam;        /* p: local scales                                     */
+  double* nu;         /* p: horseshoe auxiliaries                            */
+  double* scal;       /* [0] tau, [1] xi (horseshoe auxiliary)               */
+  double* mean;       /* p_total: running mean of scaled draws               */
+  double* m2;         /* q: running sum of squares of the unshrunk draws     */
+  double* prior_diag; double* minv; double* scale; double* b; /* p_total work */
+  double* part;       /* 16 * grid: per-CTA partial sums                     */
+  double* logdens;    /* n_iter                                              */
+  int32_t* results;   /* 8 per scan: PCG result[4], [4] positivity violation */
+  double* draws;      /* n_store x p_total                                   */
+  double* tau_draws;  /* n_store                                             */
+  double* trace; double* alphas; double* betas; /* PCG scratch (max_iter+1) */
+} pcgs_gibbs_t;
+
+/* z = X beta and its log-likelihood partials (start of a chain / resume). */
+int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream);
+/* Scan t (1-based).  `count` = number of statistics updates so far; `slot` =
+ * row of `draws` to store this scan in, or -1. */
+int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count,
+                    int32_t slot, pcgs_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -42,12 +42,14 @@ SIGNATURES = {
     "pcgs_design_create": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int, ctypes.POINTER(_P)]),
     "pcgs_design_destroy": (ctypes.c_int, [_P]),
+    "pcgs_store_selftest": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, _P]),
     "pcgs_design_info": (ctypes.c_int, [_P, _P]),
     "pcgs_matvec": (ctypes.c_int, [_P, _P, _P, _P]),
     "pcgs_matvec_t": (ctypes.c_int, [_P, _P, _P, _P]),
     "pcgs_phi_apply": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "pcgs_phi_diagonal": (ctypes.c_int, [_P, _P, _P, _P, _P]),
-    "pcgs_rhs": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _U64, _U64, _P, _P]),
+    "pcgs_rhs": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _U64, _U64, _P, _P]),
     "pcgs_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
     "pcgs_pcg_op": (ctypes.c_int, [APPLY_FN, _P, _I64, _P, _P, _P, _P, _I32, _D, _P, _P, _P,
                                    _P, _P]),
@@ -55,6 +57,8 @@ SIGNATURES = {
     "pcgs_debug_profile": (ctypes.c_int, [_P]),
     "pcgs_debug_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "pcgs_pg_draw": (ctypes.c_int, [_P, _I64, _U64, _U64, _P, _P]),
+    "pcgs_gibbs_init": (ctypes.c_int, [_P, _P, _P]),
+    "pcgs_gibbs_scan": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P]),
 }
 
 

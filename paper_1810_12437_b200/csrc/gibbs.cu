@@ -1,0 +1,293 @@
+// Device Gibbs scan for sparse Bayesian logistic regression (reference:
+// pkg/src/priorcg/gibbs.py:260-379).  One call = one scan, no host sync:
+//   omega | beta        Polya-Gamma            (gibbs.py:170-176)
+//   tau   | beta (...)  global scale           (gibbs.py:179-190; horseshoe: new)
+//   lam   | beta, tau   local scales           (gibbs.py:193-214; horseshoe: new)
+//   beta  | omega, lam, tau  randomised RHS + persistent PCG (gibbs.py:334-351)
+//   log density, Welford warm-start statistics, stored draw (gibbs.py:362-369)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+
+#include "internal.cuh"
+
+namespace {
+
+// ---------------------------------------------------------------- CSR with log-likelihood
+struct EpiLogit {  // z_i = v0 + s; acc += y_i z_i - log(1 + e^{z_i})
+  double* z;
+  const double* y;
+  double v0;
+  double acc;
+  bool multi;
+  __device__ void emit(long long seg, double s) {
+    if (multi) {
+      z[seg] = s;
+      return;
+    }
+    const double zi = v0 + s;
+    z[seg] = zi;
+    const double yi = __ldg(y + seg);
+    acc += yi * zi - (fmax(zi, 0.0) + log1p(exp(-fabs(zi))));
+  }
+};
+
+__global__ void __launch_bounds__(kThreads, 1) k_csr_logit(DesignDev D, const double* beta, const double* y,
+                                                           double* z_or_part, double* part) {
+  extern __shared__ __align__(128) double sv[];
+  __shared__ double red[64];
+  FillVecRef f{beta, D.icpt, 0};
+  const double v0 = D.icpt ? __ldg(beta) : 0.0;
+  EpiLogit e{z_or_part, y, v0, 0.0, D.csr.nslab > 1};
+  run_pass(D.csr, sv, f, e);
+  const double t = block_sum(e.acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x * kPartStride] = t;
+}
+
+// multi column slab: z_i = v0 + sum_s zpart, log-likelihood partials per CTA
+__global__ void __launch_bounds__(kThreads) k_rows_logit(DesignDev D, const double* zpart, const double* beta,
+                                                         const double* y, double* z, double* part) {
+  __shared__ double red[64];
+  const double v0 = D.icpt ? __ldg(beta) : 0.0;
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < D.n; i += (long long)gridDim.x * blockDim.x) {
+    double zi = 0.0;
+    for (int s = 0; s < D.csr.nslab; ++s) zi += zpart[(long long)s * D.n + i];
+    zi += v0;
+    z[i] = zi;
+    const double yi = __ldg(y + i);
+    acc += yi * zi - (fmax(zi, 0.0) + log1p(exp(-fabs(zi))));
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x * kPartStride] = t;
+}
+
+// ---------------------------------------------------------------- scale updates
+// Wald(mu, 1) (inverse Gaussian) by Michael-Schucany-Haas, in the
+// cancellation-free form x = mu / (1 + a + sqrt(a (a + 2))), a = mu y / 2.
+__device__ double wald1(double mu, Philox& R) {
+  const double nrm = R.normal();
+  const double a = 0.5 * mu * nrm * nrm;
+  const double x = mu / (1.0 + a + sqrt(a * (a + 2.0)));
+  return R.uniform() <= mu / (mu + x) ? x : mu * mu / x;
+}
+
+// k_global: one CTA.  Bridge (alpha = 1): phi = 1/tau ~ Gamma(a0 + p, b0 + sum|beta|)
+// (gibbs.py:179-190).  Horseshoe: xi | tau ~ IG(1, 1 + 1/tau^2), then
+// tau^2 | beta, lam, xi ~ IG((p+1)/2, 1/xi + sum beta^2 / (2 lam^2)).
+__global__ void __launch_bounds__(1024) k_global(pcgs_gibbs_t G, long long pt, int t) {
+  __shared__ double red[64];
+  const int q = G.q;
+  const long long p = pt - q;
+  double acc = 0.0;
+  for (long long j = threadIdx.x; j < p; j += blockDim.x) {
+    const double b = G.beta[q + j];
+    if (G.prior == 0) {
+      acc += G.alpha == 1.0 ? fabs(b) : pow(fabs(b), G.alpha);
+    } else {
+      const double l = G.lam[j];
+      acc += b * b / (l * l);
+    }
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) {
+    Philox R(G.seed, kStreamGlobal ^ (unsigned long long)t, 0u);
+    double tau;
+    if (G.prior == 0) {
+      const double rate = G.b0 + acc;
+      const double shape = G.a0 + (double)p / G.alpha;
+      const double phi = R.gamma(shape) / rate;
+      tau = G.alpha == 1.0 ? 1.0 / phi : pow(phi, -1.0 / G.alpha);
+    } else {
+      const double tau_old = G.scal[0];
+      const double xi = (1.0 + 1.0 / (tau_old * tau_old)) / R.exponential();
+      const double tau2 = fmin(fmax((1.0 / xi + 0.5 * acc) / R.gamma(0.5 * (double)(p + 1)), 1e-300), 1e300);
+      G.scal[1] = xi;
+      tau = sqrt(tau2);
+    }
+    G.scal[0] = tau;
+    if (!(tau > 0.0) || !isfinite(tau)) G.results[8 * (t - 1) + 4] = 1;
+  }
+}
+
+// k_local: elementwise over p_total.  Local scales (bridge: gibbs.py:193-214;
+// horseshoe: nu_j ~ IG(1, 1 + 1/lam_j^2), lam_j^2 ~ IG(1, 1/nu_j + beta_j^2/(2 tau^2))),
+// then the prior diagonal (gibbs.py:334), the preconditioner (precond.py:120-153),
+// the metric scale [gamma, tau lam] (gibbs.py:348) and the warm start (cg.py:195-211)
+// written into beta.
+__global__ void k_local(pcgs_gibbs_t G, long long pt, int t, int count) {
+  const int q = G.q;
+  const double tau = G.scal[0];
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x) {
+    if (j < q) {
+      // unshrunk coefficient: prior precision, gamma policy (precond.py:137-153)
+      double sd;
+      if (count >= 2) sd = sqrt(G.m2[j] / (double)(count - 1));
+      else sd = fmin(G.usd_sd[j], 10.0);
+      const double gam = G.gamma_scale * fmax(sd, 1e-3);
+      G.prior_diag[j] = G.usd_prec[j];
+      G.minv[j] = gam * gam;
+      G.scale[j] = gam;
+      G.beta[j] = count > 0 ? G.mean[j] : 0.0;
+      continue;
+    }
+    const long long k = j - q;
+    double lam = G.lam[k];
+    if (!G.fixed_lam) {
+      Philox R(G.seed, kStreamLocal ^ (unsigned long long)t, (unsigned)k);
+      const double b = G.beta[j];
+      if (G.prior == 0) {
+        const double ratio = fabs(b) / tau;
+        if (ratio < 1e-10) {
+          lam = fmax(fabs(R.normal()), 1e-150);
+        } else {
+          const double inv_sq = wald1(1.0 / ratio, R);
+          lam = pow(fmax(inv_sq, 1e-300), -0.5);
+        }
+      } else {
+        const double nu = (1.0 + 1.0 / (lam * lam)) / R.exponential();
+        const double lam2 = fmin(fmax((1.0 / nu + 0.5 * b * b / (tau * tau)) / R.exponential(), 1e-300), 1e300);
+        G.nu[k] = nu;
+        lam = sqrt(lam2);
+      }
+      G.lam[k] = lam;
+    }
+    if (!(lam > 0.0) || !isfinite(lam)) G.results[8 * (t - 1) + 4] = 1;
+    const double tl = tau * lam;
+    G.prior_diag[j] = 1.0 / (tl * tl);
+    G.minv[j] = tl * tl;
+    G.scale[j] = tl;
+    G.beta[j] = count > 0 ? tl * G.mean[j] : 0.0;
+  }
+}
+
+// identity / Jacobi preconditioners (gibbs.py:244-257) overwrite minv
+__global__ void k_precond(pcgs_gibbs_t G, long long pt, const double* diag_phi) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x)
+    G.minv[j] = G.precond == 1 ? 1.0 : 1.0 / diag_phi[j];
+}
+
+// k_post: one CTA.  log density (bridge: gibbs.py:217-241; horseshoe: joint
+// density given lambda).
+__global__ void __launch_bounds__(1024) k_post(pcgs_gibbs_t G, long long pt, int t, int ncta) {
+  __shared__ double red[64];
+  const int q = G.q;
+  const long long p = pt - q;
+  const double tau = G.scal[0];
+  double acc = 0.0;
+  for (int c = threadIdx.x; c < ncta; c += blockDim.x) acc += G.part[(long long)c * kPartStride];
+  const double loglik = block_sum(acc, red);
+  double pr = 0.0;
+  for (long long j = threadIdx.x; j < pt; j += blockDim.x) {
+    const double b = G.beta[j];
+    if (j < q) {
+      const double sd = G.usd_sd[j];
+      if (isfinite(sd)) {
+        const double u = b / sd;
+        pr -= 0.5 * u * u + log(sd) + 0.5 * log(2.0 * M_PI);
+      }
+    } else if (G.prior == 0) {
+      pr -= G.alpha == 1.0 ? fabs(b / tau) : pow(fabs(b / tau), G.alpha);
+    } else {
+      const double l = G.lam[j - q];
+      const double sc = tau * l;
+      const double u = b / sc;
+      pr += -log(sc) - 0.5 * u * u - 0.5 * log(2.0 * M_PI) + log(2.0 / M_PI) - log1p(l * l);
+    }
+  }
+  pr = block_sum(pr, red);
+  if (threadIdx.x == 0) {
+    double out = loglik + pr;
+    if (G.prior == 0) {
+      const double a = G.alpha;
+      out += (double)p * (log(a) - log(2.0) - lgamma(1.0 / a)) - (double)p * log(tau);
+      out += G.a0 * log(G.b0) - lgamma(G.a0) + log(a) - (a * G.a0 + 1.0) * log(tau) - G.b0 * pow(tau, -a);
+    } else {
+      out += log(2.0 / M_PI) - log1p(tau * tau);
+    }
+    G.logdens[t - 1] = out;
+  }
+}
+
+// Welford update of the scaled draws [beta_q, beta/(tau lam)] (gibbs.py:139-167)
+// and the stored draw (gibbs.py:366-369).
+__global__ void k_stats(pcgs_gibbs_t G, long long pt, int count_new, int slot) {
+  const int q = G.q;
+  const double tau = G.scal[0];
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x) {
+    const double b = G.beta[j];
+    const double scaled = j < q ? b : b / (tau * G.lam[j - q]);
+    const double delta = scaled - G.mean[j];
+    const double m = G.mean[j] + delta / (double)count_new;
+    G.mean[j] = m;
+    if (j < q) G.m2[j] += delta * (scaled - m);
+    if (slot >= 0) G.draws[(long long)slot * pt + j] = b;
+    if (slot >= 0 && j == 0) G.tau_draws[slot] = tau;
+  }
+}
+
+int launch_logit(pcgs_design* d, pcgs_gibbs_t* g, cudaStream_t s) {
+  const DesignDev& D = d->dev;
+  if (D.csr.nslab == 1) {
+    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, g->z, g->part);
+  } else {
+    Scratch S(s);
+    double* zp = S.get<double>((size_t)D.csr.nslab * D.n);
+    if (!zp) return fail(PCGS_ENOMEM, "scratch allocation failed");
+    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, zp, g->part);
+    k_rows_logit<<<D.G, kThreads, 0, s>>>(D, zp, g->beta, g->y, g->z, g->part);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream) {
+  if (!d || !g || !g->beta || !g->z || !g->y || !g->part) return fail(PCGS_EINVAL, "null argument");
+  CUDA_TRY(cudaFuncSetAttribute(k_csr_logit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_bytes(d->dev)));
+  return launch_logit(d, g, (cudaStream_t)stream);
+}
+
+int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, int32_t slot,
+                    pcgs_stream_t stream) {
+  if (!d || !g || t < 1) return fail(PCGS_EINVAL, "bad argument");
+  const DesignDev& D = d->dev;
+  cudaStream_t s = (cudaStream_t)stream;
+  const long long pt = D.pt;
+  const int eblocks = (int)std::min<long long>((pt + 255) / 256, 4 * D.G);
+  int rc;
+  // omega | beta (z = X beta of the previous scan)
+  if (!g->fixed_omega) {
+    if ((rc = pcgs_pg_draw(g->z, D.n, g->seed, (uint64_t)t, g->omega, stream))) return rc;
+  }
+  // tau | beta, then lambda | beta, tau; prior diagonal, M^-1, metric scale, x0
+  if (!g->fixed_tau) k_global<<<1, 1024, 0, s>>>(*g, pt, t);
+  k_local<<<eblocks, 256, 0, s>>>(*g, pt, t, count);
+  if (g->precond == 2) {
+    if ((rc = pcgs_phi_diagonal(d, g->omega, g->prior_diag, g->b, stream))) return rc;
+    k_precond<<<eblocks, 256, 0, s>>>(*g, pt, g->b);
+  } else if (g->precond == 1) {
+    k_precond<<<eblocks, 256, 0, s>>>(*g, pt, nullptr);
+  }
+  CUDA_TRY(cudaGetLastError());
+  // randomised right-hand side (one fused X' pass) and the PCG solve
+  if ((rc = pcgs_rhs(d, g->kappa, g->omega, g->prior_diag, nullptr, nullptr, nullptr, g->seed, (uint64_t)t, g->b,
+                     stream)))
+    return rc;
+  if ((rc = pcgs_pcg(d, g->omega, g->prior_diag, g->minv, g->scale, g->b, g->beta, g->max_iter, g->rtol, g->trace,
+                     g->alphas, g->betas, g->results + 8 * (t - 1), stream)))
+    return rc;
+  // z = X beta with the log-likelihood, log density, statistics, stored draw
+  if ((rc = launch_logit(d, g, s))) return rc;
+  k_post<<<1, 1024, 0, s>>>(*g, pt, t, D.G);
+  k_stats<<<eblocks, 256, 0, s>>>(*g, pt, count + 1, slot);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+}  // extern "C"

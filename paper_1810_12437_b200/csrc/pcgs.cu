@@ -18,179 +18,17 @@
 #include <string>
 #include <vector>
 
-#include "device.cuh"
-#include "pcgs.h"
+#include "internal.cuh"
 
 namespace cg = cooperative_groups;
-using namespace pcgs;
 
 // =====================================================================
 // error plumbing
 // =====================================================================
-static thread_local std::string g_err;
 static unsigned long long* g_prof = nullptr;  // debug: phase timestamps of the next pcgs_pcg
 static int g_tma_dir = 1;
-
-static int fail(int code, const std::string& msg) {
-  g_err = msg;
-  return code;
-}
-#define CUDA_TRY(x)                                                                  \
-  do {                                                                               \
-    cudaError_t e_ = (x);                                                            \
-    if (e_ != cudaSuccess)                                                           \
-      return fail(PCGS_ECUDA, std::string(#x " failed: ") + cudaGetErrorString(e_)); \
-  } while (0)
-
-// =====================================================================
-// design handle
-// =====================================================================
-struct pcgs_design {
-  DesignDev dev;
-  int device;
-  int64_t info[16];
-  std::vector<void*> allocs;
-};
-
-template <class T>
-static int upload(pcgs_design* D, const std::vector<T>& h, const T** out) {
-  if (h.empty()) {
-    *out = nullptr;
-    return PCGS_OK;
-  }
-  void* p = nullptr;
-  CUDA_TRY(cudaMalloc(&p, h.size() * sizeof(T)));
-  D->allocs.push_back(p);
-  CUDA_TRY(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
-  *out = (const T*)p;
-  return PCGS_OK;
-}
-
-static int upload_pass(pcgs_design* D, const PassHost& H, PassDev& P) {
-  int rc;
-  const uint16_t* idx;
-  if ((rc = upload(D, H.idx, &idx))) return rc;
-  P.vec = (const uint4*)idx;
-  const BlockDesc* b;
-  if ((rc = upload(D, H.blocks, &b))) return rc;
-  P.blocks = (const uint2*)b;
-  const WarpRange* w;
-  if ((rc = upload(D, H.warps, &w))) return rc;
-  P.warps = (const uint4*)w;
-  const Task* t;
-  if ((rc = upload(D, H.tasks, &t))) return rc;
-  P.task = (const int2*)t;
-  if ((rc = upload(D, H.cta_task_ptr, &P.cta_task_ptr))) return rc;
-  std::vector<long long> lo(H.slab_lo.begin(), H.slab_lo.end());
-  if ((rc = upload(D, lo, &P.slab_lo))) return rc;
-  if ((rc = upload(D, H.piece_ptr, &P.piece_ptr))) return rc;
-  P.nslab = H.nslab;
-  P.nseg = H.nseg;
-  return PCGS_OK;
-}
-
-// scratch buffers for one call, stream-ordered
-struct Scratch {
-  cudaStream_t s;
-  std::vector<void*> bufs;
-  explicit Scratch(cudaStream_t st) : s(st) {}
-  ~Scratch() {
-    for (void* b : bufs) cudaFreeAsync(b, s);
-  }
-  template <class T>
-  T* get(size_t count) {
-    void* p = nullptr;
-    if (count == 0) count = 1;
-    if (cudaMallocAsync(&p, count * sizeof(T), s) != cudaSuccess) return nullptr;
-    bufs.push_back(p);
-    return (T*)p;
-  }
-};
-
-// =====================================================================
-// fills and epilogues
-// =====================================================================
-struct FillVecRef {  // CSR slab of a reference-layout p_total vector
-  const double* v;
-  int icpt;
-  long long lo;
-  __device__ double operator()(int j) const { return __ldcg(v + icpt + lo + j); }
-  __device__ void operator()(double* sv, long long l, int len) {
-    lo = l;
-    fill_smem(sv, len, *this);
-  }
-};
-
-struct FillVecN {  // CSC slab of an n-vector: TMA bulk copy
-  const double* w;
-  BulkFill* bf;
-  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, w + l, len); }
-};
-
-struct FillRhs {  // u_i = kappa_i + sqrt(omega_i) * eta_i
-  const double* kappa;
-  const double* omega;
-  const double* eta;  // null: Philox
-  unsigned long long seed, stream;
-  long long lo;
-  __device__ double operator()(int j) const {
-    const long long i = lo + j;
-    double e;
-    if (eta) {
-      e = __ldg(eta + i);
-    } else {
-      Philox R(seed, stream, (unsigned)i);
-      e = R.normal();
-    }
-    return (kappa ? __ldg(kappa + i) : 0.0) + sqrt(__ldg(omega + i)) * e;
-  }
-  __device__ void operator()(double* sv, long long l, int len) {
-    lo = l;
-    fill_smem(sv, len, *this);
-  }
-};
-
-struct EpiStore {  // out[seg] = s
-  double* out;
-  __device__ void emit(long long seg, double s) { out[seg] = s; }
-};
-
-struct EpiZ {  // matvec, single column slab: out[i] = v0 + s
-  double* out;
-  double v0;
-  __device__ void emit(long long seg, double s) { out[seg] = v0 + s; }
-};
-
-struct EpiW {  // Phi apply, single column slab: w_i = omega_i (v0 + s); acc += w_i z_i
-  double* w;
-  const double* omega;
-  double v0;
-  double acc;
-  __device__ void emit(long long seg, double s) {
-    const double z = v0 + s;
-    const double wi = __ldg(omega + seg) * z;
-    w[seg] = wi;
-    acc += wi * z;
-  }
-};
-
-struct EpiCsr {  // runtime choice: multi column slab -> partial store, else EpiW
-  double* out;
-  const double* omega;
-  double v0;
-  double acc;
-  bool multi;
-  __device__ void emit(long long seg, double s) {
-    if (multi) {
-      out[seg] = s;
-    } else {
-      const double z = v0 + s;
-      const double wi = __ldg(omega + seg) * z;
-      out[seg] = wi;
-      acc += wi * z;
-    }
-  }
-};
+static thread_local std::string g_err;
+void set_last_error(const std::string& msg) { g_err = msg; }
 
 // =====================================================================
 // standalone kernels (one pass each; launched with the plan's G CTAs)
@@ -684,7 +522,6 @@ extern "C" {
 int pcgs_version(void) { return 1; }
 const char* pcgs_last_error(void) { return g_err.c_str(); }
 
-static size_t smem_bytes(const DesignDev& D) { return (size_t)D.smem_doubles * sizeof(double); }
 
 static int set_smem_attrs(const DesignDev& D) {
   const int bytes = (int)smem_bytes(D);
@@ -755,6 +592,27 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int
   I[15] = (H.csr.lds_conflict_excess + H.csc.lds_conflict_excess) * 1000000 /
           std::max<int64_t>(1, H.csr.lds_groups + H.csc.lds_groups);
   *out = D;
+  return PCGS_OK;
+}
+
+int pcgs_store_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h, const int32_t* col_idx_h, int intercept,
+                        int slab_max, int grid, int64_t* stats_h) {
+  if (!row_ptr_h || grid < 1) return fail(PCGS_EINVAL, "null argument");
+  DesignHost H;
+  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, grid, H);
+  if (!err.empty()) return fail(PCGS_EINVAL, err);
+  err = verify_design(H, row_ptr_h, col_idx_h);
+  if (stats_h) {
+    stats_h[0] = H.csr.nslab;
+    stats_h[1] = H.csc.nslab;
+    stats_h[2] = (int64_t)(H.csr.idx.size() / kVecIdx);
+    stats_h[3] = (int64_t)(H.csc.idx.size() / kVecIdx);
+    stats_h[4] = H.csc.nseg;
+    stats_h[5] = H.csr.lds_groups + H.csc.lds_groups;
+    stats_h[6] = H.csr.lds_conflict_excess + H.csc.lds_conflict_excess;
+    stats_h[7] = (int64_t)(H.csr.idx.size() + H.csc.idx.size()) * 2;
+  }
+  if (!err.empty()) return fail(PCGS_EUNSUP - 100, "store self-test failed: " + err);
   return PCGS_OK;
 }
 

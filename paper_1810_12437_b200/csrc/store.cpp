@@ -314,4 +314,80 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
   return "";
 }
 
+// Rebuilds the pattern from the tiled passes and compares it with the input
+// CSR (host-only; used by the CPU test-suite through pcgs_store_selftest).
+std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int32_t* col_idx) {
+  const int64_t n = D.n, p = D.p, pt = D.p_total;
+  // walk every warp range of a pass, calling f(segment id, index) per real index
+  auto walk = [](const PassHost& P, auto&& f) -> std::string {
+    for (size_t t = 0; t < P.tasks.size(); ++t) {
+      const Task& T = P.tasks[t];
+      const int64_t lo = P.slab_lo[T.slab], hi = P.slab_lo[T.slab + 1];
+      const uint16_t sent = (uint16_t)(hi - lo);
+      for (int w = 0; w < kWarps; ++w) {
+        const WarpRange& R = P.warps[T.warp0 + w];
+        if (R.nvec == 0) continue;
+        const uint32_t nb = (R.nvec + 31) / 32;
+        int64_t seg = -1;
+        for (uint32_t k = 0; k < nb; ++k) {
+          const BlockDesc& B = P.blocks[R.blk0 + k];
+          if (k == 0 && !(B.mask & 1u)) return std::string("warp range does not start a segment");
+          int rank = 0;
+          for (int l = 0; l < 32; ++l) {
+            const uint64_t v = (uint64_t)k * 32 + l;
+            if (v >= R.nvec) {
+              if (B.mask >> l & 1u) return std::string("segment start beyond range");
+              continue;
+            }
+            if (B.mask >> l & 1u) seg = (int64_t)B.first_id + rank++;
+            for (int e = 0; e < kVecIdx; ++e) {
+              const uint16_t ix = P.idx[((size_t)R.v0 + v) * kVecIdx + e];
+              if (ix == sent) continue;
+              if (ix > sent) return std::string("index beyond slab");
+              f(T.slab, seg, lo + ix);
+            }
+          }
+        }
+      }
+    }
+    return std::string();
+  };
+  // CSR: segment (s, i) -> column set of row i within slab s
+  std::vector<std::vector<int32_t>> got_rows(n);
+  std::string err = walk(D.csr, [&](int s, int64_t seg, int64_t col) {
+    const int64_t i = seg - (int64_t)s * n;
+    if (i >= 0 && i < n) got_rows[i].push_back((int32_t)col);
+  });
+  if (!err.empty()) return "csr: " + err;
+  for (int64_t i = 0; i < n; ++i) {
+    std::vector<int32_t>& g = got_rows[i];
+    std::sort(g.begin(), g.end());
+    if ((int64_t)g.size() != row_ptr[i + 1] - row_ptr[i] ||
+        !std::equal(g.begin(), g.end(), col_idx + row_ptr[i]))
+      return "csr: row " + std::to_string(i) + " differs";
+  }
+  // CSC: pieces -> column via piece_ptr
+  const PassHost& C = D.csc;
+  std::vector<int32_t> piece_col(C.nseg, -1);
+  for (int s = 0; s < C.nslab; ++s)
+    for (int64_t j = 0; j < pt; ++j)
+      for (int q = C.piece_ptr[(size_t)s * (pt + 1) + j]; q < C.piece_ptr[(size_t)s * (pt + 1) + j + 1]; ++q)
+        piece_col[q] = (int32_t)j;
+  std::vector<std::vector<int32_t>> got_cols(pt);
+  err = walk(C, [&](int, int64_t seg, int64_t row) {
+    if (seg >= 0 && seg < C.nseg && piece_col[seg] >= 0) got_cols[piece_col[seg]].push_back((int32_t)row);
+  });
+  if (!err.empty()) return "csc: " + err;
+  std::vector<std::vector<int32_t>> want(pt);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) want[col_idx[k]].push_back((int32_t)i);
+    if (D.intercept) want[p].push_back((int32_t)i);
+  }
+  for (int64_t j = 0; j < pt; ++j) {
+    std::sort(got_cols[j].begin(), got_cols[j].end());
+    if (got_cols[j] != want[j]) return "csc: column " + std::to_string(j) + " differs";
+  }
+  return "";
+}
+
 }  // namespace pcgs

@@ -70,4 +70,7 @@ struct DesignHost {
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
                          int intercept, int slab_max, int G, DesignHost& out);
 
+// Host-only check: reconstructs both passes and compares with the CSR.
+std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int32_t* col_idx);
+
 }  // namespace pcgs

@@ -1,0 +1,367 @@
+"""Shrinkage-prior logistic Gibbs sampler on the B200 (drop-in for priorcg.gibbs).
+
+`gibbs_run` keeps the reference's signature, scan order, warm start, gamma
+policy, pinning, thinning and abort semantics (pkg/src/priorcg/gibbs.py:260-379)
+but every scan runs on the GPU as one stream of kernels issued by
+`pcgs_gibbs_scan` (include/pcgs.h): Polya-Gamma omega, the global and local
+scales, the fused randomised right-hand side, the persistent PCG solve, X beta
+with the log-likelihood, the log density and the running statistics.  The
+host synchronises only every `sync_every` scans to check for aborts.
+
+Priors: `BridgeConfig` (alpha = 1, the reference's exact path) and
+`HorseshoeConfig` (half-Cauchy local and global scales through the auxiliary
+inverse-gamma scheme; new, not in the reference — DESIGN.md §5).
+
+RNG: the chain is keyed by Philox4x32-10 with `seed`; draws are independent of
+numpy's PCG64 stream, so chains are compared with the reference statistically
+(posterior moments within Monte Carlo error), not bit for bit.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .cg import CGConfig
+
+_PART_STRIDE = 16
+
+
+class UnsupportedUpdateError(NotImplementedError):
+    """Conditional update outside the exact device path (gibbs.py:36-37)."""
+
+
+class GibbsAbortError(RuntimeError):
+    """A scan failed; carries the 1-based iteration index (gibbs.py:40-45)."""
+
+    def __init__(self, iteration, message):
+        super().__init__(f"iteration {iteration}: {message}")
+        self.iteration = iteration
+
+
+@dataclass(frozen=True)
+class BridgeConfig:
+    """Bridge prior settings (gibbs.py:48-82)."""
+
+    alpha: float = 1.0
+    global_shape: float = 1.0
+    global_rate: float = 1.0
+    unshrunk_prior_sd: tuple = ()
+
+    def __post_init__(self):
+        if not 0.0 < self.alpha <= 1.0:
+            raise ValueError("bridge exponent alpha must lie in (0, 1]")
+        if self.global_shape <= 0.0 or self.global_rate <= 0.0:
+            raise ValueError("Gamma prior on tau^-alpha needs positive shape and rate")
+        sds = tuple(float(s) for s in self.unshrunk_prior_sd)
+        if any(s <= 0.0 or math.isnan(s) for s in sds):
+            raise ValueError("unshrunk prior sds must be positive (inf = flat)")
+        object.__setattr__(self, "unshrunk_prior_sd", sds)
+
+    @property
+    def n_unshrunk(self) -> int:
+        return len(self.unshrunk_prior_sd)
+
+    def unshrunk_precision(self) -> np.ndarray:
+        sd = np.asarray(self.unshrunk_prior_sd, dtype=np.float64)
+        out = np.zeros(sd.shape)
+        fin = np.isfinite(sd)
+        out[fin] = sd[fin] ** -2.0
+        return out
+
+
+@dataclass(frozen=True)
+class HorseshoeConfig:
+    """Horseshoe prior: beta_j ~ N(0, tau^2 lam_j^2), lam_j, tau ~ C+(0, 1).
+
+    New (the reference implements only the bridge); `unshrunk_prior_sd` has
+    the BridgeConfig meaning for the leading unshrunk block.
+    """
+
+    unshrunk_prior_sd: tuple = ()
+
+    def __post_init__(self):
+        sds = tuple(float(s) for s in self.unshrunk_prior_sd)
+        if any(s <= 0.0 or math.isnan(s) for s in sds):
+            raise ValueError("unshrunk prior sds must be positive (inf = flat)")
+        object.__setattr__(self, "unshrunk_prior_sd", sds)
+
+    @property
+    def n_unshrunk(self) -> int:
+        return len(self.unshrunk_prior_sd)
+
+    def unshrunk_precision(self) -> np.ndarray:
+        return BridgeConfig(unshrunk_prior_sd=self.unshrunk_prior_sd).unshrunk_precision()
+
+
+@dataclass
+class ShrinkageState:
+    """Sampler snapshot (gibbs.py:85-109); `nu`/`xi` are the horseshoe auxiliaries."""
+
+    beta: np.ndarray
+    omega: np.ndarray
+    lam: np.ndarray
+    tau: float
+    nu: np.ndarray | None = None
+    xi: float | None = None
+
+    def __post_init__(self):
+        self.beta = np.ascontiguousarray(self.beta, dtype=np.float64)
+        self.omega = np.ascontiguousarray(self.omega, dtype=np.float64)
+        self.lam = np.ascontiguousarray(self.lam, dtype=np.float64)
+        self.tau = float(self.tau)
+        if self.beta.size < self.lam.size:
+            raise ValueError("beta must contain the shrunk block")
+        if not np.all(np.isfinite(self.beta)):
+            raise ValueError("beta must be finite")
+        if np.any(self.omega <= 0.0) or not np.all(np.isfinite(self.omega)):
+            raise ValueError("omega must be positive and finite")
+        if np.any(self.lam <= 0.0) or not np.all(np.isfinite(self.lam)):
+            raise ValueError("lambda must be positive and finite")
+        if self.tau <= 0.0 or not math.isfinite(self.tau):
+            raise ValueError("tau must be positive and finite")
+
+
+@dataclass
+class ChainOutput:
+    """Stored draws plus running statistics (gibbs.py:112-136)."""
+
+    draws: np.ndarray
+    tau_draws: np.ndarray
+    logdensity_trace: np.ndarray
+    cg_iteration_counts: np.ndarray
+    running_mean_scaled_beta: np.ndarray | None
+    running_var_unshrunk: np.ndarray
+    final_state: ShrinkageState
+    seed: int
+    n_unshrunk: int
+    stat_count: int = field(default=0)
+
+    def scaled_beta_mean(self):
+        if self.stat_count == 0:
+            return None
+        return self.running_mean_scaled_beta
+
+    def unshrunk_sd(self):
+        if self.stat_count < 2 or self.n_unshrunk == 0:
+            return None
+        return np.sqrt(self.running_var_unshrunk)
+
+
+class _GibbsArgs(ctypes.Structure):
+    """Mirror of pcgs_gibbs_t (include/pcgs.h)."""
+
+    _fields_ = [
+        ("prior", ctypes.c_int), ("q", ctypes.c_int), ("precond", ctypes.c_int),
+        ("fixed_omega", ctypes.c_int), ("fixed_tau", ctypes.c_int), ("fixed_lam", ctypes.c_int),
+        ("max_iter", ctypes.c_int), ("rtol", ctypes.c_double),
+        ("a0", ctypes.c_double), ("b0", ctypes.c_double), ("alpha", ctypes.c_double),
+        ("gamma_scale", ctypes.c_double),
+        ("seed", ctypes.c_uint64),
+        ("y", ctypes.c_void_p), ("kappa", ctypes.c_void_p), ("usd_prec", ctypes.c_void_p),
+        ("usd_sd", ctypes.c_void_p),
+        ("beta", ctypes.c_void_p), ("z", ctypes.c_void_p), ("omega", ctypes.c_void_p),
+        ("lam", ctypes.c_void_p), ("nu", ctypes.c_void_p), ("scal", ctypes.c_void_p),
+        ("mean", ctypes.c_void_p), ("m2", ctypes.c_void_p),
+        ("prior_diag", ctypes.c_void_p), ("minv", ctypes.c_void_p), ("scale", ctypes.c_void_p),
+        ("b", ctypes.c_void_p), ("part", ctypes.c_void_p), ("logdens", ctypes.c_void_p),
+        ("results", ctypes.c_void_p), ("draws", ctypes.c_void_p), ("tau_draws", ctypes.c_void_p),
+        ("trace", ctypes.c_void_p), ("alphas", ctypes.c_void_p), ("betas", ctypes.c_void_p),
+    ]
+
+
+_PRECOND = {"prior": 0, "identity": 1, "jacobi": 2}
+
+
+class DeviceChain:
+    """Device-resident state of one chain; `scan(t)` issues one Gibbs scan."""
+
+    def __init__(self, X, y, cfg, n_iter, burn_in=0, thin=1, seed=0, preconditioner="prior",
+                 cg_config=None, init_state=None, gamma_scale=1.0, fixed_omega=None,
+                 fixed_tau=None, fixed_lam=None, device=None):
+        t = _lib.torch()
+        self.X = X
+        self.store = X.device_store(device)
+        st = self.store
+        dev = self.dev = st.device
+        f64 = t.float64
+        self.n, self.pt = X.n_rows, X.n_cols
+        self.q = cfg.n_unshrunk
+        self.p = self.pt - self.q
+        self.cfg = cfg
+        self.horseshoe = isinstance(cfg, HorseshoeConfig)
+        self.n_iter, self.burn_in, self.thin = n_iter, burn_in, thin
+        self.seed = int(seed)
+        cgc = cg_config if cg_config is not None else CGConfig()
+        if cgc.trace_level == "full":
+            raise NotImplementedError("trace_level='full' is not on the device path")
+        max_iter = cgc.max_iter if cgc.max_iter is not None else 2 * self.pt
+        self.max_iter = max_iter
+        self.n_store = max(0, (n_iter - burn_in + thin - 1) // thin) if n_iter else 0
+
+        def dt(x):
+            return _lib.to_device(x, dev)
+
+        yh = np.asarray(y, dtype=np.float64)
+        self.y = dt(yh)
+        self.kappa = dt(yh - 0.5)
+        sd = np.asarray(cfg.unshrunk_prior_sd, dtype=np.float64)
+        self.usd_sd = dt(sd if sd.size else np.zeros(1))
+        self.usd_prec = dt(cfg.unshrunk_precision() if sd.size else np.zeros(1))
+        if init_state is None:
+            beta = np.zeros(self.pt)
+            omega = np.full(self.n, 0.25)
+            lam = np.ones(self.p)
+            tau = 1.0
+            nu, xi = np.ones(self.p), 1.0
+        else:
+            beta, omega, lam, tau = init_state.beta, init_state.omega, init_state.lam, init_state.tau
+            nu = init_state.nu if init_state.nu is not None else np.ones(self.p)
+            xi = init_state.xi if init_state.xi is not None else 1.0
+            if beta.shape != (self.pt,) or lam.shape != (self.p,):
+                raise ValueError("initial state does not match the model shape")
+        self.beta = dt(beta).clone()
+        self.omega = dt(fixed_omega if fixed_omega is not None else omega).clone()
+        self.lam = dt(fixed_lam if fixed_lam is not None else lam).clone()
+        self.nu = dt(nu).clone()
+        self.scal = dt(np.array([fixed_tau if fixed_tau is not None else tau, xi, 0.0, 0.0]))
+        self.z = t.empty(self.n + 2, dtype=f64, device=dev)
+        self.mean = t.zeros(self.pt, dtype=f64, device=dev)
+        self.m2 = t.zeros(max(self.q, 1), dtype=f64, device=dev)
+        self.prior_diag = t.empty(self.pt, dtype=f64, device=dev)
+        self.minv = t.empty(self.pt, dtype=f64, device=dev)
+        self.scale = t.empty(self.pt, dtype=f64, device=dev)
+        self.b = t.empty(self.pt, dtype=f64, device=dev)
+        self.part = t.zeros(_PART_STRIDE * (st.describe()["grid"] + 1), dtype=f64, device=dev)
+        self.logdens = t.zeros(max(n_iter, 1), dtype=f64, device=dev)
+        self.results = t.zeros(8 * max(n_iter, 1), dtype=t.int32, device=dev)
+        self.draws = t.empty((max(self.n_store, 1), self.pt), dtype=f64, device=dev)
+        self.tau_draws = t.empty(max(self.n_store, 1), dtype=f64, device=dev)
+        self.trace = t.empty(max_iter + 1, dtype=f64, device=dev)
+        self.alphas = t.empty(max_iter + 1, dtype=f64, device=dev)
+        self.betas = t.empty(max_iter + 1, dtype=f64, device=dev)
+        P = _lib.ptr
+        self.args = _GibbsArgs(
+            prior=1 if self.horseshoe else 0, q=self.q, precond=_PRECOND[preconditioner],
+            fixed_omega=int(fixed_omega is not None), fixed_tau=int(fixed_tau is not None),
+            fixed_lam=int(fixed_lam is not None), max_iter=int(max_iter), rtol=float(cgc.rtol),
+            a0=float(getattr(cfg, "global_shape", 1.0)), b0=float(getattr(cfg, "global_rate", 1.0)),
+            alpha=float(getattr(cfg, "alpha", 1.0)),
+            gamma_scale=float(gamma_scale), seed=self.seed & (2 ** 64 - 1),
+            y=P(self.y), kappa=P(self.kappa), usd_prec=P(self.usd_prec), usd_sd=P(self.usd_sd),
+            beta=P(self.beta), z=P(self.z), omega=P(self.omega), lam=P(self.lam), nu=P(self.nu),
+            scal=P(self.scal), mean=P(self.mean), m2=P(self.m2), prior_diag=P(self.prior_diag),
+            minv=P(self.minv), scale=P(self.scale), b=P(self.b), part=P(self.part),
+            logdens=P(self.logdens), results=P(self.results), draws=P(self.draws),
+            tau_draws=P(self.tau_draws), trace=P(self.trace), alphas=P(self.alphas),
+            betas=P(self.betas))
+        self.count = 0
+        self.stored = 0
+        L = _lib.lib()
+        L.pcgs_gibbs_init.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_void_p]
+        L.pcgs_gibbs_scan.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+        _lib.check(L.pcgs_gibbs_init(st.handle, ctypes.byref(self.args), _lib.stream_ptr(dev)))
+
+    def scan(self, t):
+        """Issue scan t (1-based) on the current stream; no synchronisation."""
+        slot = -1
+        if t > self.burn_in and (t - self.burn_in - 1) % self.thin == 0:
+            slot = self.stored
+            self.stored += 1
+        _lib.check(_lib.lib().pcgs_gibbs_scan(self.store.handle, ctypes.byref(self.args), int(t),
+                                              int(self.count), int(slot),
+                                              _lib.stream_ptr(self.dev)))
+        self.count += 1
+
+    def check(self, t_lo, t_hi, allow_max_iter=False):
+        """Raise GibbsAbortError for the first failed scan in [t_lo, t_hi]."""
+        res = self.results[8 * (t_lo - 1): 8 * t_hi].view(-1, 8).cpu().numpy()
+        for k, r in enumerate(res):
+            t = t_lo + k
+            if r[4]:
+                raise GibbsAbortError(t, "scale positivity violated")
+            if r[1] == _lib.PCGS_NOT_PD:
+                raise GibbsAbortError(t, f"beta update failed: d'Phi d <= 0 at CG iteration {r[2]}")
+            if r[1] == _lib.PCGS_NONFINITE:
+                raise GibbsAbortError(t, f"beta update failed: non-finite value at CG iteration {r[2]}")
+            if r[1] == _lib.PCGS_MAX_ITER and not allow_max_iter:
+                raise GibbsAbortError(t, f"CG used all {r[0]} iterations without converging")
+
+    def output(self) -> ChainOutput:
+        t = self.n_iter
+        res = self.results[: 8 * max(t, 1)].view(-1, 8).cpu().numpy()[:t]
+        scal = self.scal.cpu().numpy()
+        state = ShrinkageState(self.beta.cpu().numpy(), self.omega.cpu().numpy(),
+                               self.lam.cpu().numpy(), float(scal[0]),
+                               nu=self.nu.cpu().numpy() if self.horseshoe else None,
+                               xi=float(scal[1]) if self.horseshoe else None)
+        m2 = self.m2.cpu().numpy()[: self.q]
+        var = m2 / (self.count - 1) if self.count >= 2 else np.full(self.q, np.nan)
+        return ChainOutput(
+            draws=self.draws[: self.stored].cpu().numpy(),
+            tau_draws=self.tau_draws[: self.stored].cpu().numpy(),
+            logdensity_trace=self.logdens[:t].cpu().numpy(),
+            cg_iteration_counts=res[:, 0].astype(np.int64),
+            running_mean_scaled_beta=self.mean.cpu().numpy() if self.count else None,
+            running_var_unshrunk=var, final_state=state, seed=self.seed, n_unshrunk=self.q,
+            stat_count=self.count)
+
+
+def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, preconditioner="prior",
+              cg_config=None, burn_in_sampler=None, init_state=None, local_scale_sampler=None,
+              gamma_scale=1.0, allow_max_iter=False, fixed_omega=None, fixed_tau=None,
+              fixed_lam=None, on_progress=None, device=None, sync_every=64) -> ChainOutput:
+    """Run `n_iter` scans on the GPU (gibbs.py:260-379); same arguments and output.
+
+    `sampler`/`burn_in_sampler` must be "cg" (the dense Cholesky sampler is the
+    CPU oracle's); `local_scale_sampler` is not supported on the device path.
+    """
+    y = np.asarray(y, dtype=np.float64)
+    if y.shape != (X.n_rows,):
+        raise ValueError("outcome length must match the design")
+    if not np.all((y == 0.0) | (y == 1.0)):
+        raise ValueError("outcomes must be 0/1")
+    if n_iter < 0 or burn_in < 0 or burn_in > n_iter:
+        raise ValueError("need 0 <= burn_in <= n_iter")
+    if thin < 1:
+        raise ValueError("thin must be >= 1")
+    for name in (sampler, burn_in_sampler):
+        if name not in (None, "cg", "direct"):
+            raise ValueError(f"unknown sampler {name!r}")
+    if "direct" in (sampler, burn_in_sampler):
+        raise NotImplementedError("the dense Cholesky sampler is the CPU oracle's; use sampler='cg'")
+    if preconditioner not in _PRECOND:
+        if str(preconditioner).startswith("block:"):
+            raise NotImplementedError("block-threshold preconditioning is not on the device path")
+        raise ValueError(f"unknown preconditioner {preconditioner!r}")
+    q = cfg.n_unshrunk
+    if X.n_cols - q < 0:
+        raise ValueError("more unshrunk prior sds than design columns")
+    if local_scale_sampler is not None:
+        raise NotImplementedError("custom local_scale_sampler callbacks are not on the device path")
+    if isinstance(cfg, BridgeConfig) and cfg.alpha != 1.0 and fixed_lam is None:
+        raise UnsupportedUpdateError(
+            "exact local-scale draws exist for alpha = 1 only; pin fixed_lam for other exponents")
+    ch = DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=seed,
+                     preconditioner=preconditioner, cg_config=cg_config, init_state=init_state,
+                     gamma_scale=gamma_scale, fixed_omega=fixed_omega, fixed_tau=fixed_tau,
+                     fixed_lam=fixed_lam, device=device)
+    torch = _lib.torch()
+    checked = 0
+    for t in range(1, n_iter + 1):
+        ch.scan(t)
+        if on_progress is not None:
+            torch.cuda.current_stream(ch.dev).synchronize()
+            ch.check(t, t, allow_max_iter)
+            checked = t
+            on_progress(t, n_iter)
+        elif sync_every and t - checked >= sync_every:
+            ch.check(checked + 1, t, allow_max_iter)
+            checked = t
+    if checked < n_iter:
+        ch.check(checked + 1, n_iter, allow_max_iter)
+    return ch.output()

@@ -102,3 +102,33 @@ def config2_conditioning(design: BinaryDesign, seed=0, pg_sampler=None):
     scale = np.concatenate([[gamma0], tau * lam])
     return dict(omega=omega, lam=lam, tau=tau, y=y, kappa=kappa, prior_diag=prior_diag,
                 minv=minv, scale=scale, rng=rng)
+
+
+def simulate_outcomes(design: BinaryDesign, seed=0, n_signal=10, rate=None, intercept=True):
+    """Truth beta with `n_signal` N(0,1) nonzeros at random shrunk positions;
+    y ~ Bernoulli(logistic(X beta + c)).  With `rate`, the intercept offset c is
+    set by bisection so that mean P(y=1) equals `rate` (the rare-outcome
+    configurations); otherwise c = 0.  Returns (y, beta_true) with beta_true in
+    the reference layout (intercept first when `intercept`)."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(seed + 17)
+    beta = np.zeros(design.p)
+    pos = rng.choice(design.p, size=min(n_signal, design.p), replace=False)
+    beta[pos] = rng.standard_normal(len(pos))
+    X = sp.csr_matrix((np.ones(design.nnz), design.col_idx.astype(np.int64), design.row_ptr),
+                      shape=(design.n, design.p))
+    eta = X @ beta
+    c = 0.0
+    if rate is not None:
+        lo, hi = -40.0, 40.0
+        for _ in range(200):
+            c = 0.5 * (lo + hi)
+            m = float(np.mean(1.0 / (1.0 + np.exp(-(eta + c)))))
+            if m > rate:
+                hi = c
+            else:
+                lo = c
+    prob = 1.0 / (1.0 + np.exp(-(eta + c)))
+    y = (rng.random(design.n) < prob).astype(np.float64)
+    full = np.concatenate([[c], beta]) if intercept else beta
+    return y, full

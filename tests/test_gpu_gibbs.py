@@ -1,0 +1,133 @@
+"""Device Gibbs chains vs the oracle: posterior moments within Monte Carlo
+error (BASELINE north star), the reference's abort / pinning / thinning
+semantics (test_gibbs.py:228-345), and the horseshoe conditionals."""
+import numpy as np
+import pytest
+from scipy import stats
+
+from paper_1810_12437_b200 import gibbs, synth
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+def batch_se(x, nb=10):
+    n = (len(x) // nb) * nb
+    return x[:n].reshape(nb, -1).mean(1).std(ddof=1) / np.sqrt(nb)
+
+
+def standardized_differences(a, b):
+    se = np.sqrt(np.array([batch_se(a[:, j]) ** 2 + batch_se(b[:, j]) ** 2 for j in range(a.shape[1])]))
+    keep = se > 1e-12
+    return ((a.mean(0) - b.mean(0))[keep]) / se[keep]
+
+
+@pytest.fixture(scope="module")
+def small():
+    d = synth.binary_design(600, 80, 5e-3, 0.3, seed=5)
+    y, truth = synth.simulate_outcomes(d, seed=1, n_signal=6)
+    return d, y, truth
+
+
+@pytest.mark.parametrize("prior", ["bridge", "horseshoe"])
+def test_posterior_moments_match_oracle(small, prior):
+    d, y, _ = small
+    X = d.matrix()
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    n_iter, burn = 4000, 500
+    if prior == "bridge":
+        cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+        ref = port.gibbs_bridge(Xo, y, n_iter, seed=7, burn_in=burn, unshrunk_sd=(np.inf,))
+    else:
+        cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
+        ref = port.gibbs_horseshoe(Xo, y, n_iter, seed=7, burn_in=burn, unshrunk_sd=(np.inf,))
+    out = gibbs.gibbs_run(X, y, cfg, n_iter, burn_in=burn, seed=8)
+    for a, b in ((out.draws, ref.draws), (out.draws ** 2, ref.draws ** 2)):
+        z = standardized_differences(a, b)
+        assert np.mean(np.abs(z) > 4) < 0.03
+        if prior == "bridge":  # the horseshoe mixes too slowly for a KS test on 4k draws
+            assert stats.kstest(np.clip(z, -6, 6), "norm").pvalue > 1e-3
+
+
+def test_pinned_scales_give_exact_gaussian(small):
+    """With omega, tau, lambda pinned the chain is an exact N(Phi^-1 X'kappa, Phi^-1)
+    sampler (test_gibbs.py:249-270)."""
+    d, y, _ = small
+    X = d.matrix()
+    rng = np.random.default_rng(0)
+    om = rng.uniform(0.1, 0.3, d.n)
+    lam = rng.uniform(0.5, 2.0, d.p)
+    tau = 0.3
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    out = gibbs.gibbs_run(X, y, cfg, 3000, burn_in=0, seed=2, fixed_omega=om, fixed_tau=tau, fixed_lam=lam,
+                          cg_config=gibbs.CGConfig(rtol=1e-10))
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    dense = np.zeros((d.n, d.p + 1))
+    rows = np.repeat(np.arange(d.n), np.diff(Xo.row_ptr))
+    dense[rows, Xo.col_idx] = 1.0
+    prior = np.concatenate([[0.0], (tau * lam) ** -2.0])
+    full = dense.T @ (om[:, None] * dense) + np.diag(prior)
+    cov = np.linalg.inv(full)
+    mean = cov @ (dense.T @ (y - 0.5))
+    z = (out.draws.mean(0) - mean) / np.sqrt(np.diag(cov) / len(out.draws))
+    assert np.mean(np.abs(z) > 4) < 0.02
+    emp = np.var(out.draws, axis=0)
+    assert np.median(emp / np.diag(cov)) == pytest.approx(1.0, abs=0.1)
+
+
+def test_bitwise_reproducible_and_shapes(small):
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    a = gibbs.gibbs_run(X, y, cfg, 25, burn_in=5, seed=11, thin=3)
+    b = gibbs.gibbs_run(X, y, cfg, 25, burn_in=5, seed=11, thin=3)
+    assert a.draws.shape == (7, d.p + 1) and a.tau_draws.shape == (7,)
+    assert a.logdensity_trace.shape == (25,) and a.cg_iteration_counts.shape == (25,)
+    assert np.array_equal(a.draws, b.draws) and np.array_equal(a.logdensity_trace, b.logdensity_trace)
+    assert a.stat_count == 25 and a.scaled_beta_mean() is not None and a.unshrunk_sd() is not None
+    c = gibbs.gibbs_run(X, y, cfg, 25, burn_in=5, seed=12, thin=3)
+    assert not np.array_equal(a.draws, c.draws)
+
+
+def test_max_iter_aborts_unless_allowed(small):
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    with pytest.raises(gibbs.GibbsAbortError) as err:
+        gibbs.gibbs_run(X, y, cfg, 3, seed=1, cg_config=gibbs.CGConfig(max_iter=1, rtol=1e-14))
+    assert err.value.iteration == 1
+    out = gibbs.gibbs_run(X, y, cfg, 3, seed=1, cg_config=gibbs.CGConfig(max_iter=1, rtol=1e-14),
+                          allow_max_iter=True)
+    assert np.all(out.cg_iteration_counts == 1)
+
+
+def test_resume_from_state_and_progress(small):
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
+    first = gibbs.gibbs_run(X, y, cfg, 10, seed=3)
+    seen = []
+    second = gibbs.gibbs_run(X, y, cfg, 5, seed=4, init_state=first.final_state,
+                             on_progress=lambda t, n: seen.append((t, n)))
+    assert seen == [(t, 5) for t in range(1, 6)]
+    assert np.all(np.isfinite(second.draws)) and second.final_state.xi is not None
+
+
+@pytest.mark.parametrize("pre", ["identity", "jacobi"])
+def test_other_preconditioners_same_posterior_draws_converge(small, pre):
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    out = gibbs.gibbs_run(X, y, cfg, 20, seed=5, preconditioner=pre,
+                          cg_config=gibbs.CGConfig(rtol=1e-8, max_iter=20000))
+    ref = gibbs.gibbs_run(X, y, cfg, 20, seed=5, cg_config=gibbs.CGConfig(rtol=1e-8))
+    # same seed -> same noise: draws agree to solver tolerance after the first scan
+    assert np.allclose(out.draws[0], ref.draws[0], rtol=1e-4, atol=1e-4)
+
+
+def test_paper_scale_bridge_chain_runs():
+    d = synth.config_design(3, seed=0)
+    y, _ = synth.simulate_outcomes(d, seed=0, rate=0.02)
+    out = gibbs.gibbs_run(d.matrix(), y, gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,)), 20, seed=1)
+    assert np.all(np.isfinite(out.draws)) and out.cg_iteration_counts.max() < 50
+    assert np.all(np.diff(out.logdensity_trace[5:]) < 1e4)
