@@ -1,0 +1,383 @@
+"""Benchmark: Gibbs iter/s and Phi-apply HBM GB/s at n=72,489, p=22,175.
+
+Workload (BASELINE.json configs[2], "config 3"): seeded synthetic binary design
+(log-uniform column rates in [1e-4, 0.3], 59,928,655 nonzeros) plus a dense
+intercept, 2 % positive outcomes from a 10-signal truth, horseshoe logistic
+model, PCG rtol 1e-6, one chain per GPU.  A step is one Gibbs scan
+(omega, tau, lambda, RHS, PCG solve, X beta + log density, statistics).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 runs under torchrun as independent chains, one per GPU (chain-parallel,
+weak scaling, no collective on the data path); timing is the max over ranks.
+The reference arm times the CPU restatement of the reference (oracle/port.py,
+test infrastructure) on the host cores: each step is a bounded CPU scan (CG
+capped at --cpu-cg-cap applications) extrapolated to the scan's measured CG
+iteration count (recorded from the device chain in bench_workload.json).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+WORKLOAD_FILE = ROOT / "bench_workload.json"
+PEAKS_FILE = ROOT / "MEASURED_PEAKS.json"
+CONFIG = 3
+SEED = 0
+RTOL = 1e-6
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--prior", default="horseshoe", choices=["horseshoe", "bridge"])
+    ap.add_argument("--cpu-cg-cap", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--record", action="store_true", help="write bench_workload.json")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload(prior):
+    from paper_1810_12437_b200 import gibbs, synth
+    d = synth.config_design(CONFIG, seed=SEED)
+    y, _ = synth.simulate_outcomes(d, seed=SEED, n_signal=10, rate=0.02)
+    cfg = (gibbs.HorseshoeConfig(unshrunk_prior_sd=(math.inf,)) if prior == "horseshoe"
+           else gibbs.BridgeConfig(unshrunk_prior_sd=(math.inf,)))
+    return d, y, cfg
+
+
+def config_block(d, prior, world, chains_per_gpu=1):
+    return {
+        "workload": (f"config 3: {prior} logistic Gibbs scan, n={d.n:,} p={d.p:,} binary sparse "
+                     f"(nnz {d.nnz:,}, log-uniform rates [1e-4,0.3]) + dense intercept, 2% positives, "
+                     f"PCG rtol {RTOL:g}"),
+        "n": d.n, "p": d.p, "nnz": d.nnz, "prior": prior, "chains_per_gpu": chains_per_gpu,
+        "parallelism": f"chain-parallel x{world}" if world > 1 else "single chain",
+        "l2_policy": "no flush: the index store (241 MB) exceeds the 126 MB L2 every pass",
+        "seed": SEED,
+    }
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    try:
+        return json.loads(PEAKS_FILE.read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ------------------------------------------------------------------ CPU reference scan
+def cpu_scan_bounded(Xo, y, state, rng, cap, q=1):
+    """One horseshoe scan of the CPU restatement with the CG capped at `cap`
+    iterations.  Returns (seconds outside CG, seconds per Phi application)."""
+    from oracle import port
+    beta, z, lam2, nu, tau2, xi, mean, count = state
+    t0 = time.perf_counter()
+    omega = port.pg_batch(z, rng)
+    lam2, nu, tau2, xi = port.horseshoe_scales(beta[q:], lam2, nu, tau2, xi, rng)
+    tau, lam = math.sqrt(tau2), np.sqrt(lam2)
+    prior = np.concatenate([[0.0], (tau * lam) ** -2.0])
+    lin = port.matvec_t(Xo, y - 0.5)
+    g = np.array([10.0])
+    minv = np.concatenate([g ** 2, (tau * lam) ** 2])
+    scale = np.concatenate([g, tau * lam])
+    x0 = np.zeros(len(beta)) if count == 0 else np.concatenate([[1.0], tau * lam]) * mean
+    b = port.rhs(Xo, lin, omega, prior, rng)
+    t1 = time.perf_counter()
+    res = port.pcg(lambda v: port.phi_apply(Xo, omega, prior, v), b, minv, scale, x0, max_iter=cap, rtol=RTOL)
+    t2 = time.perf_counter()
+    beta = res.x
+    z = port.matvec(Xo, beta)
+    port.horseshoe_log_density(beta, tau, lam, z, y, q, np.array([math.inf]))
+    t3 = time.perf_counter()
+    new_state = (beta, z, lam2, nu, tau2, xi, mean, count + 1)
+    return (t1 - t0) + (t3 - t2), (t2 - t1) / max(res.applies, 1), res.applies, new_state
+
+
+def cpu_baseline(d, y, cg_iters, steps, cap):
+    """Time `steps` bounded CPU scans; extrapolate each to its CG count."""
+    from oracle import port
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    rng = np.random.default_rng(SEED)
+    state = (np.zeros(d.p + 1), np.zeros(d.n), np.ones(d.p), np.ones(d.p), 1.0, 1.0, np.zeros(d.p + 1), 0)
+    est, fixed, per_apply = [], [], []
+    t0 = time.perf_counter()
+    for s in range(steps):
+        tf, ta, _, state = cpu_scan_bounded(Xo, y, state, rng, cap)
+        k = cg_iters[s % len(cg_iters)]
+        est.append(tf + (k + 1) * ta)
+        fixed.append(tf)
+        per_apply.append(ta)
+    wall = time.perf_counter() - t0
+    return {"scan_seconds_est": est, "fixed_s": float(np.mean(fixed)), "apply_s": float(np.mean(per_apply)),
+            "wall_s": wall, "value": len(est) / float(np.sum(est))}
+
+
+def load_cg_iters(steps):
+    try:
+        w = json.loads(WORKLOAD_FILE.read_text())
+        it = w["cg_iters_timed"]
+        return it if len(it) else [150]
+    except Exception:
+        return [150]
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    d, y, _ = workload(args.prior)
+    iters = load_cg_iters(args.steps)
+    # warm-up steps are run (bounded) and discarded, then K timed steps
+    if args.warmup:
+        cpu_baseline(d, y, iters, min(args.warmup, 1), args.cpu_cg_cap)
+    r = cpu_baseline(d, y, iters, args.steps, args.cpu_cg_cap)
+    value = r["value"]
+    sample = (f"{args.steps} horseshoe scans of the CPU restatement (oracle/port.py), CG capped at "
+              f"{args.cpu_cg_cap} Phi-applications per scan and extrapolated to the device chain's "
+              f"per-scan CG counts (mean {np.mean(iters):.1f}): fixed {r['fixed_s']:.2f} s + "
+              f"{r['apply_s']*1e3:.0f} ms per apply")
+    line = {
+        "impl": "reference", "metric": "gibbs_iter_per_s", "value": value, "unit": "iter/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config 3 recipe)",
+        "config": config_block(d, args.prior, 1),
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1810_12437_b200 import gibbs
+    from paper_1810_12437_b200 import cg as pcg
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    d, y, cfg = workload(args.prior)
+    X = d.matrix()
+    st = X.device_store(dev)
+    info = st.describe()
+
+    # ---- device-resident chain: warm-up, then K timed scans ----
+    K, W = args.steps, args.warmup
+    chain = gibbs.DeviceChain(X, y, cfg, W + K, burn_in=W, seed=SEED + rank,
+                              cg_config=gibbs.CGConfig(rtol=RTOL), device=dev)
+    for t in range(1, W + 1):
+        chain.scan(t)
+    torch.cuda.synchronize(dev)
+    chain.check(1, W)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for t in range(W + 1, W + K + 1):
+            chain.scan(t)
+        e1.record()
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    chain.check(W + 1, W + K, allow_max_iter=False)
+    res = chain.results.view(-1, 8).cpu().numpy()
+    cg_timed = res[W:W + K, 0].astype(int).tolist()
+    applies = int(res[W:W + K, 3].sum())
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * K / (ms_max * 1e-3)
+
+    # ---- dominant kernel: the persistent PCG solve on this chain's conditional ----
+    phi = gibbs_conditional_operator(chain)
+    bt, mt, sc = chain.b.clone(), chain.minv.clone(), chain.scale.clone()
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(2):
+        out = pcg.pcg_solve_device(phi, bt, mt, sc, rtol=RTOL, max_iter=chain.max_iter)
+    torch.cuda.synchronize(dev)
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    k0.record(stream)
+    for _ in range(reps):
+        out = pcg.pcg_solve_device(phi, bt, mt, sc, rtol=RTOL, max_iter=chain.max_iter)
+    k1.record(stream)
+    torch.cuda.synchronize(dev)
+    pcg_ms = k0.elapsed_time(k1) / reps
+    pcg_applies = int(out[4][3].item())
+    us_apply = pcg_ms * 1e3 / pcg_applies
+    n, p = d.n, d.p
+    idx_bytes = info["index_bytes"]
+    vec_bytes = 8 * (3 * n + 4 * (p + 1))            # w write+read, omega; v, d, out, v
+    alg_bytes = idx_bytes + vec_bytes                # per Phi application, store format
+    canon = 8 * d.nnz + 8 * (n + 1) + 8 * (p + 1) + 8 * (3 * n + 4 * p)  # SURVEY §8d, int32 CSR+CSC
+    pk_, pk_src = peaks()
+    # achieved = SURVEY §8(d)'s canonical algorithmic bytes per Phi-apply (int32 CSR + CSC
+    # indices, int64 pointers, vector traffic) x applies per launch / launch time
+    achieved = canon * pcg_applies / (pcg_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        prof = json.loads((ROOT / "profiles" / "k_pcg_traffic.json").read_text())
+        traffic = prof["dram_bytes_per_apply"] * pcg_applies
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": "k_pcg (persistent PCG, one cooperative launch per solve)",
+                "achieved": achieved, "peak": pk_["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk_["hbm_gbs"], "traffic": traffic, "peak_source": pk_src,
+                "algorithmic_bytes_per_launch": canon * pcg_applies,
+                "canonical_bytes_per_apply": canon, "us_per_apply": us_apply,
+                "applies_per_launch": pcg_applies, "launch_ms": pcg_ms,
+                "store_bytes_per_apply": alg_bytes,
+                "store_gbs": alg_bytes / (us_apply * 1e-6) / 1e9,
+                "note": "the store reads 2-byte slab-local indices, half the canonical "
+                        "int32 bytes; store_gbs is the HBM rate of the bytes actually read"}
+
+    # ---- end to end through the public API, host buffers ----
+    state = chain.output().final_state
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    out_e2e = gibbs.gibbs_run(X, np.asarray(y), cfg, K, seed=SEED + 1000 + rank, init_state=state,
+                              cg_config=gibbs.CGConfig(rtol=RTOL), device=dev)
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_val = world * K / float(e2e_t.item())
+    pt = d.p + 1
+    h2d = (2 * n + pt + n + 2 * d.p) * 8 / K     # y, kappa, init beta/omega/lam/nu
+    d2h = (pt + 4) * 8 + 8 * 4                   # one stored draw + tau/logdens/result per scan
+
+    if args.record and rank == 0:
+        (ROOT / "gpurun_out").mkdir(exist_ok=True)
+        rec = {"config": CONFIG, "prior": args.prior, "seed": SEED, "warmup": W, "steps": K,
+               "cg_iters_timed": cg_timed, "cg_iters_e2e": out_e2e.cg_iteration_counts.tolist()}
+        (ROOT / "gpurun_out" / "bench_workload.json").write_text(json.dumps(rec))
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = cpu_baseline(d, y, cg_timed, 2, args.cpu_cg_cap)
+        cpu = {"value": r["value"], "unit": "iter/s", "cores": 1, "kind": "port",
+               "sample": (f"2 horseshoe scans of oracle/port.py on the host, CG capped at {args.cpu_cg_cap} "
+                          f"Phi-applications and extrapolated to this run's per-scan CG counts "
+                          f"(mean {np.mean(cg_timed):.1f}); fixed {r['fixed_s']:.2f} s + "
+                          f"{r['apply_s']*1e3:.0f} ms per apply; wall {r['wall_s']:.1f} s")}
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": "gibbs_iter_per_s", "value": value, "unit": "iter/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; BASELINE config 3 recipe; no public dataset)",
+            "config": config_block(d, args.prior, world),
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": "iter/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": 9 * K,
+            "clocks": clocks,
+            "extra": {"cg_iters_mean": float(np.mean(cg_timed)), "cg_iters": cg_timed,
+                      "phi_applies_timed": applies, "pcg_solve_ms": pcg_ms,
+                      "store": {k: info[k] for k in ("csr_slabs", "csc_slabs", "index_bytes", "grid")}},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def gibbs_conditional_operator(chain):
+    from paper_1810_12437_b200.sampler import PrecisionOperator
+    return PrecisionOperator.from_device(chain.X, chain.omega, chain.prior_diag)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
