@@ -123,13 +123,17 @@ int pcgs_pcg(pcgs_design_t d, const double* omega, const double* prior_diag,
 /* Generic-operator PCG (pcg_solve with a duck-typed operator, cg.py:105-113):
  * the same loop, vector algebra on device, Phi supplied by a callback
  * fn(ctx, v, out) on device buffers of length p (returns 0 on success).
+ * dbuf/adbuf (may be NULL): caller-owned device buffers used as the search
+ * direction and its product, so a device-side callback (e.g. the row-sharded
+ * operator with its allreduce) can address them without copies.
  * trace_h/alphas_h/betas_h/result_h are HOST arrays; synchronises every
  * iteration (desk-scale path, used by the reference's operator tests). */
 typedef int (*pcgs_apply_fn)(void* ctx, const double* v, double* out);
 int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv,
-                const double* scale, const double* b, double* x, int32_t max_iter,
-                double rtol, double* trace_h, double* alphas_h, double* betas_h,
-                int32_t* result_h, pcgs_stream_t stream);
+                const double* scale, const double* b, double* x, double* dbuf,
+                double* adbuf, int32_t max_iter, double rtol, double* trace_h,
+                double* alphas_h, double* betas_h, int32_t* result_h,
+                pcgs_stream_t stream);
 
 /* Synchronous copy helper for operator callbacks: kind 0 host->device,
  * 1 device->host, 2 device->device. */

@@ -51,8 +51,8 @@ SIGNATURES = {
     "pcgs_phi_diagonal": (ctypes.c_int, [_P, _P, _P, _P, _P]),
     "pcgs_rhs": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _U64, _U64, _P, _P]),
     "pcgs_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
-    "pcgs_pcg_op": (ctypes.c_int, [APPLY_FN, _P, _I64, _P, _P, _P, _P, _I32, _D, _P, _P, _P,
-                                   _P, _P]),
+    "pcgs_pcg_op": (ctypes.c_int, [APPLY_FN, _P, _I64, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P,
+                                   _P, _P, _P]),
     "pcgs_copy": (ctypes.c_int, [_P, _P, _I64, ctypes.c_int]),
     "pcgs_debug_profile": (ctypes.c_int, [_P]),
     "pcgs_debug_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),

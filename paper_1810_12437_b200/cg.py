@@ -220,8 +220,8 @@ def _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, rtol, as_tensor):
     betas = np.zeros(max_iter)
     result = np.zeros(4, dtype=np.int32)
     t.cuda.synchronize(dev)
-    rc = L.pcgs_pcg_op(fn, None, p, _lib.ptr(md), _lib.ptr(sd), _lib.ptr(bd), _lib.ptr(x), max_iter,
-                       float(rtol), trace.ctypes.data, alphas.ctypes.data, betas.ctypes.data,
+    rc = L.pcgs_pcg_op(fn, None, p, _lib.ptr(md), _lib.ptr(sd), _lib.ptr(bd), _lib.ptr(x), None, None,
+                       max_iter, float(rtol), trace.ctypes.data, alphas.ctypes.data, betas.ctypes.data,
                        result.ctypes.data, _lib.stream_ptr(dev))
     if errors:
         raise errors[0]

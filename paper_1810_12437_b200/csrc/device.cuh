@@ -25,6 +25,7 @@ struct DesignDev {
   int icpt;
   int G;               // CTAs the static plan was built for
   int smem_doubles;    // dynamic shared memory per CTA, in doubles
+  int dbg;             // tuning experiments: bit 0 skip gathers, bit 1 skip segmented reduce
   PassDev csr, csc;
 };
 
@@ -212,7 +213,7 @@ __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, doub
 }
 
 template <class Epi>
-__device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const double* sv, Epi& epi) {
+__device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const double* sv, Epi& epi, int dbg = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint4 R = __ldg(P.warps + warp0 + warp);
   const int nvec = (int)R.y;
@@ -221,7 +222,7 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
   const uint4* base = P.vec + R.x;
   const uint2* bd = P.blocks + R.z;
   // L2 prefetch of the whole range (TMA engine; no registers or scoreboards)
-  if (lane == 0) {
+  if (lane == 0 && !(dbg & 4)) {
     const char* p0 = (const char*)base;
     const unsigned bytes = (unsigned)nvec * 16u;
     for (unsigned off = 0; off < bytes; off += 16384u) {
@@ -252,8 +253,11 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
         dsc.x = __shfl_sync(0xffffffffu, dl.x, u);
         dsc.y = __shfl_sync(0xffffffffu, dl.y, u);
         const int v = k * 32 + lane;
-        const double s = v < nvec ? gather8(q[u], sv) : 0.0;
-        block_reduce(dsc, s, lane, acc, open_id, have_open, epi);
+        double s;
+        if (dbg & 1) s = v < nvec ? (double)(q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) : 0.0;
+        else s = v < nvec ? gather8(q[u], sv) : 0.0;
+        if (dbg & 2) acc += s + (double)dsc.y;
+        else block_reduce(dsc, s, lane, acc, open_id, have_open, epi);
       }
     }
   }
@@ -266,15 +270,20 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 // Not inlined: inside the persistent PCG kernel the caller's live state is
 // saved once per pass and the streaming loop gets the whole register budget.
 template <class Fill, class Epi>
-__device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi) {
+__device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi, int dbg = 0) {
   const int c = blockIdx.x;
   const int t0 = P.cta_task_ptr[c], t1 = P.cta_task_ptr[c + 1];
   for (int t = t0; t < t1; ++t) {
     const int2 T = __ldg(P.task + t);
     const long long lo = P.slab_lo[T.x], hi = P.slab_lo[T.x + 1];
     __syncthreads();
-    fill(sv, lo, (int)(hi - lo));
-    process_warp(P, T.y, sv, epi);
+    if (dbg & 8) {
+      if (threadIdx.x == 0) sv[hi - lo] = 0.0;
+      __syncthreads();
+    } else {
+      fill(sv, lo, (int)(hi - lo));
+    }
+    process_warp(P, T.y, sv, epi, dbg);
   }
 }
 

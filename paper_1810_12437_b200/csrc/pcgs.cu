@@ -27,6 +27,7 @@ namespace cg = cooperative_groups;
 // =====================================================================
 static unsigned long long* g_prof = nullptr;  // debug: phase timestamps of the next pcgs_pcg
 static int g_tma_dir = 1;
+static int g_dbg = 0;
 static thread_local std::string g_err;
 void set_last_error(const std::string& msg) { g_err = msg; }
 
@@ -39,10 +40,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_csr_matvec(DesignDev D, const d
   const double v0 = D.icpt ? __ldg(v) : 0.0;
   if (D.csr.nslab == 1) {
     EpiZ e{out, v0};
-    run_pass(D.csr, sv, f, e);
+    run_pass(D.csr, sv, f, e, D.dbg);
   } else {
     EpiStore e{out};  // out is the (nslab x n) partial buffer
-    run_pass(D.csr, sv, f, e);
+    run_pass(D.csr, sv, f, e, D.dbg);
   }
 }
 
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_csc_vec(DesignDev D, const doub
   bulk_init(bf, &mbar);
   FillVecN f{w, &bf};
   EpiStore e{pieces};
-  run_pass(D.csc, sv, f, e);
+  run_pass(D.csc, sv, f, e, D.dbg);
 }
 
 // out[ref(j)] = column_sum(j) + diag_j * v[ref(j)]  (diag/v may be null)
@@ -650,6 +651,7 @@ static int launch_csr(pcgs_design_t d, bool phi, const double* v, const double* 
 
 int pcgs_matvec(pcgs_design_t d, const double* v, double* out, pcgs_stream_t stream) {
   if (!d || !v || !out) return fail(PCGS_EINVAL, "null argument");
+  d->dev.dbg = g_dbg;
   cudaStream_t s = (cudaStream_t)stream;
   Scratch S(s);
   return launch_csr(d, false, v, nullptr, out, s, S);
@@ -657,6 +659,7 @@ int pcgs_matvec(pcgs_design_t d, const double* v, double* out, pcgs_stream_t str
 
 int pcgs_matvec_t(pcgs_design_t d, const double* w, double* out, pcgs_stream_t stream) {
   if (!d || !w || !out) return fail(PCGS_EINVAL, "null argument");
+  d->dev.dbg = g_dbg;
   const DesignDev& D = d->dev;
   cudaStream_t s = (cudaStream_t)stream;
   Scratch S(s);
@@ -807,8 +810,8 @@ __global__ void __launch_bounds__(kThreads) k_opvec(int mode, long long p, doubl
 }
 
 int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, const double* scale, const double* b,
-                double* x, int32_t max_iter, double rtol, double* trace_h, double* alphas_h, double* betas_h,
-                int32_t* result_h, pcgs_stream_t stream) {
+                double* x, double* dbuf, double* adbuf, int32_t max_iter, double rtol, double* trace_h,
+                double* alphas_h, double* betas_h, int32_t* result_h, pcgs_stream_t stream) {
   if (!fn || p < 1 || !minv || !scale || !b || !x || !trace_h || !alphas_h || !betas_h || !result_h)
     return fail(PCGS_EINVAL, "null argument");
   if (max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
@@ -816,8 +819,8 @@ int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, cons
   Scratch S(s);
   double* r = S.get<double>(p);
   double* z = S.get<double>(p);
-  double* dv = S.get<double>(p);
-  double* Ad = S.get<double>(p);
+  double* dv = dbuf ? dbuf : S.get<double>(p);
+  double* Ad = adbuf ? adbuf : S.get<double>(p);
   double* sc = S.get<double>(2);
   if (!r || !z || !dv || !Ad || !sc) return fail(PCGS_ENOMEM, "scratch allocation failed");
   double h2[2];
@@ -884,6 +887,7 @@ int pcgs_debug_profile(void* buf) {
 
 int pcgs_debug_option(int key, int value) {
   if (key == 0) g_tma_dir = value;
+  if (key == 1) g_dbg = value;
   return PCGS_OK;
 }
 

@@ -1,0 +1,179 @@
+"""Row-sharded Phi across GPUs (BASELINE config 5).
+
+The rows of X are split into contiguous, nnz-balanced shards, one per rank
+(one process per GPU, `torch.distributed` with NCCL over NVLink).  p-length
+vectors are replicated; per Phi-apply every rank runs its local pattern-only
+passes (X_g' Omega_g X_g v, libpcgs) and one allreduce(sum) of the p-length
+partial combines them; the prior term D v is contributed by rank 0 only, so
+the allreduce result is Phi v on every rank, bitwise identical (one NCCL
+algorithm, the same inputs everywhere).  The PCG vector algebra then runs
+replicated on every rank in the device PCG engine (`pcgs_pcg_op`), with the
+operator supplied as a device-side callback - no host copies of vectors.
+
+A single process can also hold several shards of one device
+(`EmulatedGroup`): the allreduce becomes a fixed-order local sum, which is how
+the decomposition is validated on one GPU.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .cg import CGReport, _metric_scale, _n_betas, _raise_status
+from .sparse import SparseDesignMatrix
+
+
+def row_partition(row_ptr, world, intercept=True):
+    """Contiguous row ranges [lo, hi) balanced by stored entries per rank."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    n = len(row_ptr) - 1
+    weight = row_ptr + (np.arange(n + 1, dtype=np.int64) if intercept else 0)
+    total = int(weight[-1])
+    cuts = [0]
+    for r in range(1, world):
+        target = total * r / world
+        c = int(np.searchsorted(weight, target))
+        cuts.append(min(max(c, cuts[-1]), n))
+    cuts.append(n)
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def local_rows(X: SparseDesignMatrix, lo, hi) -> SparseDesignMatrix:
+    """The row block [lo, hi) of a design as its own pattern-only design."""
+    rp, ci, icpt = X.pattern()
+    sub_rp = rp[lo:hi + 1] - rp[lo]
+    sub_ci = ci[rp[lo]:rp[hi]]
+    p = X.n_cols - (1 if icpt else 0)
+    return SparseDesignMatrix.from_pattern(hi - lo, p, sub_rp, sub_ci, intercept=icpt, check=False)
+
+
+class EmulatedGroup:
+    """Stand-in for a process group when all shards live in one process."""
+
+    size = 1
+
+
+class ShardedPrecisionOperator:
+    """Phi = sum_g X_g' Omega_g X_g + D over row shards (this rank's shards
+    plus an allreduce over `group`)."""
+
+    def __init__(self, shards, omegas, prior_precision_diag, rank=0, group=None, device=None,
+                 local_apply=None):
+        t = _lib.torch()
+        self.shards = list(shards)
+        self.rank = rank
+        self.group = group
+        self.local_apply = local_apply
+        if local_apply is None:
+            self.device = _lib.cuda_device(device)
+            self.stores = [s.device_store(self.device) for s in self.shards]
+            self.omegas = [_lib.to_device(o, self.device) for o in omegas]
+            self.diag = _lib.to_device(prior_precision_diag, self.device)
+            self.zero = t.zeros_like(self.diag)
+            self.tmp = t.empty_like(self.diag)
+        else:
+            self.device = None
+            self.omegas = list(omegas)
+            self.diag = prior_precision_diag
+        self.prior_precision_diag = np.asarray(
+            prior_precision_diag.cpu().numpy() if _lib.is_tensor(prior_precision_diag)
+            else prior_precision_diag, dtype=np.float64)
+        self.dim = len(self.prior_precision_diag)
+        self.apply_count = 0
+
+    def apply_into(self, v, out):
+        """out = Phi v on device tensors (all ranks receive the same result)."""
+        self.apply_count += 1
+        for g, (st, om) in enumerate(zip(self.stores, self.omegas)):
+            d = self.diag if (self.rank == 0 and g == 0) else self.zero
+            if g == 0:
+                st.phi_apply(om, d, v, out)
+            else:
+                st.phi_apply(om, d, v, self.tmp)
+                out.add_(self.tmp)          # emulated allreduce: fixed shard order
+        self._allreduce(out)
+        return out
+
+    def _allreduce(self, out):
+        if self.group is not None and not isinstance(self.group, EmulatedGroup):
+            import torch.distributed as dist
+            dist.all_reduce(out, op=dist.ReduceOp.SUM, group=self.group)
+
+    def apply(self, v):
+        """numpy / tensor apply (for `pcg_solve`'s generic path and the tests)."""
+        if self.local_apply is not None:
+            self.apply_count += 1
+            out = None
+            for g, (sh, om) in enumerate(zip(self.shards, self.omegas)):
+                d = self.diag if (self.rank == 0 and g == 0) else np.zeros_like(self.diag)
+                y = self.local_apply(sh, om, d, v)
+                out = y if out is None else out + y
+            if self.group is not None:
+                import torch
+                import torch.distributed as dist
+                tt = torch.from_numpy(np.ascontiguousarray(out))
+                dist.all_reduce(tt, op=dist.ReduceOp.SUM, group=self.group)
+                out = tt.numpy()
+            return out
+        t = _lib.torch()
+        as_tensor = _lib.is_tensor(v)
+        vd = _lib.to_device(v, self.device)
+        out = t.empty_like(vd)
+        self.apply_into(vd, out)
+        return out if as_tensor else out.cpu().numpy()
+
+
+def sharded_pcg_solve(op: ShardedPrecisionOperator, b, M, x0=None, config=None, residual_scale=None):
+    """pcg_solve (cg.py:105-192) over a row-sharded operator: device vector
+    algebra replicated on every rank, Phi applied through the device callback."""
+    from .cg import CGConfig
+    t = _lib.torch()
+    L = _lib.lib()
+    cfg = config if config is not None else CGConfig()
+    p = int(b.shape[0])
+    max_iter = cfg.max_iter if cfg.max_iter is not None else 2 * p
+    scale = _metric_scale(op, M, residual_scale, p)
+    dev = op.device
+    bd = _lib.to_device(b, dev)
+    x = t.zeros(p, dtype=t.float64, device=dev) if x0 is None else _lib.to_device(x0, dev).clone()
+    md = _lib.to_device(np.asarray(M.inv_diagonal, dtype=np.float64), dev)
+    sd = _lib.to_device(scale, dev)
+    dbuf = t.empty(p, dtype=t.float64, device=dev)
+    adbuf = t.empty(p, dtype=t.float64, device=dev)
+    errors = []
+    xptr = _lib.ptr(x)
+
+    def cb(ctx, vptr, outptr):
+        try:
+            src = x if vptr == xptr else dbuf   # the first application is on x0 (cg.py:137)
+            op.apply_into(src, adbuf)
+            return 0
+        except BaseException as exc:
+            errors.append(exc)
+            return 1
+
+    fn = _lib.APPLY_FN(cb)
+    trace = np.zeros(max_iter + 1)
+    alphas = np.zeros(max_iter)
+    betas = np.zeros(max_iter)
+    result = np.zeros(4, dtype=np.int32)
+    t.cuda.synchronize(dev)
+    rc = L.pcgs_pcg_op(fn, None, p, _lib.ptr(md), _lib.ptr(sd), _lib.ptr(bd), _lib.ptr(x),
+                       _lib.ptr(dbuf), _lib.ptr(adbuf), max_iter, float(cfg.rtol), trace.ctypes.data,
+                       alphas.ctypes.data, betas.ctypes.data, result.ctypes.data,
+                       _lib.stream_ptr(dev))
+    if errors:
+        raise errors[0]
+    _lib.check(rc)
+    iterations, status, fail_iter, applies = (int(v) for v in result)
+    _raise_status(status, fail_iter)
+    return CGReport(
+        iterations=iterations,
+        termination="converged" if status == _lib.PCGS_CONVERGED else "max_iter",
+        rms_precond_residual_trace=trace[: iterations + 1].copy(),
+        solution=x if _lib.is_tensor(b) else x.cpu().numpy(),
+        matvec_count=applies,
+        alphas=alphas[:iterations].copy(),
+        betas=betas[:_n_betas(iterations, status)].copy(),
+        iterates=None,
+    )
