@@ -146,6 +146,9 @@ int pcgs_debug_profile(void* buf);
 /* Debug/tuning switches: key 0 = direction fill mode of pcgs_pcg (1: owners
  * publish + grid sync + TMA copy, 0: computed fill). */
 int pcgs_debug_option(int key, int value);
+/* Debug: device buffer (3 uint64 per CTA) for per-CTA pass timestamps when
+ * the debug-option key 1 bit 64 is set. */
+int pcgs_debug_cta_times(void* buf);
 
 /* omega[i] ~ PG(1, z[i]) (pg_draw_batch, polya_gamma.py:39-84), Philox keyed
  * by (seed, stream_id), one thread per draw. */

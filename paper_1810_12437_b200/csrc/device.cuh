@@ -177,7 +177,7 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
 // descriptors (start mask + first segment id) drive a segmented reduction whose
 // open segment is carried across blocks in a per-lane accumulator.
 // ---------------------------------------------------------------------------
-constexpr int kRing = 8;
+constexpr int kRing = 4;
 
 template <class Epi>
 __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, double& acc, unsigned& open_id,
@@ -269,9 +269,13 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 // walk the warp's bundle range.  `fill(sv, lo, len)` must end with a barrier.
 // Not inlined: inside the persistent PCG kernel the caller's live state is
 // saved once per pass and the streaming loop gets the whole register budget.
+__device__ unsigned long long* g_cta_times = nullptr;  // debug: per-CTA [start, filled, end]
+
 template <class Fill, class Epi>
 __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi, int dbg = 0) {
   const int c = blockIdx.x;
+  unsigned long long t_start = 0;
+  if ((dbg & 64) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int t0 = P.cta_task_ptr[c], t1 = P.cta_task_ptr[c + 1];
   for (int t = t0; t < t1; ++t) {
     const int2 T = __ldg(P.task + t);
@@ -283,7 +287,21 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
     } else {
       fill(sv, lo, (int)(hi - lo));
     }
+    if ((dbg & 64) && threadIdx.x == 0 && g_cta_times) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_cta_times[3 * c + 0] = t_start;
+      g_cta_times[3 * c + 1] = t;
+    }
     process_warp(P, T.y, sv, epi, dbg);
+  }
+  if (dbg & 64) {
+    __syncthreads();
+    if (threadIdx.x == 0 && g_cta_times) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g_cta_times[3 * c + 2] = t;
+    }
   }
 }
 

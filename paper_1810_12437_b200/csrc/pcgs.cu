@@ -238,131 +238,128 @@ __device__ __forceinline__ double owned_column_sum(const OwnState& o, const doub
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
-  cg::grid_group grid = cg::this_grid();
+  // Loop state lives in shared memory so that the inlined streaming passes
+  // get the whole register budget (1024 threads -> 64 registers).
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[64];
   __shared__ double bc[4];
+  __shared__ double st_rz, st_beta;
+  __shared__ int st_status, st_iter, st_fail, st_applies;
   __shared__ unsigned long long mbar;
   BulkFill bf;
   bulk_init(bf, &mbar);
-  const DesignDev& D = A.D;
-  const int G = gridDim.x, c = blockIdx.x, tid = threadIdx.x;
-  const long long pt = D.pt, p = D.p, n = D.n;
-  const int icpt = D.icpt;
-  const bool multi = D.csr.nslab > 1;
-  const int S = D.csc.nslab;
-  const long long dvs = (pt + 15) / 16 * 16;  // 128-byte aligned stride of the two direction buffers
+  const int tid = threadIdx.x;
 
   // ---- own slice of the p_total coordinates, kept in shared memory ----
-  const int chunk = (int)((pt + G - 1) / G);
-  const long long j0 = (long long)c * chunk;
-  const OwnState o = own_state(sv, D.smem_doubles, chunk, S);
-  for (int t = tid; t < chunk; t += kThreads) {
-    const long long j = j0 + t;
-    double xv = 0, m = 0, sc = 0, dg = 0, bv = 0;
-    if (j < pt) {
-      const long long rj = ref_index(j, p, icpt);
-      xv = A.x[rj];
-      m = __ldg(A.minv + rj);
-      sc = __ldg(A.scale + rj);
-      dg = __ldg(A.diag + rj);
-      bv = __ldg(A.b + rj);
-      A.dvg[dvs + j] = xv;  // v = x0 for the first application
+  {
+    const long long pt = A.D.pt;
+    const int chunk = (int)((pt + gridDim.x - 1) / gridDim.x);
+    const long long j0 = (long long)blockIdx.x * chunk;
+    const long long dvs = (pt + 15) / 16 * 16;
+    const OwnState o = own_state(sv, A.D.smem_doubles, chunk, A.D.csc.nslab);
+    for (int t = tid; t < chunk; t += kThreads) {
+      const long long j = j0 + t;
+      double xv = 0, m = 0, sc = 0, dg = 0, bv = 0;
+      if (j < pt) {
+        const long long rj = ref_index(j, A.D.p, A.D.icpt);
+        xv = A.x[rj];
+        m = __ldg(A.minv + rj);
+        sc = __ldg(A.scale + rj);
+        dg = __ldg(A.diag + rj);
+        bv = __ldg(A.b + rj);
+        A.dvg[dvs + j] = xv;  // v = x0 for the first application
+      }
+      o.x[t] = xv;
+      o.r[t] = 0.0;
+      o.d[t] = xv;
+      o.m[t] = m;
+      o.s[t] = sc;
+      o.D[t] = dg;
+      o.b[t] = bv;
+      o.z[t] = 0.0;
     }
-    o.x[t] = xv;
-    o.r[t] = 0.0;
-    o.d[t] = xv;
-    o.m[t] = m;
-    o.s[t] = sc;
-    o.D[t] = dg;
-    o.b[t] = bv;
-    o.z[t] = 0.0;
+    for (int t = tid; t < A.D.csc.nslab * (chunk + 1); t += kThreads) {
+      const int s = t / (chunk + 1), q = t % (chunk + 1);
+      const long long j = min(j0 + q, pt);
+      o.pp[t] = A.D.csc.piece_ptr[(long long)s * (pt + 1) + j];
+    }
+    if (tid == 0) {
+      st_rz = 0.0;
+      st_beta = 0.0;
+      st_status = PCGS_MAX_ITER;
+      st_iter = 0;
+      st_fail = -1;
+      st_applies = 0;
+    }
   }
-  for (int t = tid; t < S * (chunk + 1); t += kThreads) {
-    const int s = t / (chunk + 1), q = t % (chunk + 1);
-    const long long j = min(j0 + q, pt);
-    o.pp[t] = D.csc.piece_ptr[(long long)s * (pt + 1) + j];
-  }
-  double* part_dAd = A.part;
-  double* part_rms = A.part + 1;
-  double* part_rz = A.part + 2;
-
-  double rz = 0.0;
-  int status = PCGS_MAX_ITER, iterations = 0, fail_iter = -1, applies = 0;
-  grid.sync();
+  cg::this_grid().sync();
 
   for (int a = 0;; ++a) {
-    double beta = 0.0;
-    const bool prof = A.prof && c == 0 && tid == 0 && a < 64;
+    const long long pt = A.D.pt;
+    const int chunk = (int)((pt + gridDim.x - 1) / gridDim.x);
+    const long long j0 = (long long)blockIdx.x * chunk;
+    const long long dvs = (pt + 15) / 16 * 16;
+    const OwnState o = own_state(sv, A.D.smem_doubles, chunk, A.D.csc.nslab);
+    const bool prof = A.prof && blockIdx.x == 0 && tid == 0 && a < 64;
     // ---------------- convergence test of iteration a-1 ----------------
     if (a > 0) {
-      const double s_rms = reduce_partials(part_rms, G, bc);
-      const double s_rz = reduce_partials(part_rz, G, bc + 1);
+      const double s_rms = reduce_partials(A.part + 1, gridDim.x, bc);
+      const double s_rz = reduce_partials(A.part + 2, gridDim.x, bc + 1);
       const double rms = sqrt(s_rms / (double)pt);
-      if (c == 0 && tid == 0) A.trace[a - 1] = rms;
+      if (blockIdx.x == 0 && tid == 0) A.trace[a - 1] = rms;
       const int k = a - 1;  // iterations completed
-      if (rms <= A.rtol) {
-        status = PCGS_CONVERGED;
-        iterations = k;
-        break;
+      int stop = 0;
+      if (rms <= A.rtol) stop = 1;
+      else if (!isfinite(rms)) stop = 2;
+      double beta = 0.0;
+      if (!stop) {
+        if (a >= 2) {
+          beta = s_rz / st_rz;
+          if (blockIdx.x == 0 && tid == 0) A.betas[a - 2] = beta;
+        }
+        if (k >= A.max_iter) stop = 3;
       }
-      if (!isfinite(rms)) {
-        status = PCGS_NONFINITE;
-        iterations = k;
-        fail_iter = k;
-        break;
+      __syncthreads();
+      if (tid == 0) {
+        st_rz = s_rz;
+        st_beta = beta;
+        if (stop) {
+          st_status = stop == 1 ? PCGS_CONVERGED : stop == 2 ? PCGS_NONFINITE : PCGS_MAX_ITER;
+          st_iter = k;
+          if (stop == 2) st_fail = k;
+        }
       }
-      if (a >= 2) {
-        beta = s_rz / rz;
-        if (c == 0 && tid == 0) A.betas[a - 2] = beta;
-      }
-      rz = s_rz;
-      if (k >= A.max_iter) {
-        status = PCGS_MAX_ITER;
-        iterations = k;
-        break;
-      }
-      // new direction d = z + beta d on the owned slice
+      if (stop) break;
+      // new direction d = z + beta d on the owned slice, published for the fill
       for (int t = tid; t < chunk; t += kThreads) {
         const double dn = a == 1 ? o.z[t] : fma(beta, o.d[t], o.z[t]);
         o.d[t] = dn;
         if (j0 + t < pt) A.dvg[(a & 1) * dvs + j0 + t] = dn;
       }
-      if (A.tma_dir) grid.sync();
+      cg::this_grid().sync();
     }
     if (prof) A.prof[4 * a + 0] = gtimer();
 
     // ---------------- phase A: CSR pass, w = omega (X v) ----------------
     double acc_dAd = 0.0;
     for (int t = tid; t < chunk; t += kThreads) acc_dAd += o.D[t] * o.d[t] * o.d[t];
-    const double* vcur = A.dvg + (a == 0 ? dvs : (a & 1) * dvs);
-    double v0 = 0.0;
     {
-      EpiCsr e{multi ? A.zpart : A.w, A.omega, 0.0, 0.0, multi};
-      if (a == 0 || A.tma_dir) {
-        if (tid == 0) bc[2] = icpt ? __ldcg(vcur + p) : 0.0;
-        __syncthreads();
-        v0 = bc[2];
-        e.v0 = v0;
-        FillBulk f{vcur, &bf};
-        run_pass(D.csr, sv, f, e);
-      } else {
-        const double* zvp = A.zv;
-        const double* old = A.dvg + ((a - 1) & 1) * dvs;
-        if (tid == 0) bc[2] = icpt ? (a == 1 ? __ldcg(zvp + p) : fma(beta, __ldcg(old + p), __ldcg(zvp + p))) : 0.0;
-        __syncthreads();
-        v0 = bc[2];
-        e.v0 = v0;
-        FillDir f{zvp, old, beta, a == 1, 0};
-        run_pass(D.csr, sv, f, e);
-      }
+      const double* vcur = A.dvg + (a == 0 ? dvs : (a & 1) * dvs);
+      if (tid == 0) bc[2] = A.D.icpt ? __ldcg(vcur + A.D.p) : 0.0;
+      __syncthreads();
+      const bool multi = A.D.csr.nslab > 1;
+      EpiCsr e{multi ? A.zpart : A.w, A.omega, bc[2], 0.0, multi};
+      FillBulk f{vcur, &bf};
+      run_pass(A.D.csr, sv, f, e);
       acc_dAd += e.acc;
     }
-    if (multi) {
-      grid.sync();
-      for (long long i = (long long)c * kThreads + tid; i < n; i += (long long)G * kThreads) {
+    if (A.D.csr.nslab > 1) {
+      cg::this_grid().sync();
+      const long long n = A.D.n;
+      const double v0 = bc[2];
+      for (long long i = (long long)blockIdx.x * kThreads + tid; i < n; i += (long long)gridDim.x * kThreads) {
         double z = 0.0;
-        for (int s = 0; s < D.csr.nslab; ++s) z += __ldcg(A.zpart + (long long)s * n + i);
+        for (int s = 0; s < A.D.csr.nslab; ++s) z += __ldcg(A.zpart + (long long)s * n + i);
         z += v0;
         const double wi = __ldg(A.omega + i) * z;
         A.w[i] = wi;
@@ -371,37 +368,40 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     }
     {
       const double t = block_sum(acc_dAd, red);
-      if (tid == 0) part_dAd[c * kPartStride] = t;
+      if (tid == 0) A.part[blockIdx.x * kPartStride] = t;
     }
     if (prof) A.prof[4 * a + 1] = gtimer();
-    grid.sync();
+    cg::this_grid().sync();
 
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
     {
       FillVecN f{A.w, &bf};
       EpiStore e{A.pieces};
-      run_pass(D.csc, sv, f, e);
+      run_pass(A.D.csc, sv, f, e);
     }
     if (prof) A.prof[4 * a + 2] = gtimer();
-    grid.sync();
-    ++applies;
+    cg::this_grid().sync();
+    if (tid == 0) ++st_applies;
     if (prof) A.prof[4 * a + 3] = gtimer();
 
     // ---------------- phase C: assemble, step, residual ----------------
     double alpha = 0.0;
     if (a > 0) {
-      const double dAd = reduce_partials(part_dAd, G, bc);
+      const double dAd = reduce_partials(A.part, gridDim.x, bc);
       if (!(dAd > 0.0)) {
-        status = PCGS_NOT_PD;
-        iterations = a;
-        fail_iter = a;
+        if (tid == 0) {
+          st_status = PCGS_NOT_PD;
+          st_iter = a;
+          st_fail = a;
+        }
         break;
       }
-      alpha = rz / dAd;
-      if (c == 0 && tid == 0) A.alphas[a - 1] = alpha;
+      alpha = st_rz / dAd;
+      if (blockIdx.x == 0 && tid == 0) A.alphas[a - 1] = alpha;
     }
     double t_rms = 0.0, t_rz = 0.0;
-    const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, D.smem_doubles);
+    const int S = A.D.csc.nslab;
+    const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
     for (int t = tid; t < chunk; t += kThreads) {
       if (j0 + t >= pt) continue;
       const double Ad = owned_column_sum(o, A.pieces, S, chunk, t, sv, staged) + o.D[t] * o.d[t];
@@ -415,26 +415,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       o.r[t] = rv;
       const double zn = o.m[t] * rv;
       o.z[t] = zn;
-      if (!A.tma_dir) A.zv[j0 + t] = zn;
       const double tj = o.s[t] * rv;
       t_rms += tj * tj;
       t_rz += rv * zn;
     }
     block_sum2(t_rms, t_rz, red);
     if (tid == 0) {
-      part_rms[c * kPartStride] = t_rms;
-      part_rz[c * kPartStride] = t_rz;
+      A.part[blockIdx.x * kPartStride + 1] = t_rms;
+      A.part[blockIdx.x * kPartStride + 2] = t_rz;
     }
-    grid.sync();
+    cg::this_grid().sync();
   }
 
-  for (int t = tid; t < chunk; t += kThreads)
-    if (j0 + t < pt) A.x[ref_index(j0 + t, p, icpt)] = o.x[t];
-  if (c == 0 && tid == 0) {
-    A.result[0] = iterations;
-    A.result[1] = status;
-    A.result[2] = fail_iter;
-    A.result[3] = applies;
+  __syncthreads();
+  {
+    const long long pt = A.D.pt;
+    const int chunk = (int)((pt + gridDim.x - 1) / gridDim.x);
+    const long long j0 = (long long)blockIdx.x * chunk;
+    const OwnState o = own_state(sv, A.D.smem_doubles, chunk, A.D.csc.nslab);
+    for (int t = tid; t < chunk; t += kThreads)
+      if (j0 + t < pt) A.x[ref_index(j0 + t, A.D.p, A.D.icpt)] = o.x[t];
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    A.result[0] = st_iter;
+    A.result[1] = st_status;
+    A.result[2] = st_fail;
+    A.result[3] = st_applies;
   }
 }
 
@@ -882,6 +888,12 @@ int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, cons
 
 int pcgs_debug_profile(void* buf) {
   g_prof = (unsigned long long*)buf;
+  return PCGS_OK;
+}
+
+int pcgs_debug_cta_times(void* buf) {
+  unsigned long long* p = (unsigned long long*)buf;
+  CUDA_TRY(cudaMemcpyToSymbol(g_cta_times, &p, sizeof(p)));
   return PCGS_OK;
 }
 

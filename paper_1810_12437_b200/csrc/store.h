@@ -23,8 +23,8 @@
 
 namespace pcgs {
 
-constexpr int kWarps = 16;             // warps per CTA of the pass kernels
-constexpr int kThreads = kWarps * 32;  // 512
+constexpr int kWarps = 32;             // warps per CTA of the pass kernels
+constexpr int kThreads = kWarps * 32;  // 1024
 constexpr int kVecIdx = 8;             // uint16 indices per 16-byte vector
 
 struct WarpRange {    // 16 bytes, device-readable as uint4
