@@ -90,6 +90,27 @@ __device__ __forceinline__ double reduce_partials(const double* part, int G, dou
   return *bcast;
 }
 
+__device__ __forceinline__ void reduce_partials2(const double* part, int G, double* bcast, double& a, double& b) {
+  const int lane = threadIdx.x & 31;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int q = lane; q < G; q += 32) {
+      s0 += __ldcg(part + (long long)q * kPartStride);
+      s1 += __ldcg(part + (long long)q * kPartStride + 1);
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+      bcast[0] = s0;
+      bcast[1] = s1;
+    }
+  }
+  __syncthreads();
+  a = bcast[0];
+  b = bcast[1];
+}
+
 __device__ __forceinline__ double gather8(uint4 q, const double* sv) {
   double a = sv[q.x & 0xffffu] + sv[q.x >> 16];
   double b = sv[q.y & 0xffffu] + sv[q.y >> 16];
@@ -212,6 +233,27 @@ __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, doub
   have_open = true;
 }
 
+// L2 prefetch of a warp's whole range (TMA engine; no registers or scoreboards),
+// issued before the slab fill so the index stream is in flight during it.
+__device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int dbg) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane != 0 || (dbg & 4)) return;
+  const uint4 R = __ldg(P.warps + warp0 + warp);
+  const int nvec = (int)R.y;
+  if (nvec == 0) return;
+  const int nb = (nvec + 31) >> 5;
+  const char* p0 = (const char*)(P.vec + R.x);
+  const unsigned bytes = (unsigned)nvec * 16u;
+  for (unsigned off = 0; off < bytes; off += 16384u) {
+    const unsigned sz = bytes - off < 16384u ? bytes - off : 16384u;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0 + off), "r"(sz) : "memory");
+  }
+  const uint2* bd = P.blocks + R.z;
+  const unsigned long long d0 = (unsigned long long)bd & ~15ull;
+  const unsigned long long d1 = ((unsigned long long)(bd + nb) + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d0), "r"((unsigned)(d1 - d0)) : "memory");
+}
+
 template <class Epi>
 __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const double* sv, Epi& epi, int dbg = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -221,18 +263,6 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
   const int nb = (nvec + 31) >> 5;
   const uint4* base = P.vec + R.x;
   const uint2* bd = P.blocks + R.z;
-  // L2 prefetch of the whole range (TMA engine; no registers or scoreboards)
-  if (lane == 0 && !(dbg & 4)) {
-    const char* p0 = (const char*)base;
-    const unsigned bytes = (unsigned)nvec * 16u;
-    for (unsigned off = 0; off < bytes; off += 16384u) {
-      const unsigned sz = bytes - off < 16384u ? bytes - off : 16384u;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0 + off), "r"(sz) : "memory");
-    }
-    const unsigned long long d0 = (unsigned long long)bd & ~15ull;
-    const unsigned long long d1 = ((unsigned long long)(bd + nb) + 15ull) & ~15ull;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d0), "r"((unsigned)(d1 - d0)) : "memory");
-  }
   double acc = 0.0;
   unsigned open_id = 0;
   bool have_open = false;
@@ -280,6 +310,7 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
   for (int t = t0; t < t1; ++t) {
     const int2 T = __ldg(P.task + t);
     const long long lo = P.slab_lo[T.x], hi = P.slab_lo[T.x + 1];
+    prefetch_warp(P, T.y, dbg);
     __syncthreads();
     if (dbg & 8) {
       if (threadIdx.x == 0) sv[hi - lo] = 0.0;

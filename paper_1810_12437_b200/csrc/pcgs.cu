@@ -303,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     const bool prof = A.prof && blockIdx.x == 0 && tid == 0 && a < 64;
     // ---------------- convergence test of iteration a-1 ----------------
     if (a > 0) {
-      const double s_rms = reduce_partials(A.part + 1, gridDim.x, bc);
-      const double s_rz = reduce_partials(A.part + 2, gridDim.x, bc + 1);
+      double s_rms, s_rz;
+      reduce_partials2(A.part + 1, gridDim.x, bc, s_rms, s_rz);
       const double rms = sqrt(s_rms / (double)pt);
       if (blockIdx.x == 0 && tid == 0) A.trace[a - 1] = rms;
       const int k = a - 1;  // iterations completed
@@ -386,6 +386,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
 
     // ---------------- phase C: assemble, step, residual ----------------
     double alpha = 0.0;
+    const int S = A.D.csc.nslab;
+    const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
     if (a > 0) {
       const double dAd = reduce_partials(A.part, gridDim.x, bc);
       if (!(dAd > 0.0)) {
@@ -400,8 +402,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       if (blockIdx.x == 0 && tid == 0) A.alphas[a - 1] = alpha;
     }
     double t_rms = 0.0, t_rz = 0.0;
-    const int S = A.D.csc.nslab;
-    const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
     for (int t = tid; t < chunk; t += kThreads) {
       if (j0 + t >= pt) continue;
       const double Ad = owned_column_sum(o, A.pieces, S, chunk, t, sv, staged) + o.D[t] * o.d[t];
