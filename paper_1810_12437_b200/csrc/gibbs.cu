@@ -73,25 +73,37 @@ __device__ double wald1(double mu, Philox& R) {
   return R.uniform() <= mu / (mu + x) ? x : mu * mu / x;
 }
 
-// k_global: one CTA.  Bridge (alpha = 1): phi = 1/tau ~ Gamma(a0 + p, b0 + sum|beta|)
-// (gibbs.py:179-190).  Horseshoe: xi | tau ~ IG(1, 1 + 1/tau^2), then
-// tau^2 | beta, lam, xi ~ IG((p+1)/2, 1/xi + sum beta^2 / (2 lam^2)).
-__global__ void __launch_bounds__(1024) k_global(pcgs_gibbs_t G, long long pt, int t) {
+// Partial-sum lines (one 128-byte line per CTA, kPartStride doubles):
+//   [c*16 + 0]  log-likelihood of X beta (CSR pass)
+//   [c*16 + 1]  log-prior terms of the current draw (k_stats)
+//   [c*16 + 2]  sum feeding the next tau update (k_stats / k_tau_sums)
+__device__ __forceinline__ double tau_term(const pcgs_gibbs_t& G, double b, long long k) {
+  if (G.prior == 0) return G.alpha == 1.0 ? fabs(b) : pow(fabs(b), G.alpha);
+  const double l = G.lam[k];
+  return b * b / (l * l);
+}
+
+// partial sums for the tau update from the current beta / lambda (chain start)
+__global__ void __launch_bounds__(256) k_tau_sums(pcgs_gibbs_t G, long long pt) {
   __shared__ double red[64];
   const int q = G.q;
-  const long long p = pt - q;
   double acc = 0.0;
-  for (long long j = threadIdx.x; j < p; j += blockDim.x) {
-    const double b = G.beta[q + j];
-    if (G.prior == 0) {
-      acc += G.alpha == 1.0 ? fabs(b) : pow(fabs(b), G.alpha);
-    } else {
-      const double l = G.lam[j];
-      acc += b * b / (l * l);
-    }
-  }
+  for (long long j = q + blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x)
+    acc += tau_term(G, G.beta[j], j - q);
   acc = block_sum(acc, red);
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) G.part[(long long)blockIdx.x * kPartStride + 2] = acc;
+}
+
+// k_global: one warp.  Bridge: phi = tau^-alpha ~ Gamma(a0 + p/alpha, b0 + sum|beta|^alpha)
+// (gibbs.py:179-190).  Horseshoe: xi | tau ~ IG(1, 1 + 1/tau^2), then
+// tau^2 | beta, lam, xi ~ IG((p+1)/2, 1/xi + sum beta^2 / (2 lam^2)).
+__global__ void __launch_bounds__(32) k_global(pcgs_gibbs_t G, long long pt, int t, int ncta) {
+  const int lane = threadIdx.x;
+  double acc = 0.0;
+  for (int c = lane; c < ncta; c += 32) acc += G.part[(long long)c * kPartStride + 2];
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    const long long p = pt - G.q;
     Philox R(G.seed, kStreamGlobal ^ (unsigned long long)t, 0u);
     double tau;
     if (G.prior == 0) {
@@ -168,37 +180,19 @@ __global__ void k_precond(pcgs_gibbs_t G, long long pt, const double* diag_phi) 
     G.minv[j] = G.precond == 1 ? 1.0 : 1.0 / diag_phi[j];
 }
 
-// k_post: one CTA.  log density (bridge: gibbs.py:217-241; horseshoe: joint
-// density given lambda).
-__global__ void __launch_bounds__(1024) k_post(pcgs_gibbs_t G, long long pt, int t, int ncta) {
-  __shared__ double red[64];
-  const int q = G.q;
-  const long long p = pt - q;
-  const double tau = G.scal[0];
-  double acc = 0.0;
-  for (int c = threadIdx.x; c < ncta; c += blockDim.x) acc += G.part[(long long)c * kPartStride];
-  const double loglik = block_sum(acc, red);
-  double pr = 0.0;
-  for (long long j = threadIdx.x; j < pt; j += blockDim.x) {
-    const double b = G.beta[j];
-    if (j < q) {
-      const double sd = G.usd_sd[j];
-      if (isfinite(sd)) {
-        const double u = b / sd;
-        pr -= 0.5 * u * u + log(sd) + 0.5 * log(2.0 * M_PI);
-      }
-    } else if (G.prior == 0) {
-      pr -= G.alpha == 1.0 ? fabs(b / tau) : pow(fabs(b / tau), G.alpha);
-    } else {
-      const double l = G.lam[j - q];
-      const double sc = tau * l;
-      const double u = b / sc;
-      pr += -log(sc) - 0.5 * u * u - 0.5 * log(2.0 * M_PI) + log(2.0 / M_PI) - log1p(l * l);
-    }
-  }
-  pr = block_sum(pr, red);
-  if (threadIdx.x == 0) {
-    double out = loglik + pr;
+// k_post: one warp.  log density (bridge: gibbs.py:217-241; horseshoe: joint
+// density given lambda) from the partial lines.
+__global__ void __launch_bounds__(32) k_post(pcgs_gibbs_t G, long long pt, int t, int ncta_ll, int ncta_st) {
+  const int lane = threadIdx.x;
+  double ll = 0.0, pr = 0.0;
+  for (int c = lane; c < ncta_ll; c += 32) ll += G.part[(long long)c * kPartStride];
+  for (int c = lane; c < ncta_st; c += 32) pr += G.part[(long long)c * kPartStride + 1];
+  ll = warp_sum(ll);
+  pr = warp_sum(pr);
+  if (lane == 0) {
+    const long long p = pt - G.q;
+    const double tau = G.scal[0];
+    double out = ll + pr;
     if (G.prior == 0) {
       const double a = G.alpha;
       out += (double)p * (log(a) - log(2.0) - lgamma(1.0 / a)) - (double)p * log(tau);
@@ -210,11 +204,14 @@ __global__ void __launch_bounds__(1024) k_post(pcgs_gibbs_t G, long long pt, int
   }
 }
 
-// Welford update of the scaled draws [beta_q, beta/(tau lam)] (gibbs.py:139-167)
-// and the stored draw (gibbs.py:366-369).
-__global__ void k_stats(pcgs_gibbs_t G, long long pt, int count_new, int slot) {
+// Welford update of the scaled draws [beta_q, beta/(tau lam)] (gibbs.py:139-167),
+// the stored draw (gibbs.py:366-369), and per-CTA partials of the log-prior
+// terms of this draw and of the sum the next tau update needs.
+__global__ void __launch_bounds__(256) k_stats(pcgs_gibbs_t G, long long pt, int count_new, int slot) {
+  __shared__ double red[64];
   const int q = G.q;
   const double tau = G.scal[0];
+  double lp = 0.0, ts = 0.0;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x) {
     const double b = G.beta[j];
     const double scaled = j < q ? b : b / (tau * G.lam[j - q]);
@@ -224,6 +221,29 @@ __global__ void k_stats(pcgs_gibbs_t G, long long pt, int count_new, int slot) {
     if (j < q) G.m2[j] += delta * (scaled - m);
     if (slot >= 0) G.draws[(long long)slot * pt + j] = b;
     if (slot >= 0 && j == 0) G.tau_draws[slot] = tau;
+    if (j < q) {
+      const double sd = G.usd_sd[j];
+      if (isfinite(sd)) {
+        const double u = b / sd;
+        lp -= 0.5 * u * u + log(sd) + 0.5 * log(2.0 * M_PI);
+      }
+    } else {
+      const long long k = j - q;
+      if (G.prior == 0) {
+        lp -= G.alpha == 1.0 ? fabs(b / tau) : pow(fabs(b / tau), G.alpha);
+      } else {
+        const double l = G.lam[k];
+        const double sc = tau * l;
+        const double u = b / sc;
+        lp += -log(sc) - 0.5 * u * u - 0.5 * log(2.0 * M_PI) + log(2.0 / M_PI) - log1p(l * l);
+      }
+      ts += tau_term(G, b, k);
+    }
+  }
+  block_sum2(lp, ts, red);
+  if (threadIdx.x == 0) {
+    G.part[(long long)blockIdx.x * kPartStride + 1] = lp;
+    G.part[(long long)blockIdx.x * kPartStride + 2] = ts;
   }
 }
 
@@ -250,6 +270,8 @@ int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream) {
   if (!d || !g || !g->beta || !g->z || !g->y || !g->part) return fail(PCGS_EINVAL, "null argument");
   CUDA_TRY(cudaFuncSetAttribute(k_csr_logit, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem_bytes(d->dev)));
+  k_tau_sums<<<d->dev.G, 256, 0, (cudaStream_t)stream>>>(*g, d->dev.pt);
+  CUDA_TRY(cudaGetLastError());
   return launch_logit(d, g, (cudaStream_t)stream);
 }
 
@@ -260,13 +282,14 @@ int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, 
   cudaStream_t s = (cudaStream_t)stream;
   const long long pt = D.pt;
   const int eblocks = (int)std::min<long long>((pt + 255) / 256, 4 * D.G);
+  const int sblocks = D.G;  // k_stats grid: one partial line per CTA
   int rc;
   // omega | beta (z = X beta of the previous scan)
   if (!g->fixed_omega) {
     if ((rc = pcgs_pg_draw(g->z, D.n, g->seed, (uint64_t)t, g->omega, stream))) return rc;
   }
   // tau | beta, then lambda | beta, tau; prior diagonal, M^-1, metric scale, x0
-  if (!g->fixed_tau) k_global<<<1, 1024, 0, s>>>(*g, pt, t);
+  if (!g->fixed_tau) k_global<<<1, 32, 0, s>>>(*g, pt, t, sblocks);
   k_local<<<eblocks, 256, 0, s>>>(*g, pt, t, count);
   if (g->precond == 2) {
     if ((rc = pcgs_phi_diagonal(d, g->omega, g->prior_diag, g->b, stream))) return rc;
@@ -284,8 +307,8 @@ int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, 
     return rc;
   // z = X beta with the log-likelihood, log density, statistics, stored draw
   if ((rc = launch_logit(d, g, s))) return rc;
-  k_post<<<1, 1024, 0, s>>>(*g, pt, t, D.G);
-  k_stats<<<eblocks, 256, 0, s>>>(*g, pt, count + 1, slot);
+  k_stats<<<sblocks, 256, 0, s>>>(*g, pt, count + 1, slot);
+  k_post<<<1, 32, 0, s>>>(*g, pt, t, D.G, sblocks);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
 }
