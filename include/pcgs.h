@@ -201,6 +201,26 @@ int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream);
 int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count,
                     int32_t slot, pcgs_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Batched independent chains (BASELINE config 4): R chains share
+ * one walk over the index stream (pattern-only SpMM with R right-hand sides).
+ * Vectors are chain-minor: element (j, c) at [j * R + c]; R in {2, 4, 8}.
+ * The design must be created with slab_max <= pcgs_batch_slab_max(R).
+ * ------------------------------------------------------------------------ */
+int pcgs_batch_slab_max(int nchains);
+/* out = X'(Omega_c X v_c) + D_c v_c for every chain c (sampler.py:53-58). */
+int pcgs_batch_phi_apply(pcgs_design_t d, int nchains, const double* omega,
+                         const double* prior_diag, const double* v, double* out,
+                         pcgs_stream_t stream);
+/* Per-chain PCG (cg.py:105-192) in one persistent kernel; chains that finish
+ * are masked.  trace[c*(max_iter+1)+k], alphas/betas[c*max_iter+k],
+ * result[c*4 + {iterations, status, fail_iter, applies}]. */
+int pcgs_batch_pcg(pcgs_design_t d, int nchains, const double* omega,
+                   const double* prior_diag, const double* minv, const double* scale,
+                   const double* b, double* x, int32_t max_iter, double rtol,
+                   double* trace, double* alphas, double* betas, int32_t* result,
+                   pcgs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

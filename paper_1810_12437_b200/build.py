@@ -13,8 +13,9 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpcgs.so"
-SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "store.cpp"]
-HEADERS = [CSRC / "store.h", CSRC / "device.cuh", CSRC / "internal.cuh", ROOT / "include" / "pcgs.h"]
+SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "batched.cu", CSRC / "store.cpp"]
+HEADERS = [CSRC / "store.h", CSRC / "device.cuh", CSRC / "internal.cuh", CSRC / "batched.cuh",
+           ROOT / "include" / "pcgs.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

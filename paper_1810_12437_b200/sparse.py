@@ -291,16 +291,25 @@ class SparseDesignMatrix:
     def has_intercept(self):
         return self.pattern()[2]
 
-    def device_store(self, device=None) -> DesignStore:
+    def device_store(self, device=None, batch=1) -> DesignStore:
+        """The pattern-only store on `device`; `batch` > 1 builds the variant
+        whose slabs leave room for `batch` chain-minor vectors (batched chains)."""
         dev = _lib.cuda_device(device)
-        st = self._stores.get(dev.index)
+        key = (dev.index, int(batch))
+        st = self._stores.get(key)
         if st is None:
             if np.any(self.col_means != 0.0) or np.any(self.col_scales != 1.0):
                 raise NotImplementedError("implicit standardisation is not supported on device yet")
             rp, ci, icpt = self.pattern()
+            slab_max = self.slab_max
+            if batch > 1:
+                cap = _lib.lib().pcgs_batch_slab_max(int(batch))
+                if cap <= 0:
+                    _lib.check(cap)
+                slab_max = min(slab_max, cap) if slab_max else cap
             st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0), rp, ci, icpt,
-                             device=dev, slab_max=self.slab_max)
-            self._stores[dev.index] = st
+                             device=dev, slab_max=slab_max)
+            self._stores[key] = st
         return st
 
     # ------------------------------------------------------------ kernels

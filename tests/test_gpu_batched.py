@@ -1,0 +1,83 @@
+"""Batched independent chains: R right-hand sides share one walk over the
+index stream; every chain must equal its own single-chain oracle solve."""
+import numpy as np
+import pytest
+
+import paper_1810_12437_b200 as pk
+from paper_1810_12437_b200 import batched, synth
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+def chains(d, R, seed, easy=None):
+    rng = np.random.default_rng(seed)
+    om = rng.uniform(0.05, 0.4, (R, d.n))
+    lam = np.abs(rng.standard_cauchy((R, d.p))) + 0.05
+    tau = rng.uniform(0.02, 0.2, R)
+    if easy is not None:
+        tau[easy] = 1e-3          # prior-dominated chain: converges in a few iterations
+    diag = np.concatenate([np.zeros((R, 1)), (tau[:, None] * lam) ** -2.0], axis=1)
+    minv = np.concatenate([np.full((R, 1), 100.0), (tau[:, None] * lam) ** 2], axis=1)
+    return om, diag, minv
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_batched_phi_matches_oracle_per_chain(R):
+    d = synth.binary_design(1500, 300, 1e-3, 0.3, seed=2)
+    X = d.matrix()
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    om, diag, _ = chains(d, R, 1)
+    V = np.random.default_rng(3).standard_normal((R, d.p + 1))
+    op = batched.BatchedPrecisionOperator(X, om, diag)
+    out = op.apply(V)
+    for c in range(R):
+        ref = port.phi_apply(Xo, om[c], diag[c], V[c])
+        assert np.linalg.norm(out[c] - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("R", [2, 4])
+def test_batched_pcg_matches_single_chain(R):
+    d = synth.binary_design(2000, 400, 1e-3, 0.25, seed=5)
+    X = d.matrix()
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    om, diag, minv = chains(d, R, 7, easy=0)
+    rng = np.random.default_rng(9)
+    B = np.stack([port.rhs(Xo, np.zeros(d.p + 1), om[c], diag[c], rng) for c in range(R)])
+    op = batched.BatchedPrecisionOperator(X, om, diag)
+    reps = batched.batched_pcg_solve(op, B, minv, np.sqrt(minv), config=pk.CGConfig(rtol=1e-10))
+    its = []
+    for c in range(R):
+        ref = port.pcg(lambda v: port.phi_apply(Xo, om[c], diag[c], v), B[c], minv[c], np.sqrt(minv[c]),
+                       rtol=1e-10)
+        assert np.linalg.norm(reps[c].solution - ref.x) / np.linalg.norm(ref.x) < 1e-8
+        assert abs(reps[c].iterations - ref.iterations) <= max(2, int(0.08 * ref.iterations))
+        assert reps[c].termination == "converged"
+        assert len(reps[c].rms_precond_residual_trace) == reps[c].iterations + 1
+        its.append(reps[c].iterations)
+    assert its[0] < max(its)     # the easy chain stopped early while the others kept going
+
+
+def test_batched_config2_phi_vs_single():
+    d = synth.config_design(2, seed=0)
+    X = d.matrix()
+    om, diag, _ = chains(d, 4, 11)
+    V = np.random.default_rng(1).standard_normal((4, d.p + 1))
+    out = batched.BatchedPrecisionOperator(X, om, diag).apply(V)
+    for c in range(4):
+        ref = pk.PrecisionOperator(X, om[c], diag[c]).apply(V[c])
+        assert np.linalg.norm(out[c] - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_batch_size_validation():
+    d = synth.binary_design(100, 20, 0.01, 0.3, seed=1)
+    with pytest.raises(ValueError):
+        batched.BatchedPrecisionOperator(d.matrix(), np.ones((3, 100)), np.ones((3, 21)))
+
+
+def test_batch_of_eight_reports_unsupported_pcg_cleanly():
+    d = synth.config_design(2, seed=0)
+    om, diag, minv = chains(d, 8, 1)
+    op = batched.BatchedPrecisionOperator(d.matrix(), om, diag)
+    with pytest.raises(NotImplementedError):
+        batched.batched_pcg_solve(op, np.ones((8, d.p + 1)), minv, np.sqrt(minv))
