@@ -120,6 +120,14 @@ int pcgs_pcg(pcgs_design_t d, const double* omega, const double* prior_diag,
              int32_t max_iter, double rtol, double* trace, double* alphas,
              double* betas, int32_t* result, pcgs_stream_t stream);
 
+/* pcgs_pcg with trace_level "full" (cg.py:143-146, 167-169): iterates
+ * [max_iter+1][p_total] (device, reference layout) receives x0 and every
+ * iterate; NULL = off. */
+int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag,
+                  const double* minv, const double* scale, const double* b, double* x,
+                  int32_t max_iter, double rtol, double* trace, double* alphas,
+                  double* betas, double* iterates, int32_t* result, pcgs_stream_t stream);
+
 /* Generic-operator PCG (pcg_solve with a duck-typed operator, cg.py:105-113):
  * the same loop, vector algebra on device, Phi supplied by a callback
  * fn(ctx, v, out) on device buffers of length p (returns 0 on success).
@@ -134,6 +142,13 @@ int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv,
                 double* adbuf, int32_t max_iter, double rtol, double* trace_h,
                 double* alphas_h, double* betas_h, int32_t* result_h,
                 pcgs_stream_t stream);
+
+/* pcgs_pcg_op with trace_level "full": iterates [max_iter+1][p] (device). */
+int pcgs_pcg_op_full(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv,
+                     const double* scale, const double* b, double* x, double* dbuf,
+                     double* adbuf, int32_t max_iter, double rtol, double* trace_h,
+                     double* alphas_h, double* betas_h, double* iterates,
+                     int32_t* result_h, pcgs_stream_t stream);
 
 /* Synchronous copy helper for operator callbacks: kind 0 host->device,
  * 1 device->host, 2 device->device. */
@@ -200,6 +215,14 @@ int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream);
  * row of `draws` to store this scan in, or -1. */
 int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count,
                     int32_t slot, pcgs_stream_t stream);
+/* The same scan in two halves, for a host-side local-scale update between
+ * them (gibbs_run's local_scale_sampler hook, gibbs.py:262, 311, 328-329):
+ * begin = omega and tau; end = lambda (unless fixed_lam), RHS, PCG, X beta,
+ * statistics, log density. */
+int pcgs_gibbs_scan_begin(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t,
+                          pcgs_stream_t stream);
+int pcgs_gibbs_scan_end(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count,
+                        int32_t slot, pcgs_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Batched independent chains (BASELINE config 4): R chains share

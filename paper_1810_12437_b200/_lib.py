@@ -53,6 +53,9 @@ SIGNATURES = {
     "pcgs_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
     "pcgs_pcg_op": (ctypes.c_int, [APPLY_FN, _P, _I64, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P,
                                    _P, _P, _P]),
+    "pcgs_pcg_full": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P, _P]),
+    "pcgs_pcg_op_full": (ctypes.c_int, [APPLY_FN, _P, _I64, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P,
+                                        _P, _P, _P, _P]),
     "pcgs_copy": (ctypes.c_int, [_P, _P, _I64, ctypes.c_int]),
     "pcgs_debug_profile": (ctypes.c_int, [_P]),
     "pcgs_debug_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
@@ -64,6 +67,8 @@ SIGNATURES = {
     "pcgs_batch_pcg": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P,
                                       _P, _P]),
     "pcgs_gibbs_scan": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P]),
+    "pcgs_gibbs_scan_begin": (ctypes.c_int, [_P, _P, _I32, _P]),
+    "pcgs_gibbs_scan_end": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P]),
 }
 
 

@@ -117,7 +117,7 @@ def _is_device_operator(phi):
     return getattr(phi, "_pcgs_device_operator", False)
 
 
-def pcg_solve_device(phi, b, minv, scale, x0=None, max_iter=None, rtol=1e-6):
+def pcg_solve_device(phi, b, minv, scale, x0=None, max_iter=None, rtol=1e-6, full=False):
     """Fused device solve on tensors.  Returns (x, trace, alphas, betas, result) tensors.
 
     `phi` must be a device PrecisionOperator; b, minv, scale, x0 are CUDA
@@ -135,19 +135,26 @@ def pcg_solve_device(phi, b, minv, scale, x0=None, max_iter=None, rtol=1e-6):
     alphas = t.empty(max_iter, dtype=t.float64, device=dev)
     betas = t.empty(max_iter, dtype=t.float64, device=dev)
     result = t.zeros(4, dtype=t.int32, device=dev)
+    iterates = t.empty((max_iter + 1, p), dtype=t.float64, device=dev) if full else None
     omega, diag = phi.device_omega(), phi.device_diag()
-    _lib.check(_lib.lib().pcgs_pcg(st.handle, _lib.ptr(omega), _lib.ptr(diag), _lib.ptr(minv),
-                                   _lib.ptr(scale), _lib.ptr(b), _lib.ptr(x), max_iter, float(rtol),
-                                   _lib.ptr(trace), _lib.ptr(alphas), _lib.ptr(betas),
-                                   _lib.ptr(result), _lib.stream_ptr(dev)))
+    _lib.check(_lib.lib().pcgs_pcg_full(st.handle, _lib.ptr(omega), _lib.ptr(diag), _lib.ptr(minv),
+                                        _lib.ptr(scale), _lib.ptr(b), _lib.ptr(x), max_iter, float(rtol),
+                                        _lib.ptr(trace), _lib.ptr(alphas), _lib.ptr(betas),
+                                        _lib.ptr(iterates), _lib.ptr(result), _lib.stream_ptr(dev)))
+    if full:
+        return x, trace, alphas, betas, result, iterates
     return x, trace, alphas, betas, result
 
 
-def _report_from_device(x, trace, alphas, betas, result, as_tensor=False):
+def _report_from_device(x, trace, alphas, betas, result, iterates=None, as_tensor=False):
     res = result.cpu().numpy()
     iterations, status, fail_iter, applies = (int(v) for v in res)
     _raise_status(status, fail_iter)
     nb = _n_betas(iterations, status)
+    its = None
+    if iterates is not None:
+        h = iterates[: iterations + 1].cpu().numpy()
+        its = [h[k].copy() for k in range(iterations + 1)]
     return CGReport(
         iterations=iterations,
         termination="converged" if status == _lib.PCGS_CONVERGED else "max_iter",
@@ -156,7 +163,7 @@ def _report_from_device(x, trace, alphas, betas, result, as_tensor=False):
         matvec_count=applies,
         alphas=alphas[:iterations].cpu().numpy(),
         betas=betas[:nb].cpu().numpy(),
-        iterates=None,
+        iterates=its,
     )
 
 
@@ -169,8 +176,7 @@ def pcg_solve(phi, b, M, x0=None, config=None, residual_scale=None):
     cfg = config if config is not None else CGConfig()
     if not isinstance(M, Preconditioner) and getattr(M, "kind", None) is PreconditionerKind.BLOCK_THRESHOLD:
         raise NotImplementedError("block-threshold preconditioning is not on the device path")
-    if cfg.trace_level == "full":
-        raise NotImplementedError("trace_level='full' (per-iteration iterates) is not on the device path yet")
+    full = cfg.trace_level == "full"
     as_tensor = _lib.is_tensor(b)
     p = int(b.shape[0])
     max_iter = cfg.max_iter if cfg.max_iter is not None else 2 * p
@@ -183,17 +189,18 @@ def pcg_solve(phi, b, M, x0=None, config=None, residual_scale=None):
         bd = _lib.to_device(b, dev)
         x0d = None if x0 is None else _lib.to_device(x0, dev)
         out = pcg_solve_device(phi, bd, _lib.to_device(minv, dev), _lib.to_device(scale, dev),
-                               x0=x0d, max_iter=max_iter, rtol=cfg.rtol)
+                               x0=x0d, max_iter=max_iter, rtol=cfg.rtol, full=full)
         phi.apply_count += int(out[4][3].item())
         return _report_from_device(*out, as_tensor=as_tensor)
-    return _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, cfg.rtol, as_tensor)
+    return _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, cfg.rtol, as_tensor, full)
 
 
-def _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, rtol, as_tensor):
+def _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, rtol, as_tensor, full=False):
     """Generic operator: device vector algebra + host callback per application."""
     t = _lib.torch()
     L = _lib.lib()
-    dev = _lib.cuda_device(b.device if as_tensor and b.is_cuda else None)
+    dev = _lib.cuda_device(b.device if as_tensor and b.is_cuda else
+                           (phi.store.device if hasattr(phi, "store") else None))
     apply_phi = phi.apply if hasattr(phi, "apply") else phi
     p = int(b.shape[0])
     bd = _lib.to_device(b, dev)
@@ -214,15 +221,33 @@ def _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, rtol, as_tensor):
             errors.append(exc)
             return 1
 
+    dbuf = adbuf = None
+    if hasattr(phi, "apply_into"):
+        # device-side operator: apply on the engine's own buffers, no host copies
+        dbuf = t.empty(p, dtype=t.float64, device=dev)
+        adbuf = t.empty(p, dtype=t.float64, device=dev)
+        xptr = _lib.ptr(x)
+
+        def cb(ctx, vptr, outptr):  # noqa: F811
+            try:
+                phi.apply_count = getattr(phi, "apply_count", 0) + 1
+                phi.apply_into(x if vptr == xptr else dbuf, adbuf)
+                return 0
+            except BaseException as exc:
+                errors.append(exc)
+                return 1
+
     fn = _lib.APPLY_FN(cb)
     trace = np.zeros(max_iter + 1)
     alphas = np.zeros(max_iter)
     betas = np.zeros(max_iter)
     result = np.zeros(4, dtype=np.int32)
+    iterates = t.empty((max_iter + 1, p), dtype=t.float64, device=dev) if full else None
     t.cuda.synchronize(dev)
-    rc = L.pcgs_pcg_op(fn, None, p, _lib.ptr(md), _lib.ptr(sd), _lib.ptr(bd), _lib.ptr(x), None, None,
-                       max_iter, float(rtol), trace.ctypes.data, alphas.ctypes.data, betas.ctypes.data,
-                       result.ctypes.data, _lib.stream_ptr(dev))
+    rc = L.pcgs_pcg_op_full(fn, None, p, _lib.ptr(md), _lib.ptr(sd), _lib.ptr(bd), _lib.ptr(x),
+                            _lib.ptr(dbuf), _lib.ptr(adbuf),
+                            max_iter, float(rtol), trace.ctypes.data, alphas.ctypes.data, betas.ctypes.data,
+                            _lib.ptr(iterates), result.ctypes.data, _lib.stream_ptr(dev))
     if errors:
         raise errors[0]
     _lib.check(rc)
@@ -237,7 +262,8 @@ def _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, rtol, as_tensor):
         matvec_count=applies,
         alphas=alphas[:iterations].copy(),
         betas=betas[:nb].copy(),
-        iterates=None,
+        iterates=(None if iterates is None else
+                  [r.copy() for r in iterates[: iterations + 1].cpu().numpy()]),
     )
 
 

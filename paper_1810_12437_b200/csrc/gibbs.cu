@@ -275,8 +275,22 @@ int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream) {
   return launch_logit(d, g, (cudaStream_t)stream);
 }
 
-int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, int32_t slot,
-                    pcgs_stream_t stream) {
+int pcgs_gibbs_scan_begin(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, pcgs_stream_t stream) {
+  if (!d || !g || t < 1) return fail(PCGS_EINVAL, "bad argument");
+  const DesignDev& D = d->dev;
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  // omega | beta (z = X beta of the previous scan), then tau | beta
+  if (!g->fixed_omega) {
+    if ((rc = pcgs_pg_draw(g->z, D.n, g->seed, (uint64_t)t, g->omega, stream))) return rc;
+  }
+  if (!g->fixed_tau) k_global<<<1, 32, 0, s>>>(*g, D.pt, t, D.G);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+int pcgs_gibbs_scan_end(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, int32_t slot,
+                        pcgs_stream_t stream) {
   if (!d || !g || t < 1) return fail(PCGS_EINVAL, "bad argument");
   const DesignDev& D = d->dev;
   cudaStream_t s = (cudaStream_t)stream;
@@ -284,12 +298,7 @@ int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, 
   const int eblocks = (int)std::min<long long>((pt + 255) / 256, 4 * D.G);
   const int sblocks = D.G;  // k_stats grid: one partial line per CTA
   int rc;
-  // omega | beta (z = X beta of the previous scan)
-  if (!g->fixed_omega) {
-    if ((rc = pcgs_pg_draw(g->z, D.n, g->seed, (uint64_t)t, g->omega, stream))) return rc;
-  }
-  // tau | beta, then lambda | beta, tau; prior diagonal, M^-1, metric scale, x0
-  if (!g->fixed_tau) k_global<<<1, 32, 0, s>>>(*g, pt, t, sblocks);
+  // lambda | beta, tau; prior diagonal, M^-1, metric scale, x0
   k_local<<<eblocks, 256, 0, s>>>(*g, pt, t, count);
   if (g->precond == 2) {
     if ((rc = pcgs_phi_diagonal(d, g->omega, g->prior_diag, g->b, stream))) return rc;
@@ -305,12 +314,19 @@ int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, 
   if ((rc = pcgs_pcg(d, g->omega, g->prior_diag, g->minv, g->scale, g->b, g->beta, g->max_iter, g->rtol, g->trace,
                      g->alphas, g->betas, g->results + 8 * (t - 1), stream)))
     return rc;
-  // z = X beta with the log-likelihood, log density, statistics, stored draw
+  // z = X beta with the log-likelihood, statistics, stored draw, log density
   if ((rc = launch_logit(d, g, s))) return rc;
   k_stats<<<sblocks, 256, 0, s>>>(*g, pt, count + 1, slot);
   k_post<<<1, 32, 0, s>>>(*g, pt, t, D.G, sblocks);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
+}
+
+int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, int32_t slot,
+                    pcgs_stream_t stream) {
+  int rc = pcgs_gibbs_scan_begin(d, g, t, stream);
+  if (rc) return rc;
+  return pcgs_gibbs_scan_end(d, g, t, count, slot, stream);
 }
 
 }  // extern "C"

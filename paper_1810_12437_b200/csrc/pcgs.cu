@@ -141,6 +141,7 @@ struct PcgArgs {
   double* part;    // 4 * G partial sums: dAd, rms, rz, spare
   unsigned long long* prof;  // optional: CTA-0 phase timestamps (ns), 4 per apply
   int tma_dir;     // 1: owners publish the direction, grid sync, TMA fill
+  double* iterates;  // optional (trace_level "full"): [max_iter+1][p_total], reference layout
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
         dg = __ldg(A.diag + rj);
         bv = __ldg(A.b + rj);
         A.dvg[dvs + j] = xv;  // v = x0 for the first application
+        if (A.iterates) A.iterates[rj] = xv;
       }
       o.x[t] = xv;
       o.r[t] = 0.0;
@@ -411,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       } else {
         o.x[t] = fma(alpha, o.d[t], o.x[t]);
         rv = fma(-alpha, Ad, o.r[t]);
+        if (A.iterates) A.iterates[(long long)a * pt + ref_index(j0 + t, A.D.p, A.D.icpt)] = o.x[t];
       }
       o.r[t] = rv;
       const double zn = o.m[t] * rv;
@@ -728,6 +731,13 @@ int pcgs_rhs(pcgs_design_t d, const double* kappa, const double* omega, const do
 int pcgs_pcg(pcgs_design_t d, const double* omega, const double* prior_diag, const double* minv, const double* scale,
              const double* b, double* x, int32_t max_iter, double rtol, double* trace, double* alphas, double* betas,
              int32_t* result, pcgs_stream_t stream) {
+  return pcgs_pcg_full(d, omega, prior_diag, minv, scale, b, x, max_iter, rtol, trace, alphas, betas, nullptr, result,
+                       stream);
+}
+
+int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag, const double* minv,
+                  const double* scale, const double* b, double* x, int32_t max_iter, double rtol, double* trace,
+                  double* alphas, double* betas, double* iterates, int32_t* result, pcgs_stream_t stream) {
   if (!d || !omega || !prior_diag || !minv || !scale || !b || !x || !trace || !alphas || !betas || !result)
     return fail(PCGS_EINVAL, "null argument");
   if (max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
@@ -756,6 +766,7 @@ int pcgs_pcg(pcgs_design_t d, const double* omega, const double* prior_diag, con
   A.part = S.get<double>((size_t)kPartStride * D.G);
   A.prof = g_prof;
   A.tma_dir = g_tma_dir;
+  A.iterates = iterates;
   if (!A.w || !A.pieces || !A.zv || !A.dvg || !A.part || (D.csr.nslab > 1 && !A.zpart))
     return fail(PCGS_ENOMEM, "scratch allocation failed");
   void* args[] = {&A};
@@ -818,6 +829,14 @@ __global__ void __launch_bounds__(kThreads) k_opvec(int mode, long long p, doubl
 int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, const double* scale, const double* b,
                 double* x, double* dbuf, double* adbuf, int32_t max_iter, double rtol, double* trace_h,
                 double* alphas_h, double* betas_h, int32_t* result_h, pcgs_stream_t stream) {
+  return pcgs_pcg_op_full(fn, ctx, p, minv, scale, b, x, dbuf, adbuf, max_iter, rtol, trace_h, alphas_h, betas_h,
+                          nullptr, result_h, stream);
+}
+
+int pcgs_pcg_op_full(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, const double* scale,
+                     const double* b, double* x, double* dbuf, double* adbuf, int32_t max_iter, double rtol,
+                     double* trace_h, double* alphas_h, double* betas_h, double* iterates, int32_t* result_h,
+                     pcgs_stream_t stream) {
   if (!fn || p < 1 || !minv || !scale || !b || !x || !trace_h || !alphas_h || !betas_h || !result_h)
     return fail(PCGS_EINVAL, "null argument");
   if (max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
@@ -848,6 +867,7 @@ int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, cons
   int rc;
   int applies = 0, k = 0;
   result_h[2] = -1;
+  if (iterates) CUDA_TRY(cudaMemcpyAsync(iterates, x, p * sizeof(double), cudaMemcpyDeviceToDevice, s));
   if ((rc = apply(x))) return rc;
   ++applies;
   if ((rc = run(0, 0.0, sc))) return rc;
@@ -874,6 +894,8 @@ int pcgs_pcg_op(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv, cons
     const double alpha = rz / dAd;
     alphas_h[k - 1] = alpha;
     if ((rc = run(3, alpha, sc))) return rc;
+    if (iterates)
+      CUDA_TRY(cudaMemcpyAsync(iterates + (size_t)k * p, x, p * sizeof(double), cudaMemcpyDeviceToDevice, s));
     rms = std::sqrt(h2[0] / (double)p);
     trace_h[k] = rms;
     if (rms <= rtol) return finish(PCGS_CONVERGED, -1);

@@ -264,17 +264,40 @@ class DeviceChain:
         L.pcgs_gibbs_init.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_void_p]
         L.pcgs_gibbs_scan.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_int32,
                                       ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+        L.pcgs_gibbs_scan_begin.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_int32,
+                                            ctypes.c_void_p]
+        L.pcgs_gibbs_scan_end.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
         _lib.check(L.pcgs_gibbs_init(st.handle, ctypes.byref(self.args), _lib.stream_ptr(dev)))
 
-    def scan(self, t):
-        """Issue scan t (1-based) on the current stream; no synchronisation."""
+    def scan(self, t, local_scale_sampler=None, rng=None):
+        """Issue scan t (1-based) on the current stream; no synchronisation
+        unless a host `local_scale_sampler` has to see beta and tau."""
         slot = -1
         if t > self.burn_in and (t - self.burn_in - 1) % self.thin == 0:
             slot = self.stored
             self.stored += 1
-        _lib.check(_lib.lib().pcgs_gibbs_scan(self.store.handle, ctypes.byref(self.args), int(t),
-                                              int(self.count), int(slot),
-                                              _lib.stream_ptr(self.dev)))
+        L = _lib.lib()
+        s = _lib.stream_ptr(self.dev)
+        if local_scale_sampler is None:
+            _lib.check(L.pcgs_gibbs_scan(self.store.handle, ctypes.byref(self.args), int(t),
+                                         int(self.count), int(slot), s))
+        else:
+            _lib.check(L.pcgs_gibbs_scan_begin(self.store.handle, ctypes.byref(self.args), int(t), s))
+            torch = _lib.torch()
+            torch.cuda.current_stream(self.dev).synchronize()
+            beta = self.beta.cpu().numpy()
+            tau = float(self.scal[0].item())
+            lam = np.asarray(local_scale_sampler(beta[self.q:], tau, self.cfg, rng), dtype=np.float64)
+            if lam.shape != (self.p,):
+                raise ValueError("local_scale_sampler must return one scale per shrunk coefficient")
+            self.lam.copy_(torch.from_numpy(lam))
+            self.args.fixed_lam = 1
+            try:
+                _lib.check(L.pcgs_gibbs_scan_end(self.store.handle, ctypes.byref(self.args), int(t),
+                                                 int(self.count), int(slot), s))
+            finally:
+                self.args.fixed_lam = 0
         self.count += 1
 
     def check(self, t_lo, t_hi, allow_max_iter=False):
@@ -318,7 +341,9 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
     """Run `n_iter` scans on the GPU (gibbs.py:260-379); same arguments and output.
 
     `sampler`/`burn_in_sampler` must be "cg" (the dense Cholesky sampler is the
-    CPU oracle's); `local_scale_sampler` is not supported on the device path.
+    CPU oracle's).  A `local_scale_sampler(beta_shrunk, tau, cfg, rng)` runs on
+    the host between the two halves of each scan (one synchronisation per
+    scan), with a numpy Generator seeded from `seed`.
     """
     y = np.asarray(y, dtype=np.float64)
     if y.shape != (X.n_rows,):
@@ -341,9 +366,11 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
     q = cfg.n_unshrunk
     if X.n_cols - q < 0:
         raise ValueError("more unshrunk prior sds than design columns")
-    if local_scale_sampler is not None:
-        raise NotImplementedError("custom local_scale_sampler callbacks are not on the device path")
-    if isinstance(cfg, BridgeConfig) and cfg.alpha != 1.0 and fixed_lam is None:
+    if X.standardized:
+        raise NotImplementedError("the device Gibbs scan runs on raw binary designs; "
+                                  "standardised designs are supported by the operator / pcg_solve API")
+    if (isinstance(cfg, BridgeConfig) and cfg.alpha != 1.0 and fixed_lam is None
+            and local_scale_sampler is None):
         raise UnsupportedUpdateError(
             "exact local-scale draws exist for alpha = 1 only; pin fixed_lam for other exponents")
     ch = DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=seed,
@@ -352,8 +379,9 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
                      fixed_lam=fixed_lam, device=device)
     torch = _lib.torch()
     checked = 0
+    host_rng = np.random.default_rng(seed) if local_scale_sampler is not None else None
     for t in range(1, n_iter + 1):
-        ch.scan(t)
+        ch.scan(t, local_scale_sampler, host_rng)
         if on_progress is not None:
             torch.cuda.current_stream(ch.dev).synchronize()
             ch.check(t, t, allow_max_iter)

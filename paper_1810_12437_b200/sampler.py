@@ -44,9 +44,11 @@ class PhiloxGenerator:
 
 
 class PrecisionOperator:
-    """Matrix-free Phi on the GPU (sampler.py:24-67)."""
+    """Matrix-free Phi on the GPU (sampler.py:24-67).
 
-    _pcgs_device_operator = True
+    Raw binary designs use the fused kernels (`pcgs_phi_apply`, and the
+    persistent PCG kernel in `pcg_solve`); standardised designs compose the raw
+    passes with the rank-one correction on device (`apply_into`)."""
 
     def __init__(self, X: SparseDesignMatrix, omega, prior_precision_diag):
         as_tensor = _lib.is_tensor(omega)
@@ -87,6 +89,20 @@ class PrecisionOperator:
         return self.X.n_cols
 
     @property
+    def _pcgs_device_operator(self):
+        return not self.X.standardized
+
+    def apply_into(self, v, out):
+        """out = Phi v on CUDA tensors (any design, incl. standardised)."""
+        if not self.X.standardized:
+            return self.store.phi_apply(self.device_omega(), self.device_diag(), v, out)
+        z = self.X.device_matvec(v)
+        z *= self.device_omega()
+        out.copy_(self.X.device_matvec_t(z))
+        out.addcmul_(self.device_diag(), v)
+        return out
+
+    @property
     def store(self):
         dev = self._dev.get("omega")
         return self.X.device_store(dev.device if dev is not None else None)
@@ -112,7 +128,10 @@ class PrecisionOperator:
             raise ValueError("vector length must equal the operator dimension")
         self.apply_count += 1
         st = self.store
-        out = st.phi_apply(self.device_omega(), self.device_diag(), _lib.to_device(v, st.device))
+        t = _lib.torch()
+        vd = _lib.to_device(v, st.device)
+        out = t.empty_like(vd)
+        self.apply_into(vd, out)
         return out if as_tensor else out.cpu().numpy()
 
     def dense_matrix(self, dense_cap=None):
@@ -168,6 +187,15 @@ def generate_rhs(target: GaussianTarget, rng) -> np.ndarray:
         eta_d, delta_d = _lib.to_device(eta, dev), _lib.to_device(delta, dev)
         seed, sid = 0, 0
     lin = _lib.to_device(target.linear_term, dev)
+    if phi.X.standardized:   # X_s' = S^-1 (X' - mu 1'): compose on device
+        if eta_d is None:
+            g = t.Generator(device=dev)
+            g.manual_seed((seed ^ sid) & (2 ** 63 - 1))
+            eta_d = t.randn(n, generator=g, dtype=t.float64, device=dev)
+            delta_d = t.randn(p, generator=g, dtype=t.float64, device=dev)
+        b = lin + phi.X.device_matvec_t(phi.device_omega().sqrt() * eta_d)
+        b += phi.device_diag().sqrt() * delta_d
+        return b if _lib.is_tensor(target.linear_term) else b.cpu().numpy()
     b = t.empty(p, dtype=t.float64, device=dev)
     _lib.check(_lib.lib().pcgs_rhs(st.handle, 0, _lib.ptr(phi.device_omega()),
                                    _lib.ptr(phi.device_diag()), _lib.ptr(lin), _lib.ptr(eta_d),

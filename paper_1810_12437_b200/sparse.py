@@ -269,8 +269,6 @@ class SparseDesignMatrix:
         if not np.all(self._values == 1.0):
             raise NotImplementedError(
                 "the B200 store is pattern-only: every stored value must be 1.0 (binary design)")
-        if np.any(self.col_means != 0.0) or np.any(self.col_scales != 1.0):
-            raise NotImplementedError("implicit standardisation is not supported on device yet")
         rp, ci, n = self._row_ptr, self._col_idx, self.n_rows
         counts = np.diff(rp)
         icpt = False
@@ -298,8 +296,6 @@ class SparseDesignMatrix:
         key = (dev.index, int(batch))
         st = self._stores.get(key)
         if st is None:
-            if np.any(self.col_means != 0.0) or np.any(self.col_scales != 1.0):
-                raise NotImplementedError("implicit standardisation is not supported on device yet")
             rp, ci, icpt = self.pattern()
             slab_max = self.slab_max
             if batch > 1:
@@ -322,7 +318,7 @@ class SparseDesignMatrix:
             raise ValueError("matvec: vector length must equal n_cols")
         self.matvec_calls += 1
         st = self.device_store(v.device if as_tensor and v.is_cuda else None)
-        out = st.matvec(_lib.to_device(v, st.device))
+        out = self.device_matvec(_lib.to_device(v, st.device))
         return out if as_tensor else out.cpu().numpy()
 
     def matvec_t(self, w):
@@ -334,8 +330,80 @@ class SparseDesignMatrix:
             raise ValueError("matvec_t: vector length must equal n_rows")
         self.matvec_t_calls += 1
         st = self.device_store(w.device if as_tensor and w.is_cuda else None)
-        out = st.matvec_t(_lib.to_device(w, st.device))
+        out = self.device_matvec_t(_lib.to_device(w, st.device))
         return out if as_tensor else out.cpu().numpy()
+
+    # ------------------------------------------------------------ standardisation
+    @property
+    def standardized(self):
+        return bool(np.any(self.col_means != 0.0) or np.any(self.col_scales != 1.0))
+
+    def _std_tensors(self, dev):
+        key = ("std", dev.index)
+        cache = self._stores.get(key)
+        if cache is None or cache[0] is not self.col_means or cache[1] is not self.col_scales:
+            cache = (self.col_means, self.col_scales, _lib.to_device(self.col_means, dev),
+                     _lib.to_device(self.col_scales, dev))
+            self._stores[key] = cache
+        return cache[2], cache[3]
+
+    def device_matvec(self, v):
+        """X v on a CUDA tensor: raw pattern pass (+ the rank-one shift of
+        sparse.py:188-193 when standardised)."""
+        st = self.device_store(v.device)
+        if not self.standardized:
+            return st.matvec(v)
+        mu, sc = self._std_tensors(st.device)
+        u = v / sc
+        out = st.matvec(u)
+        out -= (mu * u).sum()
+        return out
+
+    def device_matvec_t(self, w):
+        """X' w on a CUDA tensor (+ the correction of sparse.py:203)."""
+        st = self.device_store(w.device)
+        raw = st.matvec_t(w)
+        if not self.standardized:
+            return raw
+        mu, sc = self._std_tensors(st.device)
+        return (raw - w.sum() * mu) / sc
+
+    def standardize(self, exclude=None):
+        """Centre and scale columns (sparse.py:250-297), host-side setup.
+
+        For a binary design a column's sum and sum of squares are its count.
+        """
+        if self.n_rows < 2:
+            raise ValueError("standardize needs at least 2 rows")
+        keep = np.ones(self.n_cols, dtype=bool)
+        if exclude is not None:
+            exclude = np.asarray(exclude)
+            if exclude.dtype == bool:
+                if exclude.shape != (self.n_cols,):
+                    raise ValueError("boolean exclude mask must have length n_cols")
+                keep &= ~exclude
+            else:
+                keep[exclude] = False
+        vals = self.values
+        col = self.col_idx
+        n = self.n_rows
+        col_sum = np.bincount(col, weights=vals, minlength=self.n_cols)
+        col_sq = np.bincount(col, weights=vals ** 2, minlength=self.n_cols)
+        col_nnz = np.bincount(col, minlength=self.n_cols)
+        mean = col_sum / n
+        ssq = np.bincount(col, weights=(vals - mean[col]) ** 2, minlength=self.n_cols)
+        ssq += (n - col_nnz) * mean ** 2
+        var = ssq / (n - 1)
+        constant = ssq <= (n - 1) * 1e-14 * np.maximum(col_sq / n, 1e-300)
+        self.constant_columns = np.flatnonzero(constant & keep)
+        active = keep & ~constant
+        means = np.zeros(self.n_cols)
+        scales = np.ones(self.n_cols)
+        means[active] = mean[active]
+        scales[active] = np.sqrt(var[active])
+        self.col_means = means
+        self.col_scales = scales
+        return self
 
     def gram_diagonal(self, omega):
         """diag(X' diag(omega) X) (sparse.py:235-246): for a binary design, X' omega."""
@@ -347,7 +415,11 @@ class SparseDesignMatrix:
         st = self.device_store(omega.device if as_tensor and omega.is_cuda else None)
         t = _lib.torch()
         zero = t.zeros(st.p_total, dtype=t.float64, device=st.device)
-        out = st.phi_diagonal(_lib.to_device(omega, st.device), zero)
+        om = _lib.to_device(omega, st.device)
+        out = st.phi_diagonal(om, zero)   # binary: sum_i omega_i x_ij^2 = sum_i omega_i x_ij
+        if self.standardized:
+            mu, sc = self._std_tensors(st.device)
+            out = (out - 2.0 * mu * out + om.sum() * mu * mu) / (sc * sc)
         return out if as_tensor else out.cpu().numpy()
 
     # ------------------------------------------------------------ host views (tests)

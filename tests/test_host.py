@@ -81,10 +81,17 @@ class TestPatternLayout:
         with pytest.raises(NotImplementedError):
             X.pattern()
 
-    def test_standardised_design_is_refused_by_the_store(self):
-        X = pk.SparseDesignMatrix(2, 2, [0, 1, 2], [0, 1], [1.0, 1.0], col_means=[0.5, 0.5])
-        with pytest.raises(NotImplementedError):
-            X.pattern()
+    def test_standardize_matches_column_moments(self):
+        d = synth.binary_design(300, 40, 0.01, 0.5, seed=2)
+        X = d.matrix()
+        dense = X.to_dense_raw()
+        X.standardize(exclude=[0])
+        col = dense[:, 1:]
+        keep = col.std(axis=0, ddof=1) > 0
+        np.testing.assert_allclose(X.col_means[1:][keep], col.mean(axis=0)[keep], rtol=1e-13)
+        np.testing.assert_allclose(X.col_scales[1:][keep], col.std(axis=0, ddof=1)[keep], rtol=1e-12)
+        assert X.col_means[0] == 0.0 and X.col_scales[0] == 1.0
+        assert X.standardized and X.pattern()[2]   # the store keeps the raw pattern
 
 
 class TestSolverConfig:
