@@ -63,6 +63,12 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h,
                        const int32_t* col_idx_h, int intercept, int slab_max,
                        int device, pcgs_design_t* out);
 int pcgs_design_destroy(pcgs_design_t d);
+/* Bench/test utility: native synthetic binary design (log-uniform column
+ * rates, Binomial row counts; BASELINE config 5 scale).  Call once with
+ * col_idx_h = NULL to generate and receive row_ptr_h[n+1] and *nnz_h, then
+ * again with a col_idx_h buffer of capacity `cap` to receive the columns. */
+int pcgs_synth_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint64_t seed,
+                      int64_t* row_ptr_h, int32_t* col_idx_h, int64_t cap, int64_t* nnz_h);
 /* Host-only: builds the store for a grid of `grid` CTAs and verifies that both
  * tiled passes reproduce the input pattern exactly (no GPU needed).
  * stats_h[8]: csr slabs, csc slabs, csr vectors, csc vectors, csc pieces,

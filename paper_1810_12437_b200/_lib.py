@@ -42,6 +42,7 @@ SIGNATURES = {
     "pcgs_design_create": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int,
                                           ctypes.c_int, ctypes.POINTER(_P)]),
     "pcgs_design_destroy": (ctypes.c_int, [_P]),
+    "pcgs_synth_design": (ctypes.c_int, [_I64, _I64, _D, _D, _U64, _P, _P, _I64, _P]),
     "pcgs_store_selftest": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, _P]),
     "pcgs_design_info": (ctypes.c_int, [_P, _P]),

@@ -173,14 +173,26 @@ struct FillBulk {  // TMA copy of an internal-layout vector slab
 };
 
 // Shared-memory layout of k_pcg: [slab vector | own-slice state | piece pointers]
+// The piece pointers of the owned columns are staged in shared memory when they
+// fit (pp_smem), otherwise read from the design's global piece_ptr array.
 struct OwnState {
   double *x, *r, *d, *m, *s, *D, *b, *z;
-  int* pp;  // nslab_csc x (chunk + 1) piece pointers of the owned columns
+  const int* pp;   // shared copy [s*(chunk+1) + t] or global [s*(pt+1) + j0 + t]
+  long long pp_stride, pp_off, pp_lim;  // pp_lim: last valid t (columns beyond p_total clamp)
+  __device__ __forceinline__ int ppv(int s, int t) const {
+    return pp[s * pp_stride + pp_off + (t < pp_lim ? t : pp_lim)];
+  }
 };
 
-__device__ __forceinline__ OwnState own_state(double* sv, int slab_doubles, int chunk, int nslab) {
+__host__ __device__ inline bool pp_in_smem(const DesignDev& D) {
+  const long long chunk = (D.pt + D.G - 1) / D.G;
+  const long long bytes = (long long)D.smem_doubles * 8 + chunk * 8 * 8 + (long long)D.csc.nslab * (chunk + 1) * 4;
+  return bytes + 1024 <= 227 * 1024;
+}
+
+__device__ __forceinline__ OwnState own_state(double* sv, const DesignDev& D, int chunk, long long j0) {
   OwnState o;
-  double* base = sv + slab_doubles;
+  double* base = sv + D.smem_doubles;
   o.x = base;
   o.r = base + chunk;
   o.d = base + 2 * chunk;
@@ -189,14 +201,25 @@ __device__ __forceinline__ OwnState own_state(double* sv, int slab_doubles, int 
   o.D = base + 5 * chunk;
   o.b = base + 6 * chunk;
   o.z = base + 7 * chunk;
-  o.pp = (int*)(base + 8 * chunk);
-  (void)nslab;
+  if (pp_in_smem(D)) {
+    o.pp = (const int*)(base + 8 * chunk);
+    o.pp_stride = chunk + 1;
+    o.pp_off = 0;
+    o.pp_lim = chunk;
+  } else {
+    o.pp = D.csc.piece_ptr;
+    o.pp_stride = D.pt + 1;
+    o.pp_off = j0;
+    o.pp_lim = D.pt - j0 < chunk ? (D.pt - j0 > 0 ? D.pt - j0 : 0) : chunk;
+  }
   return o;
 }
 
 size_t pcg_smem_bytes(const DesignDev& D) {
   const long long chunk = (D.pt + D.G - 1) / D.G;
-  return (size_t)D.smem_doubles * 8 + (size_t)chunk * 8 * 8 + (size_t)D.csc.nslab * (chunk + 1) * 4 + 16;
+  size_t b = (size_t)D.smem_doubles * 8 + (size_t)chunk * 8 * 8 + 16;
+  if (pp_in_smem(D)) b += (size_t)D.csc.nslab * (chunk + 1) * 4;
+  return b;
 }
 
 // Stages the pieces of the CTA's owned columns (contiguous per slab) into the
@@ -205,11 +228,11 @@ size_t pcg_smem_bytes(const DesignDev& D) {
 __device__ __forceinline__ bool stage_pieces(const OwnState& o, const double* pieces, int nslab, int chunk,
                                              double* stage, int cap) {
   int total = 0;
-  for (int s = 0; s < nslab; ++s) total += o.pp[s * (chunk + 1) + chunk] - o.pp[s * (chunk + 1)];
+  for (int s = 0; s < nslab; ++s) total += o.ppv(s, chunk) - o.ppv(s, 0);
   if (total > cap) return false;
   int off = 0;
   for (int s = 0; s < nslab; ++s) {
-    const int q0 = o.pp[s * (chunk + 1)], len = o.pp[s * (chunk + 1) + chunk] - q0;
+    const int q0 = o.ppv(s, 0), len = o.ppv(s, chunk) - q0;
 #pragma unroll 4
     for (int q = threadIdx.x; q < len; q += kThreads) stage[off + q] = __ldcg(pieces + q0 + q);
     off += len;
@@ -224,12 +247,11 @@ __device__ __forceinline__ double owned_column_sum(const OwnState& o, const doub
   double total = 0.0;
   int off = 0;
   for (int s = 0; s < nslab; ++s) {
-    const int* pp = o.pp + s * (chunk + 1);
-    const int q0 = pp[t], q1 = pp[t + 1];
+    const int q0 = o.ppv(s, t), q1 = o.ppv(s, t + 1), p0 = o.ppv(s, 0);
     double ts = 0.0;
     if (staged) {
-      for (int q = q0; q < q1; ++q) ts += stage[off + q - pp[0]];
-      off += pp[chunk] - pp[0];
+      for (int q = q0; q < q1; ++q) ts += stage[off + q - p0];
+      off += o.ppv(s, chunk) - p0;
     } else {
       for (int q = q0; q < q1; ++q) ts += __ldcg(pieces + q);
     }
@@ -257,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     const int chunk = (int)((pt + gridDim.x - 1) / gridDim.x);
     const long long j0 = (long long)blockIdx.x * chunk;
     const long long dvs = (pt + 15) / 16 * 16;
-    const OwnState o = own_state(sv, A.D.smem_doubles, chunk, A.D.csc.nslab);
+    const OwnState o = own_state(sv, A.D, chunk, j0);
     for (int t = tid; t < chunk; t += kThreads) {
       const long long j = j0 + t;
       double xv = 0, m = 0, sc = 0, dg = 0, bv = 0;
@@ -280,10 +302,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       o.b[t] = bv;
       o.z[t] = 0.0;
     }
-    for (int t = tid; t < A.D.csc.nslab * (chunk + 1); t += kThreads) {
-      const int s = t / (chunk + 1), q = t % (chunk + 1);
-      const long long j = min(j0 + q, pt);
-      o.pp[t] = A.D.csc.piece_ptr[(long long)s * (pt + 1) + j];
+    if (pp_in_smem(A.D)) {
+      int* ppw = const_cast<int*>(o.pp);
+      for (int t = tid; t < A.D.csc.nslab * (chunk + 1); t += kThreads) {
+        const int s = t / (chunk + 1), q = t % (chunk + 1);
+        const long long j = min(j0 + q, pt);
+        ppw[t] = A.D.csc.piece_ptr[(long long)s * (pt + 1) + j];
+      }
     }
     if (tid == 0) {
       st_rz = 0.0;
@@ -301,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     const int chunk = (int)((pt + gridDim.x - 1) / gridDim.x);
     const long long j0 = (long long)blockIdx.x * chunk;
     const long long dvs = (pt + 15) / 16 * 16;
-    const OwnState o = own_state(sv, A.D.smem_doubles, chunk, A.D.csc.nslab);
+    const OwnState o = own_state(sv, A.D, chunk, j0);
     const bool prof = A.prof && blockIdx.x == 0 && tid == 0 && a < 64;
     // ---------------- convergence test of iteration a-1 ----------------
     if (a > 0) {
@@ -435,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     const long long pt = A.D.pt;
     const int chunk = (int)((pt + gridDim.x - 1) / gridDim.x);
     const long long j0 = (long long)blockIdx.x * chunk;
-    const OwnState o = own_state(sv, A.D.smem_doubles, chunk, A.D.csc.nslab);
+    const OwnState o = own_state(sv, A.D, chunk, j0);
     for (int t = tid; t < chunk; t += kThreads)
       if (j0 + t < pt) A.x[ref_index(j0 + t, A.D.p, A.D.icpt)] = o.x[t];
   }
@@ -623,6 +648,25 @@ int pcgs_store_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h, const in
     stats_h[7] = (int64_t)(H.csr.idx.size() + H.csc.idx.size()) * 2;
   }
   if (!err.empty()) return fail(PCGS_EUNSUP - 100, "store self-test failed: " + err);
+  return PCGS_OK;
+}
+
+int pcgs_synth_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint64_t seed, int64_t* row_ptr_h,
+                      int32_t* col_idx_h, int64_t cap, int64_t* nnz_h) {
+  if (n < 1 || p < 0 || !(rate_lo > 0) || !(rate_hi >= rate_lo) || !row_ptr_h || !nnz_h)
+    return fail(PCGS_EINVAL, "bad argument");
+  static thread_local std::vector<int64_t> rp;
+  static thread_local std::vector<int32_t> ci;
+  if (!col_idx_h) {  // first call: generate and report nnz
+    *nnz_h = synth_binary_design(n, p, rate_lo, rate_hi, seed, rp, ci);
+    memcpy(row_ptr_h, rp.data(), (n + 1) * sizeof(int64_t));
+    return PCGS_OK;
+  }
+  if (cap < (int64_t)ci.size()) return fail(PCGS_EINVAL, "col_idx buffer too small");
+  memcpy(col_idx_h, ci.data(), ci.size() * sizeof(int32_t));
+  *nnz_h = (int64_t)ci.size();
+  std::vector<int64_t>().swap(rp);
+  std::vector<int32_t>().swap(ci);
   return PCGS_OK;
 }
 

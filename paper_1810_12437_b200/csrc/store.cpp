@@ -391,3 +391,105 @@ std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int
 }
 
 }  // namespace pcgs
+
+// ---------------------------------------------------------------------------
+// Native synthetic generator for the large BASELINE configurations (config 5:
+// 1.09e9 nonzeros).  Same recipe as synth.binary_design (log-uniform column
+// rates, Binomial(n, rate) distinct rows per column) with a xoshiro256** stream
+// instead of numpy's PCG64, and a counting-sort transpose straight into CSR.
+// Bench/test infrastructure; not on the sampling path.
+// ---------------------------------------------------------------------------
+#include <cmath>
+#include <random>
+#include <unordered_set>
+
+namespace pcgs {
+
+namespace {
+struct Xoshiro {
+  uint64_t s[4];
+  explicit Xoshiro(uint64_t seed) {
+    uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+    for (int i = 0; i < 4; ++i) {
+      z += 0x9E3779B97F4A7C15ull;
+      uint64_t x = z;
+      x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+      x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+      s[i] = x ^ (x >> 31);
+    }
+  }
+  static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  uint64_t next() {
+    const uint64_t r = rotl(s[1] * 5, 7) * 9, t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return r;
+  }
+  double uniform() { return (next() >> 11) * (1.0 / 9007199254740992.0); }
+  uint64_t below(uint64_t m) { return (uint64_t)(((__uint128_t)next() * m) >> 64); }
+};
+}  // namespace
+
+int64_t synth_binary_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint64_t seed,
+                            std::vector<int64_t>& row_ptr, std::vector<int32_t>& col_idx) {
+  Xoshiro rng(seed);
+  std::mt19937_64 eng(seed ^ 0x5DEECE66Dull);
+  std::vector<int64_t> counts(p);
+  const double la = std::log(rate_lo), lb = std::log(rate_hi);
+  for (int64_t j = 0; j < p; ++j) {
+    const double rate = std::exp(la + (lb - la) * rng.uniform());
+    std::binomial_distribution<int64_t> bin(n, rate);
+    counts[j] = bin(eng);
+  }
+  int64_t nnz = 0;
+  for (int64_t j = 0; j < p; ++j) nnz += counts[j];
+  // per-column distinct rows (Floyd's algorithm for sparse columns, a Bernoulli
+  // scan with exact count correction for dense ones), counted per row
+  std::vector<int32_t> rows_of_col;
+  rows_of_col.reserve((size_t)nnz);
+  std::vector<int64_t> col_start(p + 1, 0);
+  std::vector<uint8_t> mark;
+  std::vector<uint64_t> bits;
+  for (int64_t j = 0; j < p; ++j) {
+    const int64_t k = counts[j];
+    col_start[j] = (int64_t)rows_of_col.size();
+    if (k == 0) continue;
+    if (k * 16 < n) {  // Floyd's algorithm on a reusable bitmap
+      if (bits.empty()) bits.assign((size_t)(n + 63) / 64, 0ull);
+      const size_t first = rows_of_col.size();
+      for (int64_t t = n - k; t < n; ++t) {
+        int64_t r = (int64_t)rng.below((uint64_t)t + 1);
+        if (bits[r >> 6] >> (r & 63) & 1ull) r = t;
+        bits[r >> 6] |= 1ull << (r & 63);
+        rows_of_col.push_back((int32_t)r);
+      }
+      for (size_t q = first; q < rows_of_col.size(); ++q) bits[rows_of_col[q] >> 6] = 0ull;
+    } else {
+      mark.assign((size_t)n, 0);
+      int64_t left = k;
+      for (int64_t i = 0; i < n && left > 0; ++i) {  // selection sampling (Knuth S)
+        if (rng.uniform() * (double)(n - i) < (double)left) {
+          mark[i] = 1;
+          --left;
+        }
+      }
+      for (int64_t i = 0; i < n; ++i)
+        if (mark[i]) rows_of_col.push_back((int32_t)i);
+    }
+  }
+  col_start[p] = (int64_t)rows_of_col.size();
+  row_ptr.assign((size_t)n + 1, 0);
+  for (int32_t r : rows_of_col) row_ptr[(size_t)r + 1]++;
+  for (int64_t i = 0; i < n; ++i) row_ptr[i + 1] += row_ptr[i];
+  col_idx.assign((size_t)nnz, 0);
+  std::vector<int64_t> fill(row_ptr.begin(), row_ptr.end() - 1);
+  for (int64_t j = 0; j < p; ++j)  // columns in order -> rows' columns ascending
+    for (int64_t q = col_start[j]; q < col_start[j + 1]; ++q) col_idx[fill[rows_of_col[q]]++] = (int32_t)j;
+  return nnz;
+}
+
+}  // namespace pcgs

@@ -70,6 +70,10 @@ struct DesignHost {
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
                          int intercept, int slab_max, int G, DesignHost& out);
 
+// Native synthetic binary design (bench/test infrastructure): returns nnz.
+int64_t synth_binary_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint64_t seed,
+                            std::vector<int64_t>& row_ptr, std::vector<int32_t>& col_idx);
+
 // Host-only check: reconstructs both passes and compares with the CSR.
 std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int32_t* col_idx);
 

@@ -204,3 +204,29 @@ class TestDeviceOperator:
         r = b - phi.apply(rep.solution)
         true_rms = math.sqrt(np.mean((cond["scale"] * r) ** 2))
         assert rep.termination == "converged" and true_rms < 1e-9
+
+
+def test_many_slabs_and_global_piece_pointers():
+    """More slabs than CTAs on both passes (slab groups per CTA) and piece
+    pointers too large to stage in shared memory (read from global)."""
+    d = synth.binary_design(6000, 12000, 1e-4, 0.02, seed=12)
+    X = d.matrix()
+    X.slab_max = 40
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    st = X.device_store()
+    info = st.describe()
+    assert info["csr_slabs"] > 148 and info["csc_slabs"] > 148
+    rng = np.random.default_rng(3)
+    om = rng.uniform(0.05, 0.3, d.n)
+    lam = np.abs(rng.standard_cauchy(d.p)) + 0.05
+    diag = np.concatenate([[0.0], (0.1 * lam) ** -2.0])
+    minv = np.concatenate([[100.0], (0.1 * lam) ** 2])
+    v = rng.standard_normal(d.p + 1)
+    phi = pk.PrecisionOperator(X, om, diag)
+    ref = port.phi_apply(Xo, om, diag, v)
+    assert rel(phi.apply(v), ref) < 1e-12
+    b = port.rhs(Xo, np.zeros(d.p + 1), om, diag, rng)
+    rep = pk.pcg_solve(phi, b, pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv),
+                       config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv))
+    oref = port.pcg(lambda x: port.phi_apply(Xo, om, diag, x), b, minv, np.sqrt(minv), rtol=1e-10)
+    assert rel(rep.solution, oref.x) < 1e-8
