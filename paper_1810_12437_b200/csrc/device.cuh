@@ -233,8 +233,11 @@ __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, doub
   have_open = true;
 }
 
-// L2 prefetch of a warp's whole range (TMA engine; no registers or scoreboards),
-// issued before the slab fill so the index stream is in flight during it.
+// L2 prefetch (TMA engine; no registers or scoreboards) of the first
+// kPrefetchBlocks blocks of a warp's range, issued before the slab fill; the
+// batch loop then keeps a sliding window of kPrefetchBlocks ahead of its loads,
+// so DRAM requests arrive in consumption order.
+constexpr int kPrefetchBlocks = 16;
 __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int dbg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane != 0 || (dbg & 4)) return;
@@ -243,7 +246,8 @@ __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int d
   if (nvec == 0) return;
   const int nb = (nvec + 31) >> 5;
   const char* p0 = (const char*)(P.vec + R.x);
-  const unsigned bytes = (unsigned)nvec * 16u;
+  const unsigned total = (unsigned)nvec * 16u;
+  const unsigned bytes = (dbg & 16) ? total : min(total, (unsigned)kPrefetchBlocks * 512u);
   for (unsigned off = 0; off < bytes; off += 16384u) {
     const unsigned sz = bytes - off < 16384u ? bytes - off : 16384u;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0 + off), "r"(sz) : "memory");
@@ -269,6 +273,14 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
   // batches of kRing blocks: all loads of a batch issued together, then consumed
   for (int k0 = 0; k0 < nb; k0 += kRing) {
     uint4 q[kRing];
+    if (lane == 0 && !(dbg & 20) && k0 + kPrefetchBlocks < nb) {
+      const int kb = k0 + kPrefetchBlocks;
+      const int ke = min(nb, kb + kRing);
+      const unsigned v_end = (unsigned)min(nvec, ke * 32);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char*)(base + kb * 32)),
+                   "r"((v_end - (unsigned)kb * 32u) * 16u)
+                   : "memory");
+    }
     uint2 dl = lane < kRing && k0 + lane < nb ? __ldg(bd + k0 + lane) : make_uint2(0u, 0u);
 #pragma unroll
     for (int u = 0; u < kRing; ++u) {

@@ -28,6 +28,7 @@ namespace cg = cooperative_groups;
 static unsigned long long* g_prof = nullptr;  // debug: phase timestamps of the next pcgs_pcg
 static int g_tma_dir = 1;
 static int g_dbg = 0;
+static int g_l2_persist_mb = 0;
 static thread_local std::string g_err;
 void set_last_error(const std::string& msg) { g_err = msg; }
 
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       const bool multi = A.D.csr.nslab > 1;
       EpiCsr e{multi ? A.zpart : A.w, A.omega, bc[2], 0.0, multi};
       FillBulk f{vcur, &bf};
-      run_pass(A.D.csr, sv, f, e);
+      run_pass(A.D.csr, sv, f, e, A.D.dbg);
       acc_dAd += e.acc;
     }
     if (A.D.csr.nslab > 1) {
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     {
       FillVecN f{A.w, &bf};
       EpiStore e{A.pieces};
-      run_pass(A.D.csc, sv, f, e);
+      run_pass(A.D.csc, sv, f, e, A.D.dbg);
     }
     if (prof) A.prof[4 * a + 2] = gtimer();
     cg::this_grid().sync();
@@ -810,11 +811,40 @@ int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag
   A.part = S.get<double>((size_t)kPartStride * D.G);
   A.prof = g_prof;
   A.tma_dir = g_tma_dir;
+  A.D.dbg = g_dbg;
   A.iterates = iterates;
   if (!A.w || !A.pieces || !A.zv || !A.dvg || !A.part || (D.csr.nslab > 1 && !A.zpart))
     return fail(PCGS_ENOMEM, "scratch allocation failed");
-  void* args[] = {&A};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_pcg, D.G, kThreads, args, pcg_smem_bytes(D), s));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(D.G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pcg_smem_bytes(D);
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  attrs[na].id = cudaLaunchAttributeCooperative;
+  attrs[na].val.cooperative = 1;
+  ++na;
+  if (g_l2_persist_mb > 0) {
+    // keep the leading part of the CSC index stream resident in L2 across
+    // iterations (persisting carve-out); the rest streams
+    static bool limit_set = false;
+    const size_t want = (size_t)g_l2_persist_mb << 20;
+    if (!limit_set) {
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+      limit_set = true;
+    }
+    attrs[na].id = cudaLaunchAttributeAccessPolicyWindow;
+    attrs[na].val.accessPolicyWindow.base_ptr = (void*)D.csc.vec;
+    attrs[na].val.accessPolicyWindow.num_bytes = want;
+    attrs[na].val.accessPolicyWindow.hitRatio = 1.0f;
+    attrs[na].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attrs[na].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    ++na;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pcg, A));
   return PCGS_OK;
 }
 
@@ -966,6 +996,7 @@ int pcgs_debug_cta_times(void* buf) {
 int pcgs_debug_option(int key, int value) {
   if (key == 0) g_tma_dir = value;
   if (key == 1) g_dbg = value;
+  if (key == 2) g_l2_persist_mb = value;
   return PCGS_OK;
 }
 
