@@ -47,6 +47,13 @@ struct SlabSegs {
 };
 
 // Indices of one segment still to be placed, bucketed by shared-memory bank pair.
+//
+// A 64-bit LDS costs, per half-warp, the largest number of distinct addresses
+// sharing a bank pair (index mod 16) -- measured on B200 with
+// tools/microbench/bank_rule.cu.  Taking the fullest buckets first is close to
+// the bound for a segment that fills whole half-warps: its most popular pair
+// holds max_b c_b indices but each group takes it once, so max_b c_b - groups
+// extra wavefronts are unavoidable (~20 % for an 800-index row).
 struct Pool {
   std::array<std::vector<uint16_t>, 16> b;
   uint32_t remaining = 0;
@@ -55,25 +62,38 @@ struct Pool {
     for (uint32_t t = 0; t < len; ++t) b[d[t] & 15].push_back(d[t]);
     remaining = len;
   }
-  // an index whose bank pair is not in `used` (largest bucket first); -1 when empty
-  int pick(uint32_t used, bool& conflict) {
-    conflict = false;
-    if (remaining == 0) return -1;
-    int best = -1;
-    size_t bs = 0;
-    for (int k = 0; k < 16; ++k)
-      if (!((used >> k) & 1u) && b[k].size() > bs) { best = k; bs = b[k].size(); }
-    if (best < 0) {
-      conflict = true;
-      for (int k = 0; k < 16; ++k)
-        if (b[k].size() > bs) { best = k; bs = b[k].size(); }
-    }
-    const int v = b[best].back();
-    b[best].pop_back();
+  int take(int k) {
+    const int v = b[k].back();
+    b[k].pop_back();
     --remaining;
     return v;
   }
+  // an index whose bank pair has the lowest multiplicity in the group so far
+  // (largest bucket among those); -1 when empty
+  int pick(const uint8_t* mult) {
+    if (remaining == 0) return -1;
+    int best = -1;
+    for (int k = 0; k < 16; ++k) {
+      if (b[k].empty()) continue;
+      if (best < 0 || mult[k] < mult[best] || (mult[k] == mult[best] && b[k].size() > b[best].size()))
+        best = k;
+    }
+    return take(best);
+  }
 };
+
+// Wavefronts one (slot, half-warp) group costs beyond the first: the largest
+// number of distinct addresses sharing a bank pair, minus one.
+int group_extra(const uint16_t* ix, int n) {
+  int mult[16] = {};
+  int worst = 0;
+  for (int i = 0; i < n; ++i) {
+    bool seen = false;
+    for (int j = 0; j < i; ++j) seen |= ix[j] == ix[i];
+    if (!seen) worst = std::max(worst, ++mult[ix[i] & 15]);
+  }
+  return worst > 0 ? worst - 1 : 0;
+}
 
 // Appends one warp range (segments [s0, s1) of slab S) to the pass.
 void emit_warp(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std::vector<Pool>& pools) {
@@ -121,19 +141,29 @@ void emit_warp(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std::vector
     // bank-balanced placement: group = (slot, half-warp)
     for (int slot = 0; slot < kVecIdx; ++slot) {
       for (int h = 0; h < 2; ++h) {
-        uint32_t used = 0;
+        const int l0 = h * 16;
         bool any = false;
-        for (int l = h * 16; l < h * 16 + 16; ++l) {
-          if (lane_seg[l] < 0) continue;
-          any = true;
-          bool conflict;
-          const int ix = pools[lane_pool[l]].pick(used, conflict);
-          if (ix < 0) continue;  // pad: sentinel already in place (broadcast)
-          used |= 1u << (ix & 15);
-          P.lds_conflict_excess += conflict;
-          out[(k * 32 + l) * kVecIdx + slot] = (uint16_t)ix;
+        for (int l = l0; l < l0 + 16; ++l) any |= lane_seg[l] >= 0;
+        if (!any) continue;
+        uint16_t g[16];
+        int ng = 0;
+        {
+          uint8_t mult[16] = {};
+          bool pad_seen = false;
+          for (int l = l0; l < l0 + 16; ++l) {
+            if (lane_seg[l] < 0) continue;
+            const int ix = pools[lane_pool[l]].pick(mult);
+            if (ix < 0) {  // pad: the sentinel is already in place (one broadcast address)
+              if (!pad_seen) { pad_seen = true; ++mult[S.sentinel & 15]; g[ng++] = S.sentinel; }
+              continue;
+            }
+            ++mult[ix & 15];
+            out[(k * 32 + l) * kVecIdx + slot] = (uint16_t)ix;
+            g[ng++] = (uint16_t)ix;
+          }
         }
-        P.lds_groups += any;
+        ++P.lds_groups;
+        P.lds_conflict_excess += group_extra(g, ng);
       }
     }
   }
