@@ -34,6 +34,8 @@ extern "C" {
 #define PCGS_ECUDA (-2)    /* CUDA runtime error                            */
 #define PCGS_ENOMEM (-3)   /* device or host allocation failed              */
 #define PCGS_EUNSUP (-4)   /* configuration not supported by this build     */
+#define PCGS_EFORMAT (-5)  /* malformed input file (maps to FileFormatError) */
+#define PCGS_EIO (-6)      /* file cannot be opened/read/written (OSError)  */
 
 /* PCG termination codes written to result[1] by pcgs_pcg (device int32). */
 #define PCGS_CONVERGED 0   /* CGReport.termination == "converged"           */
@@ -42,6 +44,7 @@ extern "C" {
 #define PCGS_NONFINITE (-2)/* NumericBreakdownError(k), cg.py:141-142,172   */
 
 typedef struct pcgs_design* pcgs_design_t;
+typedef struct pcgs_mtx* pcgs_mtx_t;
 typedef void* pcgs_stream_t; /* cudaStream_t */
 
 int pcgs_version(void);
@@ -69,10 +72,31 @@ int pcgs_design_destroy(pcgs_design_t d);
  * again with a col_idx_h buffer of capacity `cap` to receive the columns. */
 int pcgs_synth_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint64_t seed,
                       int64_t* row_ptr_h, int32_t* col_idx_h, int64_t cap, int64_t* nnz_h);
+/* Streaming Matrix Market ingestion (host-only, no GPU), replacing the
+ * densifying reader of the reference (matrixio.py:48-79: scipy.io.mmread +
+ * toarray, then SparseDesignMatrix.from_dense).  `path` may be plain or gzip.
+ * pcgs_mtx_load parses the whole file in one pass into CSR and returns
+ * info_h[8] = {n, p, nnz, declared entries, field (0 pattern, 1 real,
+ * 2 integer), symmetry (0 general, 1 symmetric), format (0 coordinate,
+ * 1 array), explicit zeros dropped}; pcgs_mtx_export copies row_ptr_h[n+1]
+ * and col_idx_h[nnz] out (columns strictly increasing per row); pcgs_mtx_free
+ * releases the parse.  Values must be 0/1 (PCGS_EUNSUP otherwise: the store
+ * is pattern-only); duplicates, out-of-range or missing entries give
+ * PCGS_EFORMAT; unreadable files PCGS_EIO. */
+int pcgs_mtx_load(const char* path, pcgs_mtx_t* out, int64_t* info_h);
+int pcgs_mtx_export(pcgs_mtx_t m, int64_t* row_ptr_h, int32_t* col_idx_h);
+int pcgs_mtx_free(pcgs_mtx_t m);
+/* Writes a CSR pattern as Matrix Market "coordinate pattern general"
+ * (field 0) or "coordinate real general" with value 1 (field 1, what
+ * scipy.io.mmwrite writes for the reference's write_design,
+ * matrixio.py:35-45); gzip-compressed when gz != 0. */
+int pcgs_mtx_write(const char* path, int64_t n, int64_t p, const int64_t* row_ptr_h,
+                   const int32_t* col_idx_h, int field, int gz);
 /* Host-only: builds the store for a grid of `grid` CTAs and verifies that both
  * tiled passes reproduce the input pattern exactly (no GPU needed).
  * stats_h[8]: csr slabs, csc slabs, csr vectors, csc vectors, csc pieces,
- * shared-memory load groups, bank-conflicted picks, index bytes. */
+ * shared-memory load groups (slot x half-warp), extra shared-memory
+ * wavefronts those groups cost (bank-pair conflicts), index bytes. */
 int pcgs_store_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h,
                         const int32_t* col_idx_h, int intercept, int slab_max,
                         int grid, int64_t* stats_h);

@@ -21,6 +21,8 @@ PCGS_EINVAL = -1
 PCGS_ECUDA = -2
 PCGS_ENOMEM = -3
 PCGS_EUNSUP = -4
+PCGS_EFORMAT = -5
+PCGS_EIO = -6
 
 PCGS_CONVERGED = 0
 PCGS_MAX_ITER = 1
@@ -43,6 +45,10 @@ SIGNATURES = {
                                           ctypes.c_int, ctypes.POINTER(_P)]),
     "pcgs_design_destroy": (ctypes.c_int, [_P]),
     "pcgs_synth_design": (ctypes.c_int, [_I64, _I64, _D, _D, _U64, _P, _P, _I64, _P]),
+    "pcgs_mtx_load": (ctypes.c_int, [ctypes.c_char_p, _P, _P]),
+    "pcgs_mtx_export": (ctypes.c_int, [_P, _P, _P]),
+    "pcgs_mtx_free": (ctypes.c_int, [_P]),
+    "pcgs_mtx_write": (ctypes.c_int, [ctypes.c_char_p, _I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int]),
     "pcgs_store_selftest": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, _P]),
     "pcgs_design_info": (ctypes.c_int, [_P, _P]),
@@ -110,6 +116,11 @@ def check(rc: int) -> None:
         raise ValueError(msg)
     if rc == PCGS_EUNSUP:
         raise NotImplementedError(msg)
+    if rc == PCGS_EFORMAT:
+        from .io import FileFormatError
+        raise FileFormatError(msg)
+    if rc == PCGS_EIO:
+        raise OSError(msg)
     raise PcgsError(f"pcgs error {rc}: {msg}")
 
 

@@ -13,8 +13,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpcgs.so"
-SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "batched.cu", CSRC / "store.cpp"]
-HEADERS = [CSRC / "store.h", CSRC / "device.cuh", CSRC / "internal.cuh", CSRC / "batched.cuh",
+SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "batched.cu", CSRC / "store.cpp", CSRC / "mtx.cpp"]
+HEADERS = [CSRC / "store.h", CSRC / "mtx.h", CSRC / "device.cuh", CSRC / "internal.cuh", CSRC / "batched.cuh",
            ROOT / "include" / "pcgs.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -33,7 +33,7 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
            "-shared", "-I", str(ROOT / "include"), "-I", str(CSRC),
            "-Xptxas", "-v" if verbose else "-O3",
-           "-o", str(LIB) + ".tmp", *map(str, SOURCES)]
+           "-o", str(LIB) + ".tmp", *map(str, SOURCES), "-lz"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "mtx.h"
 
 namespace cg = cooperative_groups;
 
@@ -669,6 +670,65 @@ int pcgs_synth_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint
   std::vector<int64_t>().swap(rp);
   std::vector<int32_t>().swap(ci);
   return PCGS_OK;
+}
+
+struct pcgs_mtx {
+  pcgs::MtxPattern m;
+};
+
+static int mtx_status(int kind) {
+  return kind == pcgs::kMtxIo ? PCGS_EIO : kind == pcgs::kMtxFormat ? PCGS_EFORMAT : PCGS_EUNSUP;
+}
+
+int pcgs_mtx_load(const char* path, pcgs_mtx_t* out, int64_t* info_h) {
+  if (!path || !out || !info_h) return fail(PCGS_EINVAL, "null argument");
+  *out = nullptr;
+  auto* h = new (std::nothrow) pcgs_mtx;
+  if (!h) return fail(PCGS_ENOMEM, "host allocation failed");
+  std::string msg;
+  int rc;
+  try {
+    rc = pcgs::mtx_load(path, h->m, msg);
+  } catch (const std::bad_alloc&) {
+    delete h;
+    return fail(PCGS_ENOMEM, std::string(path) + ": host memory exhausted while parsing");
+  }
+  if (rc != pcgs::kMtxOk) {
+    delete h;
+    return fail(mtx_status(rc), msg);
+  }
+  const auto& m = h->m;
+  const int64_t info[8] = {m.n, m.p, (int64_t)m.col_idx.size(), m.entries, m.field, m.symmetry, m.format,
+                           m.zeros_dropped};
+  memcpy(info_h, info, sizeof info);
+  *out = h;
+  return PCGS_OK;
+}
+
+int pcgs_mtx_export(pcgs_mtx_t h, int64_t* row_ptr_h, int32_t* col_idx_h) {
+  if (!h || !row_ptr_h || (!col_idx_h && !h->m.col_idx.empty())) return fail(PCGS_EINVAL, "null argument");
+  memcpy(row_ptr_h, h->m.row_ptr.data(), h->m.row_ptr.size() * sizeof(int64_t));
+  if (!h->m.col_idx.empty()) memcpy(col_idx_h, h->m.col_idx.data(), h->m.col_idx.size() * sizeof(int32_t));
+  return PCGS_OK;
+}
+
+int pcgs_mtx_free(pcgs_mtx_t h) {
+  delete h;
+  return PCGS_OK;
+}
+
+int pcgs_mtx_write(const char* path, int64_t n, int64_t p, const int64_t* row_ptr_h, const int32_t* col_idx_h,
+                   int field, int gz) {
+  if (!path || n < 0 || p < 0 || !row_ptr_h || (field != 0 && field != 1)) return fail(PCGS_EINVAL, "bad argument");
+  if (row_ptr_h[0] != 0) return fail(PCGS_EINVAL, "row_ptr must start at 0");
+  for (int64_t r = 0; r < n; ++r)
+    if (row_ptr_h[r + 1] < row_ptr_h[r]) return fail(PCGS_EINVAL, "row_ptr must be non-decreasing");
+  if (row_ptr_h[n] > 0 && !col_idx_h) return fail(PCGS_EINVAL, "null col_idx");
+  for (int64_t t = 0; t < row_ptr_h[n]; ++t)
+    if (col_idx_h[t] < 0 || col_idx_h[t] >= p) return fail(PCGS_EINVAL, "column index out of range");
+  std::string msg;
+  const int rc = pcgs::mtx_write(path, n, p, row_ptr_h, col_idx_h, field, gz, msg);
+  return rc == pcgs::kMtxOk ? PCGS_OK : fail(mtx_status(rc), msg);
 }
 
 int pcgs_design_destroy(pcgs_design_t d) {

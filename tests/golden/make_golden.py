@@ -133,11 +133,79 @@ def gibbs_cases():
     np.savez_compressed(OUT / "gibbs.npz", **out)
 
 
+def io_cases():
+    """Files written by the reference's own writers (matrixio.py, stateio.py)."""
+    from priorcg import matrixio, stateio
+    d = OUT / "io"
+    d.mkdir(exist_ok=True)
+    rng = np.random.default_rng(5)
+    n, p = 23, 9
+    rp, ci = binary_pattern(rng, n, p, 0.05, 0.6)
+    X = ref_design(n, p, rp, ci, intercept=True)
+    matrixio.write_design(d / "design_sparse.mtx", X)
+    dense = np.zeros((n, p))
+    dense[np.repeat(np.arange(n), np.diff(rp)), ci] = 1.0
+    matrixio.write_design(d / "design_dense.mtx", dense)
+    matrixio.write_design_csv(d / "design.csv", dense)
+    draws = rng.standard_normal((4, 3))
+    matrixio.write_chain_csv(d / "chain.csv", draws, np.exp(rng.standard_normal(4)), rng.standard_normal(4))
+    matrixio.write_vector_csv(d / "vector.csv", rng.standard_normal(5) * 1e-7, "beta")
+    matrixio.write_spectrum_csv(d / "spectrum.csv", np.array([3.5, 1.0, 1e-3, 0.0]))
+
+    class _T:
+        pass
+    tr = _T()
+    k = 6
+    tr.rms_precond_residual = np.exp(-np.arange(k, dtype=float))
+    tr.phi_norm_error = rng.random(k)
+    tr.l2_error = rng.random(k)
+    tr.rel_coord_error = np.where(np.arange(k) == 2, np.nan, rng.random(k))
+    matrixio.write_trace_csv(d / "trace.csv", tr)
+    state = rg.ShrinkageState(rng.standard_normal(p + 1), rng.uniform(0.1, 2.0, n),
+                              rng.uniform(0.5, 3.0, p), 0.37)
+    stateio.save_state(d / "state.brgs", state)
+    np.savez(d / "expected.npz", rp=rp, ci=ci, dense=dense, draws=draws, beta=state.beta,
+             omega=state.omega, lam=state.lam, tau=state.tau)
+
+
+def error_trace_cases():
+    """diagnostics.error_trace on a full-trace reference solve."""
+    from priorcg.diagnostics import error_trace
+    rng = np.random.default_rng(31)
+    n, p = 400, 120
+    rp, ci = binary_pattern(rng, n, p, 0.01, 0.3)
+    X = ref_design(n, p, rp, ci)
+    omega = rpg.pg_draw_batch(np.zeros(n), rng)
+    tau = 0.05
+    lam = np.abs(rng.standard_cauchy(p))
+    diag = np.concatenate([[0.0], (tau * lam) ** -2.0])
+    gamma = np.array([10.0])
+    M = augmented_prior(tau, lam, gamma)
+    phi = PrecisionOperator(X, omega, diag)
+    b = X.matvec_t(rng.standard_normal(n)) + np.sqrt(diag) * rng.standard_normal(p + 1)
+    scale = np.concatenate([gamma, tau * lam])
+    rep = pcg_solve(phi, b, M, config=CGConfig(rtol=1e-12, trace_level="full"), residual_scale=scale)
+    dense = np.zeros((n, p + 1))
+    dense[:, 0] = 1.0
+    dense[np.repeat(np.arange(n), np.diff(rp)), ci + 1] = 1.0
+    A = dense.T @ (omega[:, None] * dense) + np.diag(diag)
+    x_star = np.linalg.solve(A, b)
+    x_star[5] = 0.0  # exercise the |beta*| < 1e-300 guard
+    et = error_trace(rep, x_star, phi)
+    np.savez(OUT / "errtrace.npz", n=n, p=p, rp=rp, ci=ci, omega=omega, diag=diag, minv=M.inv_diagonal,
+             scale=scale, b=b, x_star=x_star, iterates=np.array(rep.iterates),
+             rms=np.array(rep.rms_precond_residual_trace), iterations=rep.iterations,
+             rel=et.rel_coord_error, l2=et.l2_error, phin=et.phi_norm_error, guarded=et.n_guarded_coords,
+             alphas=np.array(rep.alphas), betas=np.array(rep.betas))
+
+
 if __name__ == "__main__":
     print("priorcg", priorcg.__version__)
     sparse_cases()
     pcg_cases()
     pg_cases()
     gibbs_cases()
+    io_cases()
+    error_trace_cases()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
