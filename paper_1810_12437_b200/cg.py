@@ -65,6 +65,10 @@ class CGReport:
     alphas: np.ndarray = field(default_factory=lambda: np.zeros(0))
     betas: np.ndarray = field(default_factory=lambda: np.zeros(0))
     iterates: list | None = None
+    # device copy of the iterates ((iterations+1) x p CUDA tensor) when the
+    # solve ran on the GPU at trace_level "full"; diagnostics.error_trace
+    # evaluates on it without a round trip
+    iterates_device: object = field(default=None, repr=False, compare=False)
 
     def lanczos_tridiagonal(self):
         """(diagonal, offdiagonal) of the Lanczos matrix from the CG coefficients."""
@@ -151,9 +155,10 @@ def _report_from_device(x, trace, alphas, betas, result, iterates=None, as_tenso
     iterations, status, fail_iter, applies = (int(v) for v in res)
     _raise_status(status, fail_iter)
     nb = _n_betas(iterations, status)
-    its = None
+    its = its_dev = None
     if iterates is not None:
-        h = iterates[: iterations + 1].cpu().numpy()
+        its_dev = iterates[: iterations + 1]
+        h = its_dev.cpu().numpy()
         its = [h[k].copy() for k in range(iterations + 1)]
     return CGReport(
         iterations=iterations,
@@ -164,6 +169,7 @@ def _report_from_device(x, trace, alphas, betas, result, iterates=None, as_tenso
         alphas=alphas[:iterations].cpu().numpy(),
         betas=betas[:nb].cpu().numpy(),
         iterates=its,
+        iterates_device=its_dev,
     )
 
 
@@ -264,6 +270,7 @@ def _pcg_solve_operator(phi, b, minv, scale, x0, max_iter, rtol, as_tensor, full
         betas=betas[:nb].copy(),
         iterates=(None if iterates is None else
                   [r.copy() for r in iterates[: iterations + 1].cpu().numpy()]),
+        iterates_device=None if iterates is None else iterates[: iterations + 1],
     )
 
 

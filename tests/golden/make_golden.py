@@ -199,6 +199,30 @@ def error_trace_cases():
              alphas=np.array(rep.alphas), betas=np.array(rep.betas))
 
 
+def chain_diag_cases():
+    """effective_sample_size / standardized_difference_test (diagnostics.py:236-303)."""
+    from priorcg.diagnostics import effective_sample_size, standardized_difference_test
+    rng = np.random.default_rng(17)
+    series = []
+    for phi_ar, n in ((0.0, 200), (0.5, 300), (0.9, 500), (-0.4, 150), (0.99, 64)):
+        x = np.zeros(n)
+        e = rng.standard_normal(n)
+        for t in range(1, n):
+            x[t] = phi_ar * x[t - 1] + e[t]
+        series.append(x)
+    series.append(np.full(10, 3.0))
+    series.append(np.array([1.0]))
+    ess = np.array([effective_sample_size(x) for x in series])
+    a = rng.standard_normal((120, 6)).cumsum(0) * 0.1 + rng.standard_normal((120, 6))
+    b = rng.standard_normal((90, 6)) + 0.05
+    b[:, 2] = a[:90, 2]
+    a[:, 5] = 1.0
+    b[:, 5] = 1.0
+    t = standardized_difference_test(a, b)
+    np.savez(OUT / "chaindiag.npz", lengths=[len(x) for x in series], series=np.concatenate(series), ess=ess,
+             a=a, b=b, z=t.z_scores, excluded=t.excluded, ess_a=t.ess_a, ess_b=t.ess_b)
+
+
 if __name__ == "__main__":
     print("priorcg", priorcg.__version__)
     sparse_cases()
@@ -207,5 +231,6 @@ if __name__ == "__main__":
     gibbs_cases()
     io_cases()
     error_trace_cases()
+    chain_diag_cases()
     for f in sorted(OUT.glob("*.npz")):
         print(f.name, f.stat().st_size)
