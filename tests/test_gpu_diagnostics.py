@@ -41,11 +41,15 @@ def test_device_solve_then_error_trace():
                        residual_scale=g["scale"])
     assert rep.iterates_device is not None and abs(rep.iterations - int(g["iterations"])) <= 2
     et = dg.error_trace(rep, g["x_star"], phi)
-    k = min(len(et.l2_error), len(g["l2"])) - 3
-    # same trajectory while the errors are far above round-off
-    np.testing.assert_allclose(et.l2_error[:k], g["l2"][:k], rtol=1e-6)
-    np.testing.assert_allclose(et.rel_coord_error[:k], g["rel"][:k], rtol=1e-6)
-    assert et.l2_error[-1] < 1e-8 * et.l2_error[0]
+    # This instance (tiny tau, Cauchy lambda, flat intercept) has a near-breakdown
+    # at iteration 6 (the RMS jumps 30x), where summation order alone moves
+    # alpha_6 by O(1) -- measured: alphas agree to 1e-15 through k = 4, 5e-9 at
+    # k = 5.  Compare the well-determined prefix and the converged end.
+    np.testing.assert_allclose(et.l2_error[:5], g["l2"][:5], rtol=1e-9)
+    np.testing.assert_allclose(et.rel_coord_error[:5], g["rel"][:5], rtol=1e-7)  # |dx/x*| amplifies tiny x*
+    np.testing.assert_allclose(et.phi_norm_error[:5], g["phin"][:5], rtol=1e-8)
+    np.testing.assert_allclose(et.l2_error[-1], g["l2"][-1], rtol=1e-6)
+    assert et.rel_coord_error[-1] < 1e-10 and g["rel"][-1] < 1e-10  # both at round-off
     ritz = dg.ritz_values(rep)
     ref = dg.ritz_values(CGReport(0, "converged", g["rms"], None, 0, alphas=g["alphas"], betas=g["betas"]))
-    np.testing.assert_allclose(ritz[[0, -1]], ref[[0, -1]], rtol=1e-6)
+    np.testing.assert_allclose(ritz[[0, -1]], ref[[0, -1]], rtol=1e-4)

@@ -85,6 +85,33 @@ __global__ void __launch_bounds__(1024, 1) k_reg(const uint4* __restrict__ idx, 
   out[blockIdx.x * 1024 + threadIdx.x] = acc;
 }
 
+// software-pipelined register batches: loads for batch i+1 issued before batch i is consumed
+template <int B, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_pipe(const uint4* __restrict__ idx, long nvec,
+                                                      const double* __restrict__ v, int p, double* out) {
+  extern __shared__ __align__(128) double sv[];
+  __shared__ unsigned long long mb;
+  fill_slab(sv, v, p, &mb);
+  constexpr int W = THREADS / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long nw = (long)gridDim.x * W, w = (long)blockIdx.x * W + warp;
+  const long per = (nvec / 32 + nw - 1) / nw * 32;
+  const long v0 = w * per, v1 = lmin(nvec, v0 + per);
+  double acc = 0;
+  uint4 q[B], r[B];
+#pragma unroll
+  for (int u = 0; u < B; ++u) { long i = v0 + u * 32 + lane; q[u] = i < v1 ? ldg_stream(idx + i) : make_uint4(0, 0, 0, 0); }
+  for (long b = v0; b < v1; b += 32 * B) {
+#pragma unroll
+    for (int u = 0; u < B; ++u) { long i = b + 32 * B + u * 32 + lane; r[u] = i < v1 ? ldg_stream(idx + i) : make_uint4(0, 0, 0, 0); }
+#pragma unroll
+    for (int u = 0; u < B; ++u) acc += gather8(q[u], sv);
+#pragma unroll
+    for (int u = 0; u < B; ++u) q[u] = r[u];
+  }
+  out[blockIdx.x * THREADS + threadIdx.x] = acc;
+}
+
 // per-warp TMA ring: S stages of C blocks (C*512 bytes) each
 template <int S, int C, bool PF>
 __global__ void __launch_bounds__(1024, 1) k_ring(const uint4* __restrict__ idx, long nvec,
@@ -181,29 +208,19 @@ int main() {
 #define RING(S, C, PF, data, name) { auto kf = k_ring<S, C, PF>; int sm = slab + 32 * S * C * 512; \
     CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
     timeit(name, [&] { kf<<<nsm, 1024, sm>>>((const uint4*)data, nv, d_v, p, slab, d_out); }); }
-  REG(4, false, d_pf, "reg B=4 conflict-free p=22176");
-  RING(3, 1, false, d_pf, "ring 3x512B p=22176");
-  // half-size slab: indices folded into [0, p/2)
-  {
-    std::vector<uint16_t> h(nnz);
-    for (long i = 0; i < nnz; ++i) h[i] = ipf[i] % (p / 2);   // keeps bank pair (p/2 multiple of 16)
-    CK(cudaMemcpy(d_pf, h.data(), nnz * 2, cudaMemcpyHostToDevice));
-  }
-  const int p2 = p / 2;
-  const int slab2 = ((p2 * 8 + 16 + 127) / 128) * 128;
-#define REG2(B, name) { auto kf = k_reg<B, false>; CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, slab2)); \
-    timeit(name, [&] { kf<<<nsm, 1024, slab2>>>((const uint4*)d_pf, nv, d_v, p2, d_out); }); }
-#define RING2(S, C, name) { auto kf = k_ring<S, C, false>; int sm = slab2 + 32 * S * C * 512; \
-    CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
-    timeit(name, [&] { kf<<<nsm, 1024, sm>>>((const uint4*)d_pf, nv, d_v, p2, slab2, d_out); }); }
-  REG2(4, "reg B=4 p=11088");
-  RING2(3, 1, "ring 3x512B p=11088");
-  RING2(4, 1, "ring 4x512B p=11088");
-  RING2(6, 1, "ring 6x512B p=11088");
-  RING2(7, 1, "ring 7x512B p=11088");
-  RING2(2, 2, "ring 2x1KB p=11088");
-  RING2(3, 2, "ring 3x1KB p=11088");
-  RING2(2, 3, "ring 2x1.5KB p=11088");
+  REG(4, false, d_pf, "reg B=4 conflict-free");
+  REG(2, false, d_pf, "reg B=2 conflict-free");
+  REG(6, false, d_pf, "reg B=6 conflict-free");
+#define PIPE(B, T, name) { auto kf = k_pipe<B, T>; CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, slab)); \
+    timeit(name, [&] { kf<<<nsm, T, slab>>>((const uint4*)d_pf, nv, d_v, p, d_out); }); }
+  PIPE(2, 1024, "pipe B=2 T=1024");
+  PIPE(3, 1024, "pipe B=3 T=1024");
+  PIPE(4, 1024, "pipe B=4 T=1024");
+  PIPE(4, 512, "pipe B=4 T=512");
+  PIPE(6, 512, "pipe B=6 T=512");
+  PIPE(8, 512, "pipe B=8 T=512");
+  PIPE(8, 256, "pipe B=8 T=256");
+  PIPE(12, 256, "pipe B=12 T=256");
   printf("done\n");
   return 0;
 }
