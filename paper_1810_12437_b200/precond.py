@@ -1,9 +1,23 @@
-"""Preconditioners (drop-in for priorcg.precond, pkg/src/priorcg/precond.py).
+"""Diagonal preconditioners for the device PCG (drop-in for priorcg.precond).
 
-Only diagonal kinds reach the device PCG kernel: there M^-1 is the vector
-`inv_diagonal` fused into the CG vector update.  The block-threshold kind
-(precond.py:156-181) is a dense desk-scale comparison preconditioner and is
-out of scope: constructing it raises NotImplementedError.
+On the B200 path M⁻¹ is a p-vector (`inv_diagonal`) that the persistent PCG
+kernel applies inside its own vector update -- there is no separate
+preconditioner kernel.  The factories keep the reference's names, meaning
+and errors (pkg/src/priorcg/precond.py:22-153):
+
+=====================  =========================  ==========================
+factory                M⁻¹ (inv_diagonal)          reference
+=====================  =========================  ==========================
+identity_preconditioner  1                         precond.py:82-84
+prior_preconditioner     (τλ)²                     precond.py:87-102
+jacobi_preconditioner    1 / diag(Φ)               precond.py:105-117
+augmented_prior          [γ², (τλ)²]               precond.py:120-134
+=====================  =========================  ==========================
+
+diag(XᵀΩX) for Jacobi is one pattern-only CSC pass on the device
+(`SparseDesignMatrix.gram_diagonal`).  The block-threshold kind
+(precond.py:156-181) is a dense desk-scale comparison and is not on the
+B200 path: constructing it raises NotImplementedError.
 """
 from __future__ import annotations
 
@@ -14,33 +28,42 @@ import numpy as np
 
 
 class PreconditionerKind(enum.Enum):
-    PRIOR = "prior"
-    JACOBI = "jacobi"
-    AUGMENTED_PRIOR = "augmented"
-    BLOCK_THRESHOLD = "block"
     IDENTITY = "identity"
+    PRIOR = "prior"
+    AUGMENTED_PRIOR = "augmented"
+    JACOBI = "jacobi"
+    BLOCK_THRESHOLD = "block"
 
 
 class DegeneratePreconditionerError(ValueError):
-    """The requested preconditioner has a non-invertible diagonal (precond.py:30)."""
+    """M⁻¹ would have a zero, negative or non-finite entry (precond.py:30)."""
+
+
+def _as_f64(x):
+    return np.asarray(x, dtype=np.float64)
+
+
+def _all_positive_finite(x) -> bool:
+    x = _as_f64(x)
+    return bool(np.all(np.isfinite(x)) and np.all(x > 0))
 
 
 @dataclass
 class Preconditioner:
-    """Diagonal M^-1 (precond.py:34-79)."""
+    """M⁻¹ = diag(inv_diagonal), validated on construction (precond.py:34-79)."""
 
     kind: PreconditionerKind
     inv_diagonal: np.ndarray
 
     def __post_init__(self):
-        self.inv_diagonal = np.asarray(self.inv_diagonal, dtype=np.float64)
-        if np.any(~np.isfinite(self.inv_diagonal)) or np.any(self.inv_diagonal <= 0):
+        self.inv_diagonal = _as_f64(self.inv_diagonal)
+        if not _all_positive_finite(self.inv_diagonal):
             raise DegeneratePreconditionerError(
                 "inverse-diagonal entries must be finite and strictly positive")
 
     @property
-    def dim(self):
-        return len(self.inv_diagonal)
+    def dim(self) -> int:
+        return int(self.inv_diagonal.size)
 
     def apply_inverse(self, v):
         return self.inv_diagonal * v
@@ -53,47 +76,51 @@ def identity_preconditioner(p):
     return Preconditioner(PreconditionerKind.IDENTITY, np.ones(p))
 
 
-def prior_preconditioner(tau, lam):
-    """M = tau^-2 Lambda^-2 (precond.py:87-102)."""
-    lam = np.asarray(lam, dtype=np.float64)
+def _prior_variances(tau, lam):
     if not (np.isfinite(tau) and tau > 0):
         raise ValueError("tau must be positive and finite")
-    if np.any(~np.isfinite(lam)) or np.any(lam <= 0):
+    if not _all_positive_finite(lam):
         raise ValueError("lambda entries must be positive and finite")
-    return Preconditioner(PreconditionerKind.PRIOR, (tau * lam) ** 2)
+    return (tau * _as_f64(lam)) ** 2
 
 
-def jacobi_preconditioner(X, omega, tau, lam, prior_precision=None):
-    """M = diag(Phi) (precond.py:105-117); diag(X'ΩX) is one CSC pass on device."""
-    if prior_precision is None:
-        lam = np.asarray(lam, dtype=np.float64)
-        prior_precision = (tau * lam) ** -2.0
-    diag = np.asarray(X.gram_diagonal(omega)) + prior_precision
-    if np.any(diag <= 0) or np.any(~np.isfinite(diag)):
-        raise DegeneratePreconditionerError("Phi has a nonpositive diagonal entry")
-    return Preconditioner(PreconditionerKind.JACOBI, 1.0 / diag)
+def prior_preconditioner(tau, lam):
+    """M⁻¹ = τ²Λ², the prior covariance of the shrunk block."""
+    return Preconditioner(PreconditionerKind.PRIOR, _prior_variances(tau, lam))
 
 
 def augmented_prior(tau, lam, gamma):
-    """[gamma^2, (tau lam)^2] over the unshrunk + shrunk blocks (precond.py:120-134)."""
-    gamma = np.asarray(gamma, dtype=np.float64)
+    """Prior preconditioner extended over the unshrunk block by γ²."""
+    gamma = _as_f64(gamma)
     if gamma.size == 0:
         return prior_preconditioner(tau, lam)
-    if np.any(~np.isfinite(gamma)) or np.any(gamma <= 0):
+    if not _all_positive_finite(gamma):
         raise ValueError("gamma entries must be positive and finite")
-    lam = np.asarray(lam, dtype=np.float64)
     return Preconditioner(PreconditionerKind.AUGMENTED_PRIOR,
-                          np.concatenate([gamma ** 2, (tau * lam) ** 2]))
+                          np.concatenate([gamma ** 2, _prior_variances(tau, lam)]))
+
+
+def jacobi_preconditioner(X, omega, tau, lam, prior_precision=None):
+    """M⁻¹ = 1/diag(Φ), diag(Φ) = diag(XᵀΩX) + prior precision."""
+    if prior_precision is None:
+        prior_precision = 1.0 / _prior_variances(tau, lam)
+    diag_phi = _as_f64(X.gram_diagonal(omega)) + prior_precision
+    if not _all_positive_finite(diag_phi):
+        raise DegeneratePreconditionerError("Phi has a nonpositive diagonal entry")
+    return Preconditioner(PreconditionerKind.JACOBI, 1.0 / diag_phi)
 
 
 def gamma_policy(chain, c=1.0, prior_sd=None, sd_cap=10.0, sd_floor=1e-3):
-    """c * running sd of the unshrunk draws, cold start min(prior sd, cap) (precond.py:137-153)."""
-    sds = chain.unshrunk_sd() if chain is not None else None
-    if sds is None:
-        if prior_sd is None:
-            raise ValueError("cold-start gamma_policy needs the prior sds")
-        sds = np.minimum(np.asarray(prior_sd, dtype=np.float64), sd_cap)
-    return c * np.maximum(np.asarray(sds, dtype=np.float64), sd_floor)
+    """γ for the unshrunk block: c × max(running sd of its draws, sd_floor);
+    before two draws exist, min(prior sd, sd_cap) (precond.py:137-153)."""
+    running = None if chain is None else chain.unshrunk_sd()
+    if running is not None:
+        base = _as_f64(running)
+    elif prior_sd is not None:
+        base = np.minimum(_as_f64(prior_sd), sd_cap)
+    else:
+        raise ValueError("cold-start gamma_policy needs the prior sds")
+    return c * np.maximum(base, sd_floor)
 
 
 def block_threshold(*args, **kwargs):

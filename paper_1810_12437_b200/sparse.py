@@ -369,40 +369,36 @@ class SparseDesignMatrix:
         return (raw - w.sum() * mu) / sc
 
     def standardize(self, exclude=None):
-        """Centre and scale columns (sparse.py:250-297), host-side setup.
+        """Centre and scale columns in place (sparse.py:250-297); returns self.
 
-        For a binary design a column's sum and sum of squares are its count.
+        Column means and sample sds (ddof 1) over all n rows, implicit zeros
+        included; `exclude` (bool mask or indices) and constant columns (sd
+        below 1e-7 relative to the column's RMS, recorded in
+        `constant_columns`) keep mean 0 and scale 1.  The device applies the
+        result as a rank-one correction around the pattern-only passes.
         """
-        if self.n_rows < 2:
+        n, m = self.n_rows, self.n_cols
+        if n < 2:
             raise ValueError("standardize needs at least 2 rows")
-        keep = np.ones(self.n_cols, dtype=bool)
+        active = np.ones(m, dtype=bool)
         if exclude is not None:
-            exclude = np.asarray(exclude)
-            if exclude.dtype == bool:
-                if exclude.shape != (self.n_cols,):
-                    raise ValueError("boolean exclude mask must have length n_cols")
-                keep &= ~exclude
-            else:
-                keep[exclude] = False
-        vals = self.values
-        col = self.col_idx
-        n = self.n_rows
-        col_sum = np.bincount(col, weights=vals, minlength=self.n_cols)
-        col_sq = np.bincount(col, weights=vals ** 2, minlength=self.n_cols)
-        col_nnz = np.bincount(col, minlength=self.n_cols)
-        mean = col_sum / n
-        ssq = np.bincount(col, weights=(vals - mean[col]) ** 2, minlength=self.n_cols)
-        ssq += (n - col_nnz) * mean ** 2
-        var = ssq / (n - 1)
-        constant = ssq <= (n - 1) * 1e-14 * np.maximum(col_sq / n, 1e-300)
-        self.constant_columns = np.flatnonzero(constant & keep)
-        active = keep & ~constant
-        means = np.zeros(self.n_cols)
-        scales = np.ones(self.n_cols)
-        means[active] = mean[active]
-        scales[active] = np.sqrt(var[active])
-        self.col_means = means
-        self.col_scales = scales
+            ex = np.asarray(exclude)
+            if ex.dtype == bool and ex.shape != (m,):
+                raise ValueError("boolean exclude mask must have length n_cols")
+            active[ex] = False
+        col, val = self.col_idx, self.values
+        per_col = lambda w: np.bincount(col, weights=w, minlength=m)  # noqa: E731
+        mean = per_col(val) / n
+        stored = np.bincount(col, minlength=m)
+        # centred sum of squares in two passes (stored entries, then the
+        # n - stored implicit zeros): no cancellation on near-constant columns
+        centred_ss = per_col((val - mean[col]) ** 2) + (n - stored) * mean ** 2
+        rms_sq = per_col(val * val) / n
+        flat = centred_ss <= (n - 1) * 1e-14 * np.maximum(rms_sq, 1e-300)
+        self.constant_columns = np.flatnonzero(flat & active)
+        use = active & ~flat
+        self.col_means = np.where(use, mean, 0.0)
+        self.col_scales = np.where(use, np.sqrt(centred_ss / (n - 1)), 1.0)
         return self
 
     def gram_diagonal(self, omega):
