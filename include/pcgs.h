@@ -237,6 +237,16 @@ typedef struct {
   double* draws;      /* n_store x p_total                                   */
   double* tau_draws;  /* n_store                                             */
   double* trace; double* alphas; double* betas; /* PCG scratch (max_iter+1) */
+  /* Standardised designs (SparseDesignMatrix.standardize, sparse.py:250-297):
+   * NULL for a raw design.  Otherwise p_total column scales s_j (1 for the
+   * intercept and unstandardised columns) and the scan samples the exact
+   * reparametrisation b~_j = b_j / s_j, b~_0 = b_0 - sum_j mu_j b_j / s_j,
+   * for which X_s b = X b~ on the raw pattern: beta, mean, m2 and draws hold
+   * b~ (the host maps draws back); the scale updates, log prior and tau sums
+   * use b_j = s_j b~_j, and the prior / preconditioner / metric are those of
+   * b~ (precision s_j^2 / (tau lam_j)^2).  Needs an unstandardised intercept
+   * with a flat prior as coefficient 0. */
+  const double* cscale;
 } pcgs_gibbs_t;
 
 /* z = X beta and its log-likelihood partials (start of a chain / resume). */

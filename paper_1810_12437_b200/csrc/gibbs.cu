@@ -83,13 +83,18 @@ __device__ __forceinline__ double tau_term(const pcgs_gibbs_t& G, double b, long
   return b * b / (l * l);
 }
 
+// column scale of the reparametrised coefficient j (standardised designs)
+__device__ __forceinline__ double col_scale(const pcgs_gibbs_t& G, long long j) {
+  return G.cscale ? G.cscale[j] : 1.0;
+}
+
 // partial sums for the tau update from the current beta / lambda (chain start)
 __global__ void __launch_bounds__(256) k_tau_sums(pcgs_gibbs_t G, long long pt) {
   __shared__ double red[64];
   const int q = G.q;
   double acc = 0.0;
   for (long long j = q + blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x)
-    acc += tau_term(G, G.beta[j], j - q);
+    acc += tau_term(G, col_scale(G, j) * G.beta[j], j - q);
   acc = block_sum(acc, red);
   if (threadIdx.x == 0) G.part[(long long)blockIdx.x * kPartStride + 2] = acc;
 }
@@ -132,13 +137,14 @@ __global__ void k_local(pcgs_gibbs_t G, long long pt, int t, int count) {
   const int q = G.q;
   const double tau = G.scal[0];
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x) {
+    const double cs = col_scale(G, j);
     if (j < q) {
       // unshrunk coefficient: prior precision, gamma policy (precond.py:137-153)
       double sd;
       if (count >= 2) sd = sqrt(G.m2[j] / (double)(count - 1));
-      else sd = fmin(G.usd_sd[j], 10.0);
+      else sd = fmin(G.usd_sd[j] / cs, 10.0);
       const double gam = G.gamma_scale * fmax(sd, 1e-3);
-      G.prior_diag[j] = G.usd_prec[j];
+      G.prior_diag[j] = G.usd_prec[j] * cs * cs;
       G.minv[j] = gam * gam;
       G.scale[j] = gam;
       G.beta[j] = count > 0 ? G.mean[j] : 0.0;
@@ -148,7 +154,7 @@ __global__ void k_local(pcgs_gibbs_t G, long long pt, int t, int count) {
     double lam = G.lam[k];
     if (!G.fixed_lam) {
       Philox R(G.seed, kStreamLocal ^ (unsigned long long)t, (unsigned)k);
-      const double b = G.beta[j];
+      const double b = cs * G.beta[j];
       if (G.prior == 0) {
         const double ratio = fabs(b) / tau;
         if (ratio < 1e-10) {
@@ -166,7 +172,7 @@ __global__ void k_local(pcgs_gibbs_t G, long long pt, int t, int count) {
       G.lam[k] = lam;
     }
     if (!(lam > 0.0) || !isfinite(lam)) G.results[8 * (t - 1) + 4] = 1;
-    const double tl = tau * lam;
+    const double tl = tau * lam / cs;  // prior sd of the (reparametrised) coefficient
     G.prior_diag[j] = 1.0 / (tl * tl);
     G.minv[j] = tl * tl;
     G.scale[j] = tl;
@@ -213,13 +219,14 @@ __global__ void __launch_bounds__(256) k_stats(pcgs_gibbs_t G, long long pt, int
   const double tau = G.scal[0];
   double lp = 0.0, ts = 0.0;
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < pt; j += (long long)gridDim.x * blockDim.x) {
-    const double b = G.beta[j];
-    const double scaled = j < q ? b : b / (tau * G.lam[j - q]);
+    const double bt = G.beta[j];             // sampled coordinate
+    const double b = col_scale(G, j) * bt;   // model coefficient (shrinkage, prior)
+    const double scaled = j < q ? bt : b / (tau * G.lam[j - q]);
     const double delta = scaled - G.mean[j];
     const double m = G.mean[j] + delta / (double)count_new;
     G.mean[j] = m;
     if (j < q) G.m2[j] += delta * (scaled - m);
-    if (slot >= 0) G.draws[(long long)slot * pt + j] = b;
+    if (slot >= 0) G.draws[(long long)slot * pt + j] = bt;
     if (slot >= 0 && j == 0) G.tau_draws[slot] = tau;
     if (j < q) {
       const double sd = G.usd_sd[j];

@@ -170,7 +170,37 @@ class _GibbsArgs(ctypes.Structure):
         ("b", ctypes.c_void_p), ("part", ctypes.c_void_p), ("logdens", ctypes.c_void_p),
         ("results", ctypes.c_void_p), ("draws", ctypes.c_void_p), ("tau_draws", ctypes.c_void_p),
         ("trace", ctypes.c_void_p), ("alphas", ctypes.c_void_p), ("betas", ctypes.c_void_p),
+        ("cscale", ctypes.c_void_p),
     ]
+
+
+class _Reparam:
+    """Standardised design X_s = (X - 1 mu') S^-1 with an unstandardised
+    intercept: X_s b = X b~ for b~_j = b_j / s_j (j >= 1) and
+    b~_0 = b_0 - sum_j mu_j b~_j, so the device samples b~ on the raw pattern
+    (exactly the same posterior; include/pcgs.h, pcgs_gibbs_t.cscale)."""
+
+    def __init__(self, X, cfg):
+        mu = np.asarray(X.col_means, dtype=np.float64)
+        sc = np.asarray(X.col_scales, dtype=np.float64)
+        flat0 = cfg.n_unshrunk >= 1 and not np.isfinite(cfg.unshrunk_prior_sd[0])
+        if not (X.has_intercept and mu[0] == 0.0 and sc[0] == 1.0 and flat0):
+            raise NotImplementedError(
+                "standardised designs run on the device through an exact reparametrisation that "
+                "needs an unstandardised intercept column 0 with a flat prior "
+                "(standardize(exclude=[0]) and unshrunk_prior_sd=(inf, ...))")
+        self.mu, self.s = mu, sc
+
+    def to_sampled(self, beta):
+        bt = np.asarray(beta, dtype=np.float64) / self.s
+        bt[..., 0] -= bt[..., 1:] @ self.mu[1:]
+        return bt
+
+    def to_model(self, bt):
+        bt = np.asarray(bt, dtype=np.float64)
+        beta = bt * self.s
+        beta[..., 0] = bt[..., 0] + bt[..., 1:] @ self.mu[1:]
+        return beta
 
 
 _PRECOND = {"prior": 0, "identity": 1, "jacobi": 2}
@@ -195,6 +225,7 @@ class DeviceChain:
         self.horseshoe = isinstance(cfg, HorseshoeConfig)
         self.n_iter, self.burn_in, self.thin = n_iter, burn_in, thin
         self.seed = int(seed)
+        self.reparam = _Reparam(X, cfg) if X.standardized else None
         cgc = cg_config if cg_config is not None else CGConfig()
         if cgc.trace_level == "full":
             raise NotImplementedError("trace_level='full' is not on the device path")
@@ -223,6 +254,9 @@ class DeviceChain:
             xi = init_state.xi if init_state.xi is not None else 1.0
             if beta.shape != (self.pt,) or lam.shape != (self.p,):
                 raise ValueError("initial state does not match the model shape")
+        if self.reparam is not None:
+            beta = self.reparam.to_sampled(beta)
+            self.cscale = dt(self.reparam.s)
         self.beta = dt(beta).clone()
         self.omega = dt(fixed_omega if fixed_omega is not None else omega).clone()
         self.lam = dt(fixed_lam if fixed_lam is not None else lam).clone()
@@ -257,7 +291,7 @@ class DeviceChain:
             minv=P(self.minv), scale=P(self.scale), b=P(self.b), part=P(self.part),
             logdens=P(self.logdens), results=P(self.results), draws=P(self.draws),
             tau_draws=P(self.tau_draws), trace=P(self.trace), alphas=P(self.alphas),
-            betas=P(self.betas))
+            betas=P(self.betas), cscale=P(self.cscale) if self.reparam is not None else None)
         self.count = 0
         self.stored = 0
         L = _lib.lib()
@@ -287,6 +321,8 @@ class DeviceChain:
             torch = _lib.torch()
             torch.cuda.current_stream(self.dev).synchronize()
             beta = self.beta.cpu().numpy()
+            if self.reparam is not None:
+                beta = self.reparam.to_model(beta)
             tau = float(self.scal[0].item())
             lam = np.asarray(local_scale_sampler(beta[self.q:], tau, self.cfg, rng), dtype=np.float64)
             if lam.shape != (self.p,):
@@ -318,14 +354,19 @@ class DeviceChain:
         t = self.n_iter
         res = self.results[: 8 * max(t, 1)].view(-1, 8).cpu().numpy()[:t]
         scal = self.scal.cpu().numpy()
-        state = ShrinkageState(self.beta.cpu().numpy(), self.omega.cpu().numpy(),
+        beta = self.beta.cpu().numpy()
+        draws = self.draws[: self.stored].cpu().numpy()
+        if self.reparam is not None:
+            beta = self.reparam.to_model(beta)
+            draws = self.reparam.to_model(draws)
+        state = ShrinkageState(beta, self.omega.cpu().numpy(),
                                self.lam.cpu().numpy(), float(scal[0]),
                                nu=self.nu.cpu().numpy() if self.horseshoe else None,
                                xi=float(scal[1]) if self.horseshoe else None)
         m2 = self.m2.cpu().numpy()[: self.q]
         var = m2 / (self.count - 1) if self.count >= 2 else np.full(self.q, np.nan)
         return ChainOutput(
-            draws=self.draws[: self.stored].cpu().numpy(),
+            draws=draws,
             tau_draws=self.tau_draws[: self.stored].cpu().numpy(),
             logdensity_trace=self.logdens[:t].cpu().numpy(),
             cg_iteration_counts=res[:, 0].astype(np.int64),
@@ -344,6 +385,12 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
     CPU oracle's).  A `local_scale_sampler(beta_shrunk, tau, cfg, rng)` runs on
     the host between the two halves of each scan (one synchronisation per
     scan), with a numpy Generator seeded from `seed`.
+
+    Standardised designs (`X.standardize(...)`) run through an exact
+    reparametrisation on the raw pattern (`_Reparam`; needs an unstandardised
+    intercept with a flat prior); draws and the final state come back in the
+    model's coordinates, the running statistics of the unshrunk block stay in
+    the sampled ones.
     """
     y = np.asarray(y, dtype=np.float64)
     if y.shape != (X.n_rows,):
@@ -366,9 +413,6 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
     q = cfg.n_unshrunk
     if X.n_cols - q < 0:
         raise ValueError("more unshrunk prior sds than design columns")
-    if X.standardized:
-        raise NotImplementedError("the device Gibbs scan runs on raw binary designs; "
-                                  "standardised designs are supported by the operator / pcg_solve API")
     if (isinstance(cfg, BridgeConfig) and cfg.alpha != 1.0 and fixed_lam is None
             and local_scale_sampler is None):
         raise UnsupportedUpdateError(

@@ -75,6 +75,50 @@ def test_pinned_scales_give_exact_gaussian(small):
     assert np.median(emp / np.diag(cov)) == pytest.approx(1.0, abs=0.1)
 
 
+@pytest.mark.parametrize("prior", ["bridge", "horseshoe"])
+def test_standardized_design_pinned_scales_exact_gaussian(small, prior):
+    """Standardised design (sparse.py:250-297): the device samples the exact
+    reparametrisation b~ on the raw pattern; with omega, tau, lambda pinned the
+    returned draws must be N(Phi_s^-1 X_s'kappa, Phi_s^-1) in the model's
+    coordinates."""
+    d, y, _ = small
+    X = d.matrix().standardize(exclude=[0])
+    rng = np.random.default_rng(3)
+    om = rng.uniform(0.1, 0.3, d.n)
+    lam = rng.uniform(0.5, 2.0, d.p)
+    tau = 0.2
+    cls = gibbs.BridgeConfig if prior == "bridge" else gibbs.HorseshoeConfig
+    cfg = cls(unshrunk_prior_sd=(np.inf,))
+    out = gibbs.gibbs_run(X, y, cfg, 3000, burn_in=0, seed=4, fixed_omega=om, fixed_tau=tau, fixed_lam=lam,
+                          cg_config=gibbs.CGConfig(rtol=1e-10))
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    dense = np.zeros((d.n, d.p + 1))
+    dense[np.repeat(np.arange(d.n), np.diff(Xo.row_ptr)), Xo.col_idx] = 1.0
+    dense_s = (dense - X.col_means) / X.col_scales
+    prior_prec = np.concatenate([[0.0], (tau * lam) ** -2.0])
+    cov = np.linalg.inv(dense_s.T @ (om[:, None] * dense_s) + np.diag(prior_prec))
+    mean = cov @ (dense_s.T @ (y - 0.5))
+    z = (out.draws.mean(0) - mean) / np.sqrt(np.diag(cov) / len(out.draws))
+    assert np.mean(np.abs(z) > 4) < 0.02
+    assert np.median(np.var(out.draws, axis=0) / np.diag(cov)) == pytest.approx(1.0, abs=0.1)
+    assert np.all(np.isfinite(out.logdensity_trace))
+    # the final state is reported in model coordinates too
+    np.testing.assert_allclose(dense_s @ out.final_state.beta, X.device_matvec(
+        __import__("torch").as_tensor(out.final_state.beta, device="cuda")).cpu().numpy(), rtol=1e-9, atol=1e-9)
+
+
+def test_standardized_chain_runs_free_scales(small):
+    d, y, _ = small
+    X = d.matrix().standardize(exclude=[0])
+    out = gibbs.gibbs_run(X, y, gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,)), 300, burn_in=50, seed=5)
+    assert out.draws.shape == (250, d.p + 1) and np.all(np.isfinite(out.draws))
+    assert np.all(np.isfinite(out.logdensity_trace)) and np.all(out.cg_iteration_counts > 0)
+    with pytest.raises(NotImplementedError):
+        gibbs.gibbs_run(X, y, gibbs.BridgeConfig(unshrunk_prior_sd=(5.0,)), 2)
+    Xn = d.matrix().standardize()   # intercept is constant: left untouched, still fine
+    gibbs.gibbs_run(Xn, y, gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,)), 3)
+
+
 def test_bitwise_reproducible_and_shapes(small):
     d, y, _ = small
     X = d.matrix()
