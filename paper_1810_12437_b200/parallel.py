@@ -177,3 +177,51 @@ def sharded_pcg_solve(op: ShardedPrecisionOperator, b, M, x0=None, config=None, 
         betas=betas[:_n_betas(iterations, status)].copy(),
         iterates=None,
     )
+
+
+# ---------------------------------------------------------------------------
+# Independent chains across ranks (BASELINE config 4)
+# ---------------------------------------------------------------------------
+def chain_seed(seed, chain) -> int:
+    """Per-chain seed derived from (seed, chain index): distinct, reproducible
+    and independent of how chains are spread over ranks."""
+    state = np.random.SeedSequence([int(seed) & (2 ** 63 - 1), int(chain)]).generate_state(2, dtype=np.uint32)
+    return int(state[0]) | (int(state[1]) << 32)
+
+
+def chain_assignment(n_chains, world, rank):
+    """Contiguous block of chain indices run by `rank` (sizes differ by ≤ 1)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("need 0 <= rank < world")
+    base, extra = divmod(int(n_chains), int(world))
+    lo = rank * base + min(rank, extra)
+    return list(range(lo, lo + base + (1 if rank < extra else 0)))
+
+
+def run_chains(X, y, cfg, n_iter, n_chains, seed=0, group=None, gather=True, runner=None, **kwargs):
+    """Run `n_chains` independent Gibbs chains, sharded over the ranks of
+    `group` (default: the initialised torch.distributed world, else one
+    process).  Chain c uses `chain_seed(seed, c)`; each rank runs its block
+    of chains one after another on its GPU (`gibbs_run`).  There is no
+    collective while sampling; with `gather` the outputs are all-gathered at
+    the end (object collective) and every rank returns all chains in index
+    order, otherwise only its own (as {chain: ChainOutput})."""
+    import torch.distributed as dist
+    if runner is None:
+        from .gibbs import gibbs_run as runner
+    if group is None and dist.is_available() and dist.is_initialized():
+        group = dist.group.WORLD
+    world = dist.get_world_size(group) if group is not None else 1
+    rank = dist.get_rank(group) if group is not None else 0
+    mine = {c: runner(X, y, cfg, n_iter, seed=chain_seed(seed, c), **kwargs)
+            for c in chain_assignment(n_chains, world, rank)}
+    if not gather:
+        return mine
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, mine, group=group)
+        merged = {}
+        for part in parts:
+            merged.update(part)
+        mine = merged
+    return [mine[c] for c in range(n_chains)]

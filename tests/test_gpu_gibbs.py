@@ -175,3 +175,16 @@ def test_paper_scale_bridge_chain_runs():
     out = gibbs.gibbs_run(d.matrix(), y, gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,)), 20, seed=1)
     assert np.all(np.isfinite(out.draws)) and out.cg_iteration_counts.max() < 50
     assert np.all(np.diff(out.logdensity_trace[5:]) < 1e4)
+
+
+def test_run_chains_single_process_matches_direct_runs(small):
+    from paper_1810_12437_b200 import parallel
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
+    outs = parallel.run_chains(X, y, cfg, 20, n_chains=3, seed=9, burn_in=5)
+    assert len(outs) == 3
+    for c, o in enumerate(outs):
+        ref = gibbs.gibbs_run(X, y, cfg, 20, burn_in=5, seed=parallel.chain_seed(9, c))
+        np.testing.assert_array_equal(o.draws, ref.draws)
+    assert not np.array_equal(outs[0].draws, outs[1].draws)
