@@ -7,12 +7,14 @@ and re-raises the reference's exception classes.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 import numpy as np
 
-_LIB_PATH = Path(__file__).resolve().with_name("libpcgs.so")
+# PCGS_LIBRARY points at an alternative build (A/B timing of two builds)
+_LIB_PATH = Path(os.environ.get("PCGS_LIBRARY") or Path(__file__).resolve().with_name("libpcgs.so"))
 _lock = threading.Lock()
 _lib = None
 
