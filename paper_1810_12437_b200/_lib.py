@@ -69,6 +69,7 @@ SIGNATURES = {
     "pcgs_debug_profile": (ctypes.c_int, [_P]),
     "pcgs_debug_option": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
     "pcgs_debug_cta_times": (ctypes.c_int, [_P]),
+    "pcgs_debug_sync_times": (ctypes.c_int, [_P]),
     "pcgs_pg_draw": (ctypes.c_int, [_P, _I64, _U64, _U64, _P, _P]),
     "pcgs_gibbs_init": (ctypes.c_int, [_P, _P, _P]),
     "pcgs_batch_slab_max": (ctypes.c_int, [ctypes.c_int]),

@@ -152,6 +152,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// debug: per-CTA arrival/departure stamps at the four grid barriers of one
+// PCG iteration (debug option key 1 bit 128), [8 * cta + 2 * barrier + {0,1}]
+__device__ unsigned long long* g_sync_times = nullptr;
+constexpr int kSyncTraceIter = 10;
+
 struct FillDir {  // search direction: first ? a : a + beta * b   (internal layout)
   const double* a;
   const double* b;
@@ -262,6 +267,13 @@ __device__ __forceinline__ double owned_column_sum(const OwnState& o, const doub
   return total;
 }
 
+__device__ __forceinline__ void traced_sync(const PcgArgs& A, int a, int k) {
+  const bool tr = (A.D.dbg & 128) && a == kSyncTraceIter && threadIdx.x == 0 && g_sync_times;
+  if (tr) g_sync_times[8 * blockIdx.x + 2 * k] = gtimer();
+  cg::this_grid().sync();
+  if (tr) g_sync_times[8 * blockIdx.x + 2 * k + 1] = gtimer();
+}
+
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
   // Loop state lives in shared memory so that the inlined streaming passes
   // get the whole register budget (1024 threads -> 64 registers).
@@ -365,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
         o.d[t] = dn;
         if (j0 + t < pt) A.dvg[(a & 1) * dvs + j0 + t] = dn;
       }
-      cg::this_grid().sync();
+      traced_sync(A, a, 0);
     }
     if (prof) A.prof[4 * a + 0] = gtimer();
 
@@ -400,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       if (tid == 0) A.part[blockIdx.x * kPartStride] = t;
     }
     if (prof) A.prof[4 * a + 1] = gtimer();
-    cg::this_grid().sync();
+    traced_sync(A, a, 1);
 
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
     {
@@ -409,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       run_pass(A.D.csc, sv, f, e, A.D.dbg);
     }
     if (prof) A.prof[4 * a + 2] = gtimer();
-    cg::this_grid().sync();
+    traced_sync(A, a, 2);
     if (tid == 0) ++st_applies;
     if (prof) A.prof[4 * a + 3] = gtimer();
 
@@ -454,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       A.part[blockIdx.x * kPartStride + 1] = t_rms;
       A.part[blockIdx.x * kPartStride + 2] = t_rz;
     }
-    cg::this_grid().sync();
+    traced_sync(A, a, 3);
   }
 
   __syncthreads();
@@ -1044,6 +1056,12 @@ int pcgs_pcg_op_full(pcgs_apply_fn fn, void* ctx, int64_t p, const double* minv,
 
 int pcgs_debug_profile(void* buf) {
   g_prof = (unsigned long long*)buf;
+  return PCGS_OK;
+}
+
+int pcgs_debug_sync_times(void* buf) {
+  unsigned long long* p = (unsigned long long*)buf;
+  CUDA_TRY(cudaMemcpyToSymbol(g_sync_times, &p, sizeof(p)));
   return PCGS_OK;
 }
 

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -186,6 +187,18 @@ void cut(const std::vector<uint64_t>& pre, size_t a, size_t b, int parts, std::v
   outv.push_back(b);
 }
 
+// Per-segment charge of the balancing cost model, in vectors: a segment close
+// costs a warp reduction and an epilogue (~12 vectors' worth of issue slots,
+// measured as the best per-iteration PCG time at config 2 over 0..48;
+// tools/segw_sweep.sh).  PCGS_SEG_WEIGHT overrides it (tuning experiments).
+uint64_t seg_weight16() {
+  static const uint64_t w = [] {
+    const char* e = getenv("PCGS_SEG_WEIGHT");
+    return (uint64_t)((e ? atof(e) : 12.0) * 16.0 + 0.5);
+  }();
+  return w;
+}
+
 void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G) {
   const int ns = (int)slabs.size();
   P.cta_task_ptr.assign(G + 1, 0);
@@ -196,7 +209,10 @@ void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G) {
   for (int s = 0; s < ns; ++s) {
     auto& pr = pre[s];
     pr.assign(slabs[s].segs.size() + 1, 0);
-    for (size_t q = 0; q < slabs[s].segs.size(); ++q) pr[q + 1] = pr[q] + slabs[s].segs[q].nv;
+    // cost model for balancing: a vector plus a per-segment charge (segment
+    // closes: reductions, epilogue), in 1/16 vector units
+    for (size_t q = 0; q < slabs[s].segs.size(); ++q)
+      pr[q + 1] = pr[q] + 16u * slabs[s].segs[q].nv + seg_weight16();
     sw[s] = pr.back();
     W += sw[s];
   }

@@ -23,3 +23,16 @@ for mode in [int(x) for x in sys.argv[1:]]:
               f"end min {end.min():.1f} med {np.median(end):.1f} p90 {np.percentile(end,90):.1f} max {end.max():.1f}")
         print("   slowest CTAs", np.argsort(-end)[:8], "fastest", np.argsort(end)[:8])
 _lib.lib().pcgs_debug_option(1, 0)
+if len(sys.argv) > 1 and sys.argv[1] == "0":
+    # end-time profile along the CTA index (CTAs are assigned to slabs in order)
+    _lib.lib().pcgs_debug_option(1, 64)
+    for name, fn in (("csr", lambda: st.matvec(v)), ("csc", lambda: st.matvec_t(w))):
+        ends = []
+        for _ in range(5):
+            fn()
+            torch.cuda.synchronize()
+            t = buf.cpu().numpy().reshape(-1, 3).astype(np.float64)
+            ends.append((t[:, 2] - t[:, 0].min()) / 1e3)
+        e = np.median(np.array(ends), axis=0)
+        print(name, "end by CTA group of 8:", " ".join(f"{x:.0f}" for x in e.reshape(-1, 4).mean(1)[:37]))
+    _lib.lib().pcgs_debug_option(1, 0)
