@@ -194,9 +194,10 @@ int pcgs_debug_option(int key, int value);
 /* Debug: device buffer (3 uint64 per CTA) for per-CTA pass timestamps when
  * the debug-option key 1 bit 64 is set. */
 int pcgs_debug_cta_times(void* buf);
-/* Debug: device buffer (8 uint64 per CTA) receiving, for PCG iteration 10,
+/* Debug: device buffer (16 uint64 per CTA) receiving, for PCG iteration 10,
  * each CTA's arrival / departure times at the four grid barriers of an
- * iteration when the debug-option key 1 bit 128 is set. */
+ * iteration ([0..7]) and stamps inside the step phase ([8..12]) when the
+ * debug-option key 1 bit 128 is set. */
 int pcgs_debug_sync_times(void* buf);
 
 /* omega[i] ~ PG(1, z[i]) (pg_draw_batch, polya_gamma.py:39-84), Philox keyed

@@ -153,9 +153,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 // debug: per-CTA arrival/departure stamps at the four grid barriers of one
-// PCG iteration (debug option key 1 bit 128), [8 * cta + 2 * barrier + {0,1}]
+// PCG iteration (debug option key 1 bit 128), [16 * cta + 2 * barrier + {0,1}],
+// and stamps inside phase C at [16 * cta + 8 + k]
 __device__ unsigned long long* g_sync_times = nullptr;
 constexpr int kSyncTraceIter = 10;
+constexpr int kMaxGrid = 256;  // persistent-kernel grid bound (one CTA per SM; B200: 148)
 
 struct FillDir {  // search direction: first ? a : a + beta * b   (internal layout)
   const double* a;
@@ -269,9 +271,14 @@ __device__ __forceinline__ double owned_column_sum(const OwnState& o, const doub
 
 __device__ __forceinline__ void traced_sync(const PcgArgs& A, int a, int k) {
   const bool tr = (A.D.dbg & 128) && a == kSyncTraceIter && threadIdx.x == 0 && g_sync_times;
-  if (tr) g_sync_times[8 * blockIdx.x + 2 * k] = gtimer();
+  if (tr) g_sync_times[16 * blockIdx.x + 2 * k] = gtimer();
   cg::this_grid().sync();
-  if (tr) g_sync_times[8 * blockIdx.x + 2 * k + 1] = gtimer();
+  if (tr) g_sync_times[16 * blockIdx.x + 2 * k + 1] = gtimer();
+}
+
+__device__ __forceinline__ void trace_stamp(const PcgArgs& A, int a, int k) {
+  if ((A.D.dbg & 128) && a == kSyncTraceIter && threadIdx.x == 0 && g_sync_times)
+    g_sync_times[16 * blockIdx.x + 8 + k] = gtimer();
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
@@ -428,7 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     // ---------------- phase C: assemble, step, residual ----------------
     double alpha = 0.0;
     const int S = A.D.csc.nslab;
+    trace_stamp(A, a, 0);
     const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
+    trace_stamp(A, a, 1);
     if (a > 0) {
       const double dAd = reduce_partials(A.part, gridDim.x, bc);
       if (!(dAd > 0.0)) {
@@ -442,6 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       alpha = st_rz / dAd;
       if (blockIdx.x == 0 && tid == 0) A.alphas[a - 1] = alpha;
     }
+    trace_stamp(A, a, 2);
     double t_rms = 0.0, t_rz = 0.0;
     for (int t = tid; t < chunk; t += kThreads) {
       if (j0 + t >= pt) continue;
@@ -461,11 +471,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       t_rms += tj * tj;
       t_rz += rv * zn;
     }
+    trace_stamp(A, a, 3);
     block_sum2(t_rms, t_rz, red);
     if (tid == 0) {
       A.part[blockIdx.x * kPartStride + 1] = t_rms;
       A.part[blockIdx.x * kPartStride + 2] = t_rz;
     }
+    trace_stamp(A, a, 4);
     traced_sync(A, a, 3);
   }
 
@@ -589,7 +601,7 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int
   CUDA_TRY(cudaSetDevice(device));
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-  const int G = prop.multiProcessorCount;
+  const int G = std::min(prop.multiProcessorCount, kMaxGrid);
   DesignHost H;
   std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H);
   if (!err.empty()) return fail(PCGS_EINVAL, err);

@@ -15,17 +15,22 @@ phi = pk.PrecisionOperator(X, cond["omega"], cond["prior_diag"])
 dev = phi.store.device
 b = torch.tensor(np.random.default_rng(7).standard_normal(des.p + 1) * 10, device=dev)
 mt, st = torch.tensor(cond["minv"], device=dev), torch.tensor(cond["scale"], device=dev)
-buf = torch.zeros(8 * 148, dtype=torch.int64, device=dev)
+buf = torch.zeros(16 * 148, dtype=torch.int64, device=dev)
 _lib.lib().pcgs_debug_sync_times(buf.data_ptr())
 _lib.lib().pcgs_debug_option(1, 128)
 runs = []
 for _ in range(5):
     pk.cg.pcg_solve_device(phi, b, mt, st, rtol=1e-30, max_iter=20)
     torch.cuda.synchronize()
-    runs.append(buf.cpu().numpy().reshape(148, 4, 2).astype(np.float64))
+    runs.append(buf.cpu().numpy().reshape(148, 16).astype(np.float64))
 _lib.lib().pcgs_debug_option(1, 0)
 names = ["dir", "csr", "csc", "stepC"]
-for r in runs[2:]:
+for rr in runs[2:]:
+    r = rr[:, :8].reshape(148, 4, 2)
+    c = rr[:, 8:13]
+    dep2 = r[:, 2, 1]
+    print("phase C stamps after sync2 (median us): stage-start %.2f staged %.2f dAd %.2f loop %.2f sum %.2f" %
+          tuple(np.median(c[:, k] - dep2) / 1e3 for k in range(5)))
     t0 = r[:, 0, 1].max()   # everyone left barrier 0 (start of the CSR pass)
     line = []
     prev_dep = r[:, 0, 1]
