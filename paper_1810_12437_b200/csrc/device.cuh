@@ -27,6 +27,8 @@ struct DesignDev {
   int smem_doubles;    // dynamic shared memory per CTA, in doubles
   int dbg;             // tuning experiments: bit 0 skip gathers, bit 1 skip segmented reduce
   PassDev csr, csc;
+  double* own_global;  // PCG own-slice state in global memory (8 x chunk per CTA) when it
+                       // does not fit next to the slab in shared memory (very wide designs)
 };
 
 // ------------------------------------------------------------------ utilities

@@ -195,13 +195,15 @@ struct OwnState {
 
 __host__ __device__ inline bool pp_in_smem(const DesignDev& D) {
   const long long chunk = (D.pt + D.G - 1) / D.G;
-  const long long bytes = (long long)D.smem_doubles * 8 + chunk * 8 * 8 + (long long)D.csc.nslab * (chunk + 1) * 4;
+  const long long own = D.own_global ? 0 : chunk * 8 * 8;
+  const long long bytes = (long long)D.smem_doubles * 8 + own + (long long)D.csc.nslab * (chunk + 1) * 4;
   return bytes + 1024 <= 227 * 1024;
 }
 
 __device__ __forceinline__ OwnState own_state(double* sv, const DesignDev& D, int chunk, long long j0) {
   OwnState o;
-  double* base = sv + D.smem_doubles;
+  double* base = D.own_global ? D.own_global + (size_t)blockIdx.x * 8 * chunk : sv + D.smem_doubles;
+  double* after = D.own_global ? sv + D.smem_doubles : base + 8 * chunk;
   o.x = base;
   o.r = base + chunk;
   o.d = base + 2 * chunk;
@@ -211,7 +213,7 @@ __device__ __forceinline__ OwnState own_state(double* sv, const DesignDev& D, in
   o.b = base + 6 * chunk;
   o.z = base + 7 * chunk;
   if (pp_in_smem(D)) {
-    o.pp = (const int*)(base + 8 * chunk);
+    o.pp = (const int*)after;
     o.pp_stride = chunk + 1;
     o.pp_off = 0;
     o.pp_lim = chunk;
@@ -226,7 +228,7 @@ __device__ __forceinline__ OwnState own_state(double* sv, const DesignDev& D, in
 
 size_t pcg_smem_bytes(const DesignDev& D) {
   const long long chunk = (D.pt + D.G - 1) / D.G;
-  size_t b = (size_t)D.smem_doubles * 8 + (size_t)chunk * 8 * 8 + 16;
+  size_t b = (size_t)D.smem_doubles * 8 + (D.own_global ? 0 : (size_t)chunk * 8 * 8) + 16;
   if (pp_in_smem(D)) b += (size_t)D.csc.nslab * (chunk + 1) * 4;
   return b;
 }
@@ -605,7 +607,6 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int
   DesignHost H;
   std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H);
   if (!err.empty()) return fail(PCGS_EINVAL, err);
-  if ((H.p_total + G - 1) / G > kThreads) return fail(PCGS_EUNSUP, "p_total too large for the persistent PCG slice");
   pcgs_design* D = new pcgs_design();
   D->device = device;
   DesignDev& dd = D->dev;
@@ -618,7 +619,21 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int
   for (const PassHost* P : {&H.csr, &H.csc})
     for (int q = 0; q < P->nslab; ++q) maxlen = std::max<int64_t>(maxlen, P->slab_lo[q + 1] - P->slab_lo[q]);
   dd.smem_doubles = (int)((maxlen + 1 + 15) / 16 * 16);
+  dd.own_global = nullptr;
   int rc;
+  {
+    // own-slice PCG state next to the slab when it fits, else in global memory
+    const long long chunk = (H.p_total + G - 1) / G;
+    if ((long long)dd.smem_doubles * 8 + chunk * 64 + 16 + 1024 > 227 * 1024) {
+      void* og = nullptr;
+      if (cudaMalloc(&og, (size_t)G * 8 * chunk * sizeof(double)) != cudaSuccess) {
+        pcgs_design_destroy(D);
+        return fail(PCGS_ENOMEM, "device allocation failed (PCG state)");
+      }
+      D->allocs.push_back(og);
+      dd.own_global = (double*)og;
+    }
+  }
   if ((rc = upload_pass(D, H.csr, dd.csr)) || (rc = upload_pass(D, H.csc, dd.csc))) {
     pcgs_design_destroy(D);
     return rc;

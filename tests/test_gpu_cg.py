@@ -230,3 +230,25 @@ def test_many_slabs_and_global_piece_pointers():
                        config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv))
     oref = port.pcg(lambda x: port.phi_apply(Xo, om, diag, x), b, minv, np.sqrt(minv), rtol=1e-10)
     assert rel(rep.solution, oref.x) < 1e-8
+
+
+def test_wide_design_keeps_pcg_state_in_global_memory():
+    """p_total = 200,001: the own-slice PCG state (8 x 1,352 doubles per CTA) no
+    longer fits next to the slab in shared memory and lives in global memory."""
+    d = synth.native_binary_design(4000, 200_000, 1e-4, 5e-3, seed=21)
+    X = d.matrix()
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    rng = np.random.default_rng(5)
+    om = rng.uniform(0.05, 0.3, d.n)
+    lam = rng.uniform(0.5, 2.0, d.p)
+    diag = np.concatenate([[0.0], (0.05 * lam) ** -2.0])
+    minv = np.concatenate([[100.0], (0.05 * lam) ** 2])
+    v = rng.standard_normal(d.p + 1)
+    phi = pk.PrecisionOperator(X, om, diag)
+    assert rel(phi.apply(v), port.phi_apply(Xo, om, diag, v)) < 1e-12
+    b = port.rhs(Xo, np.zeros(d.p + 1), om, diag, rng)
+    rep = pk.pcg_solve(phi, b, pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv),
+                       config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv))
+    oref = port.pcg(lambda x: port.phi_apply(Xo, om, diag, x), b, minv, np.sqrt(minv), rtol=1e-10)
+    assert rel(rep.solution, oref.x) < 1e-8
+    assert abs(rep.iterations - oref.iterations) <= 2
