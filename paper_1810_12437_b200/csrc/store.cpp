@@ -187,16 +187,23 @@ void cut(const std::vector<uint64_t>& pre, size_t a, size_t b, int parts, std::v
   outv.push_back(b);
 }
 
-// Per-segment charge of the balancing cost model, in vectors: a segment close
-// costs a warp reduction and an epilogue (~12 vectors' worth of issue slots,
-// measured as the best per-iteration PCG time at config 2 over 0..48;
-// tools/segw_sweep.sh).  PCGS_SEG_WEIGHT overrides it (tuning experiments).
-uint64_t seg_weight16() {
-  static const uint64_t w = [] {
-    const char* e = getenv("PCGS_SEG_WEIGHT");
-    return (uint64_t)((e ? atof(e) : 12.0) * 16.0 + 0.5);
-  }();
-  return w;
+// Balancing cost model, in 1/16 vector units: one unit per vector, plus a
+// charge per segment for its close (the warp reduction that ends it and its
+// epilogue).  Reductions are paid per 32-vector block that contains segment
+// starts, so short segments sharing a block share that cost: the charge is
+// emit + block * min(len, 32) / 32.  Defaults from sweeps of the PCG iteration
+// time at config 2 (tools/segw_sweep.sh); PCGS_SEG_WEIGHT / PCGS_SEG_EMIT
+// override them for tuning experiments.
+double env_or(const char* name, double dflt) {
+  const char* e = getenv(name);
+  return e ? atof(e) : dflt;
+}
+
+uint64_t seg_charge16(uint32_t nv) {
+  static const double block = env_or("PCGS_SEG_WEIGHT", 24.0);
+  static const double emit = env_or("PCGS_SEG_EMIT", 0.0);
+  const double frac = nv >= 32 ? 1.0 : (double)nv / 32.0;
+  return (uint64_t)((emit + block * frac) * 16.0 + 0.5);
 }
 
 void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G) {
@@ -212,7 +219,7 @@ void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G) {
     // cost model for balancing: a vector plus a per-segment charge (segment
     // closes: reductions, epilogue), in 1/16 vector units
     for (size_t q = 0; q < slabs[s].segs.size(); ++q)
-      pr[q + 1] = pr[q] + 16u * slabs[s].segs[q].nv + seg_weight16();
+      pr[q + 1] = pr[q] + 16u * slabs[s].segs[q].nv + seg_charge16(slabs[s].segs[q].nv);
     sw[s] = pr.back();
     W += sw[s];
   }
