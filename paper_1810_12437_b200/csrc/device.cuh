@@ -239,7 +239,19 @@ __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, doub
 // kPrefetchBlocks blocks of a warp's range, issued before the slab fill; the
 // batch loop then keeps a sliding window of kPrefetchBlocks ahead of its loads,
 // so DRAM requests arrive in consumption order.
-constexpr int kPrefetchBlocks = 16;
+// Prefetch windows (blocks of 512 B per warp), tuned on the config-2 PCG
+// iteration (tools/ab_prefetch.sh): 16/16 -> 100.0 us, 8/8 -> 96.6 us,
+// 6/6 -> 96.0 us (plateau 5..6).  A large first window floods HBM just when
+// the slab fill needs the memory system; a short sliding distance keeps the
+// prefetches in consumption order.
+#ifndef PCGS_PREFETCH_DIST
+#define PCGS_PREFETCH_DIST 6
+#endif
+constexpr int kPrefetchBlocks = PCGS_PREFETCH_DIST;  // sliding L2 prefetch distance, blocks
+#ifndef PCGS_PREFETCH0
+#define PCGS_PREFETCH0 6
+#endif
+constexpr int kPrefetchFirst = PCGS_PREFETCH0;  // blocks prefetched before the slab fill
 __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int dbg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane != 0 || (dbg & 4)) return;
@@ -249,7 +261,7 @@ __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int d
   const int nb = (nvec + 31) >> 5;
   const char* p0 = (const char*)(P.vec + R.x);
   const unsigned total = (unsigned)nvec * 16u;
-  const unsigned bytes = (dbg & 16) ? total : min(total, (unsigned)kPrefetchBlocks * 512u);
+  const unsigned bytes = (dbg & 16) ? total : min(total, (unsigned)kPrefetchFirst * 512u);
   for (unsigned off = 0; off < bytes; off += 16384u) {
     const unsigned sz = bytes - off < 16384u ? bytes - off : 16384u;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0 + off), "r"(sz) : "memory");
