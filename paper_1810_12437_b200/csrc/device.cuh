@@ -171,7 +171,10 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
     asm volatile("fence.proxy.async.global;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_addr(B.mbar)), "r"(bytes)
                  : "memory");
-    const unsigned CH = 32768;
+#ifndef PCGS_FILL_CHUNK
+#define PCGS_FILL_CHUNK 32768
+#endif
+    const unsigned CH = PCGS_FILL_CHUNK;
     for (unsigned off = 0; off < bytes; off += CH) {
       const unsigned sz = bytes - off < CH ? bytes - off : CH;
       asm volatile(
@@ -200,7 +203,15 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
 // descriptors (start mask + first segment id) drive a segmented reduction whose
 // open segment is carried across blocks in a per-lane accumulator.
 // ---------------------------------------------------------------------------
-constexpr int kRing = 4;
+// Blocks per load batch.  Tuned on the config-2 PCG iteration with the
+// prefetch windows below (tools/ab_variants.sh): 1 -> 103, 2 -> 93.4, 3 -> 94.2,
+// 4 -> 96.1, 5 -> 112 us (4+ spill at the 64-register cap); issuing the next
+// batch before consuming the current one (software pipelining) was slower
+// at every depth (2: 105.8 us).
+#ifndef PCGS_RING
+#define PCGS_RING 2
+#endif
+constexpr int kRing = PCGS_RING;
 
 template <class Epi>
 __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, double& acc, unsigned& open_id,
@@ -240,16 +251,16 @@ __device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, doub
 // batch loop then keeps a sliding window of kPrefetchBlocks ahead of its loads,
 // so DRAM requests arrive in consumption order.
 // Prefetch windows (blocks of 512 B per warp), tuned on the config-2 PCG
-// iteration (tools/ab_prefetch.sh): 16/16 -> 100.0 us, 8/8 -> 96.6 us,
-// 6/6 -> 96.0 us (plateau 5..6).  A large first window floods HBM just when
-// the slab fill needs the memory system; a short sliding distance keeps the
-// prefetches in consumption order.
+// iteration (tools/ab_prefetch.sh, ab_variants.sh): with 4-block batches
+// 16/16 -> 100.0 us, 8/8 -> 96.6, 6/6 -> 96.0; with 2-block batches 4/4 ->
+// 93.4 us.  A large first window floods HBM just when the slab fill needs the
+// memory system; a short sliding distance keeps prefetches in consumption order.
 #ifndef PCGS_PREFETCH_DIST
-#define PCGS_PREFETCH_DIST 6
+#define PCGS_PREFETCH_DIST 4
 #endif
 constexpr int kPrefetchBlocks = PCGS_PREFETCH_DIST;  // sliding L2 prefetch distance, blocks
 #ifndef PCGS_PREFETCH0
-#define PCGS_PREFETCH0 6
+#define PCGS_PREFETCH0 4
 #endif
 constexpr int kPrefetchFirst = PCGS_PREFETCH0;  // blocks prefetched before the slab fill
 __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int dbg) {

@@ -16,7 +16,14 @@ namespace pcgs {
 
 namespace {
 
-constexpr int64_t kPieceMaxVec = 256;  // CSC pieces: at most 256 vectors (load balance)
+// CSC pieces: at most this many vectors (load balance); PCGS_PIECE_MAX overrides (tuning)
+int64_t piece_max_vec() {
+  static const int64_t v = [] {
+    const char* e = getenv("PCGS_PIECE_MAX");
+    return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)256;
+  }();
+  return v;
+}
 
 std::vector<int64_t> make_slabs(int64_t len, int64_t slab_max) {
   std::vector<int64_t> lo;
@@ -332,7 +339,9 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
       for (int64_t i = 0; i < n; ++i)
         for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) row_idx[fill[col_idx[k]]++] = (int32_t)i;
     }
-    P.slab_lo = make_slabs(n, smax);
+    // PCGS_CSC_SLAB_MAX caps the row slabs separately (tuning experiments)
+    const char* cs = getenv("PCGS_CSC_SLAB_MAX");
+    P.slab_lo = make_slabs(n, cs ? std::max<int64_t>(16, std::min<int64_t>(smax, atoll(cs))) : smax);
     P.nslab = (int)P.slab_lo.size() - 1;
     P.piece_ptr.assign((size_t)P.nslab * (pt + 1), 0);
     std::vector<int64_t> cursor(col_ptr.begin(), col_ptr.end() - 1);
@@ -354,8 +363,8 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
           for (int64_t i = lo; i < hi; ++i) tmp.push_back((uint16_t)(i - lo));
         }
         const int64_t len = (int64_t)tmp.size();
-        for (int64_t a = 0; a < len; a += kPieceMaxVec * kVecIdx) {
-          const int64_t m = std::min<int64_t>(kPieceMaxVec * kVecIdx, len - a);
+        for (int64_t a = 0; a < len; a += piece_max_vec() * kVecIdx) {
+          const int64_t m = std::min<int64_t>(piece_max_vec() * kVecIdx, len - a);
           S.add(piece++, tmp.data() + a, (uint32_t)m);
         }
       }
