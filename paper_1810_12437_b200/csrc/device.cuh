@@ -1,5 +1,6 @@
 // Device building blocks shared by every pcgs kernel.
 #pragma once
+#include <type_traits>
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -211,6 +212,13 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
 #ifndef PCGS_RING
 #define PCGS_RING 2
 #endif
+// Debug modes of the streaming loop (skip gathers / reductions / prefetch,
+// debug-option key 1 bits 1, 2, 4, 16) exist only in builds with
+// -DPCGS_DEBUG_MODES=1 (tools/pass_modes.py); the production loop has none.
+#ifndef PCGS_DEBUG_MODES
+#define PCGS_DEBUG_MODES 0
+#endif
+constexpr bool kDebugModes = PCGS_DEBUG_MODES != 0;
 constexpr int kRing = PCGS_RING;
 
 template <class Epi>
@@ -265,14 +273,14 @@ constexpr int kPrefetchBlocks = PCGS_PREFETCH_DIST;  // sliding L2 prefetch dist
 constexpr int kPrefetchFirst = PCGS_PREFETCH0;  // blocks prefetched before the slab fill
 __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int dbg) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane != 0 || (dbg & 4)) return;
+  if (lane != 0 || (kDebugModes && (dbg & 4))) return;
   const uint4 R = __ldg(P.warps + warp0 + warp);
   const int nvec = (int)R.y;
   if (nvec == 0) return;
   const int nb = (nvec + 31) >> 5;
   const char* p0 = (const char*)(P.vec + R.x);
   const unsigned total = (unsigned)nvec * 16u;
-  const unsigned bytes = (dbg & 16) ? total : min(total, (unsigned)kPrefetchFirst * 512u);
+  const unsigned bytes = (kDebugModes && (dbg & 16)) ? total : min(total, (unsigned)kPrefetchFirst * 512u);
   for (unsigned off = 0; off < bytes; off += 16384u) {
     const unsigned sz = bytes - off < 16384u ? bytes - off : 16384u;
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0 + off), "r"(sz) : "memory");
@@ -295,10 +303,14 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
   double acc = 0.0;
   unsigned open_id = 0;
   bool have_open = false;
-  // batches of kRing blocks: all loads of a batch issued together, then consumed
-  for (int k0 = 0; k0 < nb; k0 += kRing) {
+  // batches of kRing blocks: all loads of a batch issued together, then
+  // consumed.  Batches of full blocks run without bound checks; the last,
+  // partial batch takes the checked path.
+  const int nfull = (nvec >> 5) / kRing * kRing;  // blocks in full batches
+  auto batch = [&](int k0, auto checked) {
+    constexpr bool kChecked = decltype(checked)::value;
     uint4 q[kRing];
-    if (lane == 0 && !(dbg & 20) && k0 + kPrefetchBlocks < nb) {
+    if (lane == 0 && !(kDebugModes && (dbg & 20)) && k0 + kPrefetchBlocks < nb) {
       const int kb = k0 + kPrefetchBlocks;
       const int ke = min(nb, kb + kRing);
       const unsigned v_end = (unsigned)min(nvec, ke * 32);
@@ -306,28 +318,30 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
                    "r"((v_end - (unsigned)kb * 32u) * 16u)
                    : "memory");
     }
-    uint2 dl = lane < kRing && k0 + lane < nb ? __ldg(bd + k0 + lane) : make_uint2(0u, 0u);
+    const uint2 dl = lane < kRing && (!kChecked || k0 + lane < nb) ? __ldg(bd + k0 + lane) : make_uint2(0u, 0u);
 #pragma unroll
     for (int u = 0; u < kRing; ++u) {
       const int v = (k0 + u) * 32 + lane;
-      if (v < nvec) q[u] = ldg_stream(base + v);
+      if (!kChecked || v < nvec) q[u] = ldg_stream(base + v);
     }
 #pragma unroll
     for (int u = 0; u < kRing; ++u) {
       const int k = k0 + u;
-      if (k < nb) {
+      if (!kChecked || k < nb) {
         uint2 dsc;
         dsc.x = __shfl_sync(0xffffffffu, dl.x, u);
         dsc.y = __shfl_sync(0xffffffffu, dl.y, u);
-        const int v = k * 32 + lane;
+        const bool live = !kChecked || k * 32 + lane < nvec;
         double s;
-        if (dbg & 1) s = v < nvec ? (double)(q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) : 0.0;
-        else s = v < nvec ? gather8(q[u], sv) : 0.0;
-        if (dbg & 2) acc += s + (double)dsc.y;
+        if (kDebugModes && (dbg & 1)) s = live ? (double)(q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) : 0.0;
+        else s = live ? gather8(q[u], sv) : 0.0;
+        if (kDebugModes && (dbg & 2)) acc += s + (double)dsc.y;
         else block_reduce(dsc, s, lane, acc, open_id, have_open, epi);
       }
     }
-  }
+  };
+  for (int k0 = 0; k0 < nfull; k0 += kRing) batch(k0, std::false_type());
+  if (nfull < nb) batch(nfull, std::true_type());
   const double c = warp_sum(acc);
   if (have_open && lane == 0) epi.emit((long long)open_id, c);
 }
