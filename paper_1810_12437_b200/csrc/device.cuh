@@ -221,14 +221,19 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
 constexpr bool kDebugModes = PCGS_DEBUG_MODES != 0;
 constexpr int kRing = PCGS_RING;
 
+// `M` is the block's segment-start mask; `first_id` (the id of the segment
+// starting at the lowest set bit) is fetched lazily by shuffling `dl_x` from
+// lane `u` -- only blocks that contain a segment start need it.
 template <class Epi>
-__device__ __forceinline__ void block_reduce(uint2 dsc, double s, int lane, double& acc, unsigned& open_id,
-                                             bool& have_open, Epi& epi) {
-  const unsigned M = dsc.y;
+__device__ __forceinline__ void block_reduce(unsigned M, unsigned dl_x, int u, double s, int lane, double& acc,
+                                             unsigned& open_id, bool& have_open, Epi& epi) {
   if (M == 0u) {
     acc += s;
     return;
   }
+  uint2 dsc;
+  dsc.x = __shfl_sync(0xffffffffu, dl_x, u);
+  dsc.y = M;
   const int f = __ffs(M) - 1;
   const int Lh = 31 - __clz(M);
   // close the open segment: its lanes < f plus every lane's carried partial
@@ -328,15 +333,13 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
     for (int u = 0; u < kRing; ++u) {
       const int k = k0 + u;
       if (!kChecked || k < nb) {
-        uint2 dsc;
-        dsc.x = __shfl_sync(0xffffffffu, dl.x, u);
-        dsc.y = __shfl_sync(0xffffffffu, dl.y, u);
+        const unsigned M = __shfl_sync(0xffffffffu, dl.y, u);
         const bool live = !kChecked || k * 32 + lane < nvec;
         double s;
         if (kDebugModes && (dbg & 1)) s = live ? (double)(q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) : 0.0;
         else s = live ? gather8(q[u], sv) : 0.0;
-        if (kDebugModes && (dbg & 2)) acc += s + (double)dsc.y;
-        else block_reduce(dsc, s, lane, acc, open_id, have_open, epi);
+        if (kDebugModes && (dbg & 2)) acc += s + (double)M;
+        else block_reduce(M, dl.x, u, s, lane, acc, open_id, have_open, epi);
       }
     }
   };
