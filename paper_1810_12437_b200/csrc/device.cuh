@@ -79,14 +79,28 @@ __device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
 // identical everywhere); only warp 0 loads them, the result is broadcast
 // through shared memory.  Must be called by the whole CTA.
 constexpr int kPartStride = 16;
+constexpr int kPartLoads = 8;  // partial loads per lane: grids up to 256 CTAs
+
+// Lane-strided sum of partials q = lane, lane+32, ... (< G) in that order; all
+// loads are issued before the first add, so the L2 round trips overlap.
+__device__ __forceinline__ double lane_partials(const double* part, int G, int lane) {
+  double v[kPartLoads];
+#pragma unroll
+  for (int u = 0; u < kPartLoads; ++u) {
+    const int q = lane + 32 * u;
+    v[u] = q < G ? __ldcg(part + (long long)q * kPartStride) : 0.0;
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int u = 0; u < kPartLoads; ++u) s += v[u];
+  return s;
+}
 
 __device__ __forceinline__ double reduce_partials(const double* part, int G, double* bcast) {
   const int lane = threadIdx.x & 31;
   __syncthreads();
   if (threadIdx.x < 32) {
-    double s = 0.0;
-    for (int q = lane; q < G; q += 32) s += __ldcg(part + (long long)q * kPartStride);
-    s = warp_sum(s);
+    const double s = warp_sum(lane_partials(part, G, lane));
     if (lane == 0) *bcast = s;
   }
   __syncthreads();
@@ -97,11 +111,7 @@ __device__ __forceinline__ void reduce_partials2(const double* part, int G, doub
   const int lane = threadIdx.x & 31;
   __syncthreads();
   if (threadIdx.x < 32) {
-    double s0 = 0.0, s1 = 0.0;
-    for (int q = lane; q < G; q += 32) {
-      s0 += __ldcg(part + (long long)q * kPartStride);
-      s1 += __ldcg(part + (long long)q * kPartStride + 1);
-    }
+    double s0 = lane_partials(part, G, lane), s1 = lane_partials(part + 1, G, lane);
     s0 = warp_sum(s0);
     s1 = warp_sum(s1);
     if (lane == 0) {

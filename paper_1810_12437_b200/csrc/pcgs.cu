@@ -438,10 +438,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     double alpha = 0.0;
     const int S = A.D.csc.nslab;
     trace_stamp(A, a, 0);
+    // warp 0's loads of the dAd partials overlap the piece staging round trip
+    double dpart = 0.0;
+    if (a > 0 && tid < 32) dpart = lane_partials(A.part, gridDim.x, tid);
     const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
     trace_stamp(A, a, 1);
     if (a > 0) {
-      const double dAd = reduce_partials(A.part, gridDim.x, bc);
+      if (tid < 32) {
+        dpart = warp_sum(dpart);
+        if (tid == 0) bc[0] = dpart;
+      }
+      __syncthreads();
+      const double dAd = bc[0];
       if (!(dAd > 0.0)) {
         if (tid == 0) {
           st_status = PCGS_NOT_PD;
