@@ -65,6 +65,11 @@ const char* pcgs_last_error(void);
 int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h,
                        const int32_t* col_idx_h, int intercept, int slab_max,
                        int device, pcgs_design_t* out);
+/* pcgs_design_create with an explicit CTA count for the static plan
+ * (0 = one CTA per SM); row-split shards hosted by one grid use SMs / n. */
+int pcgs_design_create_ex(int64_t n, int64_t p, const int64_t* row_ptr_h,
+                          const int32_t* col_idx_h, int intercept, int slab_max,
+                          int device, int grid, pcgs_design_t* out);
 int pcgs_design_destroy(pcgs_design_t d);
 /* Bench/test utility: native synthetic binary design (log-uniform column
  * rates, Binomial row counts; BASELINE config 5 scale).  Call once with
@@ -199,6 +204,36 @@ int pcgs_debug_cta_times(void* buf);
  * iteration ([0..7]) and stamps inside the step phase ([8..12]) when the
  * debug-option key 1 bit 128 is set. */
 int pcgs_debug_sync_times(void* buf);
+
+/* ------------------------------------------------------------------------
+ * Row-split PCG (replaces the per-application
+ * allreduce of parallel.ShardedPrecisionOperator around cg.py:105-192).
+ * Rows of X are split into contiguous shards, one per rank; p-vectors are
+ * replicated.  One persistent kernel per GPU runs the whole solve; the X'w
+ * pieces of every rank are exchanged inside the kernel over peer memory
+ * (one exchange barrier per iteration, no NCCL call).  A context hosts
+ * n_local consecutive ranks [rank0, rank0 + n_local) of nranks on one GPU:
+ * n_local == nranks runs every shard in one grid (single-GPU emulation),
+ * n_local == 1 is one rank per GPU, the other ranks' exchange regions mapped
+ * with CUDA IPC (pcgs_rs_exchange_handle on the owner, pcgs_rs_open_peer on
+ * every other rank).  Local shard designs must be created with the same grid
+ * (pcgs_design_create_ex) and columns.
+ * ------------------------------------------------------------------------ */
+typedef struct pcgs_rs* pcgs_rs_t;
+int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nranks,
+                   pcgs_rs_t* out);
+/* 64-byte cudaIpcMemHandle_t of local rank `local`'s exchange region. */
+int pcgs_rs_exchange_handle(pcgs_rs_t rs, int local, void* handle_h);
+int pcgs_rs_open_peer(pcgs_rs_t rs, int rank, const void* handle_h);
+/* pcgs_pcg over the row shards: omegas_h[l] = device omega of local rank l
+ * (shard rows); prior_diag, minv, scale, b, x (x0 in, solution out), trace,
+ * alphas, betas, result as pcgs_pcg (device), replicated on every rank.
+ * Asynchronous; every rank of the solve must launch it. */
+int pcgs_rs_pcg(pcgs_rs_t rs, const double* const* omegas_h, const double* prior_diag,
+                const double* minv, const double* scale, const double* b, double* x,
+                int32_t max_iter, double rtol, double* trace, double* alphas,
+                double* betas, int32_t* result, pcgs_stream_t stream);
+int pcgs_rs_destroy(pcgs_rs_t rs);
 
 /* omega[i] ~ PG(1, z[i]) (pg_draw_batch, polya_gamma.py:39-84), Philox keyed
  * by (seed, stream_id), one thread per draw. */

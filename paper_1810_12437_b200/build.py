@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpcgs.so"
-SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "batched.cu", CSRC / "store.cpp", CSRC / "mtx.cpp"]
+SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "batched.cu", CSRC / "rowsplit.cu", CSRC / "store.cpp", CSRC / "mtx.cpp"]
 HEADERS = [CSRC / "store.h", CSRC / "mtx.h", CSRC / "device.cuh", CSRC / "internal.cuh", CSRC / "batched.cuh",
            ROOT / "include" / "pcgs.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

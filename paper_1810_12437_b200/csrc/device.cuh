@@ -366,8 +366,9 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 __device__ unsigned long long* g_cta_times = nullptr;  // debug: per-CTA [start, filled, end]
 
 template <class Fill, class Epi>
-__device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi, int dbg = 0) {
-  const int c = blockIdx.x;
+__device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi, int dbg = 0,
+                                         int cta = -1) {
+  const int c = cta < 0 ? (int)blockIdx.x : cta;  // CTA index within the plan (row-split groups)
   unsigned long long t_start = 0;
   if ((dbg & 64) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   const int t0 = P.cta_task_ptr[c], t1 = P.cta_task_ptr[c + 1];

@@ -108,6 +108,12 @@ struct FillVecN {  // CSC slab of an n-vector: TMA bulk copy
   __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, w + l, len); }
 };
 
+struct FillBulk {  // TMA copy of an internal-layout vector slab
+  const double* src;
+  BulkFill* bf;
+  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, src + l, len); }
+};
+
 struct FillRhs {  // u_i = kappa_i + sqrt(omega_i) * eta_i
   const double* kappa;
   const double* omega;

@@ -175,12 +175,6 @@ struct FillDir {  // search direction: first ? a : a + beta * b   (internal layo
   }
 };
 
-struct FillBulk {  // TMA copy of an internal-layout vector slab
-  const double* src;
-  BulkFill* bf;
-  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, src + l, len); }
-};
-
 // Shared-memory layout of k_pcg: [slab vector | own-slice state | piece pointers]
 // The piece pointers of the owned columns are staged in shared memory when they
 // fit (pp_smem), otherwise read from the design's global piece_ptr array.
@@ -606,12 +600,19 @@ static int set_smem_attrs(const DesignDev& D) {
 
 int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int32_t* col_idx_h, int intercept,
                        int slab_max, int device, pcgs_design_t* out) {
+  return pcgs_design_create_ex(n, p, row_ptr_h, col_idx_h, intercept, slab_max, device, 0, out);
+}
+
+int pcgs_design_create_ex(int64_t n, int64_t p, const int64_t* row_ptr_h, const int32_t* col_idx_h, int intercept,
+                          int slab_max, int device, int grid, pcgs_design_t* out) {
   if (!out || !row_ptr_h || (!col_idx_h && row_ptr_h[n] > 0)) return fail(PCGS_EINVAL, "null argument");
   *out = nullptr;
   CUDA_TRY(cudaSetDevice(device));
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
-  const int G = std::min(prop.multiProcessorCount, kMaxGrid);
+  const int sms = std::min(prop.multiProcessorCount, kMaxGrid);
+  if (grid < 0 || grid > sms) return fail(PCGS_EINVAL, "grid must be in [0, SM count]");
+  const int G = grid > 0 ? grid : sms;
   DesignHost H;
   std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H);
   if (!err.empty()) return fail(PCGS_EINVAL, err);

@@ -1,0 +1,616 @@
+// Row-split PCG: the whole solve over R row shards in one persistent kernel
+// per GPU, with the per-iteration exchange of the X'w partials fused into the
+// kernel over peer memory (BASELINE config 5).
+//
+// Reference semantics: pcg_solve (pkg/src/priorcg/cg.py:105-192) on
+// Phi = sum_r X_r' Omega_r X_r + D (sampler.py:53-58), rows of X split into
+// contiguous shards (parallel.row_partition).  p-length vectors are
+// replicated on every rank.  Per iteration each rank
+//   A. runs its CSR pass over its rows (z_r = X_r d, w_r = omega_r z_r, and
+//      the partial z_r' Omega_r z_r),
+//   B. runs its CSC pass (pieces of X_r' w_r) into a parity-double-buffered
+//      exchange region,
+//   X. meets every other rank at one exchange barrier,
+//   C. assembles Phi d for its owned columns from the pieces of ALL ranks
+//      (peer loads over NVLink, fixed rank/slab/piece order) and takes the CG
+//      step on its replicated vectors.
+// Every rank sums the same numbers in the same order, so all ranks hold
+// bitwise identical iterates and take identical convergence decisions; there
+// is no other collective.  dAd = sum_r z_r' Omega_r z_r + d'Dd (the rank
+// partials in rank order, the prior term from the replicated owned slices).
+//
+// One grid can also host several ranks (`n_local` > 1): rank groups of Gr
+// CTAs each, the exchange barrier then being the grid barrier.  That is how
+// the decomposition runs and is validated on a single GPU; with one rank per
+// GPU (`n_local` = 1) the barrier adds a flag exchange over peer memory
+// (system-scope release/acquire) between two grid barriers.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int kRsMaxRanks = 64;
+constexpr int kRsMaxLocal = 8;    // ranks hosted by one grid
+constexpr int kMaxGridRs = 256;
+constexpr int kRsMaxPairs = 512;  // (rank, CSC slab) pairs summed per column
+
+// Exchange region of one rank (one allocation, IPC-shareable):
+//   header (64 B) | inbox flags [kRsMaxRanks] u64 | part [2][16 * G] f64 |
+//   pieces [2][nseg] f64 | piece_ptr [nslab * (pt + 1)] i32
+struct RsHeader {
+  long long nseg, pt, nslab, G, bytes;
+  long long pad[3];
+};
+
+struct RsLayout {
+  size_t flags, part, pieces, pp, bytes;
+  static RsLayout of(long long nseg, long long pt, long long nslab, long long G) {
+    RsLayout L;
+    L.flags = sizeof(RsHeader);
+    L.part = L.flags + kRsMaxRanks * sizeof(unsigned long long);
+    L.pieces = L.part + 2 * (size_t)kPartStride * G * sizeof(double);
+    L.pp = L.pieces + 2 * (size_t)std::max<long long>(nseg, 1) * sizeof(double);
+    L.bytes = L.pp + (size_t)nslab * (pt + 1) * sizeof(int) + 64;
+    L.bytes = (L.bytes + 255) / 256 * 256;
+    return L;
+  }
+};
+
+struct RsPeer {                  // every rank, as this GPU sees it
+  const double* part;            // [2][16 G] (local or peer-mapped)
+  const double* pieces;          // [2][nseg]
+  const int* pp;                 // piece_ptr, local copy
+  unsigned long long* inbox;     // the rank's flag array (peer-mapped for remote ranks)
+  long long nseg;
+  int nslab;
+  int remote;
+};
+
+struct RsGroup {                 // a rank hosted by this grid
+  DesignDev D;                   // the rank's shard, planned for Gr CTAs
+  double* w;                     // n_r (+pad)
+  double* zpart;                 // nslab_csr * n_r (multi column slab)
+  double* dvg;                   // 2 * p_total (internal layout): published directions
+  double* part;                  // exchange part [2][16 Gr]
+  double* pieces;                // exchange pieces [2][nseg]
+  double* own;                   // own-slice state in global memory (Gr * 8 * chunk), or null
+  int rank;
+};
+
+struct RsArgs {
+  const RsGroup* groups;
+  const double* omega[kRsMaxLocal];  // shard rows of each hosted rank (per call)
+  int n_local, Gr, nranks, smem_doubles;
+  const RsPeer* peers;
+  const int2* pairs;             // (rank, slab) pairs in summation order
+  int npairs;
+  unsigned long long* epoch;     // device counter: exchanges completed by earlier calls
+  const double *diag, *minv, *scale, *b;  // reference layout, replicated
+  double* x;                     // in x0 / out solution
+  int max_iter;
+  double rtol;
+  double *trace, *alphas, *betas;
+  int* result;
+};
+
+__device__ __forceinline__ double ld_peer(const double* p, bool remote) { return remote ? __ldcv(p) : __ldcg(p); }
+
+// Exchange barrier: every local CTA has published its pieces and partials;
+// then (ranks on other GPUs only) one thread signals every remote inbox and
+// waits for theirs.
+__device__ void rs_exchange(const RsArgs& A, int my_rank, unsigned long long e) {
+  if (A.n_local == A.nranks) {
+    cg::this_grid().sync();
+    return;
+  }
+  __threadfence_system();
+  cg::this_grid().sync();
+  if (blockIdx.x == 0 && threadIdx.x < A.nranks && (int)threadIdx.x != my_rank) {
+    const RsPeer& q = A.peers[threadIdx.x];
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(q.inbox + my_rank), "l"(e) : "memory");
+    const RsPeer& me = A.peers[my_rank];
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(me.inbox + threadIdx.x) : "memory");
+    } while (v < e);
+  }
+  cg::this_grid().sync();
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
+  extern __shared__ __align__(128) double sv[];
+  __shared__ double red[64];
+  __shared__ double bc[4];
+  __shared__ double st_rz;
+  __shared__ int st_status, st_iter, st_fail, st_applies;
+  __shared__ unsigned long long mbar, st_epoch;
+  __shared__ RsGroup G;
+  __shared__ int2 pairs[kRsMaxPairs];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gi = blockIdx.x / A.Gr, cta = blockIdx.x % A.Gr;
+  if (tid == 0) {
+    G = A.groups[gi];
+    st_epoch = *A.epoch;
+  }
+  const double* omega = A.omega[gi];
+  for (int k = tid; k < A.npairs; k += kThreads) pairs[k] = A.pairs[k];
+  BulkFill bf;
+  bulk_init(bf, &mbar);  // ends with a CTA barrier
+  const bool lead = gi == 0;  // the first hosted group writes the outputs
+  const long long pt = G.D.pt;
+  const int Gr = A.Gr;
+  const int chunk = (int)((pt + Gr - 1) / Gr);
+  const long long j0 = (long long)cta * chunk;
+  const long long dvs = (pt + 15) / 16 * 16;
+  double* ob = G.own ? G.own + (size_t)cta * 8 * chunk : sv + A.smem_doubles;
+  double *ox = ob, *orr = ob + chunk, *od = ob + 2 * chunk, *om = ob + 3 * chunk, *os = ob + 4 * chunk,
+         *oD = ob + 5 * chunk, *obv = ob + 6 * chunk, *oz = ob + 7 * chunk;
+  for (int t = tid; t < chunk; t += kThreads) {
+    const long long j = j0 + t;
+    double xv = 0, m = 0, sc = 0, dg = 0, bv = 0;
+    if (j < pt) {
+      const long long rj = ref_index(j, G.D.p, G.D.icpt);
+      xv = A.x[rj];
+      m = __ldg(A.minv + rj);
+      sc = __ldg(A.scale + rj);
+      dg = __ldg(A.diag + rj);
+      bv = __ldg(A.b + rj);
+      G.dvg[dvs + j] = xv;  // the first application is on x0 (cg.py:137)
+    }
+    ox[t] = xv;
+    orr[t] = 0.0;
+    od[t] = xv;
+    om[t] = m;
+    os[t] = sc;
+    oD[t] = dg;
+    obv[t] = bv;
+    oz[t] = 0.0;
+  }
+  if (tid == 0) {
+    st_rz = 0.0;
+    st_status = PCGS_MAX_ITER;
+    st_iter = 0;
+    st_fail = -1;
+    st_applies = 0;
+  }
+  cg::this_grid().sync();
+
+  for (int a = 0;; ++a) {
+    const int par = a & 1;
+    // ---------------- convergence test of iteration a-1 (replicated) ----------------
+    if (a > 0) {
+      double s_rms, s_rz;
+      reduce_partials2(G.part + (par ^ 1) * kPartStride * Gr + 1, Gr, bc, s_rms, s_rz);
+      const double rms = sqrt(s_rms / (double)pt);
+      if (lead && cta == 0 && tid == 0) A.trace[a - 1] = rms;
+      const int k = a - 1;
+      int stop = 0;
+      if (rms <= A.rtol) stop = 1;
+      else if (!isfinite(rms)) stop = 2;
+      double beta = 0.0;
+      if (!stop) {
+        if (a >= 2) {
+          beta = s_rz / st_rz;
+          if (lead && cta == 0 && tid == 0) A.betas[a - 2] = beta;
+        }
+        if (k >= A.max_iter) stop = 3;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        st_rz = s_rz;
+        if (stop) {
+          st_status = stop == 1 ? PCGS_CONVERGED : stop == 2 ? PCGS_NONFINITE : PCGS_MAX_ITER;
+          st_iter = k;
+          if (stop == 2) st_fail = k;
+        }
+      }
+      if (stop) break;
+      for (int t = tid; t < chunk; t += kThreads) {
+        const double dn = a == 1 ? oz[t] : fma(beta, od[t], oz[t]);
+        od[t] = dn;
+        if (j0 + t < pt) G.dvg[par * dvs + j0 + t] = dn;
+      }
+      cg::this_grid().sync();
+    }
+
+    // ---------------- A: CSR pass over this rank's rows ----------------
+    double acc = 0.0;
+    {
+      const double* vcur = G.dvg + (a == 0 ? dvs : par * dvs);
+      if (tid == 0) bc[2] = G.D.icpt ? __ldcg(vcur + G.D.p) : 0.0;
+      __syncthreads();
+      const bool multi = G.D.csr.nslab > 1;
+      EpiCsr e{multi ? G.zpart : G.w, omega, bc[2], 0.0, multi};
+      FillBulk f{vcur, &bf};
+      run_pass(G.D.csr, sv, f, e, 0, cta);
+      acc = e.acc;
+    }
+    if (G.D.csr.nslab > 1) {
+      cg::this_grid().sync();
+      const long long n = G.D.n;
+      const double v0 = bc[2];
+      for (long long i = (long long)cta * kThreads + tid; i < n; i += (long long)Gr * kThreads) {
+        double z = 0.0;
+        for (int s = 0; s < G.D.csr.nslab; ++s) z += __ldcg(G.zpart + (long long)s * n + i);
+        z += v0;
+        const double wi = __ldg(omega + i) * z;
+        G.w[i] = wi;
+        acc += wi * z;
+      }
+    }
+    {
+      double dterm = 0.0;
+      for (int t = tid; t < chunk; t += kThreads) dterm += oD[t] * od[t] * od[t];
+      block_sum2(acc, dterm, red);
+      if (tid == 0) {
+        G.part[par * kPartStride * Gr + cta * kPartStride + 0] = acc;    // exchanged
+        G.part[par * kPartStride * Gr + cta * kPartStride + 3] = dterm;  // local
+      }
+    }
+    cg::this_grid().sync();
+
+    // ---------------- B: CSC pass, pieces of X_r' w_r ----------------
+    {
+      FillVecN f{G.w, &bf};
+      EpiStore e{G.pieces + par * (long long)G.D.csc.nseg};
+      run_pass(G.D.csc, sv, f, e, 0, cta);
+    }
+    if (tid == 0) ++st_applies;
+    rs_exchange(A, G.rank, st_epoch + (unsigned long long)a + 1ull);
+
+    // ---------------- C: assemble owned columns over all ranks, step ----------------
+    double alpha = 0.0;
+    if (a > 0) {
+      // dAd: rank partials in rank order, then the replicated prior term
+      double s = 0.0;
+      if (tid < 32) {
+        for (int q = 0; q < A.nranks; ++q) {
+          const RsPeer& P = A.peers[q];
+          const double* pq = P.part + par * kPartStride * Gr;
+          double v = 0.0;
+          for (int c = lane; c < Gr; c += 32) v += ld_peer(pq + (long long)c * kPartStride, P.remote);
+          s += warp_sum(v);
+        }
+        double dt = lane_partials(G.part + par * kPartStride * Gr + 3, Gr, lane);
+        s += warp_sum(dt);
+        if (tid == 0) bc[0] = s;
+      }
+      __syncthreads();
+      const double dAd = bc[0];
+      if (!(dAd > 0.0)) {
+        if (tid == 0) {
+          st_status = PCGS_NOT_PD;
+          st_iter = a;
+          st_fail = a;
+        }
+        break;
+      }
+      alpha = st_rz / dAd;
+      if (lead && cta == 0 && tid == 0) A.alphas[a - 1] = alpha;
+    }
+    double t_rms = 0.0, t_rz = 0.0;
+    for (int t = warp; t < chunk; t += kWarps) {
+      const long long j = j0 + t;
+      if (j >= pt) break;
+      double s = 0.0;
+      for (int k = lane; k < A.npairs; k += 32) {
+        const int2 qs = pairs[k];
+        const RsPeer& P = A.peers[qs.x];
+        const int* pp = P.pp + (long long)qs.y * (pt + 1);
+        const int q0 = __ldg(pp + j), q1 = __ldg(pp + j + 1);
+        const double* pc = P.pieces + par * P.nseg;
+        for (int q = q0; q < q1; ++q) s += ld_peer(pc + q, P.remote);
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        const double Ad = s + oD[t] * od[t];
+        double rv;
+        if (a == 0) {
+          rv = obv[t] - Ad;
+        } else {
+          ox[t] = fma(alpha, od[t], ox[t]);
+          rv = fma(-alpha, Ad, orr[t]);
+        }
+        orr[t] = rv;
+        const double zn = om[t] * rv;
+        oz[t] = zn;
+        const double tj = os[t] * rv;
+        t_rms += tj * tj;
+        t_rz += rv * zn;
+      }
+    }
+    block_sum2(t_rms, t_rz, red);
+    if (tid == 0) {
+      G.part[par * kPartStride * Gr + cta * kPartStride + 1] = t_rms;
+      G.part[par * kPartStride * Gr + cta * kPartStride + 2] = t_rz;
+    }
+    cg::this_grid().sync();
+  }
+
+  __syncthreads();
+  if (lead) {
+    for (int t = tid; t < chunk; t += kThreads)
+      if (j0 + t < pt) A.x[ref_index(j0 + t, G.D.p, G.D.icpt)] = ox[t];
+  }
+  if (lead && cta == 0 && tid == 0) {
+    A.result[0] = st_iter;
+    A.result[1] = st_status;
+    A.result[2] = st_fail;
+    A.result[3] = st_applies;
+  }
+  // exchanges used by this call: every rank ran the same number of iterations
+  cg::this_grid().sync();
+  if (blockIdx.x == 0 && tid == 0) *A.epoch = st_epoch + (unsigned long long)st_applies;
+}
+
+}  // namespace
+
+// =====================================================================
+// context
+// =====================================================================
+struct pcgs_rs {
+  int device = 0, n_local = 0, rank0 = 0, nranks = 0, Gr = 0, smem_doubles = 0;
+  long long pt = 0, p = 0;
+  std::vector<pcgs_design_t> designs;      // local ranks
+  std::vector<void*> exch;                 // per rank: exchange base (local alloc or IPC-mapped)
+  std::vector<int> opened;                 // per rank: 1 when IPC-mapped (to close)
+  std::vector<void*> allocs;               // owned device allocations
+  std::vector<RsPeer> peers;
+  std::vector<RsHeader> hdr;
+  unsigned long long* epoch = nullptr;
+  std::vector<double*> w, zpart, dvg, own;
+  RsGroup* groups_dev = nullptr;
+  RsPeer* peers_dev = nullptr;
+  int2* pairs_dev = nullptr;
+  int npairs = 0;
+  bool own_in_smem = true;
+};
+
+namespace {
+
+int rs_alloc(pcgs_rs* R, size_t bytes, void** out) {
+  void* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, bytes));
+  R->allocs.push_back(p);
+  *out = p;
+  return PCGS_OK;
+}
+
+size_t rs_smem_bytes(const pcgs_rs* R) {
+  const long long chunk = (R->pt + R->Gr - 1) / R->Gr;
+  return (size_t)R->smem_doubles * 8 + (R->own_in_smem ? (size_t)chunk * 64 : 0) + 16;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nranks, pcgs_rs_t* out) {
+  if (!designs || !out || n_local < 1 || n_local > kRsMaxLocal || nranks < n_local || (n_local > 1 && n_local != nranks) || nranks > kRsMaxRanks || rank0 < 0 ||
+      rank0 + n_local > nranks)
+    return fail(PCGS_EINVAL, "row split: bad rank layout");
+  *out = nullptr;
+  pcgs_rs* R = new pcgs_rs();
+  R->n_local = n_local;
+  R->rank0 = rank0;
+  R->nranks = nranks;
+  R->device = designs[0]->device;
+  R->Gr = designs[0]->dev.G;
+  R->pt = designs[0]->dev.pt;
+  R->p = designs[0]->dev.p;
+  auto bail = [&](int rc) {
+    pcgs_rs_destroy(R);
+    return rc;
+  };
+  for (int l = 0; l < n_local; ++l) {
+    const DesignDev& D = designs[l]->dev;
+    if (designs[l]->device != R->device || D.G != R->Gr || D.pt != R->pt || D.p != R->p || D.icpt != designs[0]->dev.icpt)
+      return bail(fail(PCGS_EINVAL, "row split: local shards must share device, grid and columns"));
+    R->smem_doubles = std::max(R->smem_doubles, D.smem_doubles);
+    R->designs.push_back(designs[l]);
+  }
+  if ((long long)R->Gr * n_local > kMaxGridRs) return bail(fail(PCGS_EINVAL, "row split: grid too large"));
+  if (cudaSetDevice(R->device) != cudaSuccess) return bail(fail(PCGS_ECUDA, "cudaSetDevice failed"));
+  const long long chunk = (R->pt + R->Gr - 1) / R->Gr;
+  R->own_in_smem = (long long)R->smem_doubles * 8 + chunk * 64 + 16 + 1024 + 8 * kRsMaxPairs + 2048 <= 227 * 1024;
+  R->exch.assign(nranks, nullptr);
+  R->opened.assign(nranks, 0);
+  R->hdr.assign(nranks, RsHeader{});
+  R->peers.assign(nranks, RsPeer{});
+  int rc;
+  void* p;
+  if ((rc = rs_alloc(R, sizeof(unsigned long long), &p))) return bail(rc);
+  R->epoch = (unsigned long long*)p;
+  if (cudaMemset(R->epoch, 0, sizeof(unsigned long long)) != cudaSuccess) return bail(fail(PCGS_ECUDA, "memset"));
+  for (int l = 0; l < n_local; ++l) {
+    const DesignDev& D = designs[l]->dev;
+    const RsLayout L = RsLayout::of(D.csc.nseg, D.pt, D.csc.nslab, D.G);
+    if ((rc = rs_alloc(R, L.bytes, &p))) return bail(rc);
+    if (cudaMemset(p, 0, L.bytes) != cudaSuccess) return bail(fail(PCGS_ECUDA, "memset"));
+    RsHeader h{D.csc.nseg, D.pt, D.csc.nslab, D.G, (long long)L.bytes, {0, 0, 0}};
+    if (cudaMemcpy(p, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaMemcpy((char*)p + L.pp, D.csc.piece_ptr, (size_t)D.csc.nslab * (D.pt + 1) * sizeof(int),
+                   cudaMemcpyDeviceToDevice) != cudaSuccess)
+      return bail(fail(PCGS_ECUDA, "exchange setup copy failed"));
+    R->exch[rank0 + l] = p;
+    R->hdr[rank0 + l] = h;
+    const long long n = D.n;
+    double* b;
+    if ((rc = rs_alloc(R, (size_t)(n + 2) * 8, &p))) return bail(rc);
+    R->w.push_back((double*)p);
+    b = nullptr;
+    if (D.csr.nslab > 1) {
+      if ((rc = rs_alloc(R, (size_t)D.csr.nslab * n * 8, &p))) return bail(rc);
+      b = (double*)p;
+    }
+    R->zpart.push_back(b);
+    if ((rc = rs_alloc(R, (size_t)(2 * ((D.pt + 15) / 16 * 16) + 16) * 8, &p))) return bail(rc);
+    R->dvg.push_back((double*)p);
+    b = nullptr;
+    if (!R->own_in_smem) {
+      if ((rc = rs_alloc(R, (size_t)R->Gr * 8 * chunk * 8, &p))) return bail(rc);
+      b = (double*)p;
+    }
+    R->own.push_back(b);
+  }
+  if ((rc = rs_alloc(R, sizeof(RsGroup) * n_local, &p))) return bail(rc);
+  R->groups_dev = (RsGroup*)p;
+  if ((rc = rs_alloc(R, sizeof(RsPeer) * nranks, &p))) return bail(rc);
+  R->peers_dev = (RsPeer*)p;
+  if ((rc = rs_alloc(R, sizeof(int2) * kRsMaxPairs, &p))) return bail(rc);
+  R->pairs_dev = (int2*)p;
+  const int smem = (int)rs_smem_bytes(R);
+  if (cudaFuncSetAttribute(k_pcg_rs, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return bail(fail(PCGS_ECUDA, "row split: shared memory attribute"));
+  *out = R;
+  return PCGS_OK;
+}
+
+int pcgs_rs_exchange_handle(pcgs_rs_t R, int local, void* handle_h) {
+  if (!R || !handle_h || local < 0 || local >= R->n_local) return fail(PCGS_EINVAL, "bad argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaSetDevice(R->device));
+  CUDA_TRY(cudaIpcGetMemHandle(&h, R->exch[R->rank0 + local]));
+  memcpy(handle_h, &h, sizeof(h));
+  return PCGS_OK;
+}
+
+int pcgs_rs_open_peer(pcgs_rs_t R, int rank, const void* handle_h) {
+  if (!R || !handle_h || rank < 0 || rank >= R->nranks || (rank >= R->rank0 && rank < R->rank0 + R->n_local))
+    return fail(PCGS_EINVAL, "row split: peer rank out of range or local");
+  CUDA_TRY(cudaSetDevice(R->device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle_h, sizeof(h));
+  void* p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  R->exch[rank] = p;
+  R->opened[rank] = 1;
+  RsHeader hd;
+  CUDA_TRY(cudaMemcpy(&hd, p, sizeof(hd), cudaMemcpyDeviceToHost));
+  if (hd.pt != R->pt || hd.G != R->Gr) return fail(PCGS_EINVAL, "row split: peer shard has other columns or grid");
+  R->hdr[rank] = hd;
+  return PCGS_OK;
+}
+
+// Builds the peer table once every rank's exchange region is known: local
+// piece_ptr copies of remote ranks, the (rank, slab) summation order.
+static int rs_finalize(pcgs_rs* R) {
+  std::vector<int2> pairs;
+  for (int q = 0; q < R->nranks; ++q) {
+    if (!R->exch[q]) return fail(PCGS_EINVAL, "row split: rank " + std::to_string(q) + " has no exchange region");
+    const RsHeader& h = R->hdr[q];
+    const RsLayout L = RsLayout::of(h.nseg, h.pt, h.nslab, h.G);
+    RsPeer P{};
+    char* base = (char*)R->exch[q];
+    P.part = (const double*)(base + L.part);
+    P.pieces = (const double*)(base + L.pieces);
+    P.inbox = (unsigned long long*)(base + L.flags);
+    P.nseg = h.nseg;
+    P.nslab = (int)h.nslab;
+    P.remote = R->opened[q];
+    if (P.remote) {
+      if (!R->peers[q].pp) {
+        void* p;
+        int rc;
+        const size_t bytes = (size_t)h.nslab * (h.pt + 1) * sizeof(int);
+        if ((rc = rs_alloc(R, bytes, &p))) return rc;
+        CUDA_TRY(cudaMemcpy(p, base + L.pp, bytes, cudaMemcpyDeviceToDevice));
+        P.pp = (const int*)p;
+      } else {
+        P.pp = R->peers[q].pp;
+      }
+    } else {
+      P.pp = (const int*)(base + L.pp);
+    }
+    R->peers[q] = P;
+    for (int s = 0; s < P.nslab; ++s) pairs.push_back(make_int2(q, s));
+  }
+  if ((int)pairs.size() > kRsMaxPairs) return fail(PCGS_EINVAL, "row split: too many (rank, slab) pairs");
+  R->npairs = (int)pairs.size();
+  CUDA_TRY(cudaMemcpy(R->peers_dev, R->peers.data(), sizeof(RsPeer) * R->nranks, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(R->pairs_dev, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
+  std::vector<RsGroup> groups(R->n_local);
+  for (int l = 0; l < R->n_local; ++l) {
+    const int q = R->rank0 + l;
+    RsGroup& g = groups[l];
+    g.D = R->designs[l]->dev;
+    g.D.dbg = 0;
+    g.w = R->w[l];
+    g.zpart = R->zpart[l];
+    g.dvg = R->dvg[l];
+    g.part = const_cast<double*>(R->peers[q].part);
+    g.pieces = const_cast<double*>(R->peers[q].pieces);
+    g.own = R->own[l];
+    g.rank = q;
+  }
+  CUDA_TRY(cudaMemcpy(R->groups_dev, groups.data(), sizeof(RsGroup) * R->n_local, cudaMemcpyHostToDevice));
+  return PCGS_OK;
+}
+
+int pcgs_rs_pcg(pcgs_rs_t R, const double* const* omegas_h, const double* prior_diag, const double* minv,
+                const double* scale, const double* b, double* x, int32_t max_iter, double rtol, double* trace,
+                double* alphas, double* betas, int32_t* result, pcgs_stream_t stream) {
+  if (!R || !omegas_h || !prior_diag || !minv || !scale || !b || !x || !trace || !alphas || !betas || !result)
+    return fail(PCGS_EINVAL, "null argument");
+  if (max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
+  CUDA_TRY(cudaSetDevice(R->device));
+  int rc;
+  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (R->n_local > kRsMaxLocal) return fail(PCGS_EINVAL, "row split: too many ranks in one grid");
+  RsArgs A{};
+  A.groups = R->groups_dev;
+  for (int l = 0; l < R->n_local; ++l) A.omega[l] = omegas_h[l];
+  A.n_local = R->n_local;
+  A.Gr = R->Gr;
+  A.nranks = R->nranks;
+  A.smem_doubles = R->smem_doubles;
+  A.peers = R->peers_dev;
+  A.pairs = R->pairs_dev;
+  A.npairs = R->npairs;
+  A.epoch = R->epoch;
+  A.diag = prior_diag;
+  A.minv = minv;
+  A.scale = scale;
+  A.b = b;
+  A.x = x;
+  A.max_iter = max_iter;
+  A.rtol = rtol;
+  A.trace = trace;
+  A.alphas = alphas;
+  A.betas = betas;
+  A.result = result;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(R->Gr * R->n_local);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = rs_smem_bytes(R);
+  cfg.stream = s;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeCooperative;
+  attr.val.cooperative = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pcg_rs, A));
+  return PCGS_OK;
+}
+
+int pcgs_rs_destroy(pcgs_rs_t R) {
+  if (!R) return PCGS_OK;
+  cudaSetDevice(R->device);
+  cudaDeviceSynchronize();
+  for (int q = 0; q < R->nranks; ++q)
+    if (R->opened[q] && R->exch[q]) cudaIpcCloseMemHandle(R->exch[q]);
+  for (void* p : R->allocs) cudaFree(p);
+  delete R;
+  return PCGS_OK;
+}
+
+}  // extern "C"

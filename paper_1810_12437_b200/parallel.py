@@ -123,9 +123,19 @@ class ShardedPrecisionOperator:
         return out if as_tensor else out.cpu().numpy()
 
 
-def sharded_pcg_solve(op: ShardedPrecisionOperator, b, M, x0=None, config=None, residual_scale=None):
-    """pcg_solve (cg.py:105-192) over a row-sharded operator: device vector
-    algebra replicated on every rank, Phi applied through the device callback."""
+def sharded_pcg_solve(op: ShardedPrecisionOperator, b, M, x0=None, config=None, residual_scale=None,
+                      fused=None):
+    """pcg_solve (cg.py:105-192) over a row-sharded operator.
+
+    Device shards default to the fused row-split kernel (`fused_pcg_solve`:
+    one persistent kernel per GPU, exchange over peer memory).  `fused=False`
+    (and host shards, `local_apply`) runs the engine loop instead: device
+    vector algebra replicated on every rank, Phi applied through the device
+    callback with one allreduce per application."""
+    if fused is None:
+        fused = op.local_apply is None and (config is None or config.trace_level != "full")
+    if fused:
+        return fused_pcg_solve(op, b, M, x0=x0, config=config, residual_scale=residual_scale)
     from .cg import CGConfig
     t = _lib.torch()
     L = _lib.lib()
@@ -177,6 +187,117 @@ def sharded_pcg_solve(op: ShardedPrecisionOperator, b, M, x0=None, config=None, 
         betas=betas[:_n_betas(iterations, status)].copy(),
         iterates=None,
     )
+
+
+# ---------------------------------------------------------------------------
+# Fused row-split PCG: one persistent kernel per GPU, the X'w exchange over
+# peer memory inside it (libpcgs pcgs_rs_*, csrc/rowsplit.cu)
+# ---------------------------------------------------------------------------
+class RowSplitPCG:
+    """The whole row-split solve in one kernel per GPU.
+
+    * Single process, several shards (`group` None or EmulatedGroup): every
+      shard is a rank group of SMs/G CTAs in one cooperative grid; the
+      exchange barrier is the grid barrier (the single-GPU form).
+    * One shard per process over a torch.distributed `group` (one GPU per
+      rank): each rank's exchange region is shared with CUDA IPC (handles
+      all-gathered once) and the kernel's exchange barrier is a flag
+      handshake over peer memory.
+    Bitwise identical results on every rank; no collective per iteration.
+    """
+
+    def __init__(self, shards, device=None, group=None):
+        import ctypes
+        t = _lib.torch()
+        L = _lib.lib()
+        self.device = _lib.cuda_device(device)
+        self.shards = list(shards)
+        real = group is not None and not isinstance(group, EmulatedGroup)
+        if real:
+            import torch.distributed as dist
+            world, rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            world, rank = 1, 0
+        if real and world > 1 and len(self.shards) != 1:
+            raise ValueError("row split over processes: one shard per rank")
+        n_local = len(self.shards)
+        nranks = world * n_local if real else n_local
+        sms = t.cuda.get_device_properties(self.device).multi_processor_count
+        grid = 0 if n_local == 1 else sms // n_local
+        self.stores = [s.device_store(self.device, grid=grid) for s in self.shards]
+        p_total = {st.p_total for st in self.stores}
+        if len(p_total) != 1:
+            raise ValueError("row shards must share the column set")
+        self.p_total = p_total.pop()
+        handles = (ctypes.c_void_p * n_local)(*[st.handle.value for st in self.stores])
+        h = ctypes.c_void_p()
+        _lib.check(L.pcgs_rs_create(handles, n_local, rank * n_local if real else 0, nranks, ctypes.byref(h)))
+        self._h = h
+        if real and world > 1:
+            import torch.distributed as dist
+            mine = ctypes.create_string_buffer(64)
+            _lib.check(L.pcgs_rs_exchange_handle(h, 0, mine))
+            allh = [None] * world
+            dist.all_gather_object(allh, bytes(mine.raw), group=group)
+            for q, hb in enumerate(allh):
+                if q != rank:
+                    buf = ctypes.create_string_buffer(hb, 64)
+                    _lib.check(L.pcgs_rs_open_peer(h, q, buf))
+            dist.barrier(group=group)
+        self.n_local, self.nranks = n_local, nranks
+
+    def solve(self, omegas, prior_diag, minv, scale, b, x0=None, max_iter=None, rtol=1e-6):
+        """Device tensors in (omegas: one per local shard); returns (x, trace,
+        alphas, betas, result) tensors, nothing synchronised (pcg_solve_device)."""
+        import ctypes
+        t = _lib.torch()
+        dev = self.device
+        p = self.p_total
+        max_iter = 2 * p if max_iter is None else int(max_iter)
+        x = (t.zeros(p, dtype=t.float64, device=dev) if x0 is None
+             else x0.to(device=dev, dtype=t.float64).clone())
+        trace = t.empty(max_iter + 1, dtype=t.float64, device=dev)
+        alphas = t.empty(max_iter, dtype=t.float64, device=dev)
+        betas = t.empty(max_iter, dtype=t.float64, device=dev)
+        result = t.zeros(4, dtype=t.int32, device=dev)
+        om = [_lib.to_device(o, dev) for o in omegas]
+        optrs = (ctypes.c_void_p * len(om))(*[_lib.ptr(o) for o in om])
+        args = [_lib.to_device(v, dev) for v in (prior_diag, minv, scale, b)]
+        _lib.check(_lib.lib().pcgs_rs_pcg(self._h, optrs, *[_lib.ptr(a) for a in args], _lib.ptr(x),
+                                          max_iter, float(rtol), _lib.ptr(trace), _lib.ptr(alphas),
+                                          _lib.ptr(betas), _lib.ptr(result), _lib.stream_ptr(dev)))
+        self._keep = (om, args)  # alive until the next call (the launch is asynchronous)
+        return x, trace, alphas, betas, result
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().pcgs_rs_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
+
+
+def fused_pcg_solve(op: "ShardedPrecisionOperator", b, M, x0=None, config=None, residual_scale=None):
+    """pcg_solve (cg.py:105-192) over a row-sharded operator with the fused
+    row-split kernel; same report and exceptions as `sharded_pcg_solve`."""
+    from .cg import CGConfig, _report_from_device
+    cfg = config if config is not None else CGConfig()
+    if op.local_apply is not None:
+        raise ValueError("the fused row split needs device shards")
+    solver = getattr(op, "_rowsplit", None)
+    if solver is None:
+        solver = op._rowsplit = RowSplitPCG(op.shards, device=op.device, group=op.group)
+    p = int(np.asarray(b).shape[0]) if not _lib.is_tensor(b) else int(b.shape[0])
+    scale = _metric_scale(op, M, residual_scale, p)
+    # the prior term is added once by every rank in the column step (replicated)
+    out = solver.solve(op.omegas, op.diag, np.asarray(M.inv_diagonal, dtype=np.float64), scale, b,
+                       x0=None if x0 is None else _lib.to_device(x0, op.device),
+                       max_iter=cfg.max_iter, rtol=cfg.rtol)
+    rep = _report_from_device(*out, as_tensor=_lib.is_tensor(b))
+    op.apply_count += rep.matvec_count
+    return rep
 
 
 # ---------------------------------------------------------------------------

@@ -68,15 +68,15 @@ def _check_csr(n, p, row_ptr, col_idx, nvals):
 class DesignStore:
     """Owner of one libpcgs design handle on one CUDA device."""
 
-    def __init__(self, n, p, row_ptr, col_idx, intercept, device=None, slab_max=0):
+    def __init__(self, n, p, row_ptr, col_idx, intercept, device=None, slab_max=0, grid=0):
         L = _lib.lib()
         self.device = _lib.cuda_device(device)
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
         h = ctypes.c_void_p()
-        _lib.check(L.pcgs_design_create(int(n), int(p), rp.ctypes.data, ci.ctypes.data,
-                                        int(bool(intercept)), int(slab_max),
-                                        int(self.device.index), ctypes.byref(h)))
+        _lib.check(L.pcgs_design_create_ex(int(n), int(p), rp.ctypes.data, ci.ctypes.data,
+                                           int(bool(intercept)), int(slab_max),
+                                           int(self.device.index), int(grid), ctypes.byref(h)))
         self._h = h
         info = np.zeros(16, dtype=np.int64)
         _lib.check(L.pcgs_design_info(h, info.ctypes.data))
@@ -289,11 +289,12 @@ class SparseDesignMatrix:
     def has_intercept(self):
         return self.pattern()[2]
 
-    def device_store(self, device=None, batch=1) -> DesignStore:
+    def device_store(self, device=None, batch=1, grid=0) -> DesignStore:
         """The pattern-only store on `device`; `batch` > 1 builds the variant
-        whose slabs leave room for `batch` chain-minor vectors (batched chains)."""
+        whose slabs leave room for `batch` chain-minor vectors (batched chains);
+        `grid` > 0 plans it for that many CTAs (row-split shards sharing a GPU)."""
         dev = _lib.cuda_device(device)
-        key = (dev.index, int(batch))
+        key = (dev.index, int(batch), int(grid))
         st = self._stores.get(key)
         if st is None:
             rp, ci, icpt = self.pattern()
@@ -304,7 +305,7 @@ class SparseDesignMatrix:
                     _lib.check(cap)
                 slab_max = min(slab_max, cap) if slab_max else cap
             st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0), rp, ci, icpt,
-                             device=dev, slab_max=slab_max)
+                             device=dev, slab_max=slab_max, grid=grid)
             self._stores[key] = st
         return st
 

@@ -19,8 +19,9 @@ def build(d, G, om, diag):
                                              group=parallel.EmulatedGroup())
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("G", [1, 2, 5])
-def test_sharded_phi_and_pcg_match_full(G):
+def test_sharded_phi_and_pcg_match_full(G, fused):
     d = synth.binary_design(2500, 400, 1e-3, 0.3, seed=8)
     rng = np.random.default_rng(1)
     om = rng.uniform(0.05, 0.3, d.n)
@@ -35,7 +36,8 @@ def test_sharded_phi_and_pcg_match_full(G):
     b = port.rhs(Xo, np.zeros(d.p + 1), om, diag, rng)
     M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv)
     op.apply_count = 0
-    rep = parallel.sharded_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv))
+    rep = parallel.sharded_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv),
+                                     fused=fused)
     oref = port.pcg(lambda x: port.phi_apply(Xo, om, diag, x), b, minv, np.sqrt(minv), rtol=1e-10)
     assert np.linalg.norm(rep.solution - oref.x) / np.linalg.norm(oref.x) < 1e-8
     assert rep.matvec_count == rep.iterations + 1 == op.apply_count

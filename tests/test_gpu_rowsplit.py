@@ -1,0 +1,86 @@
+"""Fused row-split PCG (csrc/rowsplit.cu): G row shards hosted by one grid on
+one GPU (the single-GPU form of the one-kernel-per-GPU exchange), checked
+against the CPU oracle and the unsharded device solve."""
+import numpy as np
+import pytest
+import torch
+
+import paper_1810_12437_b200 as pk
+from paper_1810_12437_b200 import parallel, synth
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+def sharded(d, G, om, diag, slab_max=0):
+    X = d.matrix()
+    parts = parallel.row_partition(d.row_ptr, G)
+    shards = [parallel.local_rows(X, lo, hi) for lo, hi in parts]
+    for s in shards:
+        s.slab_max = slab_max
+    return parallel.ShardedPrecisionOperator(shards, [om[lo:hi] for lo, hi in parts], diag,
+                                             group=parallel.EmulatedGroup())
+
+
+def small_system(seed=8):
+    d = synth.binary_design(2500, 400, 1e-3, 0.3, seed=seed)
+    rng = np.random.default_rng(1)
+    om = rng.uniform(0.05, 0.3, d.n)
+    lam = np.abs(rng.standard_cauchy(d.p)) + 0.05
+    diag = np.concatenate([[0.0], (0.05 * lam) ** -2.0])
+    minv = np.concatenate([[100.0], (0.05 * lam) ** 2])
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    b = port.rhs(Xo, np.zeros(d.p + 1), om, diag, rng)
+    return d, om, diag, minv, Xo, b
+
+
+@pytest.mark.parametrize("G,slab_max", [(1, 0), (2, 0), (3, 0), (4, 0), (8, 0), (2, 96), (4, 200)])
+def test_fused_rowsplit_matches_oracle(G, slab_max):
+    d, om, diag, minv, Xo, b = small_system()
+    op = sharded(d, G, om, diag, slab_max)
+    M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv)
+    rep = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv))
+    oref = port.pcg(lambda x: port.phi_apply(Xo, om, diag, x), b, minv, np.sqrt(minv), rtol=1e-10)
+    assert np.linalg.norm(rep.solution - oref.x) / np.linalg.norm(oref.x) < 1e-8
+    assert abs(rep.iterations - oref.iterations) <= 2
+    assert rep.termination == "converged"
+    assert rep.matvec_count == rep.iterations + 1 == len(rep.rms_precond_residual_trace)
+    assert len(rep.alphas) == rep.iterations
+    # the trace is the reference metric: RMS of s * r at every iteration
+    assert rep.rms_precond_residual_trace[-1] <= 1e-10 < rep.rms_precond_residual_trace[-2]
+
+
+def test_fused_rowsplit_max_iter_and_warm_start():
+    d, om, diag, minv, Xo, b = small_system(seed=3)
+    op = sharded(d, 4, om, diag)
+    M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv)
+    rep = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-30, max_iter=7),
+                                   residual_scale=np.sqrt(minv))
+    assert rep.termination == "max_iter" and rep.iterations == 7 and rep.matvec_count == 8
+    full = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv))
+    # warm start at the solution: converged before the first step (cg.py:139-149)
+    warm = parallel.fused_pcg_solve(op, b, M, x0=full.solution, config=pk.CGConfig(rtol=1e-6),
+                                    residual_scale=np.sqrt(minv))
+    assert warm.iterations == 0 and warm.matvec_count == 1
+
+
+def test_fused_rowsplit_config2_against_single_gpu():
+    d = synth.config_design(2, seed=0)
+    cond = synth.config2_conditioning(d, seed=0)
+    full = pk.PrecisionOperator(d.matrix(), cond["omega"], cond["prior_diag"])
+    rng = np.random.default_rng(7)
+    b = rng.standard_normal(d.p + 1) * 10
+    M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, cond["minv"])
+    cfg = pk.CGConfig(rtol=1e-10)
+    ref = pk.pcg_solve(full, b, M, config=cfg, residual_scale=cond["scale"])
+    for G in (2, 8):
+        op = sharded(d, G, cond["omega"], cond["prior_diag"])
+        a = parallel.fused_pcg_solve(op, b, M, config=cfg, residual_scale=cond["scale"])
+        again = parallel.fused_pcg_solve(op, b, M, config=cfg, residual_scale=cond["scale"])
+        assert np.array_equal(a.solution, again.solution)          # deterministic
+        rel = np.linalg.norm(a.solution - ref.solution) / np.linalg.norm(ref.solution)
+        assert rel < 1e-8, (G, rel)
+        # summation order alone moves the count on this spectrum
+        assert abs(a.iterations - ref.iterations) <= max(2, int(0.08 * ref.iterations)), (G, a.iterations,
+                                                                                          ref.iterations)
+    torch.cuda.synchronize()
