@@ -239,6 +239,10 @@ int pcgs_rs_destroy(pcgs_rs_t rs);
  * by (seed, stream_id), one thread per draw. */
 int pcgs_pg_draw(const double* z, int64_t n, uint64_t seed, uint64_t stream_id,
                  double* omega, pcgs_stream_t stream);
+/* pcgs_pg_draw over a row shard whose first row is global row `row0`: the
+ * draws are those of the unsharded call (Philox element = global row). */
+int pcgs_pg_draw_rows(const double* z, int64_t n, int64_t row0, uint64_t seed,
+                      uint64_t stream_id, double* omega, pcgs_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Device Gibbs scan (gibbs_run, gibbs.py:260-379).  All pointers are device
@@ -303,6 +307,24 @@ int pcgs_gibbs_scan_begin(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t,
                           pcgs_stream_t stream);
 int pcgs_gibbs_scan_end(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count,
                         int32_t slot, pcgs_stream_t stream);
+
+/* Row-split Gibbs scan (gibbs_run over row shards):
+ * `g` holds the replicated state (p-vectors, scalars, outputs; its part
+ * buffer has 16 * (grid + 1) doubles) and rows[l] the rows of local rank l.
+ * Bitwise identical replicated state on every rank; the draws of omega and
+ * of the RHS noise are keyed by global row, as in the unsharded scan.
+ * Prior / identity preconditioners, unstandardised designs. */
+typedef struct {
+  const double* y;      /* shard outcomes (0/1)                               */
+  const double* kappa;  /* shard y - 1/2                                      */
+  double* z;            /* shard X beta                                       */
+  double* omega;        /* shard Polya-Gamma draws                            */
+  double* part;         /* 16 * grid: the shard's per-CTA partial lines       */
+} pcgs_rs_rows_t;
+int pcgs_rs_gibbs_init(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows,
+                       pcgs_stream_t stream);
+int pcgs_rs_gibbs_scan(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows,
+                       int32_t t, int32_t count, int32_t slot, pcgs_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Batched independent chains (BASELINE config 4): R chains share

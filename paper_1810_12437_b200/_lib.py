@@ -73,12 +73,15 @@ SIGNATURES = {
     "pcgs_debug_cta_times": (ctypes.c_int, [_P]),
     "pcgs_debug_sync_times": (ctypes.c_int, [_P]),
     "pcgs_pg_draw": (ctypes.c_int, [_P, _I64, _U64, _U64, _P, _P]),
+    "pcgs_pg_draw_rows": (ctypes.c_int, [_P, _I64, _I64, _U64, _U64, _P, _P]),
     "pcgs_gibbs_init": (ctypes.c_int, [_P, _P, _P]),
     "pcgs_rs_create": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
     "pcgs_rs_exchange_handle": (ctypes.c_int, [_P, ctypes.c_int, _P]),
     "pcgs_rs_open_peer": (ctypes.c_int, [_P, ctypes.c_int, _P]),
     "pcgs_rs_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
     "pcgs_rs_destroy": (ctypes.c_int, [_P]),
+    "pcgs_rs_gibbs_init": (ctypes.c_int, [_P, _P, _P, _P]),
+    "pcgs_rs_gibbs_scan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P]),
     "pcgs_batch_slab_max": (ctypes.c_int, [ctypes.c_int]),
     "pcgs_batch_phi_apply": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, _P]),
     "pcgs_batch_pcg": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P,

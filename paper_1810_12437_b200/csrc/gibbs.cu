@@ -11,6 +11,7 @@
 #include <string>
 
 #include "internal.cuh"
+#include "rowsplit.h"
 
 namespace {
 
@@ -334,6 +335,84 @@ int pcgs_gibbs_scan(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, 
   int rc = pcgs_gibbs_scan_begin(d, g, t, stream);
   if (rc) return rc;
   return pcgs_gibbs_scan_end(d, g, t, count, slot, stream);
+}
+
+// ---------------------------------------------------------------------------
+// Row-split scan (BASELINE config 5): rows of X over the
+// ranks of a pcgs_rs context, p-vectors replicated.  Per scan: PG draws on
+// each rank's rows (Philox keyed by global row, so the draws are those of the
+// unsharded chain), tau / lambda replicated (same keys everywhere), RHS and
+// PCG in the fused row-split kernel (one exchange for b, one per iteration),
+// X beta and the log-likelihood per rank, one scalar exchange for the log
+// density, replicated statistics.
+// ---------------------------------------------------------------------------
+static int rs_logit(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows, cudaStream_t s) {
+  for (int l = 0; l < rs_n_local(rs); ++l) {
+    pcgs_design_t d;
+    int64_t row0;
+    int rc;
+    if ((rc = rs_local(rs, l, &d, &row0))) return rc;
+    CUDA_TRY(cudaFuncSetAttribute(k_csr_logit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem_bytes(d->dev)));
+    pcgs_gibbs_t gl = *g;
+    gl.y = rows[l].y;
+    gl.z = rows[l].z;
+    gl.part = rows[l].part;
+    if ((rc = launch_logit(d, &gl, s))) return rc;
+  }
+  return PCGS_OK;
+}
+
+int pcgs_rs_gibbs_init(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows, pcgs_stream_t stream) {
+  if (!rs || !g || !rows || !g->beta || !g->part) return fail(PCGS_EINVAL, "null argument");
+  if (g->precond == 2) return fail(PCGS_EUNSUP, "row split: the Jacobi preconditioner is not sharded");
+  if (g->cscale) return fail(PCGS_EUNSUP, "row split: standardised designs are not sharded");
+  pcgs_design_t d;
+  int64_t row0;
+  int rc;
+  if ((rc = rs_local(rs, 0, &d, &row0))) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_tau_sums<<<rs_grid(rs), 256, 0, s>>>(*g, d->dev.pt);
+  CUDA_TRY(cudaGetLastError());
+  return rs_logit(rs, g, rows, s);
+}
+
+int pcgs_rs_gibbs_scan(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows, int32_t t, int32_t count,
+                       int32_t slot, pcgs_stream_t stream) {
+  if (!rs || !g || !rows || t < 1) return fail(PCGS_EINVAL, "bad argument");
+  const int nl = rs_n_local(rs), Gr = rs_grid(rs);
+  cudaStream_t s = (cudaStream_t)stream;
+  const double* omegas[8];
+  const double* kappas[8];
+  long long pt = 0;
+  int rc;
+  for (int l = 0; l < nl; ++l) {
+    pcgs_design_t d;
+    int64_t row0;
+    if ((rc = rs_local(rs, l, &d, &row0))) return rc;
+    pt = d->dev.pt;
+    if (!g->fixed_omega &&
+        (rc = pcgs_pg_draw_rows(rows[l].z, d->dev.n, row0, g->seed, (uint64_t)t, rows[l].omega, stream)))
+      return rc;
+    omegas[l] = rows[l].omega;
+    kappas[l] = rows[l].kappa;
+  }
+  if (!g->fixed_tau) k_global<<<1, 32, 0, s>>>(*g, pt, t, Gr);
+  const int eblocks = (int)std::min<long long>((pt + 255) / 256, 4 * Gr);
+  k_local<<<eblocks, 256, 0, s>>>(*g, pt, t, count);
+  if (g->precond == 1) k_precond<<<eblocks, 256, 0, s>>>(*g, pt, nullptr);
+  CUDA_TRY(cudaGetLastError());
+  RsSolve S{omegas, kappas, g->seed, (uint64_t)t, g->b, g->prior_diag, g->minv, g->scale, nullptr, g->beta,
+            g->max_iter, g->rtol, g->trace, g->alphas, g->betas, g->results + 8 * (t - 1)};
+  if ((rc = rs_solve(rs, S, s))) return rc;
+  if ((rc = rs_logit(rs, g, rows, s))) return rc;
+  const double* parts[8];
+  for (int l = 0; l < nl; ++l) parts[l] = rows[l].part;
+  if ((rc = rs_sum(rs, parts, g->part, s))) return rc;  // line 0, slot 0: total log-likelihood
+  k_stats<<<Gr, 256, 0, s>>>(*g, pt, count + 1, slot);
+  k_post<<<1, 32, 0, s>>>(*g, pt, t, 1, Gr);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
 }
 
 }  // extern "C"

@@ -120,13 +120,14 @@ struct FillRhs {  // u_i = kappa_i + sqrt(omega_i) * eta_i
   const double* eta;  // null: Philox
   unsigned long long seed, stream;
   long long lo;
+  long long row0 = 0;  // global index of local row 0 (row shards): Philox keys are global rows
   __device__ double operator()(int j) const {
     const long long i = lo + j;
     double e;
     if (eta) {
       e = __ldg(eta + i);
     } else {
-      Philox R(seed, stream, (unsigned)i);
+      Philox R(seed, stream, (unsigned)(row0 + i));
       e = R.normal();
     }
     return (kappa ? __ldg(kappa + i) : 0.0) + sqrt(__ldg(omega + i)) * e;

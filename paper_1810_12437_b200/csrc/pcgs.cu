@@ -572,9 +572,10 @@ __device__ double pg_draw1(double z, Philox& R) {
   }
 }
 
-__global__ void k_pg(const double* z, long long n, unsigned long long seed, unsigned long long stream, double* omega) {
+__global__ void k_pg(const double* z, long long n, unsigned long long seed, unsigned long long stream, double* omega,
+                     long long row0) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    Philox R(seed, stream, (unsigned)i);
+    Philox R(seed, stream, (unsigned)(row0 + i));
     omega[i] = pg_draw1(z[i], R);
   }
 }
@@ -1125,11 +1126,16 @@ int pcgs_copy(void* dst, const void* src, int64_t bytes, int kind) {
 
 int pcgs_pg_draw(const double* z, int64_t n, uint64_t seed, uint64_t stream_id, double* omega,
                  pcgs_stream_t stream) {
+  return pcgs_pg_draw_rows(z, n, 0, seed, stream_id, omega, stream);
+}
+
+int pcgs_pg_draw_rows(const double* z, int64_t n, int64_t row0, uint64_t seed, uint64_t stream_id, double* omega,
+                      pcgs_stream_t stream) {
   if (n < 0 || (n > 0 && (!z || !omega))) return fail(PCGS_EINVAL, "null argument");
   if (n == 0) return PCGS_OK;
   cudaStream_t s = (cudaStream_t)stream;
   const int blocks = (int)std::min<int64_t>((n + 127) / 128, 148 * 16);
-  k_pg<<<blocks, 128, 0, s>>>(z, n, seed, kStreamPG ^ stream_id, omega);
+  k_pg<<<blocks, 128, 0, s>>>(z, n, seed, kStreamPG ^ stream_id, omega, row0);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
 }

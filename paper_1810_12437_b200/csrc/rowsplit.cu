@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "rowsplit.h"
 
 namespace cg = cooperative_groups;
 
@@ -43,19 +44,20 @@ constexpr int kMaxGridRs = 256;
 constexpr int kRsMaxPairs = 512;  // (rank, CSC slab) pairs summed per column
 
 // Exchange region of one rank (one allocation, IPC-shareable):
-//   header (64 B) | inbox flags [kRsMaxRanks] u64 | part [2][16 * G] f64 |
+//   header (64 B) | inbox flags [kRsMaxRanks] u64 | scalar slot (64 B) | part [2][16 * G] f64 |
 //   pieces [2][nseg] f64 | piece_ptr [nslab * (pt + 1)] i32
 struct RsHeader {
-  long long nseg, pt, nslab, G, bytes;
-  long long pad[3];
+  long long nseg, pt, nslab, G, bytes, n;
+  long long pad[2];
 };
 
 struct RsLayout {
-  size_t flags, part, pieces, pp, bytes;
+  size_t flags, scal, part, pieces, pp, bytes;
   static RsLayout of(long long nseg, long long pt, long long nslab, long long G) {
     RsLayout L;
     L.flags = sizeof(RsHeader);
-    L.part = L.flags + kRsMaxRanks * sizeof(unsigned long long);
+    L.scal = L.flags + kRsMaxRanks * sizeof(unsigned long long);
+    L.part = L.scal + 64;
     L.pieces = L.part + 2 * (size_t)kPartStride * G * sizeof(double);
     L.pp = L.pieces + 2 * (size_t)std::max<long long>(nseg, 1) * sizeof(double);
     L.bytes = L.pp + (size_t)nslab * (pt + 1) * sizeof(int) + 64;
@@ -69,7 +71,8 @@ struct RsPeer {                  // every rank, as this GPU sees it
   const double* pieces;          // [2][nseg]
   const int* pp;                 // piece_ptr, local copy
   unsigned long long* inbox;     // the rank's flag array (peer-mapped for remote ranks)
-  long long nseg;
+  double* scal;                  // the rank's scalar exchange slot
+  long long nseg, n, row0;       // pieces per parity; shard rows; first global row
   int nslab;
   int remote;
 };
@@ -99,6 +102,19 @@ struct RsArgs {
   double rtol;
   double *trace, *alphas, *betas;
   int* result;
+  // generate_rhs before the solve (sampler.py:94-107): b = X'(kappa + sqrt(omega) eta) + sqrt(d) delta
+  int rhs;
+  const double* kappa[kRsMaxLocal];
+  unsigned long long seed, stream_id;
+  double* b_out;                 // replicated b (reference layout), written by the lead group
+};
+
+struct RsSumArgs {               // sum of a per-CTA partial over every rank's CTAs
+  const double* part[kRsMaxLocal];
+  int ncta, n_local, nranks, my_rank;
+  const RsPeer* peers;
+  unsigned long long* epoch;
+  double* out;
 };
 
 __device__ __forceinline__ double ld_peer(const double* p, bool remote) { return remote ? __ldcv(p) : __ldcg(p); }
@@ -123,6 +139,22 @@ __device__ void rs_exchange(const RsArgs& A, int my_rank, unsigned long long e) 
     } while (v < e);
   }
   cg::this_grid().sync();
+}
+
+// This lane's share of column j's pieces over every (rank, slab) pair of the
+// parity-`par` buffers; the warp sum of the lane shares is the column total.
+__device__ __forceinline__ double rs_lane_pieces(const RsArgs& A, const int2* pairs, long long pt, long long j,
+                                                  int par, int lane) {
+  double s = 0.0;
+  for (int k = lane; k < A.npairs; k += 32) {
+    const int2 qs = pairs[k];
+    const RsPeer& P = A.peers[qs.x];
+    const int* pp = P.pp + (long long)qs.y * (pt + 1);
+    const int q0 = __ldg(pp + j), q1 = __ldg(pp + j + 1);
+    const double* pc = P.pieces + par * P.nseg;
+    for (int q = q0; q < q1; ++q) s += ld_peer(pc + q, P.remote);
+  }
+  return s;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
@@ -182,6 +214,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
     st_applies = 0;
   }
   cg::this_grid().sync();
+
+  // ---------------- R: the randomised right-hand side (one exchange) ----------------
+  int e_off = 0;
+  if (A.rhs) {
+    {
+      FillRhs f{A.kappa[gi], omega, nullptr, A.seed, kStreamEta ^ A.stream_id, 0, A.peers[G.rank].row0};
+      EpiStore e{G.pieces + (long long)G.D.csc.nseg};  // parity 1: iteration 0 writes parity 0
+      run_pass(G.D.csc, sv, f, e, 0, cta);
+    }
+    rs_exchange(A, G.rank, st_epoch + 1ull);
+    for (int t = warp; t < chunk; t += kWarps) {
+      const long long j = j0 + t;
+      if (j >= pt) break;
+      const double s = warp_sum(rs_lane_pieces(A, pairs, pt, j, 1, lane));
+      if (lane == 0) {
+        const long long rj = ref_index(j, G.D.p, G.D.icpt);
+        Philox R(A.seed, kStreamDelta ^ A.stream_id, (unsigned)rj);
+        const double bj = s + sqrt(oD[t]) * R.normal();
+        obv[t] = bj;
+        if (lead && A.b_out) A.b_out[rj] = bj;
+      }
+    }
+    e_off = 1;
+    __syncthreads();
+  }
 
   for (int a = 0;; ++a) {
     const int par = a & 1;
@@ -264,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
     if (tid == 0) ++st_applies;
-    rs_exchange(A, G.rank, st_epoch + (unsigned long long)a + 1ull);
+    rs_exchange(A, G.rank, st_epoch + (unsigned long long)(e_off + a) + 1ull);
 
     // ---------------- C: assemble owned columns over all ranks, step ----------------
     double alpha = 0.0;
@@ -300,15 +357,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
     for (int t = warp; t < chunk; t += kWarps) {
       const long long j = j0 + t;
       if (j >= pt) break;
-      double s = 0.0;
-      for (int k = lane; k < A.npairs; k += 32) {
-        const int2 qs = pairs[k];
-        const RsPeer& P = A.peers[qs.x];
-        const int* pp = P.pp + (long long)qs.y * (pt + 1);
-        const int q0 = __ldg(pp + j), q1 = __ldg(pp + j + 1);
-        const double* pc = P.pieces + par * P.nseg;
-        for (int q = q0; q < q1; ++q) s += ld_peer(pc + q, P.remote);
-      }
+      double s = rs_lane_pieces(A, pairs, pt, j, par, lane);
       s = warp_sum(s);
       if (lane == 0) {
         const double Ad = s + oD[t] * od[t];
@@ -348,7 +397,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
   }
   // exchanges used by this call: every rank ran the same number of iterations
   cg::this_grid().sync();
-  if (blockIdx.x == 0 && tid == 0) *A.epoch = st_epoch + (unsigned long long)st_applies;
+  if (blockIdx.x == 0 && tid == 0) *A.epoch = st_epoch + (unsigned long long)(e_off + st_applies);
+}
+
+// Sum over ranks (rank order) of per-CTA partials (line slot 0): one warp.
+// Ranks on other GPUs publish their local sums in their scalar slots and meet
+// at a flag exchange (one epoch).
+__global__ void __launch_bounds__(32) k_rs_sum(RsSumArgs A) {
+  const int lane = threadIdx.x;
+  double v[kRsMaxLocal];
+  for (int l = 0; l < A.n_local; ++l) {
+    double x = 0.0;
+    for (int c = lane; c < A.ncta; c += 32) x += __ldcg(A.part[l] + (long long)c * kPartStride);
+    v[l] = warp_sum(x);
+  }
+  if (A.n_local == A.nranks) {
+    if (lane == 0) {
+      double t = 0.0;
+      for (int l = 0; l < A.n_local; ++l) t += v[l];
+      *A.out = t;
+    }
+    return;
+  }
+  const unsigned long long e = *A.epoch + 1ull;
+  const RsPeer& me = A.peers[A.my_rank];
+  if (lane == 0) *me.scal = v[0];
+  __threadfence_system();
+  __syncwarp();
+  for (int q = lane; q < A.nranks; q += 32) {
+    if (q == A.my_rank) continue;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(A.peers[q].inbox + A.my_rank), "l"(e) : "memory");
+    unsigned long long f;
+    do {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(me.inbox + q) : "memory");
+    } while (f < e);
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double t = 0.0;
+    for (int q = 0; q < A.nranks; ++q) t += q == A.my_rank ? v[0] : ld_peer(A.peers[q].scal, true);
+    *A.out = t;
+    *A.epoch = e;
+  }
 }
 
 }  // namespace
@@ -435,7 +525,7 @@ int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nra
     const RsLayout L = RsLayout::of(D.csc.nseg, D.pt, D.csc.nslab, D.G);
     if ((rc = rs_alloc(R, L.bytes, &p))) return bail(rc);
     if (cudaMemset(p, 0, L.bytes) != cudaSuccess) return bail(fail(PCGS_ECUDA, "memset"));
-    RsHeader h{D.csc.nseg, D.pt, D.csc.nslab, D.G, (long long)L.bytes, {0, 0, 0}};
+    RsHeader h{D.csc.nseg, D.pt, D.csc.nslab, D.G, (long long)L.bytes, D.n, {0, 0}};
     if (cudaMemcpy(p, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess ||
         cudaMemcpy((char*)p + L.pp, D.csc.piece_ptr, (size_t)D.csc.nslab * (D.pt + 1) * sizeof(int),
                    cudaMemcpyDeviceToDevice) != cudaSuccess)
@@ -513,7 +603,10 @@ static int rs_finalize(pcgs_rs* R) {
     P.part = (const double*)(base + L.part);
     P.pieces = (const double*)(base + L.pieces);
     P.inbox = (unsigned long long*)(base + L.flags);
+    P.scal = (double*)(base + L.scal);
     P.nseg = h.nseg;
+    P.n = h.n;
+    P.row0 = q == 0 ? 0 : R->peers[q - 1].row0 + R->peers[q - 1].n;
     P.nslab = (int)h.nslab;
     P.remote = R->opened[q];
     if (P.remote) {
@@ -558,48 +651,10 @@ static int rs_finalize(pcgs_rs* R) {
 int pcgs_rs_pcg(pcgs_rs_t R, const double* const* omegas_h, const double* prior_diag, const double* minv,
                 const double* scale, const double* b, double* x, int32_t max_iter, double rtol, double* trace,
                 double* alphas, double* betas, int32_t* result, pcgs_stream_t stream) {
-  if (!R || !omegas_h || !prior_diag || !minv || !scale || !b || !x || !trace || !alphas || !betas || !result)
-    return fail(PCGS_EINVAL, "null argument");
-  if (max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
-  CUDA_TRY(cudaSetDevice(R->device));
-  int rc;
-  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
-  cudaStream_t s = (cudaStream_t)stream;
-  if (R->n_local > kRsMaxLocal) return fail(PCGS_EINVAL, "row split: too many ranks in one grid");
-  RsArgs A{};
-  A.groups = R->groups_dev;
-  for (int l = 0; l < R->n_local; ++l) A.omega[l] = omegas_h[l];
-  A.n_local = R->n_local;
-  A.Gr = R->Gr;
-  A.nranks = R->nranks;
-  A.smem_doubles = R->smem_doubles;
-  A.peers = R->peers_dev;
-  A.pairs = R->pairs_dev;
-  A.npairs = R->npairs;
-  A.epoch = R->epoch;
-  A.diag = prior_diag;
-  A.minv = minv;
-  A.scale = scale;
-  A.b = b;
-  A.x = x;
-  A.max_iter = max_iter;
-  A.rtol = rtol;
-  A.trace = trace;
-  A.alphas = alphas;
-  A.betas = betas;
-  A.result = result;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(R->Gr * R->n_local);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = rs_smem_bytes(R);
-  cfg.stream = s;
-  cudaLaunchAttribute attr;
-  attr.id = cudaLaunchAttributeCooperative;
-  attr.val.cooperative = 1;
-  cfg.attrs = &attr;
-  cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pcg_rs, A));
-  return PCGS_OK;
+  if (!R || !omegas_h || !b) return fail(PCGS_EINVAL, "null argument");
+  RsSolve S{omegas_h, nullptr, 0, 0, nullptr, prior_diag, minv, scale, b, x, max_iter, rtol, trace, alphas, betas,
+            result};
+  return rs_solve(R, S, (cudaStream_t)stream);
 }
 
 int pcgs_rs_destroy(pcgs_rs_t R) {
@@ -614,3 +669,83 @@ int pcgs_rs_destroy(pcgs_rs_t R) {
 }
 
 }  // extern "C"
+
+int rs_solve(pcgs_rs_t R, const RsSolve& S, cudaStream_t s) {
+  if (!R || !S.omegas || !S.diag || !S.minv || !S.scale || (!S.b && !S.kappas) || !S.x || !S.trace || !S.alphas ||
+      !S.betas || !S.result)
+    return fail(PCGS_EINVAL, "null argument");
+  if (S.max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
+  CUDA_TRY(cudaSetDevice(R->device));
+  int rc;
+  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
+  RsArgs A{};
+  A.groups = R->groups_dev;
+  for (int l = 0; l < R->n_local; ++l) {
+    A.omega[l] = S.omegas[l];
+    A.kappa[l] = S.kappas ? S.kappas[l] : nullptr;
+  }
+  A.n_local = R->n_local;
+  A.Gr = R->Gr;
+  A.nranks = R->nranks;
+  A.smem_doubles = R->smem_doubles;
+  A.peers = R->peers_dev;
+  A.pairs = R->pairs_dev;
+  A.npairs = R->npairs;
+  A.epoch = R->epoch;
+  A.diag = S.diag;
+  A.minv = S.minv;
+  A.scale = S.scale;
+  A.b = S.kappas ? S.diag : S.b;  // unread when the RHS is generated
+  A.x = S.x;
+  A.max_iter = S.max_iter;
+  A.rtol = S.rtol;
+  A.trace = S.trace;
+  A.alphas = S.alphas;
+  A.betas = S.betas;
+  A.result = S.result;
+  A.rhs = S.kappas ? 1 : 0;
+  A.seed = S.seed;
+  A.stream_id = S.stream_id;
+  A.b_out = S.b_out;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(R->Gr * R->n_local);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = rs_smem_bytes(R);
+  cfg.stream = s;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeCooperative;
+  attr.val.cooperative = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pcg_rs, A));
+  return PCGS_OK;
+}
+
+int rs_sum(pcgs_rs_t R, const double* const* parts, double* out, cudaStream_t s) {
+  int rc;
+  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
+  RsSumArgs A{};
+  for (int l = 0; l < R->n_local; ++l) A.part[l] = parts[l];
+  A.ncta = R->Gr;
+  A.n_local = R->n_local;
+  A.nranks = R->nranks;
+  A.my_rank = R->rank0;
+  A.peers = R->peers_dev;
+  A.epoch = R->epoch;
+  A.out = out;
+  k_rs_sum<<<1, 32, 0, s>>>(A);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+int rs_local(pcgs_rs_t R, int l, pcgs_design_t* d, int64_t* row0) {
+  if (!R || l < 0 || l >= R->n_local) return fail(PCGS_EINVAL, "bad local rank");
+  int rc;
+  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
+  *d = R->designs[l];
+  *row0 = R->peers[R->rank0 + l].row0;
+  return PCGS_OK;
+}
+
+int rs_n_local(pcgs_rs_t R) { return R->n_local; }
+int rs_grid(pcgs_rs_t R) { return R->Gr; }

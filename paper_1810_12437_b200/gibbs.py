@@ -214,9 +214,8 @@ class DeviceChain:
                  fixed_tau=None, fixed_lam=None, device=None):
         t = _lib.torch()
         self.X = X
-        self.store = X.device_store(device)
-        st = self.store
-        dev = self.dev = st.device
+        self._open_device(X, device)
+        dev = self.dev
         f64 = t.float64
         self.n, self.pt = X.n_rows, X.n_cols
         self.q = cfg.n_unshrunk
@@ -269,7 +268,7 @@ class DeviceChain:
         self.minv = t.empty(self.pt, dtype=f64, device=dev)
         self.scale = t.empty(self.pt, dtype=f64, device=dev)
         self.b = t.empty(self.pt, dtype=f64, device=dev)
-        self.part = t.zeros(_PART_STRIDE * (st.describe()["grid"] + 1), dtype=f64, device=dev)
+        self.part = t.zeros(_PART_STRIDE * (self.grid + 1), dtype=f64, device=dev)
         self.logdens = t.zeros(max(n_iter, 1), dtype=f64, device=dev)
         self.results = t.zeros(8 * max(n_iter, 1), dtype=t.int32, device=dev)
         self.draws = t.empty((max(self.n_store, 1), self.pt), dtype=f64, device=dev)
@@ -302,7 +301,16 @@ class DeviceChain:
                                             ctypes.c_void_p]
         L.pcgs_gibbs_scan_end.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
-        _lib.check(L.pcgs_gibbs_init(st.handle, ctypes.byref(self.args), _lib.stream_ptr(dev)))
+        self._init_device()
+
+    def _open_device(self, X, device):
+        self.store = X.device_store(device)
+        self.dev = self.store.device
+        self.grid = self.store.describe()["grid"]
+
+    def _init_device(self):
+        _lib.check(_lib.lib().pcgs_gibbs_init(self.store.handle, ctypes.byref(self.args),
+                                              _lib.stream_ptr(self.dev)))
 
     def scan(self, t, local_scale_sampler=None, rng=None):
         """Issue scan t (1-based) on the current stream; no synchronisation

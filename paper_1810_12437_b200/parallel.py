@@ -16,6 +16,8 @@ the decomposition is validated on one GPU.
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
@@ -207,7 +209,6 @@ class RowSplitPCG:
     """
 
     def __init__(self, shards, device=None, group=None):
-        import ctypes
         t = _lib.torch()
         L = _lib.lib()
         self.device = _lib.cuda_device(device)
@@ -249,7 +250,6 @@ class RowSplitPCG:
     def solve(self, omegas, prior_diag, minv, scale, b, x0=None, max_iter=None, rtol=1e-6):
         """Device tensors in (omegas: one per local shard); returns (x, trace,
         alphas, betas, result) tensors, nothing synchronised (pcg_solve_device)."""
-        import ctypes
         t = _lib.torch()
         dev = self.device
         p = self.p_total
@@ -298,6 +298,131 @@ def fused_pcg_solve(op: "ShardedPrecisionOperator", b, M, x0=None, config=None, 
     rep = _report_from_device(*out, as_tensor=_lib.is_tensor(b))
     op.apply_count += rep.matvec_count
     return rep
+
+
+# ---------------------------------------------------------------------------
+# Row-split Gibbs scan (BASELINE config 5): gibbs_run with X's rows over ranks
+# ---------------------------------------------------------------------------
+class _RsRows(ctypes.Structure):
+    """Mirror of pcgs_rs_rows_t (include/pcgs.h)."""
+    _fields_ = [("y", ctypes.c_void_p), ("kappa", ctypes.c_void_p), ("z", ctypes.c_void_p),
+                ("omega", ctypes.c_void_p), ("part", ctypes.c_void_p)]
+
+
+def _row_split_chain_class():
+    from .gibbs import DeviceChain, _GibbsArgs, _PART_STRIDE
+
+    class RowSplitChain(DeviceChain):
+        """DeviceChain whose scans run over row shards (`RowSplitPCG` context):
+        replicated p-state, full-length row vectors of which each hosted rank
+        owns its contiguous range."""
+
+        def __init__(self, X, y, cfg, n_iter, parts, hosted, group=None, device=None, **kw):
+            self._parts, self._hosted, self._group = parts, hosted, group
+            super().__init__(X, y, cfg, n_iter, device=device, **kw)
+
+        def _open_device(self, X, device):
+            if X.standardized:
+                raise NotImplementedError("row split: standardised designs are not sharded")
+            shards = [local_rows(X, *self._parts[r]) for r in self._hosted]
+            self.rs = RowSplitPCG(shards, device=device, group=self._group)
+            self.store = None
+            self.dev = self.rs.device
+            self.grid = self.rs.stores[0].describe()["grid"]
+
+        def _init_device(self):
+            t = _lib.torch()
+            L = _lib.lib()
+            P = _lib.ptr
+            self._parts_buf = [t.zeros(_PART_STRIDE * (self.grid + 1), dtype=t.float64, device=self.dev)
+                               for _ in self._hosted]
+            rows = (_RsRows * len(self._hosted))()
+            for k, r in enumerate(self._hosted):
+                lo, _ = self._parts[r]
+                off = 8 * lo
+                rows[k] = _RsRows(P(self.y) + off, P(self.kappa) + off, P(self.z) + off, P(self.omega) + off,
+                                  P(self._parts_buf[k]))
+            self._rows = rows
+            L.pcgs_rs_gibbs_init.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_void_p,
+                                             ctypes.c_void_p]
+            L.pcgs_rs_gibbs_scan.argtypes = [ctypes.c_void_p, ctypes.POINTER(_GibbsArgs), ctypes.c_void_p,
+                                             ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
+            _lib.check(L.pcgs_rs_gibbs_init(self.rs._h, ctypes.byref(self.args), ctypes.addressof(rows),
+                                            _lib.stream_ptr(self.dev)))
+
+        def scan(self, t, local_scale_sampler=None, rng=None):
+            if local_scale_sampler is not None:
+                raise NotImplementedError("row split: local_scale_sampler is not sharded")
+            slot = -1
+            if t > self.burn_in and (t - self.burn_in - 1) % self.thin == 0:
+                slot = self.stored
+                self.stored += 1
+            _lib.check(_lib.lib().pcgs_rs_gibbs_scan(self.rs._h, ctypes.byref(self.args),
+                                                     ctypes.addressof(self._rows), int(t), int(self.count),
+                                                     int(slot), _lib.stream_ptr(self.dev)))
+            self.count += 1
+
+        def output(self):
+            out = super().output()
+            real = self._group is not None and not isinstance(self._group, EmulatedGroup)
+            if real:
+                # every rank holds only its own rows of omega: gather them
+                import torch.distributed as dist
+                lo, hi = self._parts[self._hosted[0]]
+                mine = self.omega[lo:hi].cpu().numpy()
+                allp = [None] * dist.get_world_size(self._group)
+                dist.all_gather_object(allp, mine, group=self._group)
+                out.final_state.omega[:] = np.concatenate(allp)
+            return out
+
+    return RowSplitChain
+
+
+def row_split_gibbs_run(X, y, cfg, n_iter, shards=None, group=None, burn_in=0, seed=0, thin=1,
+                        preconditioner="prior", cg_config=None, init_state=None, gamma_scale=1.0,
+                        allow_max_iter=False, fixed_omega=None, fixed_tau=None, fixed_lam=None,
+                        device=None, sync_every=64):
+    """gibbs_run (gibbs.py:260-379) with the rows of X split over ranks.
+
+    With a torch.distributed `group` of W processes (one GPU each) rank r
+    holds row shard r of an nnz-balanced partition; without one, `shards`
+    row shards (default 2) are hosted by one process on one GPU.  Same
+    output as gibbs_run on every rank: replicated state, the draws of omega
+    and of the RHS noise keyed by global row (the unsharded chain's keys; only
+    summation order differs).  Prior or identity preconditioning; no
+    local_scale_sampler and no standardised designs on this path."""
+    from .gibbs import GibbsAbortError, _PRECOND  # noqa: F401
+    y = np.asarray(y, dtype=np.float64)
+    if y.shape != (X.n_rows,) or not np.all((y == 0.0) | (y == 1.0)):
+        raise ValueError("outcomes must be 0/1, one per design row")
+    if n_iter < 0 or burn_in < 0 or burn_in > n_iter or thin < 1:
+        raise ValueError("need 0 <= burn_in <= n_iter and thin >= 1")
+    if preconditioner not in ("prior", "identity"):
+        raise NotImplementedError("row split: prior or identity preconditioning")
+    real = group is not None and not isinstance(group, EmulatedGroup)
+    rp, _, icpt = X.pattern()
+    if real:
+        import torch.distributed as dist
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        parts = row_partition(rp, world, intercept=icpt)
+        hosted = [rank]
+    else:
+        nsh = int(shards or 2)
+        parts = row_partition(rp, nsh, intercept=icpt)
+        hosted = list(range(nsh))
+    Chain = _row_split_chain_class()
+    ch = Chain(X, y, cfg, n_iter, parts, hosted, group=group, device=device, burn_in=burn_in, thin=thin,
+               seed=seed, preconditioner=preconditioner, cg_config=cg_config, init_state=init_state,
+               gamma_scale=gamma_scale, fixed_omega=fixed_omega, fixed_tau=fixed_tau, fixed_lam=fixed_lam)
+    checked = 0
+    for t in range(1, n_iter + 1):
+        ch.scan(t)
+        if sync_every and t - checked >= sync_every:
+            ch.check(checked + 1, t, allow_max_iter)
+            checked = t
+    if checked < n_iter:
+        ch.check(checked + 1, n_iter, allow_max_iter)
+    return ch.output()
 
 
 # ---------------------------------------------------------------------------

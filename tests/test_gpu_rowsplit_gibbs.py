@@ -1,0 +1,86 @@
+"""Row-split Gibbs scan (BASELINE config 5's mode): G row shards hosted by one
+grid on one GPU, against the unsharded device chain (same Philox keys, only
+summation order differs) and the exact Gaussian under pinned scales."""
+import numpy as np
+import pytest
+
+from paper_1810_12437_b200 import gibbs, parallel, synth
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def small():
+    d = synth.binary_design(600, 80, 5e-3, 0.3, seed=5)
+    y, truth = synth.simulate_outcomes(d, seed=1, n_signal=6)
+    return d, y, truth
+
+
+@pytest.mark.parametrize("shards", [1, 2, 3])
+@pytest.mark.parametrize("prior", ["bridge", "horseshoe"])
+def test_pinned_omega_chain_tracks_unsharded(small, prior, shards):
+    """With omega pinned the scan is a continuous map of the previous draw
+    (tau, lambda and the RHS noise use the same keys), so the sharded chain
+    follows the unsharded one to rounding."""
+    d, y, _ = small
+    X = d.matrix()
+    om = np.random.default_rng(3).uniform(0.1, 0.3, d.n)
+    cfg = (gibbs.BridgeConfig if prior == "bridge" else gibbs.HorseshoeConfig)(unshrunk_prior_sd=(np.inf,))
+    kw = dict(seed=4, fixed_omega=om, cg_config=gibbs.CGConfig(rtol=1e-10))
+    ref = gibbs.gibbs_run(X, y, cfg, 12, **kw)
+    out = parallel.row_split_gibbs_run(X, y, cfg, 12, shards=shards, **kw)
+    scale = np.abs(ref.draws).max()
+    assert np.abs(out.draws - ref.draws).max() < 1e-6 * scale
+    np.testing.assert_allclose(out.tau_draws, ref.tau_draws, rtol=1e-6)
+    np.testing.assert_allclose(out.logdensity_trace, ref.logdensity_trace, rtol=1e-8)
+    assert np.abs(out.cg_iteration_counts - ref.cg_iteration_counts).max() <= 2
+
+
+def test_free_chain_moments_match_unsharded(small):
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    n_iter, burn = 1500, 300
+    ref = gibbs.gibbs_run(X, y, cfg, n_iter, burn_in=burn, seed=9)
+    out = parallel.row_split_gibbs_run(X, y, cfg, n_iter, burn_in=burn, seed=9, shards=3)
+    assert out.draws.shape == ref.draws.shape
+    assert np.all(np.isfinite(out.draws)) and out.final_state.omega.shape == (d.n,)
+
+    def batch_se(x, nb=10):
+        n = (len(x) // nb) * nb
+        return x[:n].reshape(nb, -1).mean(1).std(ddof=1) / np.sqrt(nb)
+
+    se = np.sqrt([batch_se(ref.draws[:, j]) ** 2 + batch_se(out.draws[:, j]) ** 2 for j in range(d.p + 1)])
+    keep = se > 1e-12
+    z = (out.draws.mean(0) - ref.draws.mean(0))[keep] / se[keep]
+    assert np.mean(np.abs(z) > 4) < 0.03
+
+
+def test_pinned_scales_exact_gaussian(small):
+    d, y, _ = small
+    X = d.matrix()
+    rng = np.random.default_rng(0)
+    om = rng.uniform(0.1, 0.3, d.n)
+    lam = rng.uniform(0.5, 2.0, d.p)
+    tau = 0.3
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    out = parallel.row_split_gibbs_run(X, y, cfg, 3000, seed=2, shards=2, fixed_omega=om, fixed_tau=tau,
+                                       fixed_lam=lam, cg_config=gibbs.CGConfig(rtol=1e-10))
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    dense = np.zeros((d.n, d.p + 1))
+    rows = np.repeat(np.arange(d.n), np.diff(Xo.row_ptr))
+    dense[rows, Xo.col_idx] = 1.0
+    prior = np.concatenate([[0.0], (tau * lam) ** -2.0])
+    cov = np.linalg.inv(dense.T @ (om[:, None] * dense) + np.diag(prior))
+    mean = cov @ (dense.T @ (y - 0.5))
+    z = (out.draws.mean(0) - mean) / np.sqrt(np.diag(cov) / len(out.draws))
+    assert np.mean(np.abs(z) > 4) < 0.02
+    assert np.median(np.var(out.draws, axis=0) / np.diag(cov)) == pytest.approx(1.0, abs=0.1)
+
+
+def test_unsupported_options_raise(small):
+    d, y, _ = small
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    with pytest.raises(NotImplementedError):
+        parallel.row_split_gibbs_run(d.matrix(), y, cfg, 2, preconditioner="jacobi")
