@@ -8,12 +8,13 @@
 // replicated on every rank.  Per iteration each rank
 //   A. runs its CSR pass over its rows (z_r = X_r d, w_r = omega_r z_r, and
 //      the partial z_r' Omega_r z_r),
-//   B. runs its CSC pass (pieces of X_r' w_r) into a parity-double-buffered
-//      exchange region,
+//   B. runs its CSC pass (pieces of X_r' w_r), then, after a local grid
+//      barrier, sums the pieces of every column into its partial vector
+//      g_r = X_r' w_r in a parity-double-buffered exchange region,
 //   X. meets every other rank at one exchange barrier,
-//   C. assembles Phi d for its owned columns from the pieces of ALL ranks
-//      (peer loads over NVLink, fixed rank/slab/piece order) and takes the CG
-//      step on its replicated vectors.
+//   C. forms Phi d = sum_q g_q + D d for its owned columns (coalesced peer
+//      loads over NVLink, rank order) and takes the CG step on its replicated
+//      vectors.
 // Every rank sums the same numbers in the same order, so all ranks hold
 // bitwise identical iterates and take identical convergence decisions; there
 // is no other collective.  dAd = sum_r z_r' Omega_r z_r + d'Dd (the rank
@@ -41,26 +42,25 @@ namespace {
 constexpr int kRsMaxRanks = 64;
 constexpr int kRsMaxLocal = 8;    // ranks hosted by one grid
 constexpr int kMaxGridRs = 256;
-constexpr int kRsMaxPairs = 512;  // (rank, CSC slab) pairs summed per column
 
 // Exchange region of one rank (one allocation, IPC-shareable):
-//   header (64 B) | inbox flags [kRsMaxRanks] u64 | scalar slot (64 B) | part [2][16 * G] f64 |
-//   pieces [2][nseg] f64 | piece_ptr [nslab * (pt + 1)] i32
+//   header (64 B) | inbox flags [kRsMaxRanks] u64 | scalar slot (64 B) |
+//   part [2][16 * G] f64 | gsum [2][p_total (padded)] f64
 struct RsHeader {
-  long long nseg, pt, nslab, G, bytes, n;
-  long long pad[2];
+  long long pt, G, bytes, n;
+  long long pad[4];
 };
 
 struct RsLayout {
-  size_t flags, scal, part, pieces, pp, bytes;
-  static RsLayout of(long long nseg, long long pt, long long nslab, long long G) {
+  size_t flags, scal, part, gsum, gstride, bytes;
+  static RsLayout of(long long pt, long long G) {
     RsLayout L;
     L.flags = sizeof(RsHeader);
     L.scal = L.flags + kRsMaxRanks * sizeof(unsigned long long);
     L.part = L.scal + 64;
-    L.pieces = L.part + 2 * (size_t)kPartStride * G * sizeof(double);
-    L.pp = L.pieces + 2 * (size_t)std::max<long long>(nseg, 1) * sizeof(double);
-    L.bytes = L.pp + (size_t)nslab * (pt + 1) * sizeof(int) + 64;
+    L.gsum = L.part + 2 * (size_t)kPartStride * G * sizeof(double);
+    L.gstride = (size_t)(pt + 31) / 32 * 32;  // doubles per parity
+    L.bytes = L.gsum + 2 * L.gstride * sizeof(double);
     L.bytes = (L.bytes + 255) / 256 * 256;
     return L;
   }
@@ -68,12 +68,10 @@ struct RsLayout {
 
 struct RsPeer {                  // every rank, as this GPU sees it
   const double* part;            // [2][16 G] (local or peer-mapped)
-  const double* pieces;          // [2][nseg]
-  const int* pp;                 // piece_ptr, local copy
+  const double* gsum;            // [2][gstride]: X_q' w_q, internal column layout
   unsigned long long* inbox;     // the rank's flag array (peer-mapped for remote ranks)
   double* scal;                  // the rank's scalar exchange slot
-  long long nseg, n, row0;       // pieces per parity; shard rows; first global row
-  int nslab;
+  long long gstride, n, row0;    // doubles per gsum parity; shard rows; first global row
   int remote;
 };
 
@@ -82,8 +80,10 @@ struct RsGroup {                 // a rank hosted by this grid
   double* w;                     // n_r (+pad)
   double* zpart;                 // nslab_csr * n_r (multi column slab)
   double* dvg;                   // 2 * p_total (internal layout): published directions
+  double* pieces;                // local CSC pieces (nseg)
   double* part;                  // exchange part [2][16 Gr]
-  double* pieces;                // exchange pieces [2][nseg]
+  double* gsum;                  // exchange gsum [2][gstride]
+  long long gstride;
   double* own;                   // own-slice state in global memory (Gr * 8 * chunk), or null
   int rank;
 };
@@ -93,8 +93,6 @@ struct RsArgs {
   const double* omega[kRsMaxLocal];  // shard rows of each hosted rank (per call)
   int n_local, Gr, nranks, smem_doubles;
   const RsPeer* peers;
-  const int2* pairs;             // (rank, slab) pairs in summation order
-  int npairs;
   unsigned long long* epoch;     // device counter: exchanges completed by earlier calls
   const double *diag, *minv, *scale, *b;  // reference layout, replicated
   double* x;                     // in x0 / out solution
@@ -141,18 +139,49 @@ __device__ void rs_exchange(const RsArgs& A, int my_rank, unsigned long long e) 
   cg::this_grid().sync();
 }
 
-// This lane's share of column j's pieces over every (rank, slab) pair of the
-// parity-`par` buffers; the warp sum of the lane shares is the column total.
-__device__ __forceinline__ double rs_lane_pieces(const RsArgs& A, const int2* pairs, long long pt, long long j,
-                                                  int par, int lane) {
+// Local column sums: g[j] = sum of this shard's CSC pieces of column j
+// (slab-major, piece order), for the CTA's owned columns; the piece pointers
+// of up to 8 slabs are loaded before the pieces, so a column costs two L2
+// round trips per 8 slabs.
+__device__ __forceinline__ void rs_assemble(const RsGroup& G, long long j0, int chunk, double* g) {
+  const long long pt = G.D.pt;
+  const int S = G.D.csc.nslab;
+  for (int t = threadIdx.x; t < chunk; t += kThreads) {
+    const long long j = j0 + t;
+    if (j >= pt) break;
+    double s = 0.0;
+    for (int s0 = 0; s0 < S; s0 += 8) {
+      int q0[8], q1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int* pp = G.D.csc.piece_ptr + (long long)(s0 + u) * (pt + 1) + j;
+        q0[u] = s0 + u < S ? __ldg(pp) : 0;
+        q1[u] = s0 + u < S ? __ldg(pp + 1) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        for (int q = q0[u]; q < q1[u]; ++q) s += __ldcg(G.pieces + q);
+    }
+    g[j] = s;
+  }
+}
+
+// sum over ranks (rank order) of g_q[j], parity `par`
+__device__ __forceinline__ double rs_gather(const RsArgs& A, long long j, int par) {
+  double v[kRsMaxRanks > 8 ? 8 : kRsMaxRanks];
   double s = 0.0;
-  for (int k = lane; k < A.npairs; k += 32) {
-    const int2 qs = pairs[k];
-    const RsPeer& P = A.peers[qs.x];
-    const int* pp = P.pp + (long long)qs.y * (pt + 1);
-    const int q0 = __ldg(pp + j), q1 = __ldg(pp + j + 1);
-    const double* pc = P.pieces + par * P.nseg;
-    for (int q = q0; q < q1; ++q) s += ld_peer(pc + q, P.remote);
+  for (int q0 = 0; q0 < A.nranks; q0 += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u;
+      v[u] = 0.0;
+      if (q < A.nranks) {
+        const RsPeer& P = A.peers[q];
+        v[u] = ld_peer(P.gsum + par * P.gstride + j, P.remote);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += v[u];
   }
   return s;
 }
@@ -165,7 +194,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
   __shared__ int st_status, st_iter, st_fail, st_applies;
   __shared__ unsigned long long mbar, st_epoch;
   __shared__ RsGroup G;
-  __shared__ int2 pairs[kRsMaxPairs];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gi = blockIdx.x / A.Gr, cta = blockIdx.x % A.Gr;
   if (tid == 0) {
@@ -173,7 +201,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
     st_epoch = *A.epoch;
   }
   const double* omega = A.omega[gi];
-  for (int k = tid; k < A.npairs; k += kThreads) pairs[k] = A.pairs[k];
   BulkFill bf;
   bulk_init(bf, &mbar);  // ends with a CTA barrier
   const bool lead = gi == 0;  // the first hosted group writes the outputs
@@ -220,21 +247,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
   if (A.rhs) {
     {
       FillRhs f{A.kappa[gi], omega, nullptr, A.seed, kStreamEta ^ A.stream_id, 0, A.peers[G.rank].row0};
-      EpiStore e{G.pieces + (long long)G.D.csc.nseg};  // parity 1: iteration 0 writes parity 0
+      EpiStore e{G.pieces};
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
+    cg::this_grid().sync();
+    rs_assemble(G, j0, chunk, G.gsum + G.gstride);  // parity 1: iteration 0 writes parity 0
     rs_exchange(A, G.rank, st_epoch + 1ull);
-    for (int t = warp; t < chunk; t += kWarps) {
+    for (int t = tid; t < chunk; t += kThreads) {
       const long long j = j0 + t;
       if (j >= pt) break;
-      const double s = warp_sum(rs_lane_pieces(A, pairs, pt, j, 1, lane));
-      if (lane == 0) {
-        const long long rj = ref_index(j, G.D.p, G.D.icpt);
-        Philox R(A.seed, kStreamDelta ^ A.stream_id, (unsigned)rj);
-        const double bj = s + sqrt(oD[t]) * R.normal();
-        obv[t] = bj;
-        if (lead && A.b_out) A.b_out[rj] = bj;
-      }
+      const long long rj = ref_index(j, G.D.p, G.D.icpt);
+      Philox R(A.seed, kStreamDelta ^ A.stream_id, (unsigned)rj);
+      const double bj = rs_gather(A, j, 1) + sqrt(oD[t]) * R.normal();
+      obv[t] = bj;
+      if (lead && A.b_out) A.b_out[rj] = bj;
     }
     e_off = 1;
     __syncthreads();
@@ -314,30 +340,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
     }
     cg::this_grid().sync();
 
-    // ---------------- B: CSC pass, pieces of X_r' w_r ----------------
+    // ---------------- B: CSC pass, local column sums g_r = X_r' w_r ----------------
     {
       FillVecN f{G.w, &bf};
-      EpiStore e{G.pieces + par * (long long)G.D.csc.nseg};
+      EpiStore e{G.pieces};
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
+    cg::this_grid().sync();
+    if (cta == 0 && tid < 32) {  // this rank's z'Omega z total (slot 4 of line 0), exchanged
+      const double t = warp_sum(lane_partials(G.part + par * kPartStride * Gr, Gr, lane));
+      if (tid == 0) G.part[par * kPartStride * Gr + 4] = t;
+    }
+    rs_assemble(G, j0, chunk, G.gsum + par * G.gstride);
     if (tid == 0) ++st_applies;
     rs_exchange(A, G.rank, st_epoch + (unsigned long long)(e_off + a) + 1ull);
 
     // ---------------- C: assemble owned columns over all ranks, step ----------------
     double alpha = 0.0;
     if (a > 0) {
-      // dAd: rank partials in rank order, then the replicated prior term
-      double s = 0.0;
+      // dAd: the ranks' z'Omega z totals in rank order, then the replicated prior term
       if (tid < 32) {
-        for (int q = 0; q < A.nranks; ++q) {
+        double v = 0.0;
+        for (int q = lane; q < A.nranks; q += 32) {
           const RsPeer& P = A.peers[q];
-          const double* pq = P.part + par * kPartStride * Gr;
-          double v = 0.0;
-          for (int c = lane; c < Gr; c += 32) v += ld_peer(pq + (long long)c * kPartStride, P.remote);
-          s += warp_sum(v);
+          v = ld_peer(P.part + par * kPartStride * Gr + 4, P.remote);
         }
-        double dt = lane_partials(G.part + par * kPartStride * Gr + 3, Gr, lane);
-        s += warp_sum(dt);
+        // rank order: lane q holds rank q (nranks <= 64: two rounds at most)
+        double s = 0.0;
+        for (int q = 0; q < A.nranks && q < 32; ++q) s += __shfl_sync(0xffffffffu, v, q);
+        if (A.nranks > 32) {
+          double v2 = 0.0;
+          if (lane + 32 < A.nranks) {
+            const RsPeer& P = A.peers[lane + 32];
+            v2 = ld_peer(P.part + par * kPartStride * Gr + 4, P.remote);
+          }
+          for (int q = 32; q < A.nranks; ++q) s += __shfl_sync(0xffffffffu, v2, q - 32);
+        }
+        s += warp_sum(lane_partials(G.part + par * kPartStride * Gr + 3, Gr, lane));
         if (tid == 0) bc[0] = s;
       }
       __syncthreads();
@@ -354,27 +393,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       if (lead && cta == 0 && tid == 0) A.alphas[a - 1] = alpha;
     }
     double t_rms = 0.0, t_rz = 0.0;
-    for (int t = warp; t < chunk; t += kWarps) {
+    for (int t = tid; t < chunk; t += kThreads) {
       const long long j = j0 + t;
       if (j >= pt) break;
-      double s = rs_lane_pieces(A, pairs, pt, j, par, lane);
-      s = warp_sum(s);
-      if (lane == 0) {
-        const double Ad = s + oD[t] * od[t];
-        double rv;
-        if (a == 0) {
-          rv = obv[t] - Ad;
-        } else {
-          ox[t] = fma(alpha, od[t], ox[t]);
-          rv = fma(-alpha, Ad, orr[t]);
-        }
-        orr[t] = rv;
-        const double zn = om[t] * rv;
-        oz[t] = zn;
-        const double tj = os[t] * rv;
-        t_rms += tj * tj;
-        t_rz += rv * zn;
+      const double Ad = rs_gather(A, j, par) + oD[t] * od[t];
+      double rv;
+      if (a == 0) {
+        rv = obv[t] - Ad;
+      } else {
+        ox[t] = fma(alpha, od[t], ox[t]);
+        rv = fma(-alpha, Ad, orr[t]);
       }
+      orr[t] = rv;
+      const double zn = om[t] * rv;
+      oz[t] = zn;
+      const double tj = os[t] * rv;
+      t_rms += tj * tj;
+      t_rz += rv * zn;
     }
     block_sum2(t_rms, t_rz, red);
     if (tid == 0) {
@@ -459,8 +494,8 @@ struct pcgs_rs {
   std::vector<double*> w, zpart, dvg, own;
   RsGroup* groups_dev = nullptr;
   RsPeer* peers_dev = nullptr;
-  int2* pairs_dev = nullptr;
-  int npairs = 0;
+  std::vector<double*> pieces;
+  bool ready = false;
   bool own_in_smem = true;
 };
 
@@ -510,7 +545,7 @@ int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nra
   if ((long long)R->Gr * n_local > kMaxGridRs) return bail(fail(PCGS_EINVAL, "row split: grid too large"));
   if (cudaSetDevice(R->device) != cudaSuccess) return bail(fail(PCGS_ECUDA, "cudaSetDevice failed"));
   const long long chunk = (R->pt + R->Gr - 1) / R->Gr;
-  R->own_in_smem = (long long)R->smem_doubles * 8 + chunk * 64 + 16 + 1024 + 8 * kRsMaxPairs + 2048 <= 227 * 1024;
+  R->own_in_smem = (long long)R->smem_doubles * 8 + chunk * 64 + 16 + 1024 + 2048 <= 227 * 1024;
   R->exch.assign(nranks, nullptr);
   R->opened.assign(nranks, 0);
   R->hdr.assign(nranks, RsHeader{});
@@ -522,16 +557,16 @@ int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nra
   if (cudaMemset(R->epoch, 0, sizeof(unsigned long long)) != cudaSuccess) return bail(fail(PCGS_ECUDA, "memset"));
   for (int l = 0; l < n_local; ++l) {
     const DesignDev& D = designs[l]->dev;
-    const RsLayout L = RsLayout::of(D.csc.nseg, D.pt, D.csc.nslab, D.G);
+    const RsLayout L = RsLayout::of(D.pt, D.G);
     if ((rc = rs_alloc(R, L.bytes, &p))) return bail(rc);
     if (cudaMemset(p, 0, L.bytes) != cudaSuccess) return bail(fail(PCGS_ECUDA, "memset"));
-    RsHeader h{D.csc.nseg, D.pt, D.csc.nslab, D.G, (long long)L.bytes, D.n, {0, 0}};
-    if (cudaMemcpy(p, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy((char*)p + L.pp, D.csc.piece_ptr, (size_t)D.csc.nslab * (D.pt + 1) * sizeof(int),
-                   cudaMemcpyDeviceToDevice) != cudaSuccess)
+    RsHeader h{D.pt, D.G, (long long)L.bytes, D.n, {0, 0, 0, 0}};
+    if (cudaMemcpy(p, &h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess)
       return bail(fail(PCGS_ECUDA, "exchange setup copy failed"));
     R->exch[rank0 + l] = p;
     R->hdr[rank0 + l] = h;
+    if ((rc = rs_alloc(R, (size_t)std::max<long long>(D.csc.nseg, 1) * 8, &p))) return bail(rc);
+    R->pieces.push_back((double*)p);
     const long long n = D.n;
     double* b;
     if ((rc = rs_alloc(R, (size_t)(n + 2) * 8, &p))) return bail(rc);
@@ -555,8 +590,6 @@ int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nra
   R->groups_dev = (RsGroup*)p;
   if ((rc = rs_alloc(R, sizeof(RsPeer) * nranks, &p))) return bail(rc);
   R->peers_dev = (RsPeer*)p;
-  if ((rc = rs_alloc(R, sizeof(int2) * kRsMaxPairs, &p))) return bail(rc);
-  R->pairs_dev = (int2*)p;
   const int smem = (int)rs_smem_bytes(R);
   if (cudaFuncSetAttribute(k_pcg_rs, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return bail(fail(PCGS_ECUDA, "row split: shared memory attribute"));
@@ -593,43 +626,23 @@ int pcgs_rs_open_peer(pcgs_rs_t R, int rank, const void* handle_h) {
 // Builds the peer table once every rank's exchange region is known: local
 // piece_ptr copies of remote ranks, the (rank, slab) summation order.
 static int rs_finalize(pcgs_rs* R) {
-  std::vector<int2> pairs;
   for (int q = 0; q < R->nranks; ++q) {
     if (!R->exch[q]) return fail(PCGS_EINVAL, "row split: rank " + std::to_string(q) + " has no exchange region");
     const RsHeader& h = R->hdr[q];
-    const RsLayout L = RsLayout::of(h.nseg, h.pt, h.nslab, h.G);
+    const RsLayout L = RsLayout::of(h.pt, h.G);
     RsPeer P{};
     char* base = (char*)R->exch[q];
     P.part = (const double*)(base + L.part);
-    P.pieces = (const double*)(base + L.pieces);
+    P.gsum = (const double*)(base + L.gsum);
     P.inbox = (unsigned long long*)(base + L.flags);
     P.scal = (double*)(base + L.scal);
-    P.nseg = h.nseg;
+    P.gstride = (long long)L.gstride;
     P.n = h.n;
     P.row0 = q == 0 ? 0 : R->peers[q - 1].row0 + R->peers[q - 1].n;
-    P.nslab = (int)h.nslab;
     P.remote = R->opened[q];
-    if (P.remote) {
-      if (!R->peers[q].pp) {
-        void* p;
-        int rc;
-        const size_t bytes = (size_t)h.nslab * (h.pt + 1) * sizeof(int);
-        if ((rc = rs_alloc(R, bytes, &p))) return rc;
-        CUDA_TRY(cudaMemcpy(p, base + L.pp, bytes, cudaMemcpyDeviceToDevice));
-        P.pp = (const int*)p;
-      } else {
-        P.pp = R->peers[q].pp;
-      }
-    } else {
-      P.pp = (const int*)(base + L.pp);
-    }
     R->peers[q] = P;
-    for (int s = 0; s < P.nslab; ++s) pairs.push_back(make_int2(q, s));
   }
-  if ((int)pairs.size() > kRsMaxPairs) return fail(PCGS_EINVAL, "row split: too many (rank, slab) pairs");
-  R->npairs = (int)pairs.size();
   CUDA_TRY(cudaMemcpy(R->peers_dev, R->peers.data(), sizeof(RsPeer) * R->nranks, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(R->pairs_dev, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
   std::vector<RsGroup> groups(R->n_local);
   for (int l = 0; l < R->n_local; ++l) {
     const int q = R->rank0 + l;
@@ -640,11 +653,14 @@ static int rs_finalize(pcgs_rs* R) {
     g.zpart = R->zpart[l];
     g.dvg = R->dvg[l];
     g.part = const_cast<double*>(R->peers[q].part);
-    g.pieces = const_cast<double*>(R->peers[q].pieces);
+    g.gsum = const_cast<double*>(R->peers[q].gsum);
+    g.gstride = R->peers[q].gstride;
+    g.pieces = R->pieces[l];
     g.own = R->own[l];
     g.rank = q;
   }
   CUDA_TRY(cudaMemcpy(R->groups_dev, groups.data(), sizeof(RsGroup) * R->n_local, cudaMemcpyHostToDevice));
+  R->ready = true;
   return PCGS_OK;
 }
 
@@ -677,7 +693,7 @@ int rs_solve(pcgs_rs_t R, const RsSolve& S, cudaStream_t s) {
   if (S.max_iter < 1) return fail(PCGS_EINVAL, "max_iter must be at least 1");
   CUDA_TRY(cudaSetDevice(R->device));
   int rc;
-  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
+  if (!R->ready && (rc = rs_finalize(R))) return rc;
   RsArgs A{};
   A.groups = R->groups_dev;
   for (int l = 0; l < R->n_local; ++l) {
@@ -689,8 +705,6 @@ int rs_solve(pcgs_rs_t R, const RsSolve& S, cudaStream_t s) {
   A.nranks = R->nranks;
   A.smem_doubles = R->smem_doubles;
   A.peers = R->peers_dev;
-  A.pairs = R->pairs_dev;
-  A.npairs = R->npairs;
   A.epoch = R->epoch;
   A.diag = S.diag;
   A.minv = S.minv;
@@ -723,7 +737,7 @@ int rs_solve(pcgs_rs_t R, const RsSolve& S, cudaStream_t s) {
 
 int rs_sum(pcgs_rs_t R, const double* const* parts, double* out, cudaStream_t s) {
   int rc;
-  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
+  if (!R->ready && (rc = rs_finalize(R))) return rc;
   RsSumArgs A{};
   for (int l = 0; l < R->n_local; ++l) A.part[l] = parts[l];
   A.ncta = R->Gr;
@@ -741,7 +755,7 @@ int rs_sum(pcgs_rs_t R, const double* const* parts, double* out, cudaStream_t s)
 int rs_local(pcgs_rs_t R, int l, pcgs_design_t* d, int64_t* row0) {
   if (!R || l < 0 || l >= R->n_local) return fail(PCGS_EINVAL, "bad local rank");
   int rc;
-  if (R->npairs == 0 && (rc = rs_finalize(R))) return rc;
+  if (!R->ready && (rc = rs_finalize(R))) return rc;
   *d = R->designs[l];
   *row0 = R->peers[R->rank0 + l].row0;
   return PCGS_OK;
