@@ -49,8 +49,10 @@ def parse():
     ap.add_argument("--cpu-cg-cap", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--record", action="store_true", help="write bench_workload.json")
-    ap.add_argument("--workload", default="config3", choices=["config3", "config5"],
-                    help="config5: the row-split run (rows of X over the N ranks, strong scaling)")
+    ap.add_argument("--workload", default="config3", choices=["config3", "config4", "config5"],
+                    help="config4: 8 independent chains per GPU side by side (weak scaling); "
+                         "config5: the row-split run (rows of X over the N ranks, strong scaling)")
+    ap.add_argument("--concurrent", type=int, default=4, help="config4: chains side by side per wave")
     return ap.parse_args()
 
 
@@ -467,6 +469,85 @@ def run_rowsplit(args):
         dist.destroy_process_group()
 
 
+def run_config4(args):
+    """BASELINE config 4: independent chains on the config-2/3 design, 8 per
+    GPU (chain c seeded chain_seed(0, c)), run in waves of --concurrent chains
+    side by side, each on its own stream with the store planned for
+    SMs/concurrent CTAs.  Step = one scan of every chain of the rank; value =
+    chain-iterations per second over all ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_1810_12437_b200 import gibbs, parallel
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    d, y, cfg = workload(args.prior)
+    X = d.matrix()
+    K, W, R = args.steps, args.warmup, max(1, args.concurrent)
+    per_gpu = 8
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    grid = 0 if R == 1 else sms // R
+    chains_idx = parallel.chain_assignment(per_gpu * world, world, rank)
+    total_ms, cg = 0.0, []
+    with ClockSampler(local) as clk:
+        for w0 in range(0, len(chains_idx), R):
+            wave = chains_idx[w0:w0 + R]
+            streams = [torch.cuda.Stream(dev) for _ in wave]
+            chains = []
+            for c, s in zip(wave, streams):
+                with torch.cuda.stream(s):
+                    chains.append(gibbs.DeviceChain(X, y, cfg, W + K, burn_in=W, seed=parallel.chain_seed(SEED, c),
+                                                    cg_config=gibbs.CGConfig(rtol=RTOL), device=dev, grid=grid))
+            for t in range(1, W + 1):
+                for ch, s in zip(chains, streams):
+                    with torch.cuda.stream(s):
+                        ch.scan(t)
+            torch.cuda.synchronize(dev)
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            cur = torch.cuda.current_stream(dev)
+            e0.record(cur)
+            for s in streams:
+                s.wait_stream(cur)
+            for t in range(W + 1, W + K + 1):
+                for ch, s in zip(chains, streams):
+                    with torch.cuda.stream(s):
+                        ch.scan(t)
+            for s in streams:
+                cur.wait_stream(s)
+            e1.record(cur)
+            torch.cuda.synchronize(dev)
+            total_ms += e0.elapsed_time(e1)
+            for ch in chains:
+                ch.check(1, W + K)
+                cg += ch.results.view(-1, 8).cpu().numpy()[W:W + K, 0].astype(int).tolist()
+    ms_t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(ms_t.item())
+    if rank == 0:
+        line = {
+            "metric": "gibbs_iter_per_s", "value": world * per_gpu * K / (ms_max * 1e-3), "unit": "chain-iter/s",
+            "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; BASELINE config 4 recipe; no public dataset)",
+            "config": {"workload": f"config 4: {per_gpu} independent {args.prior} chains per GPU on the "
+                                   f"n={d.n:,} p={d.p:,} design (nnz {d.nnz:,}), waves of {R} side by side",
+                       "chains_per_gpu": per_gpu, "concurrent": R, "grid_per_chain": grid or sms,
+                       "parallelism": f"chain-parallel x{world}", "seed": SEED},
+            "clocks": clk.summary(),
+            "extra": {"cg_iters_mean": float(np.mean(cg)), "chain_iterations_timed": per_gpu * K},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def gibbs_conditional_operator(chain):
     from paper_1810_12437_b200.sampler import PrecisionOperator
     return PrecisionOperator.from_device(chain.X, chain.omega, chain.prior_diag)
@@ -478,6 +559,8 @@ def main():
         run_reference(args)
     elif args.workload == "config5":
         run_rowsplit(args)
+    elif args.workload == "config4":
+        run_config4(args)
     else:
         run_ours(args)
 

@@ -211,9 +211,10 @@ class DeviceChain:
 
     def __init__(self, X, y, cfg, n_iter, burn_in=0, thin=1, seed=0, preconditioner="prior",
                  cg_config=None, init_state=None, gamma_scale=1.0, fixed_omega=None,
-                 fixed_tau=None, fixed_lam=None, device=None):
+                 fixed_tau=None, fixed_lam=None, device=None, grid=0):
         t = _lib.torch()
         self.X = X
+        self._grid_req = int(grid)
         self._open_device(X, device)
         dev = self.dev
         f64 = t.float64
@@ -304,7 +305,7 @@ class DeviceChain:
         self._init_device()
 
     def _open_device(self, X, device):
-        self.store = X.device_store(device)
+        self.store = X.device_store(device, grid=self._grid_req)
         self.dev = self.store.device
         self.grid = self.store.describe()["grid"]
 
@@ -383,23 +384,9 @@ class DeviceChain:
             stat_count=self.count)
 
 
-def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, preconditioner="prior",
-              cg_config=None, burn_in_sampler=None, init_state=None, local_scale_sampler=None,
-              gamma_scale=1.0, allow_max_iter=False, fixed_omega=None, fixed_tau=None,
-              fixed_lam=None, on_progress=None, device=None, sync_every=64) -> ChainOutput:
-    """Run `n_iter` scans on the GPU (gibbs.py:260-379); same arguments and output.
-
-    `sampler`/`burn_in_sampler` must be "cg" (the dense Cholesky sampler is the
-    CPU oracle's).  A `local_scale_sampler(beta_shrunk, tau, cfg, rng)` runs on
-    the host between the two halves of each scan (one synchronisation per
-    scan), with a numpy Generator seeded from `seed`.
-
-    Standardised designs (`X.standardize(...)`) run through an exact
-    reparametrisation on the raw pattern (`_Reparam`; needs an unstandardised
-    intercept with a flat prior); draws and the final state come back in the
-    model's coordinates, the running statistics of the unshrunk block stay in
-    the sampled ones.
-    """
+def _check_run_args(X, y, cfg, n_iter, burn_in, thin, sampler, burn_in_sampler, preconditioner,
+                    fixed_lam, local_scale_sampler):
+    """gibbs_run's argument checks (gibbs.py:260-300); returns y as float64."""
     y = np.asarray(y, dtype=np.float64)
     if y.shape != (X.n_rows,):
         raise ValueError("outcome length must match the design")
@@ -425,10 +412,35 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
             and local_scale_sampler is None):
         raise UnsupportedUpdateError(
             "exact local-scale draws exist for alpha = 1 only; pin fixed_lam for other exponents")
+    return y
+
+
+def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, preconditioner="prior",
+              cg_config=None, burn_in_sampler=None, init_state=None, local_scale_sampler=None,
+              gamma_scale=1.0, allow_max_iter=False, fixed_omega=None, fixed_tau=None,
+              fixed_lam=None, on_progress=None, device=None, sync_every=64, grid=0) -> ChainOutput:
+    """Run `n_iter` scans on the GPU (gibbs.py:260-379); same arguments and output.
+
+    `sampler`/`burn_in_sampler` must be "cg" (the dense Cholesky sampler is the
+    CPU oracle's).  A `local_scale_sampler(beta_shrunk, tau, cfg, rng)` runs on
+    the host between the two halves of each scan (one synchronisation per
+    scan), with a numpy Generator seeded from `seed`.
+
+    `grid` > 0 plans the store for that many CTAs (chains sharing a GPU
+    concurrently, `parallel.run_chains`); 0 = one CTA per SM.
+
+    Standardised designs (`X.standardize(...)`) run through an exact
+    reparametrisation on the raw pattern (`_Reparam`; needs an unstandardised
+    intercept with a flat prior); draws and the final state come back in the
+    model's coordinates, the running statistics of the unshrunk block stay in
+    the sampled ones.
+    """
+    y = _check_run_args(X, y, cfg, n_iter, burn_in, thin, sampler, burn_in_sampler, preconditioner,
+                        fixed_lam, local_scale_sampler)
     ch = DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=seed,
                      preconditioner=preconditioner, cg_config=cg_config, init_state=init_state,
                      gamma_scale=gamma_scale, fixed_omega=fixed_omega, fixed_tau=fixed_tau,
-                     fixed_lam=fixed_lam, device=device)
+                     fixed_lam=fixed_lam, device=device, grid=grid)
     torch = _lib.torch()
     checked = 0
     host_rng = np.random.default_rng(seed) if local_scale_sampler is not None else None
@@ -445,3 +457,50 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
     if checked < n_iter:
         ch.check(checked + 1, n_iter, allow_max_iter)
     return ch.output()
+
+
+def gibbs_run_concurrent(X, y, cfg, n_iter, seeds, concurrent=4, burn_in=0, thin=1,
+                         preconditioner="prior", cg_config=None, init_state=None, gamma_scale=1.0,
+                         allow_max_iter=False, fixed_omega=None, fixed_tau=None, fixed_lam=None,
+                         device=None, sync_every=64) -> list:
+    """Independent chains (one per seed) sharing one GPU: waves of `concurrent`
+    chains, each chain on its own CUDA stream with the store planned for
+    SMs // concurrent CTAs, so the chains' persistent PCG kernels run side by
+    side.  Chain c's output equals gibbs_run(..., seed=seeds[c],
+    grid=SMs // concurrent) bit for bit (deterministic kernels; the streams
+    only change what runs beside it)."""
+    torch = _lib.torch()
+    y = _check_run_args(X, y, cfg, n_iter, burn_in, thin, "cg", None, preconditioner, fixed_lam, None)
+    dev = _lib.cuda_device(device)
+    concurrent = max(1, int(concurrent))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    grid = 0 if concurrent == 1 else sms // concurrent
+    outs = []
+    seeds = list(seeds)
+    for w0 in range(0, len(seeds), concurrent):
+        wave = seeds[w0:w0 + concurrent]
+        chains, streams = [], []
+        for sd in wave:
+            streams.append(torch.cuda.Stream(dev))
+            with torch.cuda.stream(streams[-1]):
+                chains.append(DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=sd,
+                                          preconditioner=preconditioner, cg_config=cg_config,
+                                          init_state=init_state, gamma_scale=gamma_scale,
+                                          fixed_omega=fixed_omega, fixed_tau=fixed_tau, fixed_lam=fixed_lam,
+                                          device=dev, grid=grid))
+        checked = 0
+        for t in range(1, n_iter + 1):
+            for ch, s in zip(chains, streams):
+                with torch.cuda.stream(s):
+                    ch.scan(t)
+            if sync_every and t - checked >= sync_every:
+                for ch, s in zip(chains, streams):
+                    with torch.cuda.stream(s):
+                        ch.check(checked + 1, t, allow_max_iter)
+                checked = t
+        for ch, s in zip(chains, streams):
+            with torch.cuda.stream(s):
+                if checked < n_iter:
+                    ch.check(checked + 1, n_iter, allow_max_iter)
+                outs.append(ch.output())
+    return outs

@@ -444,23 +444,37 @@ def chain_assignment(n_chains, world, rank):
     return list(range(lo, lo + base + (1 if rank < extra else 0)))
 
 
-def run_chains(X, y, cfg, n_iter, n_chains, seed=0, group=None, gather=True, runner=None, **kwargs):
+def run_chains(X, y, cfg, n_iter, n_chains, seed=0, group=None, gather=True, runner=None, concurrent=None,
+               **kwargs):
     """Run `n_chains` independent Gibbs chains, sharded over the ranks of
     `group` (default: the initialised torch.distributed world, else one
-    process).  Chain c uses `chain_seed(seed, c)`; each rank runs its block
-    of chains one after another on its GPU (`gibbs_run`).  There is no
+    process).  Chain c uses `chain_seed(seed, c)`.  Each rank runs its block
+    of chains on its GPU in waves of `concurrent` chains side by side (one
+    CUDA stream each, the store planned for SMs // concurrent CTAs;
+    `gibbs.gibbs_run_concurrent`; default min(4, chains on the rank)), or one
+    after another with `concurrent=1` / a custom `runner`.  There is no
     collective while sampling; with `gather` the outputs are all-gathered at
     the end (object collective) and every rank returns all chains in index
     order, otherwise only its own (as {chain: ChainOutput})."""
     import torch.distributed as dist
-    if runner is None:
-        from .gibbs import gibbs_run as runner
     if group is None and dist.is_available() and dist.is_initialized():
         group = dist.group.WORLD
     world = dist.get_world_size(group) if group is not None else 1
     rank = dist.get_rank(group) if group is not None else 0
-    mine = {c: runner(X, y, cfg, n_iter, seed=chain_seed(seed, c), **kwargs)
-            for c in chain_assignment(n_chains, world, rank)}
+    block = chain_assignment(n_chains, world, rank)
+    host_hooks = kwargs.get("local_scale_sampler") is not None or kwargs.get("on_progress") is not None
+    if concurrent is None:
+        concurrent = 1 if (runner is not None or host_hooks) else min(4, max(1, len(block)))
+    if concurrent > 1 and runner is None and not host_hooks:
+        from .gibbs import gibbs_run_concurrent
+        kw = {k: v for k, v in kwargs.items() if k not in ("sampler", "burn_in_sampler")}
+        outs = gibbs_run_concurrent(X, y, cfg, n_iter, [chain_seed(seed, c) for c in block],
+                                    concurrent=concurrent, **kw)
+        mine = dict(zip(block, outs))
+    else:
+        if runner is None:
+            from .gibbs import gibbs_run as runner
+        mine = {c: runner(X, y, cfg, n_iter, seed=chain_seed(seed, c), **kwargs) for c in block}
     if not gather:
         return mine
     if world > 1:

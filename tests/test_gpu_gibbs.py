@@ -182,9 +182,28 @@ def test_run_chains_single_process_matches_direct_runs(small):
     d, y, _ = small
     X = d.matrix()
     cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
-    outs = parallel.run_chains(X, y, cfg, 20, n_chains=3, seed=9, burn_in=5)
+    outs = parallel.run_chains(X, y, cfg, 20, n_chains=3, seed=9, burn_in=5, concurrent=1)
     assert len(outs) == 3
     for c, o in enumerate(outs):
         ref = gibbs.gibbs_run(X, y, cfg, 20, burn_in=5, seed=parallel.chain_seed(9, c))
         np.testing.assert_array_equal(o.draws, ref.draws)
     assert not np.array_equal(outs[0].draws, outs[1].draws)
+
+
+@pytest.mark.parametrize("concurrent", [2, 4])
+def test_concurrent_chains_match_direct_runs_on_the_same_plan(small, concurrent):
+    """Chains side by side on their own streams (sub-grid plans) give exactly
+    the draws of direct runs on the same plan: concurrency changes nothing."""
+    import torch
+    from paper_1810_12437_b200 import parallel
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
+    outs = parallel.run_chains(X, y, cfg, 30, n_chains=5, seed=3, burn_in=5, concurrent=concurrent,
+                               sync_every=7)
+    grid = torch.cuda.get_device_properties(0).multi_processor_count // concurrent
+    for c, o in enumerate(outs):
+        ref = gibbs.gibbs_run(X, y, cfg, 30, burn_in=5, seed=parallel.chain_seed(3, c), grid=grid)
+        np.testing.assert_array_equal(o.draws, ref.draws)
+        np.testing.assert_array_equal(o.cg_iteration_counts, ref.cg_iteration_counts)
+        np.testing.assert_array_equal(o.final_state.omega, ref.final_state.omega)
