@@ -657,6 +657,11 @@ int pcgs_design_create_ex(int64_t n, int64_t p, const int64_t* row_ptr_h, const 
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // scratch freed on one chain's stream must not be handed to another
+    // stream behind an inserted dependency: that would serialise chains that
+    // run side by side (gibbs_run_concurrent)
+    int no = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
   int64_t* I = D->info;
   memset(I, 0, sizeof(D->info));
