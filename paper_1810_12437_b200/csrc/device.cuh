@@ -132,6 +132,38 @@ __device__ __forceinline__ double gather8(uint4 q, const double* sv) {
   return (a + b) + (c + d);
 }
 
+// The same sum from a 32-bit shared-window address `sb` of the slab: each
+// address is one extract plus one LEA (sb + index * 8), where the generic
+// form costs a shift, a mask and an add per index.
+__device__ __forceinline__ double lds64(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+// halves of a packed index pair, zero-extended by a byte permute (opaque to
+// the optimiser, so the address stays extract + LEA)
+__device__ __forceinline__ unsigned lo16(unsigned x) {
+  unsigned r;
+  asm("prmt.b32 %0, %1, 0, 0x4410;" : "=r"(r) : "r"(x));
+  return r;
+}
+__device__ __forceinline__ unsigned hi16(unsigned x) {
+  unsigned r;
+  asm("prmt.b32 %0, %1, 0, 0x4432;" : "=r"(r) : "r"(x));
+  return r;
+}
+__device__ __forceinline__ unsigned slab_addr(unsigned sb, unsigned idx) { return sb + (idx << 3); }
+__device__ __forceinline__ double gather8s(uint4 q, unsigned sb) {
+  const double a = lds64(slab_addr(sb, lo16(q.x))) + lds64(slab_addr(sb, hi16(q.x)));
+  const double b = lds64(slab_addr(sb, lo16(q.y))) + lds64(slab_addr(sb, hi16(q.y)));
+  const double c = lds64(slab_addr(sb, lo16(q.z))) + lds64(slab_addr(sb, hi16(q.z)));
+  const double d = lds64(slab_addr(sb, lo16(q.w))) + lds64(slab_addr(sb, hi16(q.w)));
+  return (a + b) + (c + d);
+}
+#ifndef PCGS_LDS_ASM
+#define PCGS_LDS_ASM 1
+#endif
+
 // ------------------------------------------------------------------ fills
 // sv[j] = f(j) for j in [0, len); sv[len] = 0 (the segment sentinel).  Loads are
 // batched 16 per thread so the fill is one or two L2 round trips.
@@ -230,6 +262,10 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
 #endif
 constexpr bool kDebugModes = PCGS_DEBUG_MODES != 0;
 constexpr int kRing = PCGS_RING;
+static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
+#ifndef PCGS_LANE_PREFETCH
+#define PCGS_LANE_PREFETCH 1
+#endif
 
 // `M` is the block's segment-start mask; `first_id` (the id of the segment
 // starting at the lowest set bit) is fetched lazily by shuffling `dl_x` from
@@ -315,6 +351,7 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
   const int nb = (nvec + 31) >> 5;
   const uint4* base = P.vec + R.x;
   const uint2* bd = P.blocks + R.z;
+  const unsigned sb = smem_addr(sv);
   double acc = 0.0;
   unsigned open_id = 0;
   bool have_open = false;
@@ -325,15 +362,29 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
   auto batch = [&](int k0, auto checked) {
     constexpr bool kChecked = decltype(checked)::value;
     uint4 q[kRing];
-    if (lane == 0 && !(kDebugModes && (dbg & 20)) && k0 + kPrefetchBlocks < nb) {
-      const int kb = k0 + kPrefetchBlocks;
-      const int ke = min(nb, kb + kRing);
-      const unsigned v_end = (unsigned)min(nvec, ke * 32);
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char*)(base + kb * 32)),
-                   "r"((v_end - (unsigned)kb * 32u) * 16u)
-                   : "memory");
+    if (!(kDebugModes && (dbg & 20))) {
+#if PCGS_LANE_PREFETCH
+      // sliding L2 prefetch, one 128-byte line per lane (4 lines per block):
+      // a per-lane prefetch needs no uniform address (the bulk form costs a
+      // waterfall loop of R2UR conversions per batch)
+      const unsigned off = (unsigned)(k0 + kPrefetchBlocks) * 512u + (unsigned)lane * 128u;
+      if (lane < 4 * kRing && off < (unsigned)nvec * 16u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)base + off));
+#else
+      if (lane == 0 && k0 + kPrefetchBlocks < nb) {
+        const int kb = k0 + kPrefetchBlocks;
+        const int ke = min(nb, kb + kRing);
+        const unsigned v_end = (unsigned)min(nvec, ke * 32);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char*)(base + kb * 32)),
+                     "r"((v_end - (unsigned)kb * 32u) * 16u)
+                     : "memory");
+      }
+#endif
     }
-    const uint2 dl = lane < kRing && (!kChecked || k0 + lane < nb) ? __ldg(bd + k0 + lane) : make_uint2(0u, 0u);
+    // block descriptors of the batch: lane u's copy feeds block u (full
+    // batches load unconditionally: no divergent branch around the load)
+    const uint2 dl = !kChecked ? __ldg(bd + k0 + (lane & (kRing - 1)))
+                               : (lane < kRing && k0 + lane < nb ? __ldg(bd + k0 + lane) : make_uint2(0u, 0u));
 #pragma unroll
     for (int u = 0; u < kRing; ++u) {
       const int v = (k0 + u) * 32 + lane;
@@ -347,7 +398,7 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
         const bool live = !kChecked || k * 32 + lane < nvec;
         double s;
         if (kDebugModes && (dbg & 1)) s = live ? (double)(q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) : 0.0;
-        else s = live ? gather8(q[u], sv) : 0.0;
+        else s = live ? (PCGS_LDS_ASM ? gather8s(q[u], sb) : gather8(q[u], sv)) : 0.0;
         if (kDebugModes && (dbg & 2)) acc += s + (double)M;
         else block_reduce(M, dl.x, u, s, lane, acc, open_id, have_open, epi);
       }
