@@ -157,6 +157,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // and stamps inside phase C at [16 * cta + 8 + k]
 __device__ unsigned long long* g_sync_times = nullptr;
 constexpr int kSyncTraceIter = 10;
+#ifndef PCGS_FLAT_STEP
+#define PCGS_FLAT_STEP 1
+#endif
 constexpr int kMaxGrid = 256;  // persistent-kernel grid bound (one CTA per SM; B200: 148)
 
 struct FillDir {  // search direction: first ? a : a + beta * b   (internal layout)
@@ -263,6 +266,65 @@ __device__ __forceinline__ double owned_column_sum(const OwnState& o, const doub
     total += ts;
   }
   return total;
+}
+
+// Step-phase column sums for up to 8 CSC slabs (the common case): the pieces
+// of the owned columns are staged in ONE round of loads (the slab ranges are
+// concatenated; every thread finds its slab among <= 8 offsets), then each
+// column is summed by a group of G = 4 or 8 lanes, lane g taking slabs
+// g, g+G, ... and the group adding its lane sums by an xor tree (fixed order,
+// so the result is deterministic).  Returns false when the pieces do not fit
+// the idle slab area (then the generic path runs).
+constexpr int kFlatSlabs = 8;
+__device__ __forceinline__ bool stage_pieces_flat(const OwnState& o, const double* pieces, int S, int chunk,
+                                                  double* stage, int cap) {
+  int p0[kFlatSlabs], off[kFlatSlabs + 1];
+  off[0] = 0;
+#pragma unroll
+  for (int s = 0; s < kFlatSlabs; ++s) {
+    p0[s] = s < S ? o.ppv(s, 0) : 0;
+    off[s + 1] = off[s] + (s < S ? o.ppv(s, chunk) - p0[s] : 0);
+  }
+  const int total = off[kFlatSlabs];
+  if (total > cap) return false;
+  for (int i = threadIdx.x; i < total; i += kThreads) {
+    int s = 0;
+#pragma unroll
+    for (int u = 1; u < kFlatSlabs; ++u) s += i >= off[u] ? 1 : 0;
+    int ps = p0[0], os = off[0];
+#pragma unroll
+    for (int u = 1; u < kFlatSlabs; ++u)
+      if (s == u) {
+        ps = p0[u];
+        os = off[u];
+      }
+    stage[i] = __ldcg(pieces + ps + (i - os));
+  }
+  __syncthreads();
+  return true;
+}
+
+// Sum of column t over the staged slabs taken by lane g of a G-lane group,
+// then the group total (every lane of the group receives it).  All lanes of
+// the warp must call it (shuffles).
+template <int G>
+__device__ __forceinline__ double group_column_sum(const OwnState& o, int S, int chunk, int t, int g,
+                                                   const double* stage) {
+  double sum = 0.0;
+  if (t < chunk) {
+    int off = 0;
+    for (int s = 0; s < S; ++s) {
+      const int p0 = o.ppv(s, 0);
+      if ((s & (G - 1)) == g) {
+        const int q0 = o.ppv(s, t) - p0, q1 = o.ppv(s, t + 1) - p0;
+        for (int q = q0; q < q1; ++q) sum += stage[off + q];
+      }
+      off += o.ppv(s, chunk) - p0;
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < G; m <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+  return sum;
 }
 
 __device__ __forceinline__ void traced_sync(const PcgArgs& A, int a, int k) {
@@ -435,7 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     // warp 0's loads of the dAd partials overlap the piece staging round trip
     double dpart = 0.0;
     if (a > 0 && tid < 32) dpart = lane_partials(A.part, gridDim.x, tid);
-    const bool staged = stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
+    const bool flat = PCGS_FLAT_STEP && S <= kFlatSlabs && stage_pieces_flat(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
+    const bool staged = flat || stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
     trace_stamp(A, a, 1);
     if (a > 0) {
       if (tid < 32) {
@@ -457,9 +520,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     }
     trace_stamp(A, a, 2);
     double t_rms = 0.0, t_rz = 0.0;
-    for (int t = tid; t < chunk; t += kThreads) {
-      if (j0 + t >= pt) continue;
-      const double Ad = owned_column_sum(o, A.pieces, S, chunk, t, sv, staged) + o.D[t] * o.d[t];
+    constexpr int GS = 4;  // lanes per column in the flat path (slabs g, g+4)
+    for (int t0 = 0; t0 < chunk; t0 += (flat ? kThreads / GS : kThreads)) {
+      int t;
+      double Ad;
+      if (flat) {
+        t = t0 + tid / GS;
+        const double cs = group_column_sum<GS>(o, S, chunk, t, tid & (GS - 1), sv);
+        if ((tid & (GS - 1)) != 0 || t >= chunk || j0 + t >= pt) continue;
+        Ad = cs + o.D[t] * o.d[t];
+      } else {
+        t = t0 + tid;
+        if (t >= chunk || j0 + t >= pt) continue;
+        Ad = owned_column_sum(o, A.pieces, S, chunk, t, sv, staged) + o.D[t] * o.d[t];
+      }
       double rv;
       if (a == 0) {
         rv = o.b[t] - Ad;
