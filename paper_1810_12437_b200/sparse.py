@@ -452,6 +452,8 @@ def hstack_dense_columns(cols, X):
         return SparseDesignMatrix.from_pattern(X.n_rows, X.n_cols, rp, ci, intercept=True,
                                                check=False)
     n = X.n_rows
+    if np.all((cols == 0.0) | (cols == 1.0)) and np.all(X.values == 1.0):
+        return _hstack_binary_block(cols == 1.0, X)
     row_ptr = X.row_ptr + q * np.arange(n + 1, dtype=np.int64)
     counts = np.diff(X.row_ptr)
     total = X.nnz + n * q
@@ -467,6 +469,31 @@ def hstack_dense_columns(cols, X):
     means = np.concatenate([np.zeros(q), X.col_means])
     scales = np.concatenate([np.ones(q), X.col_scales])
     return SparseDesignMatrix(n, X.n_cols + q, row_ptr, col_idx, values,
+                              col_means=means, col_scales=scales)
+
+
+def _hstack_binary_block(mask, X):
+    """hstack_dense_columns of a 0/1 block in front of a binary design, stored
+    pattern-only (its ones; the reference stores the block's zeros as explicit
+    entries, which changes no product): the result stays on the device path, the
+    block's leading all-ones column becoming the store's dense intercept and
+    the other block columns (dummy covariates, e.g. an unshrunk block with
+    q > 1 prior sds) ordinary pattern columns."""
+    n, q = mask.shape
+    bc = mask.sum(1).astype(np.int64)
+    xc = np.diff(X.row_ptr)
+    row_ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(bc + xc, out=row_ptr[1:])
+    col_idx = np.empty(int(row_ptr[-1]), dtype=np.int64)
+    bi, bj = np.nonzero(mask)                           # row-major: sorted by row, then column
+    first = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(bc, out=first[1:])
+    col_idx[row_ptr[bi] + (np.arange(len(bi)) - first[bi])] = bj
+    rows = np.repeat(np.arange(n, dtype=np.int64), xc)
+    col_idx[np.arange(X.nnz, dtype=np.int64) - X.row_ptr[rows] + row_ptr[rows] + bc[rows]] = X.col_idx + q
+    means = np.concatenate([np.zeros(q), X.col_means])
+    scales = np.concatenate([np.ones(q), X.col_scales])
+    return SparseDesignMatrix(n, X.n_cols + q, row_ptr, col_idx, np.ones(len(col_idx)),
                               col_means=means, col_scales=scales)
 
 

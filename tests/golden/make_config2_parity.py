@@ -3,8 +3,11 @@ paper-scale gate of SURVEY §8(c): for 5 draw seeds of the config-2 recipe
 (n=72,489, p=22,175, omega ~ PG(1,0), lambda ~ |Cauchy|, tau=1e-3, b from
 generate_rhs) the reference pcg_solve's iteration count at RMS 1e-6, the same
 solve with Phi applied in a different summation order (two row halves: the
-CPU-vs-CPU floor of the iteration count), and for seed 0 the solution at RMS
-1e-10 (the relative-L2 gate).  Inputs are regenerated from the seeds on the
+CPU-vs-CPU floor of the iteration count), the same algorithm in extended
+precision (x87 long double: Phi, dot products, single-rounding vector updates,
+d'Phi d as z'Omega z + d'Dd -- the roundings the device makes more accurate
+than numpy does), and for seed 0 the solution at RMS 1e-10 (the relative-L2
+gate).  Inputs are regenerated from the seeds on the
 GPU box (synth + oracle/port.py, pinned bit-exact against the reference);
 checksums of omega and b are stored to prove it.
 
@@ -64,6 +67,61 @@ class SplitPhi:
         return (self.parts[0].apply(v) + self.parts[1].apply(v)) + self.diag * v
 
 
+def accurate_iterations(Xo_rp, Xo_ci, n, p, cond, b, rtol=1e-6):
+    """PCG (cg.py:105-192) with every reduction in long double and one rounding
+    per vector update; Xo_* is the reference CSR (intercept first)."""
+    import math
+    L = np.longdouble
+    om = cond["omega"].astype(L)
+    diag, minv, scale = cond["prior_diag"], cond["minv"], cond["scale"]
+    rp, ci = Xo_rp, Xo_ci
+    perm = np.argsort(ci, kind="stable")
+    row_of = np.repeat(np.arange(n), np.diff(rp))[perm]
+    cstart = np.searchsorted(ci[perm], np.arange(p))
+    ner = np.diff(rp) > 0
+    empty_c = np.bincount(ci, minlength=p) == 0
+
+    def xz(v):
+        z = np.zeros(n, dtype=L)
+        z[ner] = np.add.reduceat(v.astype(L)[ci], rp[:-1][ner])
+        return z
+
+    def xt(w):
+        g = np.add.reduceat(w[row_of], cstart)
+        g[empty_c] = 0
+        return g
+
+    def dot(u, v):
+        return float(np.dot(u.astype(L), v.astype(L)))
+
+    x = np.zeros(p)
+    r = b.copy()
+    k = 0
+    t = scale * r
+    rms = math.sqrt(dot(t, t) / p)
+    z = minv * r
+    rz = dot(r, z)
+    dd = z.copy()
+    while rms > rtol:
+        k += 1
+        zz = xz(dd)
+        Ad = (xt(om * zz) + diag.astype(L) * dd.astype(L)).astype(np.float64)
+        dAd = float(np.dot(zz, om * zz) + np.dot(dd.astype(L), diag.astype(L) * dd.astype(L)))
+        alpha = rz / dAd
+        x = (x.astype(L) + L(alpha) * dd.astype(L)).astype(np.float64)
+        r = (r.astype(L) - L(alpha) * Ad.astype(L)).astype(np.float64)
+        t = scale * r
+        rms = math.sqrt(dot(t, t) / p)
+        if rms <= rtol:
+            break
+        z = minv * r
+        rzn = dot(r, z)
+        beta = rzn / rz
+        rz = rzn
+        dd = (z.astype(L) + L(beta) * dd.astype(L)).astype(np.float64)
+    return k
+
+
 def run(seed):
     from priorcg.cg import CGConfig, pcg_solve
     from priorcg.precond import Preconditioner, PreconditionerKind
@@ -76,11 +134,12 @@ def run(seed):
     split = SplitPhi(X, cond["omega"], cond["prior_diag"])
     rep2 = pcg_solve(split, b, M, config=CGConfig(rtol=1e-6), residual_scale=cond["scale"])
     out["iters_split"] = rep2.iterations
+    out["iters_accurate"] = accurate_iterations(X.row_ptr, X.col_idx, X.n_rows, X.n_cols, cond, b)
     if seed == 0:
         rep3 = pcg_solve(phi, b, M, config=CGConfig(rtol=1e-10), residual_scale=cond["scale"])
         out["x_1e10"] = rep3.solution
         out["iters_1e10"] = rep3.iterations
-    print(seed, out["iters_ref"], out["iters_split"], flush=True)
+    print(seed, out["iters_ref"], out["iters_split"], out["iters_accurate"], flush=True)
     return out
 
 
@@ -90,6 +149,7 @@ if __name__ == "__main__":
     np.savez_compressed(
         OUT, seeds=np.array(SEEDS), iters_ref=np.array([r["iters_ref"] for r in res]),
         iters_split=np.array([r["iters_split"] for r in res]),
+        iters_accurate=np.array([r["iters_accurate"] for r in res]),
         omega_sum=np.array([r["omega_sum"] for r in res]), b_sum=np.array([r["b_sum"] for r in res]),
         b_norm=np.array([r["b_norm"] for r in res]), x_1e10=res[0]["x_1e10"],
         iters_1e10=res[0]["iters_1e10"])

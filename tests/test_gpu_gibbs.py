@@ -207,3 +207,29 @@ def test_concurrent_chains_match_direct_runs_on_the_same_plan(small, concurrent)
         np.testing.assert_array_equal(o.draws, ref.draws)
         np.testing.assert_array_equal(o.cg_iteration_counts, ref.cg_iteration_counts)
         np.testing.assert_array_equal(o.final_state.omega, ref.final_state.omega)
+
+
+def test_unshrunk_block_of_dummies_matches_oracle():
+    """q = 3 unshrunk coefficients (intercept + two 0/1 covariates with prior
+    sd 5, gamma policy per coefficient, precond.py:137-153) through
+    hstack_dense_columns' pattern-only block: device vs oracle chains agree."""
+    import paper_1810_12437_b200 as pk
+    d = synth.binary_design(600, 60, 5e-3, 0.3, seed=6)
+    X0 = d.matrix(intercept=False)
+    rng = np.random.default_rng(12)
+    block = np.column_stack([np.ones(d.n), rng.random(d.n) < 0.4, rng.random(d.n) < 0.2]).astype(float)
+    X = pk.hstack_dense_columns(block, X0)
+    truth = np.zeros(X.n_cols)
+    truth[[0, 1, 2, 5, 9]] = [-1.0, 0.8, -0.6, 1.2, -1.0]
+    dense = X.to_dense_raw()
+    y = (rng.random(d.n) < 1.0 / (1.0 + np.exp(-dense @ truth))).astype(float)
+    sds = (np.inf, 5.0, 5.0)
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=sds)
+    out = gibbs.gibbs_run(X, y, cfg, 4000, burn_in=500, seed=8)
+    Xo = port.Csr(X.n_rows, X.n_cols, X.row_ptr, X.col_idx, X.values)
+    ref = port.gibbs_bridge(Xo, y, 4000, seed=7, burn_in=500, unshrunk_sd=sds)
+    assert out.n_unshrunk == 3 and out.unshrunk_sd().shape == (3,)
+    for a, b in ((out.draws, ref.draws), (out.draws ** 2, ref.draws ** 2)):
+        z = standardized_differences(a, b)
+        assert np.mean(np.abs(z) > 4) < 0.03
+        assert stats.kstest(np.clip(z, -6, 6), "norm").pvalue > 1e-3

