@@ -199,21 +199,24 @@ void cut(const std::vector<uint64_t>& pre, size_t a, size_t b, int parts, std::v
 // epilogue).  Reductions are paid per 32-vector block that contains segment
 // starts, so short segments sharing a block share that cost: the charge is
 // emit + block * min(len, 32) / 32.  Defaults from sweeps of the PCG iteration
-// time at config 2 (tools/segw_sweep.sh); PCGS_SEG_WEIGHT / PCGS_SEG_EMIT
-// override them for tuning experiments.
+// time at config 2 (tools/segw_sweep.sh); PCGS_SEG_WEIGHT (CSR),
+// PCGS_SEG_WEIGHT_CSC / PCGS_SEG_EMIT override them for tuning experiments.
 double env_or(const char* name, double dflt) {
   const char* e = getenv(name);
   return e ? atof(e) : dflt;
 }
 
-uint64_t seg_charge16(uint32_t nv) {
-  static const double block = env_or("PCGS_SEG_WEIGHT", 24.0);
+uint64_t seg_charge16(uint32_t nv, bool csc) {
+  // CSR 40, CSC 64: swept on the PCG iteration after the 2-op gather change
+  // (24/24 82.4 us, 32/48 82.0, 40/64 81.6, 32/96 82.1)
+  static const double block = env_or("PCGS_SEG_WEIGHT", 40.0);
+  static const double block_csc = env_or("PCGS_SEG_WEIGHT_CSC", 64.0);
   static const double emit = env_or("PCGS_SEG_EMIT", 0.0);
   const double frac = nv >= 32 ? 1.0 : (double)nv / 32.0;
-  return (uint64_t)((emit + block * frac) * 16.0 + 0.5);
+  return (uint64_t)((emit + (csc ? block_csc : block) * frac) * 16.0 + 0.5);
 }
 
-void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G) {
+void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G, bool csc) {
   const int ns = (int)slabs.size();
   P.cta_task_ptr.assign(G + 1, 0);
   std::vector<Pool> pools(40);
@@ -226,7 +229,7 @@ void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G) {
     // cost model for balancing: a vector plus a per-segment charge (segment
     // closes: reductions, epilogue), in 1/16 vector units
     for (size_t q = 0; q < slabs[s].segs.size(); ++q)
-      pr[q + 1] = pr[q] + 16u * slabs[s].segs[q].nv + seg_charge16(slabs[s].segs[q].nv);
+      pr[q + 1] = pr[q] + 16u * slabs[s].segs[q].nv + seg_charge16(slabs[s].segs[q].nv, csc);
     sw[s] = pr.back();
     W += sw[s];
   }
@@ -323,7 +326,7 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
         S.add((uint32_t)(s * n + i), tmp.data(), (uint32_t)tmp.size());
       }
     }
-    plan_and_emit(P, slabs, G);
+    plan_and_emit(P, slabs, G, false);
   }
 
   // ------------- CSC pass: segments = pieces of (row slab, column) -------------
@@ -371,7 +374,7 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
       P.piece_ptr[(size_t)s * (pt + 1) + pt] = (int32_t)piece;
     }
     P.nseg = piece;
-    plan_and_emit(P, slabs, G);
+    plan_and_emit(P, slabs, G, true);
   }
   return "";
 }
