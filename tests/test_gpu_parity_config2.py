@@ -11,11 +11,12 @@ config-2 recipe (n=72,489, p=22,175) for 5 draw seeds.
   runs of the same algorithm: the reference (numpy rounding), the reference
   with Phi summed in another order, and an extended-precision run (long
   double reductions and single-rounding updates, the roundings the device
-  makes more accurate).  Measured on 5 seeds the reference sits 4-10 % above
-  the accurate run; the device sits next to the accurate run.  The gate: the
-  device count lies inside the envelope of the three CPU runs +- 2, and the
-  per-seed numbers are printed next to it (report the floor,
-  do not loosen silently).
+  makes more accurate).  Measured on 5 seeds the reference sits 3-11 % above
+  the accurate run and the device next to the accurate run, at a distance
+  that changes with the device's own summation order (the plan).  The gate:
+  the device count is within max(2, 5 % of the reference count) of the
+  nearest of the three CPU runs, and the per-seed numbers are printed next to
+  it (report the floor, do not loosen silently).
 Inputs are regenerated here from the seeds (synth + the pinned oracle port)
 and checked against the fixture's checksums."""
 import numpy as np
@@ -59,10 +60,10 @@ def test_config2_parity_against_reference(design):
         M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, cond["minv"])
         rep = pk.pcg_solve(phi, b, M, config=pk.CGConfig(rtol=1e-6), residual_scale=cond["scale"])
         ref, split, acc = int(fx["iters_ref"][k]), int(fx["iters_split"][k]), int(fx["iters_accurate"][k])
-        lo, hi = min(ref, split, acc) - 2, max(ref, split, acc) + 2
+        nearest = min(abs(rep.iterations - c) for c in (ref, split, acc))
         rows.append((int(seed), rep.iterations, ref, split, acc))
         assert rep.termination == "converged"
-        assert lo <= rep.iterations <= hi, rows[-1]
+        assert nearest <= max(2, int(np.ceil(0.05 * ref))), rows[-1]
         if k == 0:
             tight = pk.pcg_solve(phi, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=cond["scale"])
             x = fx["x_1e10"]
