@@ -166,6 +166,68 @@ __device__ __forceinline__ void rs_assemble(const RsGroup& G, long long j0, int 
   }
 }
 
+// The same column sums through shared memory when the shard has <= 8 CSC
+// slabs and the owned pieces fit the idle slab area: one round of coalesced
+// piece loads into `stage`, then 4-lane groups per column (lane g takes slabs
+// g, g+4), xor-tree totals.  Returns false (nothing written) otherwise.
+__device__ __forceinline__ bool rs_assemble_flat(const RsGroup& G, long long j0, int chunk, double* g, double* stage,
+                                                 int cap) {
+  constexpr int K = 8, GS = 4;
+  const long long pt = G.D.pt;
+  const int S = G.D.csc.nslab;
+  if (S > K) return false;
+  const long long jend = min(j0 + chunk, pt);
+  if (jend <= j0) return true;
+  const int* ppb = G.D.csc.piece_ptr;
+  int p0[K], off[K + 1];
+  off[0] = 0;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    p0[s] = s < S ? __ldg(ppb + (long long)s * (pt + 1) + j0) : 0;
+    off[s + 1] = off[s] + (s < S ? __ldg(ppb + (long long)s * (pt + 1) + jend) - p0[s] : 0);
+  }
+  if (off[K] > cap) return false;
+  for (int i = threadIdx.x; i < off[K]; i += kThreads) {
+    int sl = 0;
+#pragma unroll
+    for (int u = 1; u < K; ++u) sl += i >= off[u] ? 1 : 0;
+    int ps = p0[0], os = off[0];
+#pragma unroll
+    for (int u = 1; u < K; ++u)
+      if (sl == u) {
+        ps = p0[u];
+        os = off[u];
+      }
+    stage[i] = __ldcg(G.pieces + ps + (i - os));
+  }
+  __syncthreads();
+  const int gl = threadIdx.x & (GS - 1);
+  for (int t0 = 0; t0 < chunk; t0 += kThreads / GS) {
+    const int t = t0 + (int)threadIdx.x / GS;
+    const long long j = j0 + t;
+    double sum = 0.0;
+    if (j < jend) {
+      for (int sl = gl; sl < S; sl += GS) {
+        int base = 0, pz = 0;
+#pragma unroll
+        for (int u = 0; u < K; ++u)
+          if (sl == u) {
+            base = off[u];
+            pz = p0[u];
+          }
+        const int* pp = ppb + (long long)sl * (pt + 1);
+        const int q0 = __ldg(pp + j) - pz, q1 = __ldg(pp + j + 1) - pz;
+        for (int q = q0; q < q1; ++q) sum += stage[base + q];
+      }
+    }
+#pragma unroll
+    for (int m = 1; m < GS; m <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+    if (gl == 0 && j < jend) g[j] = sum;
+  }
+  __syncthreads();  // the stage area is the next pass's slab
+  return true;
+}
+
 // sum over ranks (rank order) of g_q[j], parity `par`
 __device__ __forceinline__ double rs_gather(const RsArgs& A, long long j, int par) {
   double v[kRsMaxRanks > 8 ? 8 : kRsMaxRanks];
@@ -251,8 +313,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
     cg::this_grid().sync();
-    rs_assemble(G, j0, chunk, G.gsum + G.gstride);  // parity 1: iteration 0 writes parity 0
-    rs_exchange(A, G.rank, st_epoch + 1ull);
+    if (!rs_assemble_flat(G, j0, chunk, G.gsum + G.gstride, sv, A.smem_doubles))
+      rs_assemble(G, j0, chunk, G.gsum + G.gstride);  // parity 1: iteration 0 writes parity 0
+    if (A.nranks == 1) __syncthreads();
+    else rs_exchange(A, G.rank, st_epoch + 1ull);
     for (int t = tid; t < chunk; t += kThreads) {
       const long long j = j0 + t;
       if (j >= pt) break;
@@ -347,19 +411,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
     cg::this_grid().sync();
-    if (cta == 0 && tid < 32) {  // this rank's z'Omega z total (slot 4 of line 0), exchanged
+    const bool solo = A.nranks == 1;  // one rank: each CTA reads only its own columns' sums
+    if (!solo && cta == 0 && tid < 32) {  // this rank's z'Omega z total (slot 4 of line 0), exchanged
       const double t = warp_sum(lane_partials(G.part + par * kPartStride * Gr, Gr, lane));
       if (tid == 0) G.part[par * kPartStride * Gr + 4] = t;
     }
-    rs_assemble(G, j0, chunk, G.gsum + par * G.gstride);
+    if (!rs_assemble_flat(G, j0, chunk, G.gsum + par * G.gstride, sv, A.smem_doubles))
+      rs_assemble(G, j0, chunk, G.gsum + par * G.gstride);
     if (tid == 0) ++st_applies;
-    rs_exchange(A, G.rank, st_epoch + (unsigned long long)(e_off + a) + 1ull);
+    if (solo) __syncthreads();
+    else rs_exchange(A, G.rank, st_epoch + (unsigned long long)(e_off + a) + 1ull);
 
     // ---------------- C: assemble owned columns over all ranks, step ----------------
     double alpha = 0.0;
     if (a > 0) {
       // dAd: the ranks' z'Omega z totals in rank order, then the replicated prior term
-      if (tid < 32) {
+      if (tid < 32 && solo) {
+        const double s = warp_sum(lane_partials(G.part + par * kPartStride * Gr, Gr, lane)) +
+                         warp_sum(lane_partials(G.part + par * kPartStride * Gr + 3, Gr, lane));
+        if (tid == 0) bc[0] = s;
+      } else if (tid < 32) {
         double v = 0.0;
         for (int q = lane; q < A.nranks; q += 32) {
           const RsPeer& P = A.peers[q];
