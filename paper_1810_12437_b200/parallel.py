@@ -195,6 +195,24 @@ def sharded_pcg_solve(op: ShardedPrecisionOperator, b, M, x0=None, config=None, 
 # Fused row-split PCG: one persistent kernel per GPU, the X'w exchange over
 # peer memory inside it (libpcgs pcgs_rs_*, csrc/rowsplit.cu)
 # ---------------------------------------------------------------------------
+def exchange_ipc_handles(L, h, group):
+    """Share every rank's exchange region: all-gather the 64-byte CUDA IPC
+    handles (one object collective at setup) and map every other rank's
+    region (pcgs_rs_open_peer); a barrier makes sure every rank has mapped its
+    peers before any kernel can signal them.  `L` is the library binding."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = ctypes.create_string_buffer(64)
+    _lib.check(L.pcgs_rs_exchange_handle(h, 0, mine))
+    allh = [None] * world
+    dist.all_gather_object(allh, bytes(mine.raw), group=group)
+    for q, hb in enumerate(allh):
+        if q != rank:
+            _lib.check(L.pcgs_rs_open_peer(h, q, ctypes.create_string_buffer(hb, 64)))
+    dist.barrier(group=group)
+    return allh
+
+
 class RowSplitPCG:
     """The whole row-split solve in one kernel per GPU.
 
@@ -235,16 +253,7 @@ class RowSplitPCG:
         _lib.check(L.pcgs_rs_create(handles, n_local, rank * n_local if real else 0, nranks, ctypes.byref(h)))
         self._h = h
         if real and world > 1:
-            import torch.distributed as dist
-            mine = ctypes.create_string_buffer(64)
-            _lib.check(L.pcgs_rs_exchange_handle(h, 0, mine))
-            allh = [None] * world
-            dist.all_gather_object(allh, bytes(mine.raw), group=group)
-            for q, hb in enumerate(allh):
-                if q != rank:
-                    buf = ctypes.create_string_buffer(hb, 64)
-                    _lib.check(L.pcgs_rs_open_peer(h, q, buf))
-            dist.barrier(group=group)
+            exchange_ipc_handles(L, h, group)
         self.n_local, self.nranks = n_local, nranks
 
     def solve(self, omegas, prior_diag, minv, scale, b, x0=None, max_iter=None, rtol=1e-6):

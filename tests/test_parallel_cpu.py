@@ -105,3 +105,44 @@ def test_local_rows_reassemble():
         rows.extend(np.split(ci, rp[1:-1]))
     ref = np.split(d.col_idx, d.row_ptr[1:-1])
     assert len(rows) == len(ref) and all(np.array_equal(a, b) for a, b in zip(rows, ref))
+
+
+class _FakeRsLib:
+    """Stands in for libpcgs in the IPC handle exchange: rank r's handle is 64
+    bytes of r; records which peer handles a rank maps."""
+
+    def __init__(self, rank):
+        self.rank, self.opened = rank, {}
+
+    def pcgs_rs_exchange_handle(self, h, local, buf):
+        import ctypes
+        ctypes.memmove(buf, bytes([self.rank]) * 64, 64)
+        return 0
+
+    def pcgs_rs_open_peer(self, h, q, buf):
+        self.opened[q] = bytes(buf.raw[:64])
+        return 0
+
+
+def _ipc_worker(rank, world, port_, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        L = _FakeRsLib(rank)
+        allh = parallel.exchange_ipc_handles(L, None, dist.group.WORLD)
+        q.put((rank, [h[0] for h in allh], {k: v[0] for k, v in L.opened.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_split_ipc_handle_exchange_gloo():
+    """The multi-process plumbing of the fused row split (one rank per GPU):
+    every rank maps exactly the other ranks' exchange regions, by rank."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_ipc_worker, args=(world, _free_port(), q), nprocs=world, join=True, start_method="spawn")
+    got = sorted(q.get() for _ in range(world))
+    for rank, handles, opened in got:
+        assert handles == list(range(world))
+        assert opened == {p: p for p in range(world) if p != rank}
