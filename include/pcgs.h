@@ -193,8 +193,9 @@ int pcgs_copy(void* dst, const void* src, int64_t bytes, int kind);
  * (globaltimer ns; 4 per operator application) of subsequent pcgs_pcg calls;
  * NULL disables. */
 int pcgs_debug_profile(void* buf);
-/* Debug/tuning switches: key 0 = direction fill mode of pcgs_pcg (1: owners
- * publish + grid sync + TMA copy, 0: computed fill). */
+/* Debug/tuning switches: key 1 = debug bits of the pass kernels (64: per-CTA
+ * pass timestamps, 128: barrier trace of PCG iteration 10), key 2 = L2
+ * persisting window over the CSC index stream in MB (0 = off). */
 int pcgs_debug_option(int key, int value);
 /* Debug: device buffer (3 uint64 per CTA) for per-CTA pass timestamps when
  * the debug-option key 1 bit 64 is set. */

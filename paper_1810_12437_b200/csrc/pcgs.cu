@@ -27,7 +27,6 @@ namespace cg = cooperative_groups;
 // error plumbing
 // =====================================================================
 static unsigned long long* g_prof = nullptr;  // debug: phase timestamps of the next pcgs_pcg
-static int g_tma_dir = 1;
 static int g_dbg = 0;
 static int g_l2_persist_mb = 0;
 static thread_local std::string g_err;
@@ -142,7 +141,6 @@ struct PcgArgs {
   double* dvg;     // 2 * p_total internal layout: search directions
   double* part;    // 4 * G partial sums: dAd, rms, rz, spare
   unsigned long long* prof;  // optional: CTA-0 phase timestamps (ns), 4 per apply
-  int tma_dir;     // 1: owners publish the direction, grid sync, TMA fill
   double* iterates;  // optional (trace_level "full"): [max_iter+1][p_total], reference layout
 };
 
@@ -345,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[64];
   __shared__ double bc[4];
-  __shared__ double st_rz, st_beta;
+  __shared__ double st_rz;
   __shared__ int st_status, st_iter, st_fail, st_applies;
   __shared__ unsigned long long mbar;
   BulkFill bf;
@@ -391,7 +389,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     }
     if (tid == 0) {
       st_rz = 0.0;
-      st_beta = 0.0;
       st_status = PCGS_MAX_ITER;
       st_iter = 0;
       st_fail = -1;
@@ -428,7 +425,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       __syncthreads();
       if (tid == 0) {
         st_rz = s_rz;
-        st_beta = beta;
         if (stop) {
           st_status = stop == 1 ? PCGS_CONVERGED : stop == 2 ? PCGS_NONFINITE : PCGS_MAX_ITER;
           st_iter = k;
@@ -998,7 +994,6 @@ int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag
   A.dvg = S.get<double>(2 * ((D.pt + 15) / 16 * 16) + 16);
   A.part = S.get<double>((size_t)kPartStride * D.G);
   A.prof = g_prof;
-  A.tma_dir = g_tma_dir;
   A.D.dbg = g_dbg;
   A.iterates = iterates;
   if (!A.w || !A.pieces || !A.zv || !A.dvg || !A.part || (D.csr.nslab > 1 && !A.zpart))
@@ -1188,7 +1183,6 @@ int pcgs_debug_cta_times(void* buf) {
 }
 
 int pcgs_debug_option(int key, int value) {
-  if (key == 0) g_tma_dir = value;
   if (key == 1) g_dbg = value;
   if (key == 2) g_l2_persist_mb = value;
   return PCGS_OK;

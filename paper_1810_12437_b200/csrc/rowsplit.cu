@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
   __shared__ int st_status, st_iter, st_fail, st_applies;
   __shared__ unsigned long long mbar, st_epoch;
   __shared__ RsGroup G;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int gi = blockIdx.x / A.Gr, cta = blockIdx.x % A.Gr;
   if (tid == 0) {
     G = A.groups[gi];
