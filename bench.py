@@ -206,22 +206,33 @@ def run_reference(args):
         return
     d, y, _ = workload(args.prior)
     iters = load_cg_iters(args.steps)
-    # warm-up steps are run (bounded) and discarded, then K timed steps
-    if args.warmup:
-        cpu_baseline(d, y, iters, min(args.warmup, 1), args.cpu_cg_cap)
-    r = cpu_baseline(d, y, iters, args.steps, args.cpu_cg_cap)
-    value = r["value"]
+    # N > 1: our arm runs one chain per GPU, so the reference runs one chain per
+    # host core, up to N, side by side (the reference path itself is single-threaded)
+    procs = max(1, min(world, os.cpu_count() or 1))
+    if procs > 1:
+        import multiprocessing as mpc
+        with mpc.get_context("fork").Pool(procs) as pool:
+            rs = pool.starmap(cpu_baseline, [(d, y, iters, args.steps, args.cpu_cg_cap)] * procs)
+        r = rs[0]
+        value = float(sum(x["value"] for x in rs))
+    else:
+        # warm-up steps are run (bounded) and discarded, then K timed steps
+        if args.warmup:
+            cpu_baseline(d, y, iters, min(args.warmup, 1), args.cpu_cg_cap)
+        r = cpu_baseline(d, y, iters, args.steps, args.cpu_cg_cap)
+        value = r["value"]
     sample = (f"{args.steps} horseshoe scans of the CPU restatement (oracle/port.py), CG capped at "
               f"{args.cpu_cg_cap} Phi-applications per scan and extrapolated to the device chain's "
               f"per-scan CG counts (mean {np.mean(iters):.1f}): fixed {r['fixed_s']:.2f} s + "
-              f"{r['apply_s']*1e3:.0f} ms per apply")
+              f"{r['apply_s']*1e3:.0f} ms per apply"
+              + (f"; {procs} chains side by side, one per core (value = their sum)" if procs > 1 else ""))
     line = {
         "impl": "reference", "metric": "gibbs_iter_per_s", "value": value, "unit": "iter/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; BASELINE config 3 recipe)",
-        "config": config_block(d, args.prior, 1),
-        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port", "sample": sample},
+        "config": config_block(d, args.prior, world),
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": procs, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
