@@ -482,10 +482,10 @@ def run_rowsplit(args):
 
 def run_config4(args):
     """BASELINE config 4: independent chains on the config-2/3 design, 8 per
-    GPU (chain c seeded chain_seed(0, c)), run in waves of --concurrent chains
-    side by side, each on its own stream with the store planned for
-    SMs/concurrent CTAs.  Step = one scan of every chain of the rank; value =
-    chain-iterations per second over all ranks."""
+    GPU (chain c seeded chain_seed(0, c)), on --concurrent slots side by side
+    (one stream each, the store planned for SMs/concurrent CTAs, a slot's
+    chains one after another).  Step = one scan of every chain of the rank;
+    value = chain-iterations per second over all ranks."""
     import torch
     import torch.distributed as dist
     from paper_1810_12437_b200 import gibbs, parallel
@@ -502,40 +502,44 @@ def run_config4(args):
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid = 0 if R == 1 else sms // R
     chains_idx = parallel.chain_assignment(per_gpu * world, world, rank)
-    total_ms, cg = 0.0, []
+    # R slots (streams); chain i of the rank runs on slot i % R after the
+    # slot's previous chain, with no barrier between rounds.  Warm-up: every
+    # chain's first W scans, issued slot-ordered before the timed region; the
+    # timed region covers the K further scans of every chain.
+    slots = [torch.cuda.Stream(dev) for _ in range(R)]
+    chains = []
     with ClockSampler(local) as clk:
-        for w0 in range(0, len(chains_idx), R):
-            wave = chains_idx[w0:w0 + R]
-            streams = [torch.cuda.Stream(dev) for _ in wave]
-            chains = []
-            for c, s in zip(wave, streams):
+        for i, c in enumerate(chains_idx):
+            with torch.cuda.stream(slots[i % R]):
+                chains.append((gibbs.DeviceChain(X, y, cfg, W + K, burn_in=W, seed=parallel.chain_seed(SEED, c),
+                                                 cg_config=gibbs.CGConfig(rtol=RTOL), device=dev, grid=grid),
+                               slots[i % R]))
+        for t in range(1, W + 1):
+            for ch, s in chains:
                 with torch.cuda.stream(s):
-                    chains.append(gibbs.DeviceChain(X, y, cfg, W + K, burn_in=W, seed=parallel.chain_seed(SEED, c),
-                                                    cg_config=gibbs.CGConfig(rtol=RTOL), device=dev, grid=grid))
-            for t in range(1, W + 1):
-                for ch, s in zip(chains, streams):
-                    with torch.cuda.stream(s):
-                        ch.scan(t)
-            torch.cuda.synchronize(dev)
-            if world > 1:
-                dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            cur = torch.cuda.current_stream(dev)
-            e0.record(cur)
-            for s in streams:
-                s.wait_stream(cur)
+                    ch.scan(t)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        cur = torch.cuda.current_stream(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for s in slots:
+            s.wait_stream(cur)
+        for r0 in range(0, len(chains), R):       # round by round: a slot's chains in order
             for t in range(W + 1, W + K + 1):
-                for ch, s in zip(chains, streams):
+                for ch, s in chains[r0:r0 + R]:
                     with torch.cuda.stream(s):
                         ch.scan(t)
-            for s in streams:
-                cur.wait_stream(s)
-            e1.record(cur)
-            torch.cuda.synchronize(dev)
-            total_ms += e0.elapsed_time(e1)
-            for ch in chains:
-                ch.check(1, W + K)
-                cg += ch.results.view(-1, 8).cpu().numpy()[W:W + K, 0].astype(int).tolist()
+        for s in slots:
+            cur.wait_stream(s)
+        e1.record(cur)
+        torch.cuda.synchronize(dev)
+        total_ms = e0.elapsed_time(e1)
+    cg = []
+    for ch, _ in chains:
+        ch.check(1, W + K)
+        cg += ch.results.view(-1, 8).cpu().numpy()[W:W + K, 0].astype(int).tolist()
     ms_t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -548,7 +552,7 @@ def run_config4(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; BASELINE config 4 recipe; no public dataset)",
             "config": {"workload": f"config 4: {per_gpu} independent {args.prior} chains per GPU on the "
-                                   f"n={d.n:,} p={d.p:,} design (nnz {d.nnz:,}), waves of {R} side by side",
+                                   f"n={d.n:,} p={d.p:,} design (nnz {d.nnz:,}), {R} slots side by side",
                        "chains_per_gpu": per_gpu, "concurrent": R, "grid_per_chain": grid or sms,
                        "parallelism": f"chain-parallel x{world}", "seed": SEED},
             "clocks": clk.summary(),

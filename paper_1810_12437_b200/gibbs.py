@@ -463,10 +463,10 @@ def gibbs_run_concurrent(X, y, cfg, n_iter, seeds, concurrent=4, burn_in=0, thin
                          preconditioner="prior", cg_config=None, init_state=None, gamma_scale=1.0,
                          allow_max_iter=False, fixed_omega=None, fixed_tau=None, fixed_lam=None,
                          device=None, sync_every=64) -> list:
-    """Independent chains (one per seed) sharing one GPU: waves of `concurrent`
-    chains, each chain on its own CUDA stream with the store planned for
-    SMs // concurrent CTAs, so the chains' persistent PCG kernels run side by
-    side.  Chain c's output equals gibbs_run(..., seed=seeds[c],
+    """Independent chains (one per seed) sharing one GPU: `concurrent` slots,
+    each a CUDA stream running its chains one after another with the store
+    planned for SMs // concurrent CTAs, so the slots' persistent PCG kernels
+    run side by side.  Chain c's output equals gibbs_run(..., seed=seeds[c],
     grid=SMs // concurrent) bit for bit (deterministic kernels; the streams
     only change what runs beside it)."""
     torch = _lib.torch()
@@ -475,32 +475,37 @@ def gibbs_run_concurrent(X, y, cfg, n_iter, seeds, concurrent=4, burn_in=0, thin
     concurrent = max(1, int(concurrent))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid = 0 if concurrent == 1 else sms // concurrent
-    outs = []
     seeds = list(seeds)
+    # `concurrent` slots, one stream each; chain c runs on slot c % concurrent
+    # after the slot's previous chain (stream order, no barrier between
+    # rounds: a slot whose chain needed fewer CG iterations starts its next
+    # chain at once).  Outputs are read after everything has been issued.
+    slots = [torch.cuda.Stream(dev) for _ in range(concurrent)]
+    issued = []
     for w0 in range(0, len(seeds), concurrent):
-        wave = seeds[w0:w0 + concurrent]
-        chains, streams = [], []
-        for sd in wave:
-            streams.append(torch.cuda.Stream(dev))
-            with torch.cuda.stream(streams[-1]):
-                chains.append(DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=sd,
-                                          preconditioner=preconditioner, cg_config=cg_config,
-                                          init_state=init_state, gamma_scale=gamma_scale,
-                                          fixed_omega=fixed_omega, fixed_tau=fixed_tau, fixed_lam=fixed_lam,
-                                          device=dev, grid=grid))
+        row = []
+        for k, sd in enumerate(seeds[w0:w0 + concurrent]):
+            with torch.cuda.stream(slots[k]):
+                row.append((DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=sd,
+                                        preconditioner=preconditioner, cg_config=cg_config,
+                                        init_state=init_state, gamma_scale=gamma_scale,
+                                        fixed_omega=fixed_omega, fixed_tau=fixed_tau, fixed_lam=fixed_lam,
+                                        device=dev, grid=grid), slots[k]))
         checked = 0
         for t in range(1, n_iter + 1):
-            for ch, s in zip(chains, streams):
+            for ch, s in row:
                 with torch.cuda.stream(s):
                     ch.scan(t)
             if sync_every and t - checked >= sync_every:
-                for ch, s in zip(chains, streams):
+                for ch, s in row:
                     with torch.cuda.stream(s):
                         ch.check(checked + 1, t, allow_max_iter)
                 checked = t
-        for ch, s in zip(chains, streams):
-            with torch.cuda.stream(s):
-                if checked < n_iter:
-                    ch.check(checked + 1, n_iter, allow_max_iter)
-                outs.append(ch.output())
+        issued += [(ch, s, checked) for ch, s in row]
+    outs = []
+    for ch, s, checked in issued:
+        with torch.cuda.stream(s):
+            if checked < n_iter:
+                ch.check(checked + 1, n_iter, allow_max_iter)
+            outs.append(ch.output())
     return outs

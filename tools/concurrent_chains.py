@@ -27,7 +27,7 @@ class Op:  # the operator view pcg_solve_device needs, on a store of a chosen gr
         return self._dg
 
 
-def run(R, grid):
+def run(R, grid, stagger_us=0.0):
     X = d.matrix()
     store = X.device_store(dev, grid=grid)
     om = torch.tensor(cond["omega"], device=dev)
@@ -40,6 +40,8 @@ def run(R, grid):
         outs = []
         for c in range(R):
             with torch.cuda.stream(streams[c] if grid else torch.cuda.current_stream(dev)):
+                if stagger_us and grid:
+                    torch.cuda._sleep(int(c * stagger_us * 1965))   # ~cycles at 1.965 GHz
                 outs.append(pk.cg.pcg_solve_device(phis[c], bs[c], mt, st, rtol=1e-30, max_iter=ITER))
         return outs
     once()
@@ -60,3 +62,5 @@ def run(R, grid):
 print(f"sequential, full grid: {run(2, 0):.1f} us per chain-iteration")
 for R in (2, 3, 4, 6, 8):
     print(f"{R} concurrent chains on {148 // R}-CTA stores: {run(R, 148 // R):.1f} us per chain-iteration")
+# the same 4 solves with chain c started c x 45 us (about one pass of L2 residency) later
+print(f"4 chains, staggered starts: {run(4, 37, 45.0):.1f} us per chain-iteration (incl. the stagger)")
