@@ -88,6 +88,45 @@ def phi_apply(X: Csr, omega, prior_diag, v):
     return out
 
 
+def phi_apply_exact_ld(X: Csr, omega, prior_diag, v):
+    """Phi v with every sum accumulated in x87 long double (64-bit mantissa),
+    returned in long double; rounded once to float64 (phi_apply_exact) it is
+    to within an ulp the correctly rounded Phi v
+    of sampler.py:53-58 (binary, unstandardised designs).  Used to measure the
+    TRUE residual b - Phi x of a solution, independent of any fp64 summation
+    order (tests/test_gpu_parity_config2.py)."""
+    L = np.longdouble
+    if not hasattr(X, "_csc_perm"):
+        X._csc_perm = np.argsort(X.col_idx, kind="stable")
+        X._csc_rows = X.row_of[X._csc_perm]
+        cnt = np.bincount(X.col_idx, minlength=X.p)
+        X._csc_start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+        X._csc_nonempty = cnt > 0
+    v = np.asarray(v, dtype=np.float64)
+    z = np.zeros(X.n, dtype=L)
+    if X.nonempty.size:
+        z[X.nonempty] = np.add.reduceat(v.astype(L)[X.col_idx], X.row_ptr[X.nonempty])
+    w = np.asarray(omega, dtype=np.float64).astype(L) * z
+    g = np.zeros(X.p, dtype=L)
+    ne = X._csc_nonempty
+    g[ne] = np.add.reduceat(w[X._csc_rows], X._csc_start[ne])
+    return g + np.asarray(prior_diag).astype(L) * v.astype(L)
+
+
+def phi_apply_exact(X: Csr, omega, prior_diag, v):
+    """phi_apply_exact_ld rounded once to float64."""
+    return phi_apply_exact_ld(X, omega, prior_diag, v).astype(np.float64)
+
+
+def true_rms(X: Csr, omega, prior_diag, b, x, scale):
+    """RMS of the scaled TRUE residual s*(b - Phi x) (the cg.py:150-151 metric),
+    Phi x from phi_apply_exact and the difference taken in long double."""
+    L = np.longdouble
+    L_ax = phi_apply_exact_ld(X, omega, prior_diag, x)
+    t = np.asarray(scale).astype(L) * (np.asarray(b).astype(L) - L_ax)
+    return float(np.sqrt(np.dot(t, t) / len(b)))
+
+
 def gram_diagonal(X: Csr, omega):
     """diag(X' Omega X) (sparse.py:235-246)."""
     w = np.asarray(omega)[X.row_of]

@@ -28,8 +28,10 @@ struct DesignDev {
   int smem_doubles;    // dynamic shared memory per CTA, in doubles
   int dbg;             // tuning experiments: bit 0 skip gathers, bit 1 skip segmented reduce
   PassDev csr, csc;
-  double* own_global;  // PCG own-slice state in global memory (8 x chunk per CTA) when it
-                       // does not fit next to the slab in shared memory (very wide designs)
+  int own_in_global;   // PCG own-slice state does not fit next to the slab in shared memory
+                       // (very wide designs): it lives in global memory instead
+  double* own_global;  // that buffer (8 x chunk per CTA); allocated per solve, never per
+                       // design, so solves on one design from several streams stay apart
 };
 
 // ------------------------------------------------------------------ utilities

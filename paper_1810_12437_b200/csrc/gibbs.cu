@@ -276,8 +276,8 @@ extern "C" {
 
 int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream) {
   if (!d || !g || !g->beta || !g->z || !g->y || !g->part) return fail(PCGS_EINVAL, "null argument");
-  CUDA_TRY(cudaFuncSetAttribute(k_csr_logit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_bytes(d->dev)));
+  int rc0;
+  if ((rc0 = raise_smem_limit(k_csr_logit))) return rc0;
   k_tau_sums<<<d->dev.G, 256, 0, (cudaStream_t)stream>>>(*g, d->dev.pt);
   CUDA_TRY(cudaGetLastError());
   return launch_logit(d, g, (cudaStream_t)stream);
@@ -352,8 +352,7 @@ static int rs_logit(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows, c
     int64_t row0;
     int rc;
     if ((rc = rs_local(rs, l, &d, &row0))) return rc;
-    CUDA_TRY(cudaFuncSetAttribute(k_csr_logit, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem_bytes(d->dev)));
+    if ((rc = raise_smem_limit(k_csr_logit))) return rc;
     pcgs_gibbs_t gl = *g;
     gl.y = rows[l].y;
     gl.z = rows[l].z;

@@ -182,3 +182,20 @@ struct EpiCsr {  // runtime choice: multi column slab -> partial store, else Epi
 
 
 inline size_t smem_bytes(const DesignDev& D) { return (size_t)D.smem_doubles * sizeof(double); }
+
+// Raises a kernel's dynamic shared-memory limit to the device's opt-in maximum
+// (minus its static shared memory).  The limit is a per-kernel, per-process
+// attribute: setting it to a design's own need would lower it for designs
+// created earlier, so every kernel is always set to the maximum (idempotent;
+// the launch's dynamicSmemBytes decides what is actually used).
+template <class K>
+inline int raise_smem_limit(K kernel) {
+  int dev = 0, optin = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa;
+  CUDA_TRY(cudaFuncGetAttributes(&fa, kernel));
+  CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin - (int)fa.sharedSizeBytes));
+  return PCGS_OK;
+}

@@ -190,15 +190,15 @@ struct OwnState {
 
 __host__ __device__ inline bool pp_in_smem(const DesignDev& D) {
   const long long chunk = (D.pt + D.G - 1) / D.G;
-  const long long own = D.own_global ? 0 : chunk * 8 * 8;
+  const long long own = D.own_in_global ? 0 : chunk * 8 * 8;
   const long long bytes = (long long)D.smem_doubles * 8 + own + (long long)D.csc.nslab * (chunk + 1) * 4;
   return bytes + 1024 <= 227 * 1024;
 }
 
 __device__ __forceinline__ OwnState own_state(double* sv, const DesignDev& D, int chunk, long long j0) {
   OwnState o;
-  double* base = D.own_global ? D.own_global + (size_t)blockIdx.x * 8 * chunk : sv + D.smem_doubles;
-  double* after = D.own_global ? sv + D.smem_doubles : base + 8 * chunk;
+  double* base = D.own_in_global ? D.own_global + (size_t)blockIdx.x * 8 * chunk : sv + D.smem_doubles;
+  double* after = D.own_in_global ? sv + D.smem_doubles : base + 8 * chunk;
   o.x = base;
   o.r = base + chunk;
   o.d = base + 2 * chunk;
@@ -223,7 +223,7 @@ __device__ __forceinline__ OwnState own_state(double* sv, const DesignDev& D, in
 
 size_t pcg_smem_bytes(const DesignDev& D) {
   const long long chunk = (D.pt + D.G - 1) / D.G;
-  size_t b = (size_t)D.smem_doubles * 8 + (D.own_global ? 0 : (size_t)chunk * 8 * 8) + 16;
+  size_t b = (size_t)D.smem_doubles * 8 + (D.own_in_global ? 0 : (size_t)chunk * 8 * 8) + 16;
   if (pp_in_smem(D)) b += (size_t)D.csc.nslab * (chunk + 1) * 4;
   return b;
 }
@@ -659,13 +659,12 @@ int pcgs_version(void) { return 1; }
 const char* pcgs_last_error(void) { return g_err.c_str(); }
 
 
-static int set_smem_attrs(const DesignDev& D) {
-  const int bytes = (int)smem_bytes(D);
-  CUDA_TRY(cudaFuncSetAttribute(k_csr_matvec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CUDA_TRY(cudaFuncSetAttribute(k_csr_phi, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CUDA_TRY(cudaFuncSetAttribute(k_csc_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CUDA_TRY(cudaFuncSetAttribute(k_csc<FillRhs>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-  CUDA_TRY(cudaFuncSetAttribute(k_pcg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pcg_smem_bytes(D)));
+static int set_smem_attrs() {
+  int rc;
+  if ((rc = raise_smem_limit(k_csr_matvec)) || (rc = raise_smem_limit(k_csr_phi)) ||
+      (rc = raise_smem_limit(k_csc_vec)) || (rc = raise_smem_limit(k_csc<FillRhs>)) ||
+      (rc = raise_smem_limit(k_pcg)))
+    return rc;
   return PCGS_OK;
 }
 
@@ -702,23 +701,16 @@ int pcgs_design_create_ex(int64_t n, int64_t p, const int64_t* row_ptr_h, const 
   dd.own_global = nullptr;
   int rc;
   {
-    // own-slice PCG state next to the slab when it fits, else in global memory
+    // own-slice PCG state next to the slab when it fits, else in global
+    // memory allocated by each solve (pcgs_pcg_full)
     const long long chunk = (H.p_total + G - 1) / G;
-    if ((long long)dd.smem_doubles * 8 + chunk * 64 + 16 + 1024 > 227 * 1024) {
-      void* og = nullptr;
-      if (cudaMalloc(&og, (size_t)G * 8 * chunk * sizeof(double)) != cudaSuccess) {
-        pcgs_design_destroy(D);
-        return fail(PCGS_ENOMEM, "device allocation failed (PCG state)");
-      }
-      D->allocs.push_back(og);
-      dd.own_global = (double*)og;
-    }
+    dd.own_in_global = (long long)dd.smem_doubles * 8 + chunk * 64 + 16 + 1024 > 227 * 1024;
   }
   if ((rc = upload_pass(D, H.csr, dd.csr)) || (rc = upload_pass(D, H.csc, dd.csc))) {
     pcgs_design_destroy(D);
     return rc;
   }
-  if ((rc = set_smem_attrs(dd))) {
+  if ((rc = set_smem_attrs())) {
     pcgs_design_destroy(D);
     return rc;
   }
@@ -996,6 +988,11 @@ int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag
   A.prof = g_prof;
   A.D.dbg = g_dbg;
   A.iterates = iterates;
+  if (D.own_in_global) {  // per-solve state: concurrent solves on one design must not share it
+    const long long chunk = (D.pt + D.G - 1) / D.G;
+    A.D.own_global = S.get<double>((size_t)D.G * 8 * chunk);
+    if (!A.D.own_global) return fail(PCGS_ENOMEM, "scratch allocation failed (PCG state)");
+  }
   if (!A.w || !A.pieces || !A.zv || !A.dvg || !A.part || (D.csr.nslab > 1 && !A.zpart))
     return fail(PCGS_ENOMEM, "scratch allocation failed");
   cudaLaunchConfig_t cfg = {};

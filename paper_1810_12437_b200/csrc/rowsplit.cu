@@ -661,9 +661,7 @@ int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nra
   R->groups_dev = (RsGroup*)p;
   if ((rc = rs_alloc(R, sizeof(RsPeer) * nranks, &p))) return bail(rc);
   R->peers_dev = (RsPeer*)p;
-  const int smem = (int)rs_smem_bytes(R);
-  if (cudaFuncSetAttribute(k_pcg_rs, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return bail(fail(PCGS_ECUDA, "row split: shared memory attribute"));
+  if ((rc = raise_smem_limit(k_pcg_rs))) return bail(rc);
   *out = R;
   return PCGS_OK;
 }

@@ -459,53 +459,64 @@ def gibbs_run(X, y, cfg, n_iter, burn_in=0, sampler="cg", seed=0, thin=1, precon
     return ch.output()
 
 
-def gibbs_run_concurrent(X, y, cfg, n_iter, seeds, concurrent=4, burn_in=0, thin=1,
-                         preconditioner="prior", cg_config=None, init_state=None, gamma_scale=1.0,
-                         allow_max_iter=False, fixed_omega=None, fixed_tau=None, fixed_lam=None,
-                         device=None, sync_every=64) -> list:
+def gibbs_run_concurrent(X, y, cfg, n_iter, seeds, concurrent=4, burn_in=0, thin=1, sampler="cg",
+                         preconditioner="prior", cg_config=None, burn_in_sampler=None, init_state=None,
+                         gamma_scale=1.0, allow_max_iter=False, fixed_omega=None, fixed_tau=None,
+                         fixed_lam=None, device=None, poll_s=2e-4) -> list:
     """Independent chains (one per seed) sharing one GPU: `concurrent` slots,
-    each a CUDA stream running its chains one after another with the store
-    planned for SMs // concurrent CTAs, so the slots' persistent PCG kernels
-    run side by side.  Chain c's output equals gibbs_run(..., seed=seeds[c],
-    grid=SMs // concurrent) bit for bit (deterministic kernels; the streams
-    only change what runs beside it)."""
+    each a CUDA stream, with the store planned for SMs // concurrent CTAs so
+    the slots' persistent PCG kernels run side by side.  Chain c's output
+    equals gibbs_run(..., seed=seeds[c], grid=SMs // concurrent) bit for bit
+    (deterministic kernels; the slot only changes what runs beside it).
+
+    Every chain is issued whole (all its scans) onto a free slot; the host then
+    waits for whichever slot finishes first (stream polling, no blocking call
+    on a busy stream), reads that chain's output, checks it for aborts and
+    frees it before issuing the next chain there.  Device memory is bounded by
+    `concurrent` chains.  Aborts are reported when the failed chain finishes
+    (GibbsAbortError for its first failed scan, as gibbs_run raises it)."""
+    import time
     torch = _lib.torch()
-    y = _check_run_args(X, y, cfg, n_iter, burn_in, thin, "cg", None, preconditioner, fixed_lam, None)
+    y = _check_run_args(X, y, cfg, n_iter, burn_in, thin, sampler, burn_in_sampler, preconditioner,
+                        fixed_lam, None)
     dev = _lib.cuda_device(device)
     concurrent = max(1, int(concurrent))
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid = 0 if concurrent == 1 else sms // concurrent
     seeds = list(seeds)
-    # `concurrent` slots, one stream each; chain c runs on slot c % concurrent
-    # after the slot's previous chain (stream order, no barrier between
-    # rounds: a slot whose chain needed fewer CG iterations starts its next
-    # chain at once).  Outputs are read after everything has been issued.
     slots = [torch.cuda.Stream(dev) for _ in range(concurrent)]
-    issued = []
-    for w0 in range(0, len(seeds), concurrent):
-        row = []
-        for k, sd in enumerate(seeds[w0:w0 + concurrent]):
-            with torch.cuda.stream(slots[k]):
-                row.append((DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=sd,
-                                        preconditioner=preconditioner, cg_config=cg_config,
-                                        init_state=init_state, gamma_scale=gamma_scale,
-                                        fixed_omega=fixed_omega, fixed_tau=fixed_tau, fixed_lam=fixed_lam,
-                                        device=dev, grid=grid), slots[k]))
-        checked = 0
-        for t in range(1, n_iter + 1):
-            for ch, s in row:
-                with torch.cuda.stream(s):
-                    ch.scan(t)
-            if sync_every and t - checked >= sync_every:
-                for ch, s in row:
-                    with torch.cuda.stream(s):
-                        ch.check(checked + 1, t, allow_max_iter)
-                checked = t
-        issued += [(ch, s, checked) for ch, s in row]
-    outs = []
-    for ch, s, checked in issued:
-        with torch.cuda.stream(s):
-            if checked < n_iter:
-                ch.check(checked + 1, n_iter, allow_max_iter)
-            outs.append(ch.output())
+    busy = {}          # slot -> (chain index, DeviceChain)
+    outs = [None] * len(seeds)
+
+    def finish(k):
+        c, ch = busy.pop(k)
+        with torch.cuda.stream(slots[k]):
+            slots[k].synchronize()
+            ch.check(1, n_iter, allow_max_iter) if n_iter else None
+            outs[c] = ch.output()
+
+    def free_slot():
+        while True:
+            for k in range(concurrent):
+                if k not in busy:
+                    return k
+            for k in list(busy):
+                if slots[k].query():
+                    finish(k)
+                    return k
+            time.sleep(poll_s)
+
+    for c, sd in enumerate(seeds):
+        k = free_slot()
+        with torch.cuda.stream(slots[k]):
+            ch = DeviceChain(X, y, cfg, n_iter, burn_in=burn_in, thin=thin, seed=sd,
+                             preconditioner=preconditioner, cg_config=cg_config,
+                             init_state=init_state, gamma_scale=gamma_scale,
+                             fixed_omega=fixed_omega, fixed_tau=fixed_tau, fixed_lam=fixed_lam,
+                             device=dev, grid=grid)
+            for t in range(1, n_iter + 1):
+                ch.scan(t)
+        busy[k] = (c, ch)
+    for k in sorted(busy):
+        finish(k)
     return outs

@@ -458,10 +458,12 @@ def run_chains(X, y, cfg, n_iter, n_chains, seed=0, group=None, gather=True, run
     """Run `n_chains` independent Gibbs chains, sharded over the ranks of
     `group` (default: the initialised torch.distributed world, else one
     process).  Chain c uses `chain_seed(seed, c)`.  Each rank runs its block
-    of chains on its GPU in waves of `concurrent` chains side by side (one
-    CUDA stream each, the store planned for SMs // concurrent CTAs;
-    `gibbs.gibbs_run_concurrent`; default min(4, chains on the rank)), or one
-    after another with `concurrent=1` / a custom `runner`.  There is no
+    of chains on its GPU on `concurrent` slots side by side (one CUDA stream
+    each, the store planned for SMs // concurrent CTAs;
+    `gibbs.gibbs_run_concurrent`; default 4, independent of how many chains
+    the rank holds, so a chain's floating-point trajectory depends on its
+    seed only, never on the world size), or one after another with
+    `concurrent=1` / a custom `runner`.  There is no
     collective while sampling; with `gather` the outputs are all-gathered at
     the end (object collective) and every rank returns all chains in index
     order, otherwise only its own (as {chain: ChainOutput})."""
@@ -473,10 +475,10 @@ def run_chains(X, y, cfg, n_iter, n_chains, seed=0, group=None, gather=True, run
     block = chain_assignment(n_chains, world, rank)
     host_hooks = kwargs.get("local_scale_sampler") is not None or kwargs.get("on_progress") is not None
     if concurrent is None:
-        concurrent = 1 if (runner is not None or host_hooks) else min(4, max(1, len(block)))
+        concurrent = 1 if (runner is not None or host_hooks) else 4
     if concurrent > 1 and runner is None and not host_hooks:
         from .gibbs import gibbs_run_concurrent
-        kw = {k: v for k, v in kwargs.items() if k not in ("sampler", "burn_in_sampler")}
+        kw = {k: v for k, v in kwargs.items() if k != "sync_every"}
         outs = gibbs_run_concurrent(X, y, cfg, n_iter, [chain_seed(seed, c) for c in block],
                                     concurrent=concurrent, **kw)
         mine = dict(zip(block, outs))

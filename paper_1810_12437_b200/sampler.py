@@ -211,3 +211,12 @@ def cg_sample(target: GaussianTarget, M: Preconditioner, rng, x0=None,
     report = pcg_solve(target.precision, b, M, x0=x0, config=config,
                        residual_scale=residual_scale)
     return report.solution, report
+
+
+def direct_sample(target: GaussianTarget, rng, dense_cap=None) -> np.ndarray:
+    """The reference's dense Cholesky draw (sampler.py:123-135) is not rebuilt
+    on the device (a desk-scale oracle only); use
+    `cg_sample`, which draws from the same distribution matrix-free."""
+    raise NotImplementedError(
+        "direct_sample (dense Cholesky) is not on the device path; use cg_sample, which draws "
+        "beta ~ N(Phi^-1 b_lin, Phi^-1) matrix-free on the GPU")

@@ -502,3 +502,24 @@ def _check_cap(dim, dense_cap, what):
         raise DimensionCapError(
             f"{what}: dimension {dim} exceeds the dense cap {dense_cap}; "
             "use the matrix-free CG path or raise the cap explicitly")
+
+
+class DenseSymmetric:
+    """Square symmetric matrix under the dense dimension cap (sparse.py:344-359).
+
+    Kept for the drop-in namespace: the dense Cholesky path it feeds
+    (`direct_sample`) is the CPU oracle's and is not on the device path."""
+
+    def __init__(self, entries, dense_cap=DEFAULT_DENSE_CAP):
+        a = np.ascontiguousarray(entries, dtype=np.float64)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise ValueError("expected a square matrix")
+        _check_cap(a.shape[0], dense_cap, "DenseSymmetric")
+        top = float(np.abs(a).max()) if a.size else 0.0
+        if a.size and float(np.abs(a - a.T).max()) > 1e-12 * max(top, 1.0):
+            raise ValueError("matrix is not symmetric to 1e-12 relative")
+        self.entries = a
+
+    @property
+    def dim(self):
+        return self.entries.shape[0]

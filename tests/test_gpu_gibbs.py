@@ -233,3 +233,37 @@ def test_unshrunk_block_of_dummies_matches_oracle():
         z = standardized_differences(a, b)
         assert np.mean(np.abs(z) > 4) < 0.03
         assert stats.kstest(np.clip(z, -6, 6), "norm").pvalue > 1e-3
+
+
+def test_concurrent_chains_on_a_wide_design_keep_their_state_apart():
+    """A design too wide for the PCG own-slice state to sit next to the slab in
+    shared memory (p_total / grid > ~700 at grid 37) keeps that state in
+    global memory; it is allocated per solve, so four chains side by side on
+    one design stay bitwise equal to direct runs (a per-design
+    buffer made concurrent solves overwrite each other)."""
+    import torch
+    from paper_1810_12437_b200 import parallel
+    d = synth.binary_design(30_000, 40_000, 2e-5, 2e-4, seed=21)
+    y, _ = synth.simulate_outcomes(d, seed=2, n_signal=5)
+    X = d.matrix()
+    cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
+    outs = parallel.run_chains(X, y, cfg, 12, n_chains=4, seed=5, burn_in=2, concurrent=4)
+    grid = torch.cuda.get_device_properties(0).multi_processor_count // 4
+    for c, o in enumerate(outs):
+        ref = gibbs.gibbs_run(X, y, cfg, 12, burn_in=2, seed=parallel.chain_seed(5, c), grid=grid)
+        np.testing.assert_array_equal(o.draws, ref.draws)
+        np.testing.assert_array_equal(o.cg_iteration_counts, ref.cg_iteration_counts)
+
+
+def test_store_plans_of_different_shared_memory_needs_interleave(small):
+    """The per-kernel shared-memory limit is process-wide: a grid-37 plan (more
+    own-slice state per CTA), then a full-grid plan, then the grid-37 plan
+    again must all launch (the limit used to follow the most
+    recently created store)."""
+    d, y, _ = small
+    X = d.matrix()
+    cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
+    a = gibbs.gibbs_run(X, y, cfg, 3, seed=1, grid=37)
+    gibbs.gibbs_run(X, y, cfg, 3, seed=1)
+    b = gibbs.gibbs_run(X, y, cfg, 3, seed=1, grid=37)
+    np.testing.assert_array_equal(a.draws, b.draws)
