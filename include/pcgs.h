@@ -294,6 +294,21 @@ typedef struct {
   const double* cscale;
 } pcgs_gibbs_t;
 
+/* Validation entry point for the scale updates of the scan (the same device
+ * functions k_global / k_local call; replaces the reference's
+ * update_global_scale gibbs.py:179-190 and update_local_scales gibbs.py:193-214
+ * as a unit under test, mirroring test_gibbs.py:114-140).  prior 0 bridge,
+ * 1 horseshoe.  mode 0: `count` independent global draws from the sum
+ * `b_or_acc` (bridge: sum |beta|^alpha; horseshoe: sum beta^2/lam^2) over p
+ * coefficients and tau_old = `tau`, out = tau, aux = xi (horseshoe);
+ * mode 1: `count` independent local draws of one coefficient b = `b_or_acc`
+ * given tau and lam_old, out = lam, aux = nu (horseshoe);
+ * mode 2 / 3: one thread iterating the global / local update `count` times
+ * (the auxiliary-variable Gibbs chain), out = the chain of tau / lam. */
+int pcgs_scale_draws(int prior, int mode, int64_t count, double b_or_acc, double tau,
+                     double lam_old, int64_t p, double a0, double b0, double alpha,
+                     uint64_t seed, double* out, double* aux, pcgs_stream_t stream);
+
 /* z = X beta and its log-likelihood partials (start of a chain / resume). */
 int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream);
 /* Scan t (1-based).  `count` = number of statistics updates so far; `slot` =

@@ -454,8 +454,11 @@ def gibbs_bridge(X: Csr, y, n_iter, seed=0, burn_in=0, thin=1, alpha=1.0, a0=1.0
 
 # ============================================================== horseshoe (NEW, no reference)
 def ig_draw(shape, rate, rng):
-    """Inverse-gamma(shape, rate) = rate / Gamma(shape, 1)."""
-    return rate / rng.gamma(shape)
+    """Inverse-gamma(shape, rate) = rate / Gamma(shape, 1), one independent
+    Gamma variate per element of `rate`."""
+    if np.ndim(rate) == 0:
+        return rate / rng.gamma(shape)
+    return rate / rng.gamma(shape, size=np.shape(rate))
 
 
 def horseshoe_scales(beta_shrunk, lam2, nu, tau2, xi, rng):

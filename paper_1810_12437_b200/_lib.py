@@ -75,6 +75,8 @@ SIGNATURES = {
     "pcgs_pg_draw": (ctypes.c_int, [_P, _I64, _U64, _U64, _P, _P]),
     "pcgs_pg_draw_rows": (ctypes.c_int, [_P, _I64, _I64, _U64, _U64, _P, _P]),
     "pcgs_gibbs_init": (ctypes.c_int, [_P, _P, _P]),
+    "pcgs_scale_draws": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _I64, _D, _D, _D, _I64, _D, _D, _D,
+                                        _U64, _P, _P, _P]),
     "pcgs_rs_create": (ctypes.c_int, [_P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
     "pcgs_rs_exchange_handle": (ctypes.c_int, [_P, ctypes.c_int, _P]),
     "pcgs_rs_open_peer": (ctypes.c_int, [_P, ctypes.c_int, _P]),

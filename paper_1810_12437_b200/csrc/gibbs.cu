@@ -74,6 +74,81 @@ __device__ double wald1(double mu, Philox& R) {
   return R.uniform() <= mu / (mu + x) ? x : mu * mu / x;
 }
 
+// The conditional draws of the scale updates, shared by the scan kernels and
+// the validation entry point pcgs_scale_draws.
+//
+// Global scale.  Bridge (gibbs.py:179-190): phi = tau^-alpha ~
+// Gamma(a0 + p/alpha, b0 + sum|beta|^alpha), acc = that sum.  Horseshoe (new,
+// DESIGN.md §5): xi | tau ~ IG(1, 1 + 1/tau^2), then tau^2 | beta, lam, xi ~
+// IG((p+1)/2, 1/xi + acc/2), acc = sum beta^2 / lam^2; *xi receives xi.
+__device__ double global_draw(int prior, double a0, double b0, double alpha, long long p, double acc,
+                              double tau_old, Philox& R, double* xi) {
+  if (prior == 0) {
+    const double phi = R.gamma(a0 + (double)p / alpha) / (b0 + acc);
+    return alpha == 1.0 ? 1.0 / phi : pow(phi, -1.0 / alpha);
+  }
+  *xi = (1.0 + 1.0 / (tau_old * tau_old)) / R.exponential();
+  const double tau2 = fmin(fmax((1.0 / *xi + 0.5 * acc) / R.gamma(0.5 * (double)(p + 1)), 1e-300), 1e300);
+  return sqrt(tau2);
+}
+
+// Local scale of one coefficient b.  Bridge alpha = 1 (gibbs.py:193-214):
+// 1/lam^2 ~ Wald(tau/|b|, 1), the |b|/tau < 1e-10 limit lam = |N(0,1)|
+// floored at 1e-150, 1/lam^2 floored at 1e-300.  Horseshoe: nu ~
+// IG(1, 1 + 1/lam_old^2), lam^2 ~ IG(1, 1/nu + b^2/(2 tau^2)) clamped to
+// [1e-300, 1e300]; *nu receives nu.
+__device__ double local_draw(int prior, double b, double tau, double lam_old, Philox& R, double* nu) {
+  if (prior == 0) {
+    const double ratio = fabs(b) / tau;
+    if (ratio < 1e-10) return fmax(fabs(R.normal()), 1e-150);
+    const double inv_sq = wald1(1.0 / ratio, R);
+    return pow(fmax(inv_sq, 1e-300), -0.5);
+  }
+  *nu = (1.0 + 1.0 / (lam_old * lam_old)) / R.exponential();
+  const double lam2 = fmin(fmax((1.0 / *nu + 0.5 * b * b / (tau * tau)) / R.exponential(), 1e-300), 1e300);
+  return sqrt(lam2);
+}
+
+// Validation kernel (pcgs_scale_draws): mode 0 = count independent global
+// draws from (acc, tau_old) with the scan keys t = 1..count; mode 1 = count
+// independent local draws of coefficient b from lam_old (element keys);
+// mode 2 / 3 = ONE thread iterating the global / local update count times
+// from tau_old / lam_old (the auxiliary-variable Gibbs chain, whose
+// stationary law is the exact conditional of tau given acc / of lam given b).
+__global__ void k_scale_draws(int prior, int mode, long long count, double b_or_acc, double tau, double lam_old,
+                              long long p, double a0, double b0, double alpha, unsigned long long seed,
+                              double* out, double* aux) {
+  if (mode >= 2) {
+    if (blockIdx.x != 0 || threadIdx.x != 0) return;
+    double cur = mode == 2 ? tau : lam_old;
+    for (long long i = 0; i < count; ++i) {
+      double a = 0.0;
+      if (mode == 2) {
+        Philox R(seed, kStreamGlobal ^ (unsigned long long)(i + 1), 0u);
+        cur = global_draw(prior, a0, b0, alpha, p, b_or_acc, cur, R, &a);
+      } else {
+        Philox R(seed, kStreamLocal ^ (unsigned long long)(i + 1), 0u);
+        cur = local_draw(prior, b_or_acc, tau, cur, R, &a);
+      }
+      out[i] = cur;
+      if (aux) aux[i] = a;
+    }
+    return;
+  }
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x) {
+    double a = 0.0, v;
+    if (mode == 0) {
+      Philox R(seed, kStreamGlobal ^ (unsigned long long)(i + 1), 0u);
+      v = global_draw(prior, a0, b0, alpha, p, b_or_acc, tau, R, &a);
+    } else {
+      Philox R(seed, kStreamLocal ^ 1ull, (unsigned)i);
+      v = local_draw(prior, b_or_acc, tau, lam_old, R, &a);
+    }
+    out[i] = v;
+    if (aux) aux[i] = a;
+  }
+}
+
 // Partial-sum lines (one 128-byte line per CTA, kPartStride doubles):
 //   [c*16 + 0]  log-likelihood of X beta (CSR pass)
 //   [c*16 + 1]  log-prior terms of the current draw (k_stats)
@@ -109,21 +184,10 @@ __global__ void __launch_bounds__(32) k_global(pcgs_gibbs_t G, long long pt, int
   for (int c = lane; c < ncta; c += 32) acc += G.part[(long long)c * kPartStride + 2];
   acc = warp_sum(acc);
   if (lane == 0) {
-    const long long p = pt - G.q;
     Philox R(G.seed, kStreamGlobal ^ (unsigned long long)t, 0u);
-    double tau;
-    if (G.prior == 0) {
-      const double rate = G.b0 + acc;
-      const double shape = G.a0 + (double)p / G.alpha;
-      const double phi = R.gamma(shape) / rate;
-      tau = G.alpha == 1.0 ? 1.0 / phi : pow(phi, -1.0 / G.alpha);
-    } else {
-      const double tau_old = G.scal[0];
-      const double xi = (1.0 + 1.0 / (tau_old * tau_old)) / R.exponential();
-      const double tau2 = fmin(fmax((1.0 / xi + 0.5 * acc) / R.gamma(0.5 * (double)(p + 1)), 1e-300), 1e300);
-      G.scal[1] = xi;
-      tau = sqrt(tau2);
-    }
+    double xi = G.scal[1];
+    const double tau = global_draw(G.prior, G.a0, G.b0, G.alpha, pt - G.q, acc, G.scal[0], R, &xi);
+    if (G.prior != 0) G.scal[1] = xi;
     G.scal[0] = tau;
     if (!(tau > 0.0) || !isfinite(tau)) G.results[8 * (t - 1) + 4] = 1;
   }
@@ -155,21 +219,9 @@ __global__ void k_local(pcgs_gibbs_t G, long long pt, int t, int count) {
     double lam = G.lam[k];
     if (!G.fixed_lam) {
       Philox R(G.seed, kStreamLocal ^ (unsigned long long)t, (unsigned)k);
-      const double b = cs * G.beta[j];
-      if (G.prior == 0) {
-        const double ratio = fabs(b) / tau;
-        if (ratio < 1e-10) {
-          lam = fmax(fabs(R.normal()), 1e-150);
-        } else {
-          const double inv_sq = wald1(1.0 / ratio, R);
-          lam = pow(fmax(inv_sq, 1e-300), -0.5);
-        }
-      } else {
-        const double nu = (1.0 + 1.0 / (lam * lam)) / R.exponential();
-        const double lam2 = fmin(fmax((1.0 / nu + 0.5 * b * b / (tau * tau)) / R.exponential(), 1e-300), 1e300);
-        G.nu[k] = nu;
-        lam = sqrt(lam2);
-      }
+      double nu = 0.0;
+      lam = local_draw(G.prior, cs * G.beta[j], tau, lam, R, &nu);
+      if (G.prior != 0) G.nu[k] = nu;
       G.lam[k] = lam;
     }
     if (!(lam > 0.0) || !isfinite(lam)) G.results[8 * (t - 1) + 4] = 1;
@@ -273,6 +325,20 @@ int launch_logit(pcgs_design* d, pcgs_gibbs_t* g, cudaStream_t s) {
 }  // namespace
 
 extern "C" {
+
+int pcgs_scale_draws(int prior, int mode, int64_t count, double b_or_acc, double tau, double lam_old, int64_t p,
+                     double a0, double b0, double alpha, uint64_t seed, double* out, double* aux,
+                     pcgs_stream_t stream) {
+  if ((prior != 0 && prior != 1) || mode < 0 || mode > 3 || count < 0 || (count > 0 && !out))
+    return fail(PCGS_EINVAL, "bad argument");
+  if (prior == 0 && mode % 2 == 1 && alpha != 1.0) return fail(PCGS_EUNSUP, "bridge local draws need alpha = 1");
+  if (count == 0) return PCGS_OK;
+  const int blocks = mode >= 2 ? 1 : (int)std::min<int64_t>((count + 255) / 256, 148 * 8);
+  k_scale_draws<<<blocks, mode >= 2 ? 32 : 256, 0, (cudaStream_t)stream>>>(
+      prior, mode, count, b_or_acc, tau, lam_old, p, a0, b0, alpha, seed, out, aux);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
 
 int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream) {
   if (!d || !g || !g->beta || !g->z || !g->y || !g->part) return fail(PCGS_EINVAL, "null argument");

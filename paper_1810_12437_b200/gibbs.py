@@ -520,3 +520,23 @@ def gibbs_run_concurrent(X, y, cfg, n_iter, seeds, concurrent=4, burn_in=0, thin
     for k in sorted(busy):
         finish(k)
     return outs
+
+
+def scale_draws(prior, mode, count, b_or_acc, tau=1.0, lam_old=1.0, p=1, a0=1.0, b0=1.0, alpha=1.0,
+                seed=0, device=None):
+    """Draws of the scan's scale updates on the device (pcgs_scale_draws):
+    the same device functions the scan kernels use, exposed for validation
+    against their analytic conditionals (test_gibbs.py:114-140 style).
+    `prior` is "bridge" or "horseshoe"; `mode` 0 = independent global draws
+    (returns tau, xi), 1 = independent local draws (lam, nu), 2 / 3 = the
+    single-thread auxiliary chain of the global / local update (tau or lam
+    per step, and the auxiliary)."""
+    torch = _lib.torch()
+    dev = _lib.cuda_device(device)
+    out = torch.empty(max(int(count), 1), dtype=torch.float64, device=dev)
+    aux = torch.empty_like(out)
+    _lib.check(_lib.lib().pcgs_scale_draws(
+        0 if prior == "bridge" else 1, int(mode), int(count), float(b_or_acc), float(tau),
+        float(lam_old), int(p), float(a0), float(b0), float(alpha), int(seed) & (2 ** 64 - 1),
+        _lib.ptr(out), _lib.ptr(aux), _lib.stream_ptr(dev)))
+    return out[:count].cpu().numpy(), aux[:count].cpu().numpy()

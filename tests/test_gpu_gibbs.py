@@ -1,25 +1,30 @@
 """Device Gibbs chains vs the oracle: posterior moments within Monte Carlo
-error (BASELINE north star), the reference's abort / pinning / thinning
-semantics (test_gibbs.py:228-345), and the horseshoe conditionals."""
+error (BASELINE north star) judged as the reference judges its own chains --
+ESS-adjusted standardized differences plus a KS test of the z-scores against
+N(0, 1) at p >= 0.01 (test_acceptance.py:417-436, diagnostics.py:274-303) --
+the device log density against the reference formula (gibbs.py:217-241),
+and the reference's abort / pinning / thinning semantics
+(test_gibbs.py:228-345)."""
 import numpy as np
 import pytest
 from scipy import stats
 
-from paper_1810_12437_b200 import gibbs, synth
+from paper_1810_12437_b200 import diagnostics, gibbs, synth
 from oracle import port
 
 pytestmark = pytest.mark.gpu
 
 
-def batch_se(x, nb=10):
-    n = (len(x) // nb) * nb
-    return x[:n].reshape(nb, -1).mean(1).std(ddof=1) / np.sqrt(nb)
-
-
-def standardized_differences(a, b):
-    se = np.sqrt(np.array([batch_se(a[:, j]) ** 2 + batch_se(b[:, j]) ** 2 for j in range(a.shape[1])]))
-    keep = se > 1e-12
-    return ((a.mean(0) - b.mean(0))[keep]) / se[keep]
+def chains_agree(a, b, label):
+    """Reference acceptance rule (test_acceptance.py:429-433) on the first and
+    second moments: KS of the non-excluded ESS-adjusted z-scores vs N(0,1)."""
+    for name, da, db in (("mean", a, b), ("second moment", a ** 2, b ** 2)):
+        t = diagnostics.standardized_difference_test(da, db)
+        kept = t.z_scores[~t.excluded]
+        assert kept.size >= 0.8 * da.shape[1], (label, name, kept.size)
+        pv = stats.kstest(kept, "norm").pvalue
+        print(f"{label} {name}: {kept.size} z-scores, KS p = {pv:.3f}, max |z| = {np.abs(kept).max():.2f}")
+        assert pv >= 0.01, (label, name, pv)
 
 
 @pytest.fixture(scope="module")
@@ -29,12 +34,12 @@ def small():
     return d, y, truth
 
 
-@pytest.mark.parametrize("prior", ["bridge", "horseshoe"])
-def test_posterior_moments_match_oracle(small, prior):
+@pytest.mark.parametrize("prior,n_iter", [("bridge", 4000), ("horseshoe", 8000)])
+def test_posterior_moments_match_oracle(small, prior, n_iter):
     d, y, _ = small
     X = d.matrix()
     Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
-    n_iter, burn = 4000, 500
+    burn = 500
     if prior == "bridge":
         cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
         ref = port.gibbs_bridge(Xo, y, n_iter, seed=7, burn_in=burn, unshrunk_sd=(np.inf,))
@@ -42,11 +47,58 @@ def test_posterior_moments_match_oracle(small, prior):
         cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
         ref = port.gibbs_horseshoe(Xo, y, n_iter, seed=7, burn_in=burn, unshrunk_sd=(np.inf,))
     out = gibbs.gibbs_run(X, y, cfg, n_iter, burn_in=burn, seed=8)
-    for a, b in ((out.draws, ref.draws), (out.draws ** 2, ref.draws ** 2)):
-        z = standardized_differences(a, b)
-        assert np.mean(np.abs(z) > 4) < 0.03
-        if prior == "bridge":  # the horseshoe mixes too slowly for a KS test on 4k draws
-            assert stats.kstest(np.clip(z, -6, 6), "norm").pvalue > 1e-3
+    chains_agree(out.draws, ref.draws, prior)
+
+
+def test_config1_horseshoe_chain_matches_oracle():
+    """BASELINE config 1 (n=2,000, p=500, rates logU[1e-3, 0.2], 10 signals,
+    horseshoe, PCG rtol 1e-6): device vs oracle chains by the reference's
+    paired-chain rule.  The BASELINE run is 200 scans; the comparison needs
+    more draws for ESS, so both chains run 2,200 scans (200 burn-in)."""
+    d = synth.config_design(1, seed=0)
+    y, _ = synth.simulate_outcomes(d, seed=0, n_signal=10)
+    X = d.matrix()
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
+    out200 = gibbs.gibbs_run(X, y, cfg, 200, seed=3)
+    assert out200.draws.shape == (200, d.p + 1) and np.all(np.isfinite(out200.logdensity_trace))
+    out = gibbs.gibbs_run(X, y, cfg, 2200, burn_in=200, seed=3)
+    ref = port.gibbs_horseshoe(Xo, y, 2200, seed=4, burn_in=200, unshrunk_sd=(np.inf,))
+    chains_agree(out.draws, ref.draws, "config 1 horseshoe")
+
+
+def test_bridge_log_density_equals_reference_formula(small):
+    """Every scan's device log density equals gibbs.py:217-241 evaluated (by the
+    pinned port) at that scan's draw and tau, to 1e-10 relative."""
+    d, y, _ = small
+    X = d.matrix()
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    for cfg in (gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,)),
+                gibbs.BridgeConfig(global_shape=1.5, global_rate=0.7, unshrunk_prior_sd=(4.0,))):
+        out = gibbs.gibbs_run(X, y, cfg, 40, seed=11)
+        for t in range(40):
+            beta, tau = out.draws[t], out.tau_draws[t]
+            ref = port.bridge_log_density(beta, tau, port.matvec(Xo, beta), y, 1, cfg.alpha, cfg.global_shape,
+                                          cfg.global_rate, cfg.unshrunk_prior_sd)
+            assert out.logdensity_trace[t] == pytest.approx(ref, rel=1e-10), t
+
+
+def test_horseshoe_log_density_equals_port_formula(small):
+    """The horseshoe log density (port.horseshoe_log_density) of
+    scan t, with the lambda of scan t (the final state of a t-scan run; runs
+    are deterministic prefixes of one chain), to 1e-10 relative."""
+    d, y, _ = small
+    X = d.matrix()
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    for sd in ((np.inf,), (3.0,)):
+        cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=sd)
+        full = gibbs.gibbs_run(X, y, cfg, 6, seed=12)
+        for t in (1, 2, 4, 6):
+            o = gibbs.gibbs_run(X, y, cfg, t, seed=12)
+            st = o.final_state
+            np.testing.assert_array_equal(o.logdensity_trace, full.logdensity_trace[:t])
+            ref = port.horseshoe_log_density(st.beta, st.tau, st.lam, port.matvec(Xo, st.beta), y, 1, sd)
+            assert o.logdensity_trace[-1] == pytest.approx(ref, rel=1e-10), t
 
 
 def test_pinned_scales_give_exact_gaussian(small):
@@ -229,10 +281,7 @@ def test_unshrunk_block_of_dummies_matches_oracle():
     Xo = port.Csr(X.n_rows, X.n_cols, X.row_ptr, X.col_idx, X.values)
     ref = port.gibbs_bridge(Xo, y, 4000, seed=7, burn_in=500, unshrunk_sd=sds)
     assert out.n_unshrunk == 3 and out.unshrunk_sd().shape == (3,)
-    for a, b in ((out.draws, ref.draws), (out.draws ** 2, ref.draws ** 2)):
-        z = standardized_differences(a, b)
-        assert np.mean(np.abs(z) > 4) < 0.03
-        assert stats.kstest(np.clip(z, -6, 6), "norm").pvalue > 1e-3
+    chains_agree(out.draws, ref.draws, "q=3 dummies")
 
 
 def test_concurrent_chains_on_a_wide_design_keep_their_state_apart():

@@ -41,20 +41,18 @@ def test_free_chain_moments_match_unsharded(small):
     d, y, _ = small
     X = d.matrix()
     cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
-    n_iter, burn = 1500, 300
-    ref = gibbs.gibbs_run(X, y, cfg, n_iter, burn_in=burn, seed=9)
+    n_iter, burn = 4000, 500
+    ref = gibbs.gibbs_run(X, y, cfg, n_iter, burn_in=burn, seed=10)
     out = parallel.row_split_gibbs_run(X, y, cfg, n_iter, burn_in=burn, seed=9, shards=3)
     assert out.draws.shape == ref.draws.shape
     assert np.all(np.isfinite(out.draws)) and out.final_state.omega.shape == (d.n,)
-
-    def batch_se(x, nb=10):
-        n = (len(x) // nb) * nb
-        return x[:n].reshape(nb, -1).mean(1).std(ddof=1) / np.sqrt(nb)
-
-    se = np.sqrt([batch_se(ref.draws[:, j]) ** 2 + batch_se(out.draws[:, j]) ** 2 for j in range(d.p + 1)])
-    keep = se > 1e-12
-    z = (out.draws.mean(0) - ref.draws.mean(0))[keep] / se[keep]
-    assert np.mean(np.abs(z) > 4) < 0.03
+    from scipy import stats
+    from paper_1810_12437_b200 import diagnostics
+    for a, b in ((out.draws, ref.draws), (out.draws ** 2, ref.draws ** 2)):
+        t = diagnostics.standardized_difference_test(a, b)
+        kept = t.z_scores[~t.excluded]
+        assert kept.size >= 0.8 * a.shape[1]
+        assert stats.kstest(kept, "norm").pvalue >= 0.01
 
 
 def test_pinned_scales_exact_gaussian(small):
