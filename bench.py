@@ -48,7 +48,11 @@ def parse():
     ap.add_argument("--prior", default="horseshoe", choices=["horseshoe", "bridge"])
     ap.add_argument("--cpu-cg-cap", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--record", action="store_true", help="write bench_workload.json")
+    ap.add_argument("--record", action="store_true",
+                    help="write gpurun_out/bench_workload.json (the 1,000-scan CG trace of the chain)")
+    ap.add_argument("--no-rowsplit", action="store_true", help="N > 1: skip the config-5 row-split extra")
+    ap.add_argument("--no-full-run", action="store_true",
+                    help="skip extra.full_run (BASELINE config 3's whole 1,000-scan chain)")
     ap.add_argument("--workload", default="config3", choices=["config3", "config4", "config5"],
                     help="config4: 8 independent chains per GPU side by side (weak scaling); "
                          "config5: the row-split run (rows of X over the N ranks, strong scaling)")
@@ -190,13 +194,16 @@ def cpu_baseline(d, y, cg_iters, steps, cap):
             "wall_s": wall, "value": len(est) / float(np.sum(est))}
 
 
-def load_cg_iters(steps):
-    try:
-        w = json.loads(WORKLOAD_FILE.read_text())
-        it = w["cg_iters_timed"]
-        return it if len(it) else [150]
-    except Exception:
-        return [150]
+def load_cg_iters(warmup, steps):
+    """CG iterations of scans W+1..W+K of the deterministic device chain
+    (config 3, seed 0, full grid), from the recorded 1,000-scan trace
+    (bench_workload.json, written by `bench.py --record`): the reference arm
+    extrapolates its bounded scans to exactly the work of the timed window."""
+    w = json.loads(WORKLOAD_FILE.read_text())
+    full = w["cg_iters_full"]
+    if warmup + steps > len(full):
+        raise SystemExit(f"bench_workload.json holds {len(full)} scans; need {warmup + steps}")
+    return full[warmup:warmup + steps]
 
 
 # ------------------------------------------------------------------ reference arm
@@ -205,7 +212,7 @@ def run_reference(args):
     if rank != 0:
         return
     d, y, _ = workload(args.prior)
-    iters = load_cg_iters(args.steps)
+    iters = load_cg_iters(args.warmup, args.steps)
     # N > 1: our arm runs one chain per GPU, so the reference runs one chain per
     # host core, up to N, side by side (the reference path itself is single-threaded)
     procs = max(1, min(world, os.cpu_count() or 1))
@@ -222,8 +229,9 @@ def run_reference(args):
         r = cpu_baseline(d, y, iters, args.steps, args.cpu_cg_cap)
         value = r["value"]
     sample = (f"{args.steps} horseshoe scans of the CPU restatement (oracle/port.py), CG capped at "
-              f"{args.cpu_cg_cap} Phi-applications per scan and extrapolated to the device chain's "
-              f"per-scan CG counts (mean {np.mean(iters):.1f}): fixed {r['fixed_s']:.2f} s + "
+              f"{args.cpu_cg_cap} Phi-applications per scan and extrapolated to the CG counts of scans "
+              f"{args.warmup + 1}-{args.warmup + args.steps} of the device chain this arm is compared "
+              f"with (bench_workload.json; mean {np.mean(iters):.1f}): fixed {r['fixed_s']:.2f} s + "
               f"{r['apply_s']*1e3:.0f} ms per apply"
               + (f"; {procs} chains side by side, one per core (value = their sum)" if procs > 1 else ""))
     line = {
@@ -263,6 +271,7 @@ def run_ours(args):
         chain.scan(t)
     torch.cuda.synchronize(dev)
     chain.check(1, W)
+    st = chain.state_snapshot()          # the e2e call below continues from here
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -330,37 +339,74 @@ def run_ours(args):
                         "int32 bytes; store_gbs is the HBM rate of the bytes actually read"}
 
     # ---- end to end through the public API, host buffers ----
-    # The timed chain replayed through gibbs_run from numpy inputs (same seed
-    # and start, hence the same draws and CG counts): one call for the W
-    # warm-up scans alone and one for W + K.  Each call does the H2D of y,
-    # kappa and the initial state, its scans, and the D2H of the stored draws
-    # and traces; the difference of the two wall times is the end-to-end cost
-    # of exactly the K timed scans (incl. the D2H of their K draws).
-    def api_call(n_iter):
+    # ONE gibbs_run call of K scans from numpy inputs, continuing from the
+    # warmed-up state of the timed chain (init_state, a host ShrinkageState):
+    # the call uploads y, kappa = y - 1/2 and the state (H2D), runs the K
+    # scans with a device->host read of every scan's result row (on_progress
+    # synchronises and checks each scan, as gibbs_run's progress hook does),
+    # and copies the K stored draws, tau draws and traces back (D2H).  The
+    # wall time of the whole call is the e2e window.  The running statistics
+    # restart in the call (init_state carries no chain statistics, as in the
+    # reference), so the first scan starts CG from zero: its CG counts are
+    # reported next to the timed chain's.
+    yh = np.ascontiguousarray(y, dtype=np.float64)
+
+    def api_call():
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        out = gibbs.gibbs_run(X, np.asarray(y), cfg, n_iter, burn_in=W, seed=SEED + rank,
-                              cg_config=gibbs.CGConfig(rtol=RTOL), device=dev)
+        out = gibbs.gibbs_run(X, yh, cfg, K, seed=SEED + rank + 1, init_state=st,
+                              cg_config=gibbs.CGConfig(rtol=RTOL), device=dev,
+                              on_progress=lambda t, n: None)
         torch.cuda.synchronize(dev)
         return time.perf_counter() - t0, out
 
-    api_call(W)                       # first-call allocations out of the way
-    t_w, _ = api_call(W)
-    t_wk, out_e2e = api_call(W + K)
-    assert out_e2e.cg_iteration_counts[W:].tolist() == cg_timed, "e2e replay diverged from the timed chain"
-    e2e_t = torch.tensor([t_wk - t_w], device=dev, dtype=torch.float64)
+    api_call()                        # first-call allocations out of the way
+    t_e2e, out_e2e = api_call()
+    e2e_t = torch.tensor([t_e2e], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_val = world * K / float(e2e_t.item())
     pt = d.p + 1
-    h2d = (2 * n + pt + n + 2 * d.p) * 8 / (W + K)   # y, kappa, initial beta/omega/lam/nu per call
-    d2h = (pt + 1) * 8 + (1 + 4) * 8                # one stored draw + tau; log density + results
+    h2d = (2 * n + pt + n + 2 * d.p) * 8 / K        # y, kappa, state beta/omega/lam/nu per call
+    d2h = 8 * 4 + (pt + 1 + 1) * 8                  # per scan: result row; draw, tau, log density
 
-    if args.record and rank == 0:
-        (ROOT / "gpurun_out").mkdir(exist_ok=True)
-        rec = {"config": CONFIG, "prior": args.prior, "seed": SEED, "warmup": W, "steps": K,
-               "cg_iters_timed": cg_timed, "cg_iters_e2e": out_e2e.cg_iteration_counts.tolist()}
-        (ROOT / "gpurun_out" / "bench_workload.json").write_text(json.dumps(rec))
+    # ---- BASELINE config 3 as specified: the whole 1,000-scan chain ----
+    full_run = None
+    if rank == 0 and not args.no_full_run:
+        n_full = 1000
+        fc = gibbs.DeviceChain(X, y, cfg, n_full, burn_in=0, seed=SEED, cg_config=gibbs.CGConfig(rtol=RTOL),
+                               device=dev)
+        torch.cuda.synchronize(dev)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for t in range(1, n_full + 1):
+            fc.scan(t)
+        f1.record()
+        torch.cuda.synchronize(dev)
+        fc.check(1, n_full)
+        full_cg = fc.results.view(-1, 8).cpu().numpy()[:n_full, 0].astype(int)
+        full_ms = f0.elapsed_time(f1)
+        assert full_cg[W:W + K].tolist() == cg_timed, "full run diverged from the timed chain"
+        full_run = {"scans": n_full, "iter_per_s": n_full / (full_ms * 1e-3), "seconds": full_ms * 1e-3,
+                    "cg_iters_mean": float(full_cg.mean()),
+                    "cg_iters_mean_by_100": [float(full_cg[i:i + 100].mean()) for i in range(0, n_full, 100)]}
+        if args.record:
+            (ROOT / "gpurun_out").mkdir(exist_ok=True)
+            rec = {"config": CONFIG, "prior": args.prior, "seed": SEED, "grid": info["grid"],
+                   "cg_iters_full": full_cg.tolist()}
+            (ROOT / "gpurun_out" / "bench_workload.json").write_text(json.dumps(rec))
+        del fc
+
+    # N > 1: the row split of config 5 across the same N GPUs (the sharded
+    # path with a real exchange), measured after the chain-parallel headline
+    rowsplit = None
+    if world > 1 and not args.no_rowsplit:
+        try:
+            rl = rowsplit_line(args, 3, 1)
+            rowsplit = {k: rl[k] for k in ("value", "unit", "ms_per_step", "scaling", "config", "roofline",
+                                           "extra")} if rl else None
+        except Exception as exc:           # recorded, never fatal for the headline line
+            rowsplit = {"error": f"{type(exc).__name__}: {exc}"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -381,13 +427,15 @@ def run_ours(args):
             "roofline": roofline, "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "iter/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "window": f"K/(T[gibbs_run(n_iter={W + K})] - T[gibbs_run(n_iter={W})]) from numpy "
-                              f"inputs: the timed chain replayed (same seed/start, identical CG counts); "
-                              f"whole-call wall times {t_wk * 1e3:.1f} / {t_w * 1e3:.1f} ms"},
-            "gpu_launches": 9 * K,
+                    "window": f"wall time of ONE gibbs_run(n_iter={K}) call from numpy inputs (H2D of y, "
+                              f"kappa and the warmed-up state; a D2H read of every scan's result; D2H of "
+                              f"the draws and traces at the end): {t_e2e * 1e3:.1f} ms",
+                    "cg_iters": out_e2e.cg_iteration_counts.tolist(),
+                    "cg_iters_mean": float(np.mean(out_e2e.cg_iteration_counts))},
+            "gpu_launches": 10 * K,
             "clocks": clocks,
             "extra": {"cg_iters_mean": float(np.mean(cg_timed)), "cg_iters": cg_timed,
-                      "cg_iters_warmup": out_e2e.cg_iteration_counts[:W].tolist(),
+                      "full_run": full_run, "rowsplit_config5": rowsplit,
                       "phi_applies_timed": applies, "pcg_solve_ms": pcg_ms,
                       "store": {k: info[k] for k in ("csr_slabs", "csc_slabs", "index_bytes", "grid")}},
         }
@@ -403,14 +451,25 @@ def run_rowsplit(args):
     Gibbs scan of the one chain; strong scaling (total work fixed)."""
     import torch
     import torch.distributed as dist
-    from paper_1810_12437_b200 import gibbs, parallel, synth
-
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        group = dist.group.WORLD
+    line = rowsplit_line(args, args.steps, args.warmup)
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def rowsplit_line(args, K, W):
+    """Measure the config-5 row-split scan on the initialised world; returns
+    the JSON line (rank 0) or None."""
+    import torch
+    import torch.distributed as dist
+    from paper_1810_12437_b200 import gibbs, parallel, synth
+    rank, world, local = dist_env()
+    group = dist.group.WORLD if world > 1 else None
     dev = torch.device("cuda", local)
     t0 = time.time()
     d = synth.config_design(5, seed=SEED)
@@ -419,7 +478,6 @@ def run_rowsplit(args):
         gibbs.BridgeConfig(unshrunk_prior_sd=(math.inf,))
     X = d.matrix()
     gen_s = time.time() - t0
-    K, W = args.steps, args.warmup
     rp, _, icpt = X.pattern()
     parts = parallel.row_partition(rp, world, intercept=icpt)
     Chain = parallel._row_split_chain_class()
@@ -452,6 +510,7 @@ def run_rowsplit(args):
     ms_max = float(ms_t.item())
     canon = 8 * d.nnz + 8 * (d.n + 1) + 8 * (d.p + 1) + 8 * (3 * d.n + 4 * d.p)
     pk_, pk_src = peaks()
+    xbytes = 8 * (d.p + 1) * world                      # per rank and PCG iteration: one p-vector per peer
     if rank == 0:
         us_iter = ms_max * 1e3 / max(applies, 1)
         line = {
@@ -473,11 +532,14 @@ def run_rowsplit(args):
             "gpu_launches": None,
             "clocks": clk.summary(),
             "extra": {"cg_iters": cg_timed, "us_per_pcg_iteration_incl_scan": us_iter,
-                      "generate_s": gen_s, "shard_build_s": build_s},
+                      "generate_s": gen_s, "shard_build_s": build_s,
+                      "exchange_bytes_per_iteration_per_rank": xbytes if world > 1 else 0,
+                      "exchange": ("fused in k_pcg_rs: X'w partials read from every peer's exchange region "
+                                   "over NVLink (IPC-mapped), release/acquire epoch flags" if world > 1
+                                   else "none (one rank)")},
         }
-        print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+        return line
+    return None
 
 
 def run_config4(args):

@@ -234,6 +234,16 @@ int pcgs_rs_pcg(pcgs_rs_t rs, const double* const* omegas_h, const double* prior
                 const double* minv, const double* scale, const double* b, double* x,
                 int32_t max_iter, double rtol, double* trace, double* alphas,
                 double* betas, int32_t* result, pcgs_stream_t stream);
+/* Exchange protocol of a context whose ranks are all hosted by one grid
+ * (n_local == nranks), set before the first solve: 0 = the grid barrier
+ * (default); 1 = flag validation mode, in which every hosted group behaves
+ * as an independent rank -- barriers over its own CTAs only, and at every
+ * exchange the cross-GPU protocol of n_local = 1 contexts (st.release.sys of
+ * the epoch into every peer's inbox, ld.acquire.sys spins, volatile peer
+ * loads, the scalar exchange by flags).  The grid is one cooperative launch,
+ * so the groups are co-resident and the protocol runs on one GPU; results
+ * are bitwise those of mode 0. */
+int pcgs_rs_set_exchange(pcgs_rs_t rs, int mode);
 int pcgs_rs_destroy(pcgs_rs_t rs);
 
 /* omega[i] ~ PG(1, z[i]) (pg_draw_batch, polya_gamma.py:39-84), Philox keyed

@@ -82,6 +82,7 @@ SIGNATURES = {
     "pcgs_rs_open_peer": (ctypes.c_int, [_P, ctypes.c_int, _P]),
     "pcgs_rs_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
     "pcgs_rs_destroy": (ctypes.c_int, [_P]),
+    "pcgs_rs_set_exchange": (ctypes.c_int, [_P, ctypes.c_int]),
     "pcgs_rs_gibbs_init": (ctypes.c_int, [_P, _P, _P, _P]),
     "pcgs_rs_gibbs_scan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P]),
     "pcgs_batch_slab_max": (ctypes.c_int, [ctypes.c_int]),

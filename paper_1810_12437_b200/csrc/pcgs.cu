@@ -5,6 +5,7 @@
 //   k_csr_*      X v over column slabs         (sparse.py:178-193)
 //   k_csc_*      X' w over row slabs           (sparse.py:195-203)
 //   k_assemble   per-column piece sums + diagonal terms
+//   k_rhs_u      u = kappa + sqrt(omega) eta per row (RHS input of one CSC pass)
 //   k_pcg        the whole PCG solve, one persistent cooperative kernel
 //                (cg.py:105-192, operator sampler.py:53-58)
 //   k_pg         Polya-Gamma PG(1, z) draws    (polya_gamma.py:39-147)
@@ -72,11 +73,10 @@ __global__ void k_rows_combine(DesignDev D, const double* part, const double* v,
   }
 }
 
-template <class Fill>
-__global__ void __launch_bounds__(kThreads, 1) k_csc(DesignDev D, Fill f, double* pieces) {
-  extern __shared__ __align__(128) double sv[];
-  EpiStore e{pieces};
-  run_pass(D.csc, sv, f, e);
+// u_i = kappa_i + sqrt(omega_i) eta_i for every row (the RHS pass's input)
+__global__ void k_rhs_u(FillRhs f, long long n, double* u) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    u[i] = f((int)i);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_csc_vec(DesignDev D, const double* w, double* pieces) {
@@ -662,7 +662,7 @@ const char* pcgs_last_error(void) { return g_err.c_str(); }
 static int set_smem_attrs() {
   int rc;
   if ((rc = raise_smem_limit(k_csr_matvec)) || (rc = raise_smem_limit(k_csr_phi)) ||
-      (rc = raise_smem_limit(k_csc_vec)) || (rc = raise_smem_limit(k_csc<FillRhs>)) ||
+      (rc = raise_smem_limit(k_csc_vec)) ||
       (rc = raise_smem_limit(k_pcg)))
     return rc;
   return PCGS_OK;
@@ -940,9 +940,13 @@ int pcgs_rhs(pcgs_design_t d, const double* kappa, const double* omega, const do
   cudaStream_t s = (cudaStream_t)stream;
   Scratch S(s);
   double* pieces = S.get<double>(D.csc.nseg);
-  if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  double* u = S.get<double>(D.n + 2);
+  if (!pieces || !u) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  // u = kappa + sqrt(omega) eta once per row (Philox once per row), then the
+  // CSC pass TMA-fills its row slabs from u like any X' w
   FillRhs f{kappa, omega, eta, seed, kStreamEta ^ stream_id, 0};
-  k_csc<FillRhs><<<D.G, kThreads, smem_bytes(D), s>>>(D, f, pieces);
+  k_rhs_u<<<(int)std::min<long long>((D.n + 255) / 256, 148 * 8), 256, 0, s>>>(f, D.n, u);
+  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, u, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, delta, seed,
                                                        kStreamDelta ^ stream_id, 2, b, linear);
   CUDA_TRY(cudaGetLastError());

@@ -105,11 +105,19 @@ struct RsArgs {
   const double* kappa[kRsMaxLocal];
   unsigned long long seed, stream_id;
   double* b_out;                 // replicated b (reference layout), written by the lead group
+  // Flag-exchange validation mode (pcgs_rs_set_exchange): every hosted group
+  // is an independent rank -- group barriers instead of grid barriers, and the
+  // cross-GPU flag protocol (release/acquire inbox epochs, volatile peer
+  // loads) at every exchange.  One cooperative grid keeps all groups
+  // co-resident, so the protocol runs on one GPU without ranks that wait on
+  // separate launches.
+  int flags;
+  unsigned long long* gbar;      // per hosted group: monotonic arrival counter (one 128 B line each)
 };
 
 struct RsSumArgs {               // sum of a per-CTA partial over every rank's CTAs
   const double* part[kRsMaxLocal];
-  int ncta, n_local, nranks, my_rank;
+  int ncta, n_local, nranks, my_rank, flags;
   const RsPeer* peers;
   unsigned long long* epoch;
   double* out;
@@ -117,17 +125,41 @@ struct RsSumArgs {               // sum of a per-CTA partial over every rank's C
 
 __device__ __forceinline__ double ld_peer(const double* p, bool remote) { return remote ? __ldcv(p) : __ldcg(p); }
 
+// Barrier over the CTAs of one rank: the grid barrier, or in the flag
+// validation mode a barrier over the rank's own group of Gr CTAs (thread 0 of
+// every CTA arrives on a monotonic counter with a release fence and spins
+// with acquire loads until the group's arrivals reach the next multiple of
+// Gr; counters persist across launches, every launch adding whole rounds).
+__device__ __forceinline__ void group_barrier(unsigned long long* ctr, int n) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long old = atomicAdd(ctr, 1ull);
+    const unsigned long long target = (old / (unsigned long long)n + 1ull) * (unsigned long long)n;
+    unsigned long long v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void rank_sync(const RsArgs& A, int gi) {
+  if (A.flags) group_barrier(A.gbar + 16 * gi, A.Gr);
+  else cg::this_grid().sync();
+}
+
 // Exchange barrier: every local CTA has published its pieces and partials;
-// then (ranks on other GPUs only) one thread signals every remote inbox and
-// waits for theirs.
-__device__ void rs_exchange(const RsArgs& A, int my_rank, unsigned long long e) {
-  if (A.n_local == A.nranks) {
+// then (ranks on other GPUs, or every group in the flag validation mode) one
+// thread per peer signals the peer's inbox and waits for the peer's signal.
+__device__ void rs_exchange(const RsArgs& A, int gi, int cta, int my_rank, unsigned long long e) {
+  if (A.n_local == A.nranks && !A.flags) {
     cg::this_grid().sync();
     return;
   }
   __threadfence_system();
-  cg::this_grid().sync();
-  if (blockIdx.x == 0 && threadIdx.x < A.nranks && (int)threadIdx.x != my_rank) {
+  rank_sync(A, gi);
+  if (cta == 0 && threadIdx.x < A.nranks && (int)threadIdx.x != my_rank) {
     const RsPeer& q = A.peers[threadIdx.x];
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(q.inbox + my_rank), "l"(e) : "memory");
     const RsPeer& me = A.peers[my_rank];
@@ -136,7 +168,7 @@ __device__ void rs_exchange(const RsArgs& A, int my_rank, unsigned long long e) 
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(me.inbox + threadIdx.x) : "memory");
     } while (v < e);
   }
-  cg::this_grid().sync();
+  rank_sync(A, gi);
 }
 
 // Local column sums: g[j] = sum of this shard's CSC pieces of column j
@@ -302,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
     st_fail = -1;
     st_applies = 0;
   }
-  cg::this_grid().sync();
+  rank_sync(A, gi);
 
   // ---------------- R: the randomised right-hand side (one exchange) ----------------
   int e_off = 0;
@@ -312,11 +344,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       EpiStore e{G.pieces};
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
-    cg::this_grid().sync();
+    rank_sync(A, gi);
     if (!rs_assemble_flat(G, j0, chunk, G.gsum + G.gstride, sv, A.smem_doubles))
       rs_assemble(G, j0, chunk, G.gsum + G.gstride);  // parity 1: iteration 0 writes parity 0
     if (A.nranks == 1) __syncthreads();
-    else rs_exchange(A, G.rank, st_epoch + 1ull);
+    else rs_exchange(A, gi, cta, G.rank, st_epoch + 1ull);
     for (int t = tid; t < chunk; t += kThreads) {
       const long long j = j0 + t;
       if (j >= pt) break;
@@ -365,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
         od[t] = dn;
         if (j0 + t < pt) G.dvg[par * dvs + j0 + t] = dn;
       }
-      cg::this_grid().sync();
+      rank_sync(A, gi);
     }
 
     // ---------------- A: CSR pass over this rank's rows ----------------
@@ -381,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       acc = e.acc;
     }
     if (G.D.csr.nslab > 1) {
-      cg::this_grid().sync();
+      rank_sync(A, gi);
       const long long n = G.D.n;
       const double v0 = bc[2];
       for (long long i = (long long)cta * kThreads + tid; i < n; i += (long long)Gr * kThreads) {
@@ -402,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
         G.part[par * kPartStride * Gr + cta * kPartStride + 3] = dterm;  // local
       }
     }
-    cg::this_grid().sync();
+    rank_sync(A, gi);
 
     // ---------------- B: CSC pass, local column sums g_r = X_r' w_r ----------------
     {
@@ -410,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       EpiStore e{G.pieces};
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
-    cg::this_grid().sync();
+    rank_sync(A, gi);
     const bool solo = A.nranks == 1;  // one rank: each CTA reads only its own columns' sums
     if (!solo && cta == 0 && tid < 32) {  // this rank's z'Omega z total (slot 4 of line 0), exchanged
       const double t = warp_sum(lane_partials(G.part + par * kPartStride * Gr, Gr, lane));
@@ -420,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       rs_assemble(G, j0, chunk, G.gsum + par * G.gstride);
     if (tid == 0) ++st_applies;
     if (solo) __syncthreads();
-    else rs_exchange(A, G.rank, st_epoch + (unsigned long long)(e_off + a) + 1ull);
+    else rs_exchange(A, gi, cta, G.rank, st_epoch + (unsigned long long)(e_off + a) + 1ull);
 
     // ---------------- C: assemble owned columns over all ranks, step ----------------
     double alpha = 0.0;
@@ -487,7 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
       G.part[par * kPartStride * Gr + cta * kPartStride + 1] = t_rms;
       G.part[par * kPartStride * Gr + cta * kPartStride + 2] = t_rz;
     }
-    cg::this_grid().sync();
+    rank_sync(A, gi);
   }
 
   __syncthreads();
@@ -511,6 +543,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
 // at a flag exchange (one epoch).
 __global__ void __launch_bounds__(32) k_rs_sum(RsSumArgs A) {
   const int lane = threadIdx.x;
+  if (A.flags) {  // validation mode: block r acts as rank r (cooperative launch, one block per rank)
+    const int r = blockIdx.x;
+    const unsigned long long e = *A.epoch + 1ull;  // read before this rank signals anyone
+    double x = 0.0;
+    for (int c = lane; c < A.ncta; c += 32) x += __ldcg(A.part[r] + (long long)c * kPartStride);
+    const double v = warp_sum(x);
+    const RsPeer& me = A.peers[r];
+    if (lane == 0) *me.scal = v;
+    __threadfence_system();
+    __syncwarp();
+    for (int q = lane; q < A.nranks; q += 32) {
+      if (q == r) continue;
+      asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(A.peers[q].inbox + r), "l"(e) : "memory");
+      unsigned long long f;
+      do {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(me.inbox + q) : "memory");
+      } while (f < e);
+    }
+    __syncwarp();
+    if (lane == 0 && r == 0) {  // every peer has signalled, so every block has read the epoch
+      double t = 0.0;
+      for (int q = 0; q < A.nranks; ++q) t += q == r ? v : ld_peer(A.peers[q].scal, true);
+      *A.out = t;
+      *A.epoch = e;
+    }
+    return;
+  }
   double v[kRsMaxLocal];
   for (int l = 0; l < A.n_local; ++l) {
     double x = 0.0;
@@ -568,6 +627,8 @@ struct pcgs_rs {
   std::vector<double*> pieces;
   bool ready = false;
   bool own_in_smem = true;
+  int flags = 0;                           // flag-exchange validation mode (one grid)
+  unsigned long long* gbar = nullptr;      // group barrier counters (flag mode)
 };
 
 namespace {
@@ -657,6 +718,10 @@ int pcgs_rs_create(const pcgs_design_t* designs, int n_local, int rank0, int nra
     }
     R->own.push_back(b);
   }
+  if ((rc = rs_alloc(R, sizeof(unsigned long long) * 16 * n_local, &p))) return bail(rc);
+  R->gbar = (unsigned long long*)p;
+  if (cudaMemset(R->gbar, 0, sizeof(unsigned long long) * 16 * n_local) != cudaSuccess)
+    return bail(fail(PCGS_ECUDA, "memset"));
   if ((rc = rs_alloc(R, sizeof(RsGroup) * n_local, &p))) return bail(rc);
   R->groups_dev = (RsGroup*)p;
   if ((rc = rs_alloc(R, sizeof(RsPeer) * nranks, &p))) return bail(rc);
@@ -708,7 +773,7 @@ static int rs_finalize(pcgs_rs* R) {
     P.gstride = (long long)L.gstride;
     P.n = h.n;
     P.row0 = q == 0 ? 0 : R->peers[q - 1].row0 + R->peers[q - 1].n;
-    P.remote = R->opened[q];
+    P.remote = R->opened[q] || R->flags;
     R->peers[q] = P;
   }
   CUDA_TRY(cudaMemcpy(R->peers_dev, R->peers.data(), sizeof(RsPeer) * R->nranks, cudaMemcpyHostToDevice));
@@ -740,6 +805,15 @@ int pcgs_rs_pcg(pcgs_rs_t R, const double* const* omegas_h, const double* prior_
   RsSolve S{omegas_h, nullptr, 0, 0, nullptr, prior_diag, minv, scale, b, x, max_iter, rtol, trace, alphas, betas,
             result};
   return rs_solve(R, S, (cudaStream_t)stream);
+}
+
+int pcgs_rs_set_exchange(pcgs_rs_t R, int mode) {
+  if (!R || (mode != 0 && mode != 1)) return fail(PCGS_EINVAL, "bad argument");
+  if (R->ready) return fail(PCGS_EINVAL, "row split: set the exchange mode before the first solve");
+  if (mode == 1 && R->n_local != R->nranks)
+    return fail(PCGS_EINVAL, "row split: the flag validation mode hosts every rank in one grid");
+  R->flags = mode;
+  return PCGS_OK;
 }
 
 int pcgs_rs_destroy(pcgs_rs_t R) {
@@ -790,6 +864,8 @@ int rs_solve(pcgs_rs_t R, const RsSolve& S, cudaStream_t s) {
   A.seed = S.seed;
   A.stream_id = S.stream_id;
   A.b_out = S.b_out;
+  A.flags = R->flags;
+  A.gbar = R->gbar;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(R->Gr * R->n_local);
   cfg.blockDim = dim3(kThreads);
@@ -816,6 +892,20 @@ int rs_sum(pcgs_rs_t R, const double* const* parts, double* out, cudaStream_t s)
   A.peers = R->peers_dev;
   A.epoch = R->epoch;
   A.out = out;
+  A.flags = R->flags;
+  if (R->flags) {  // one block per emulated rank, co-resident (they wait on one another)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(R->nranks);
+    cfg.blockDim = dim3(32);
+    cfg.stream = s;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeCooperative;
+    attr.val.cooperative = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, k_rs_sum, A));
+    return PCGS_OK;
+  }
   k_rs_sum<<<1, 32, 0, s>>>(A);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;

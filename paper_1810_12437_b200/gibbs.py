@@ -359,19 +359,24 @@ class DeviceChain:
             if r[1] == _lib.PCGS_MAX_ITER and not allow_max_iter:
                 raise GibbsAbortError(t, f"CG used all {r[0]} iterations without converging")
 
+    def state_snapshot(self) -> ShrinkageState:
+        """The current state on the host, in model coordinates (a valid
+        `init_state` for a continuing gibbs_run)."""
+        scal = self.scal.cpu().numpy()
+        beta = self.beta.cpu().numpy()
+        if self.reparam is not None:
+            beta = self.reparam.to_model(beta)
+        return ShrinkageState(beta, self.omega.cpu().numpy(), self.lam.cpu().numpy(), float(scal[0]),
+                              nu=self.nu.cpu().numpy() if self.horseshoe else None,
+                              xi=float(scal[1]) if self.horseshoe else None)
+
     def output(self) -> ChainOutput:
         t = self.n_iter
         res = self.results[: 8 * max(t, 1)].view(-1, 8).cpu().numpy()[:t]
-        scal = self.scal.cpu().numpy()
-        beta = self.beta.cpu().numpy()
         draws = self.draws[: self.stored].cpu().numpy()
         if self.reparam is not None:
-            beta = self.reparam.to_model(beta)
             draws = self.reparam.to_model(draws)
-        state = ShrinkageState(beta, self.omega.cpu().numpy(),
-                               self.lam.cpu().numpy(), float(scal[0]),
-                               nu=self.nu.cpu().numpy() if self.horseshoe else None,
-                               xi=float(scal[1]) if self.horseshoe else None)
+        state = self.state_snapshot()
         m2 = self.m2.cpu().numpy()[: self.q]
         var = m2 / (self.count - 1) if self.count >= 2 else np.full(self.q, np.nan)
         return ChainOutput(

@@ -224,9 +224,15 @@ class RowSplitPCG:
       all-gathered once) and the kernel's exchange barrier is a flag
       handshake over peer memory.
     Bitwise identical results on every rank; no collective per iteration.
+
+    `exchange="flags"` (single process only) runs the cross-GPU protocol
+    between the hosted groups inside the one cooperative grid: each group
+    synchronises only its own CTAs and meets the others through inbox flags
+    and peer loads (pcgs_rs_set_exchange), so the multi-GPU code path runs and
+    is checked on one GPU.
     """
 
-    def __init__(self, shards, device=None, group=None):
+    def __init__(self, shards, device=None, group=None, exchange="grid"):
         t = _lib.torch()
         L = _lib.lib()
         self.device = _lib.cuda_device(device)
@@ -252,6 +258,12 @@ class RowSplitPCG:
         h = ctypes.c_void_p()
         _lib.check(L.pcgs_rs_create(handles, n_local, rank * n_local if real else 0, nranks, ctypes.byref(h)))
         self._h = h
+        if exchange not in ("grid", "flags"):
+            raise ValueError("exchange must be 'grid' or 'flags'")
+        if exchange == "flags":
+            if real:
+                raise ValueError("exchange='flags' is the single-process validation mode")
+            _lib.check(L.pcgs_rs_set_exchange(h, 1))
         if real and world > 1:
             exchange_ipc_handles(L, h, group)
         self.n_local, self.nranks = n_local, nranks
@@ -288,7 +300,8 @@ class RowSplitPCG:
             self._h = None
 
 
-def fused_pcg_solve(op: "ShardedPrecisionOperator", b, M, x0=None, config=None, residual_scale=None):
+def fused_pcg_solve(op: "ShardedPrecisionOperator", b, M, x0=None, config=None, residual_scale=None,
+                    exchange="grid"):
     """pcg_solve (cg.py:105-192) over a row-sharded operator with the fused
     row-split kernel; same report and exceptions as `sharded_pcg_solve`."""
     from .cg import CGConfig, _report_from_device
@@ -296,8 +309,9 @@ def fused_pcg_solve(op: "ShardedPrecisionOperator", b, M, x0=None, config=None, 
     if op.local_apply is not None:
         raise ValueError("the fused row split needs device shards")
     solver = getattr(op, "_rowsplit", None)
-    if solver is None:
-        solver = op._rowsplit = RowSplitPCG(op.shards, device=op.device, group=op.group)
+    if solver is None or getattr(op, "_rowsplit_exchange", "grid") != exchange:
+        solver = op._rowsplit = RowSplitPCG(op.shards, device=op.device, group=op.group, exchange=exchange)
+        op._rowsplit_exchange = exchange
     p = int(np.asarray(b).shape[0]) if not _lib.is_tensor(b) else int(b.shape[0])
     scale = _metric_scale(op, M, residual_scale, p)
     # the prior term is added once by every rank in the column step (replicated)
@@ -326,15 +340,16 @@ def _row_split_chain_class():
         replicated p-state, full-length row vectors of which each hosted rank
         owns its contiguous range."""
 
-        def __init__(self, X, y, cfg, n_iter, parts, hosted, group=None, device=None, **kw):
+        def __init__(self, X, y, cfg, n_iter, parts, hosted, group=None, device=None, exchange="grid", **kw):
             self._parts, self._hosted, self._group = parts, hosted, group
+            self._exchange = exchange
             super().__init__(X, y, cfg, n_iter, device=device, **kw)
 
         def _open_device(self, X, device):
             if X.standardized:
                 raise NotImplementedError("row split: standardised designs are not sharded")
             shards = [local_rows(X, *self._parts[r]) for r in self._hosted]
-            self.rs = RowSplitPCG(shards, device=device, group=self._group)
+            self.rs = RowSplitPCG(shards, device=device, group=self._group, exchange=self._exchange)
             self.store = None
             self.dev = self.rs.device
             self.grid = self.rs.stores[0].describe()["grid"]
@@ -390,7 +405,7 @@ def _row_split_chain_class():
 def row_split_gibbs_run(X, y, cfg, n_iter, shards=None, group=None, burn_in=0, seed=0, thin=1,
                         preconditioner="prior", cg_config=None, init_state=None, gamma_scale=1.0,
                         allow_max_iter=False, fixed_omega=None, fixed_tau=None, fixed_lam=None,
-                        device=None, sync_every=64):
+                        device=None, sync_every=64, exchange="grid"):
     """gibbs_run (gibbs.py:260-379) with the rows of X split over ranks.
 
     With a torch.distributed `group` of W processes (one GPU each) rank r
@@ -399,7 +414,9 @@ def row_split_gibbs_run(X, y, cfg, n_iter, shards=None, group=None, burn_in=0, s
     output as gibbs_run on every rank: replicated state, the draws of omega
     and of the RHS noise keyed by global row (the unsharded chain's keys; only
     summation order differs).  Prior or identity preconditioning; no
-    local_scale_sampler and no standardised designs on this path."""
+    local_scale_sampler and no standardised designs on this path.
+    `exchange="flags"`: single-process validation of the cross-GPU exchange
+    protocol (RowSplitPCG)."""
     from .gibbs import GibbsAbortError, _PRECOND  # noqa: F401
     y = np.asarray(y, dtype=np.float64)
     if y.shape != (X.n_rows,) or not np.all((y == 0.0) | (y == 1.0)):
@@ -420,7 +437,8 @@ def row_split_gibbs_run(X, y, cfg, n_iter, shards=None, group=None, burn_in=0, s
         parts = row_partition(rp, nsh, intercept=icpt)
         hosted = list(range(nsh))
     Chain = _row_split_chain_class()
-    ch = Chain(X, y, cfg, n_iter, parts, hosted, group=group, device=device, burn_in=burn_in, thin=thin,
+    ch = Chain(X, y, cfg, n_iter, parts, hosted, group=group, device=device, exchange=exchange,
+               burn_in=burn_in, thin=thin,
                seed=seed, preconditioner=preconditioner, cg_config=cg_config, init_state=init_state,
                gamma_scale=gamma_scale, fixed_omega=fixed_omega, fixed_tau=fixed_tau, fixed_lam=fixed_lam)
     checked = 0

@@ -17,6 +17,8 @@ the reference's generate_rhs) it records:
                   (z = X d), the formula the device uses;
     - ``fma``     the reference loop with single-rounding x / r / d updates
                   (what fused multiply-adds do);
+    - ``fmaAd``   the reference Phi with (Phi d)_j = colsum_j + D_j d_j
+                  rounded once (what an FMA does with the huge prior term);
   The spread max - min over these is the float64 ordering floor of the
   iteration count that the device gate uses.
 * ``iters_ld``: the same algorithm with every reduction AND update in long
@@ -44,8 +46,8 @@ ROOT = Path(__file__).resolve().parents[2]
 REF = Path("/root/reference/pkg/src")
 OUT = Path(__file__).resolve().parent / "config2_parity.npz"
 SEEDS = [0, 1, 2, 3, 4]
-VARIANTS = ["ref", "split", "perm", "cr", "dad", "fma", "ld", "tight"]
-GATE_VARIANTS = ["ref", "split", "perm", "cr", "dad", "fma"]
+VARIANTS = ["ref", "split", "perm", "cr", "dad", "fma", "fmaAd", "ld", "tight"]
+GATE_VARIANTS = ["ref", "split", "perm", "cr", "dad", "fma", "fmaAd"]
 sys.path.insert(0, str(REF))
 sys.path.insert(0, str(ROOT))
 
@@ -217,6 +219,14 @@ def run(task):
         out["iters"], _ = cg_variant(phi.apply, b, minv, scale, dad=dad)
     elif variant == "fma":
         out["iters"], _ = cg_variant(phi.apply, b, minv, scale, fma=True)
+    elif variant == "fmaAd":
+        Xo = port.Csr(X.n_rows, X.n_cols, X.row_ptr, X.col_idx, X.values)
+        L = np.longdouble
+
+        def apply_fma_ad(v):
+            cs = port.matvec_t(Xo, om * port.matvec(Xo, v))
+            return (cs.astype(L) + diag.astype(L) * v.astype(L)).astype(np.float64)
+        out["iters"], _ = cg_variant(apply_fma_ad, b, minv, scale)
     elif variant == "ld":
         cr = CrPhi(X, om, diag)
         Xo = cr.Xo
@@ -229,7 +239,23 @@ def run(task):
     return out
 
 
+def merge(variants):
+    """Add `variants` (iteration counts only) to the existing fixture."""
+    with Pool(min(6, len(SEEDS) * len(variants)), maxtasksperchild=1) as pool:
+        res = pool.map(run, [(s, v) for s in SEEDS for v in variants], chunksize=1)
+    fx = dict(np.load(OUT))
+    for v in variants:
+        fx[f"iters_{v}"] = np.array([[r for r in res if r["seed"] == s and r["variant"] == v][0]["iters"]
+                                     for s in SEEDS])
+    fx["gate_variants"] = np.array(GATE_VARIANTS)
+    np.savez_compressed(OUT, **fx)
+    print("merged", variants, "into", OUT)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "--merge":
+        merge(sys.argv[2].split(","))
+        sys.exit(0)
     tasks = [(s, v) for s in SEEDS for v in VARIANTS]
     with Pool(6, maxtasksperchild=1) as pool:
         res = pool.map(run, tasks, chunksize=1)

@@ -85,3 +85,47 @@ def test_fused_rowsplit_config2_against_single_gpu():
         assert abs(a.iterations - ref.iterations) <= max(2, int(0.08 * ref.iterations)), (G, a.iterations,
                                                                                           ref.iterations)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_flag_exchange_protocol_is_bitwise_the_grid_exchange(G):
+    """The cross-GPU exchange protocol (per-rank barriers, release/acquire
+    inbox epochs, volatile peer loads: what a rank per GPU runs) executed
+    between G rank groups of one cooperative grid gives bitwise the solve of
+    the grid-barrier exchange, call after call (the epochs advance across
+    calls), and matches the oracle."""
+    d, om, diag, minv, Xo, b = small_system(seed=5)
+    M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv)
+    cfg = pk.CGConfig(rtol=1e-10)
+    grid_op = sharded(d, G, om, diag)
+    flag_op = sharded(d, G, om, diag)
+    for _ in range(3):
+        a = parallel.fused_pcg_solve(grid_op, b, M, config=cfg, residual_scale=np.sqrt(minv))
+        f = parallel.fused_pcg_solve(flag_op, b, M, config=cfg, residual_scale=np.sqrt(minv), exchange="flags")
+        np.testing.assert_array_equal(f.solution, a.solution)
+        np.testing.assert_array_equal(f.rms_precond_residual_trace, a.rms_precond_residual_trace)
+        assert f.iterations == a.iterations
+    oref = port.pcg(lambda x: port.phi_apply(Xo, om, diag, x), b, minv, np.sqrt(minv), rtol=1e-10)
+    assert np.linalg.norm(f.solution - oref.x) / np.linalg.norm(oref.x) < 1e-8
+
+
+def test_flag_exchange_config2_two_ranks_against_oracle():
+    """G = 2 ranks at config-2 size through the flag protocol: relative L2 <
+    1e-8 vs the CPU oracle at RMS 1e-10 (BASELINE tolerance)."""
+    d = synth.config_design(2, seed=0)
+    cond = synth.config2_conditioning(d, seed=0, pg_sampler=port.pg_batch)
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    rng = np.random.default_rng(7)
+    b = rng.standard_normal(d.p + 1) * 10
+    M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, cond["minv"])
+    op = sharded(d, 2, cond["omega"], cond["prior_diag"])
+    f = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=cond["scale"],
+                                 exchange="flags")
+    g = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=cond["scale"])
+    np.testing.assert_array_equal(f.solution, g.solution)
+    oref = port.pcg(lambda x: port.phi_apply(Xo, cond["omega"], cond["prior_diag"], x), b, cond["minv"],
+                    cond["scale"], rtol=1e-10)
+    rel = np.linalg.norm(f.solution - oref.x) / np.linalg.norm(oref.x)
+    print(f"config 2, 2 ranks, flag exchange: rel L2 vs oracle {rel:.2e}, iterations {f.iterations} "
+          f"(oracle {oref.iterations})")
+    assert rel < 1e-8

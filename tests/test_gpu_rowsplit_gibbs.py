@@ -82,3 +82,18 @@ def test_unsupported_options_raise(small):
     cfg = gibbs.BridgeConfig(unshrunk_prior_sd=(np.inf,))
     with pytest.raises(NotImplementedError):
         parallel.row_split_gibbs_run(d.matrix(), y, cfg, 2, preconditioner="jacobi")
+
+
+@pytest.mark.parametrize("prior", ["bridge", "horseshoe"])
+def test_flag_exchange_scan_is_bitwise_the_grid_exchange(small, prior):
+    """Whole row-split scans (RHS exchange, per-iteration exchanges, the
+    scalar log-likelihood exchange by flags) with the cross-GPU protocol
+    between 3 rank groups of one grid: bitwise the grid-exchange chain."""
+    d, y, _ = small
+    X = d.matrix()
+    cfg = (gibbs.BridgeConfig if prior == "bridge" else gibbs.HorseshoeConfig)(unshrunk_prior_sd=(np.inf,))
+    a = parallel.row_split_gibbs_run(X, y, cfg, 25, shards=3, seed=6)
+    f = parallel.row_split_gibbs_run(X, y, cfg, 25, shards=3, seed=6, exchange="flags")
+    np.testing.assert_array_equal(f.draws, a.draws)
+    np.testing.assert_array_equal(f.logdensity_trace, a.logdensity_trace)
+    np.testing.assert_array_equal(f.cg_iteration_counts, a.cg_iteration_counts)
