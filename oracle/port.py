@@ -205,6 +205,105 @@ def pcg(apply, b, minv, scale, x0=None, max_iter=None, rtol=1e-6) -> PcgResult:
                      np.array(alphas), np.array(betas), applies)
 
 
+def _reordered(X: Csr) -> Csr:
+    """The same matrix with the rows in reverse order and every row's columns
+    reversed (cached): another reduceat / bincount summation order."""
+    if not hasattr(X, "_rev"):
+        n = X.n
+        cnt = np.diff(X.row_ptr)[::-1]
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(cnt, out=rp[1:])
+        ci = X.col_idx[::-1].copy()            # rows reversed AND columns reversed within rows
+        X._rev = Csr(n, X.p, rp, ci, np.ones(len(ci)))
+    return X._rev
+
+
+def phi_apply_ordered(X: Csr, omega, prior_diag, v, order="ref"):
+    """Phi v in float64 with a chosen summation order: "ref" (the reference's,
+    sampler.py:53-58), "rev" (rows and row entries reversed), "split" (two row
+    halves summed afterwards), "cr" (correctly rounded: phi_apply_exact)."""
+    if order == "ref":
+        return phi_apply(X, omega, prior_diag, v)
+    if order == "cr":
+        return phi_apply_exact(X, omega, prior_diag, v)
+    if order == "rev":
+        Xr = _reordered(X)
+        return phi_apply(Xr, np.asarray(omega)[::-1], prior_diag, v)
+    if order == "split":
+        h = X.n // 2
+        out = np.zeros(X.p)
+        for lo, hi in ((0, h), (h, X.n)):
+            rp = X.row_ptr[lo:hi + 1] - X.row_ptr[lo]
+            sl = slice(X.row_ptr[lo], X.row_ptr[hi])
+            Xs = Csr(hi - lo, X.p, rp, X.col_idx[sl], X.values[sl], X.col_means, X.col_scales)
+            out = out + matvec_t(Xs, np.asarray(omega)[lo:hi] * matvec(Xs, v))
+        return out + prior_diag * v
+    raise ValueError(order)
+
+
+def pcg_long_double(X: Csr, omega, prior_diag, b, minv, scale, x0=None, rtol=1e-6, max_iter=None):
+    """The PCG recurrence of cg.py:105-192 with every operation in long
+    double (Phi from phi_apply_exact_ld): the extended-precision reference
+    point of the iteration-count band.  Returns the iteration count."""
+    L = np.longdouble
+    p = len(b)
+    max_iter = 2 * p if max_iter is None else max_iter
+    bL, mL, sL = (np.asarray(a, dtype=np.float64).astype(L) for a in (b, minv, scale))
+    x = np.zeros(p, dtype=L) if x0 is None else np.asarray(x0, dtype=np.float64).astype(L)
+    r = bL - phi_apply_exact_ld(X, omega, prior_diag, x.astype(np.float64))
+    t = sL * r
+    rms = math.sqrt(float(np.dot(t, t)) / p)
+    k = 0
+    if rms <= rtol:
+        return 0
+    z = mL * r
+    rz = np.dot(r, z)
+    d = z.copy()
+    while k < max_iter:
+        k += 1
+        Ad = _phi_ld_vec(X, omega, prior_diag, d)
+        alpha = rz / np.dot(d, Ad)
+        x = x + alpha * d
+        r = r - alpha * Ad
+        t = sL * r
+        rms = math.sqrt(float(np.dot(t, t)) / p)
+        if rms <= rtol:
+            break
+        z = mL * r
+        rzn = np.dot(r, z)
+        d = z + (rzn / rz) * d
+        rz = rzn
+    return k
+
+
+def _phi_ld_vec(X: Csr, omega, prior_diag, v):
+    """phi_apply_exact_ld for a long-double input vector (no rounding to float64)."""
+    L = np.longdouble
+    phi_apply_exact_ld(X, omega, prior_diag, np.zeros(X.p))      # builds the CSC caches
+    z = np.zeros(X.n, dtype=L)
+    if X.nonempty.size:
+        z[X.nonempty] = np.add.reduceat(v[X.col_idx], X.row_ptr[X.nonempty])
+    w = np.asarray(omega, dtype=np.float64).astype(L) * z
+    g = np.zeros(X.p, dtype=L)
+    ne = X._csc_nonempty
+    g[ne] = np.add.reduceat(w[X._csc_rows], X._csc_start[ne])
+    return g + np.asarray(prior_diag).astype(L) * v
+
+
+def iteration_band(X: Csr, omega, prior_diag, b, minv, scale, rtol=1e-6, max_iter=None):
+    """The iteration-count band of a PCG solve (tests' parity gate for the
+    count): the counts of the float64 recurrence under the summation orders of
+    phi_apply_ordered and of the long-double recurrence; F = max(2, spread of
+    the float64 counts); band = [min(all) - F, reference + F].  Returns
+    (lo, hi, counts dict)."""
+    counts = {o: pcg(lambda v, o=o: phi_apply_ordered(X, omega, prior_diag, v, o), b, minv, scale,
+                     rtol=rtol, max_iter=max_iter).iterations for o in ("ref", "rev", "split", "cr")}
+    counts["ld"] = pcg_long_double(X, omega, prior_diag, b, minv, scale, rtol=rtol, max_iter=max_iter)
+    f64 = [counts[o] for o in ("ref", "rev", "split", "cr")]
+    F = max(2, max(f64) - min(f64))
+    return min(min(f64), counts["ld"]) - F, counts["ref"] + F, counts
+
+
 def metric_scale(prior_diag, minv, residual_scale=None, prior_kind=True):
     """Termination scale precedence (cg.py:89-102)."""
     if residual_scale is not None:

@@ -51,7 +51,8 @@ def test_batched_pcg_matches_single_chain(R):
         ref = port.pcg(lambda v: port.phi_apply(Xo, om[c], diag[c], v), B[c], minv[c], np.sqrt(minv[c]),
                        rtol=1e-10)
         assert np.linalg.norm(reps[c].solution - ref.x) / np.linalg.norm(ref.x) < 1e-8
-        assert abs(reps[c].iterations - ref.iterations) <= max(2, int(0.08 * ref.iterations))
+        lo, hi, counts = port.iteration_band(Xo, om[c], diag[c], B[c], minv[c], np.sqrt(minv[c]), rtol=1e-10)
+        assert lo <= reps[c].iterations <= hi, (c, reps[c].iterations, counts)
         assert reps[c].termination == "converged"
         assert len(reps[c].rms_precond_residual_trace) == reps[c].iterations + 1
         its.append(reps[c].iterations)

@@ -185,8 +185,9 @@ class TestDeviceOperator:
                            config=pk.CGConfig(rtol=1e-10), residual_scale=scale)
         assert rel(rep.solution, ref.x) < 1e-8
         # iteration count at rtol 1e-10 on an outlier-heavy spectrum moves with summation
-        # order alone (SURVEY §6 measured 1-9 CPU vs CPU); allow that floor
-        assert abs(rep.iterations - ref.iterations) <= max(2, int(0.08 * ref.iterations))
+        # order alone: the band of float64 orderings and the long-double recurrence
+        lo, hi, counts = port.iteration_band(Xo, om, diag, b, minv, scale, rtol=1e-10)
+        assert lo <= rep.iterations <= hi, (rep.iterations, counts)
 
     def test_config2_true_residual(self):
         """Paper scale: the returned solution satisfies the stopping rule for

@@ -1,0 +1,94 @@
+"""The paper's preconditioner race on device (reference acceptance criterion 6,
+pkg/tests/test_acceptance.py:275-316; the paper's Fig. 1 comparison): frozen
+Gibbs states at desk scale for 10 and 50 true signals, 8 shared right-hand
+sides, relative-coordinate error curves of the device PCG with the prior
+preconditioner and with Jacobi (diag(X'ΩX) from one device CSC pass), judged
+by the reference's three conditions:
+
+  (a) the 10-signal prior curve reaches 1e-6 within 0.2 p iterations;
+  (b) past iteration 10 the prior curve is never above the Jacobi curve;
+  (c) the 10-signal prior curve crosses 1e-6 before the 50-signal one.
+
+The reference runs the race on a dense factor-structured design (simulate_
+design, n=2500, p=1000, 99 factors); the device path takes binary patterns,
+so the same race runs on the binary design of BASELINE config 1's recipe at
+the reference's desk size (n=2500, p=1000, rates logU[1e-3, 0.2], no
+intercept, bridge prior as BridgeConfig()), the frozen states drawn by the
+device chain itself (300 scans)."""
+import numpy as np
+import pytest
+import scipy.linalg
+
+import paper_1810_12437_b200 as pk
+from paper_1810_12437_b200 import diagnostics, synth
+from oracle import port
+
+pytestmark = pytest.mark.gpu
+
+
+def geometric_mean_curve(curves):
+    length = max(len(c) for c in curves)
+    padded = np.stack([np.concatenate([c, np.full(length - len(c), c[-1])]) for c in curves])
+    return np.exp(np.mean(np.log(np.maximum(padded, 1e-300)), axis=0))
+
+
+def first_at_or_below(curve, threshold):
+    hit = np.flatnonzero(curve <= threshold)
+    return int(hit[0]) if hit.size else -1
+
+
+@pytest.fixture(scope="module")
+def desk():
+    d = synth.binary_design(2500, 1000, 1e-3, 0.2, seed=606)
+    X = d.matrix(intercept=False)
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx, intercept=False)
+    dense = np.zeros((d.n, d.p))
+    dense[np.repeat(np.arange(d.n), np.diff(Xo.row_ptr)), Xo.col_idx] = 1.0
+    built = {}
+    for k in (10, 50):
+        y, _ = synth.simulate_outcomes(d, seed=42 + k, n_signal=k, intercept=False)
+        chain = pk.gibbs_run(X, y, pk.BridgeConfig(), 300, seed=7)
+        st = chain.final_state
+        prior = (st.tau * st.lam) ** -2.0
+        phi = pk.PrecisionOperator(X, st.omega, prior)
+        target = pk.GaussianTarget.from_pseudo_outcome(phi, (y - 0.5) / st.omega)
+        full = dense.T @ (st.omega[:, None] * dense) + np.diag(prior)
+        built[k] = dict(X=X, st=st, phi=phi, target=target, chol=scipy.linalg.cholesky(full, lower=True),
+                        scale=st.tau * st.lam)
+    return built
+
+
+def error_curves(entry, M, rhs, max_iter):
+    cfg = pk.CGConfig(rtol=1e-14, max_iter=max_iter, trace_level="full")
+    curves = []
+    for b in rhs:
+        rep = pk.pcg_solve(entry["phi"], b, M, config=cfg, residual_scale=entry["scale"])
+        x_star = scipy.linalg.cho_solve((entry["chol"], True), b)
+        curves.append(np.asarray(diagnostics.error_trace(rep, x_star, entry["phi"]).rel_coord_error))
+    return curves
+
+
+def test_prior_preconditioner_wins_the_race(desk):
+    rng = np.random.default_rng(606)
+    res = {}
+    for k in (10, 50):
+        e = desk[k]
+        rhs = [pk.generate_rhs(e["target"], rng) for _ in range(8)]
+        M_prior = pk.prior_preconditioner(e["st"].tau, e["st"].lam)
+        res[k] = {"prior": geometric_mean_curve(error_curves(e, M_prior, rhs, 700))}
+        if k == 10:
+            M_jac = pk.jacobi_preconditioner(e["X"], e["st"].omega, e["st"].tau, e["st"].lam)
+            res[10]["jacobi"] = geometric_mean_curve(error_curves(e, M_jac, rhs, 2000))
+    p = 1000
+    hit10 = first_at_or_below(res[10]["prior"], 1e-6)
+    hit50 = first_at_or_below(res[50]["prior"], 1e-6)
+    hitj = first_at_or_below(res[10]["jacobi"], 1e-6)
+    pr, jc = res[10]["prior"], res[10]["jacobi"]
+    n = max(len(pr), len(jc))
+    pad = lambda c: np.concatenate([c, np.full(n - len(c), c[-1])])  # noqa: E731
+    ratio = pad(pr)[11:] / pad(jc)[11:]
+    print(f"race: 10-signal prior reaches 1e-6 at {hit10} (Jacobi {hitj}), 50-signal prior at {hit50}; "
+          f"max prior/Jacobi error ratio past 10 = {ratio.max():.3f}")
+    assert 0 <= hit10 <= 0.2 * p
+    assert np.all(ratio <= 1.0)
+    assert 0 <= hit10 < hit50

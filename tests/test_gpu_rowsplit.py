@@ -42,8 +42,9 @@ def test_fused_rowsplit_matches_oracle(G, slab_max):
     rep = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=np.sqrt(minv))
     oref = port.pcg(lambda x: port.phi_apply(Xo, om, diag, x), b, minv, np.sqrt(minv), rtol=1e-10)
     assert np.linalg.norm(rep.solution - oref.x) / np.linalg.norm(oref.x) < 1e-8
-    # the iteration floor of summation order on this 80-iteration system (max(2, 8 %))
-    assert abs(rep.iterations - oref.iterations) <= max(2, int(0.08 * oref.iterations))
+    # the iteration band of summation order on this system (float64 orderings, long double)
+    lo, hi, counts = port.iteration_band(Xo, om, diag, b, minv, np.sqrt(minv), rtol=1e-10)
+    assert lo <= rep.iterations <= hi, (rep.iterations, counts)
     assert rep.termination == "converged"
     assert rep.matvec_count == rep.iterations + 1 == len(rep.rms_precond_residual_trace)
     assert len(rep.alphas) == rep.iterations
@@ -65,25 +66,30 @@ def test_fused_rowsplit_max_iter_and_warm_start():
     assert warm.iterations == 0 and warm.matvec_count == 1
 
 
-def test_fused_rowsplit_config2_against_single_gpu():
+def test_fused_rowsplit_config2_against_reference():
+    """Config 2, fixture seed 0 (the reference's own solves,
+    tests/golden/config2_parity.npz): G = 2 and 8 row shards, relative L2 vs
+    the reference's RMS-1e-10 solution < 1e-8, and at RMS 1e-6 the count in
+    the reference's float64 / long-double band (test_gpu_parity_config2)."""
+    from test_gpu_parity_config2 import FIX, floor_band, inputs
+    fx = np.load(FIX)
     d = synth.config_design(2, seed=0)
-    cond = synth.config2_conditioning(d, seed=0)
-    full = pk.PrecisionOperator(d.matrix(), cond["omega"], cond["prior_diag"])
-    rng = np.random.default_rng(7)
-    b = rng.standard_normal(d.p + 1) * 10
+    Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+    cond, b = inputs(d, Xo, int(fx["seeds"][0]))
     M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, cond["minv"])
-    cfg = pk.CGConfig(rtol=1e-10)
-    ref = pk.pcg_solve(full, b, M, config=cfg, residual_scale=cond["scale"])
+    lo, hi, F, counts = floor_band(fx, 0)
+    x_star = fx["x_1e10"][0]
     for G in (2, 8):
         op = sharded(d, G, cond["omega"], cond["prior_diag"])
-        a = parallel.fused_pcg_solve(op, b, M, config=cfg, residual_scale=cond["scale"])
-        again = parallel.fused_pcg_solve(op, b, M, config=cfg, residual_scale=cond["scale"])
+        a = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=cond["scale"])
+        again = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-10), residual_scale=cond["scale"])
         assert np.array_equal(a.solution, again.solution)          # deterministic
-        rel = np.linalg.norm(a.solution - ref.solution) / np.linalg.norm(ref.solution)
+        rel = np.linalg.norm(a.solution - x_star) / np.linalg.norm(x_star)
         assert rel < 1e-8, (G, rel)
-        # summation order alone moves the count on this spectrum
-        assert abs(a.iterations - ref.iterations) <= max(2, int(0.08 * ref.iterations)), (G, a.iterations,
-                                                                                          ref.iterations)
+        r6 = parallel.fused_pcg_solve(op, b, M, config=pk.CGConfig(rtol=1e-6), residual_scale=cond["scale"])
+        print(f"config 2 seed 0, {G} shards: rel L2 {rel:.2e}; {r6.iterations} iterations at RMS 1e-6 "
+              f"(band [{lo}, {hi}], reference {int(fx['iters_ref'][0])})")
+        assert lo <= r6.iterations <= hi, (G, r6.iterations, lo, hi)
     torch.cuda.synchronize()
 
 
