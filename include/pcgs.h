@@ -354,23 +354,39 @@ int pcgs_rs_gibbs_scan(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows
 
 /* ------------------------------------------------------------------------
  * Batched independent chains (BASELINE config 4): R chains share
- * one walk over the index stream (pattern-only SpMM with R right-hand sides).
- * Vectors are chain-minor: element (j, c) at [j * R + c]; R in {2, 4, 8}.
- * The design must be created with slab_max <= pcgs_batch_slab_max(R).
+ * one walk over the pattern (pattern-only SpMM with R right-hand sides)
+ * through a SLICED store: a warp is 32/R slots of R lanes, lane (slot, c)
+ * sums chain c of one output piece.  Device vectors are chain-minor:
+ * element (j, c) at [j * R + c], reference coordinates (intercept first);
+ * R in {2, 4, 8}.  Replaces, per chain, PrecisionOperator.apply
+ * (sampler.py:53-58) and pcg_solve (cg.py:105-192).
  * ------------------------------------------------------------------------ */
-int pcgs_batch_slab_max(int nchains);
-/* out = X'(Omega_c X v_c) + D_c v_c for every chain c (sampler.py:53-58). */
-int pcgs_batch_phi_apply(pcgs_design_t d, int nchains, const double* omega,
-                         const double* prior_diag, const double* v, double* out,
-                         pcgs_stream_t stream);
-/* Per-chain PCG (cg.py:105-192) in one persistent kernel; chains that finish
- * are masked.  trace[c*(max_iter+1)+k], alphas/betas[c*max_iter+k],
+typedef struct pcgs_batch* pcgs_batch_t;
+/* Validates the CSR (sparse.py:94-117) and builds the sliced store for
+ * `nchains` chains on `device`, planned for `grid` CTAs (0: one per SM);
+ * slab_max 0 = the largest slab the chains fit in shared memory. */
+int pcgs_batch_create(int64_t n, int64_t p, const int64_t* row_ptr_h,
+                      const int32_t* col_idx_h, int intercept, int nchains,
+                      int slab_max, int device, int grid, pcgs_batch_t* out);
+int pcgs_batch_destroy(pcgs_batch_t b);
+/* info[16]: n, p, p_total, nnz, csr/csc slabs, csr/csc vectors, csr/csc
+ * pieces, nchains, grid, device, index bytes, slab_max, bank-conflict ppm. */
+int pcgs_batch_info(pcgs_batch_t b, int64_t* info);
+/* Host-only: builds the sliced store and rebuilds the pattern from it
+ * (stats[9]: slabs, vectors, pieces, LDS groups, conflict excess, padding). */
+int pcgs_batch_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h,
+                        const int32_t* col_idx_h, int intercept, int nchains,
+                        int slab_max, int grid, int64_t* stats);
+/* out_c = X'(Omega_c X v_c) + D_c v_c for every chain c. */
+int pcgs_batch_phi_apply(pcgs_batch_t b, const double* omega, const double* prior_diag,
+                         const double* v, double* out, pcgs_stream_t stream);
+/* Per-chain PCG in one persistent kernel; chains that finish are masked.
+ * trace[c*(max_iter+1)+k], alphas/betas[c*max_iter+k],
  * result[c*4 + {iterations, status, fail_iter, applies}]. */
-int pcgs_batch_pcg(pcgs_design_t d, int nchains, const double* omega,
-                   const double* prior_diag, const double* minv, const double* scale,
-                   const double* b, double* x, int32_t max_iter, double rtol,
-                   double* trace, double* alphas, double* betas, int32_t* result,
-                   pcgs_stream_t stream);
+int pcgs_batch_pcg(pcgs_batch_t b, const double* omega, const double* prior_diag,
+                   const double* minv, const double* scale, const double* rhs, double* x,
+                   int32_t max_iter, double rtol, double* trace, double* alphas,
+                   double* betas, int32_t* result, pcgs_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -85,10 +85,14 @@ SIGNATURES = {
     "pcgs_rs_set_exchange": (ctypes.c_int, [_P, ctypes.c_int]),
     "pcgs_rs_gibbs_init": (ctypes.c_int, [_P, _P, _P, _P]),
     "pcgs_rs_gibbs_scan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _I32, _P]),
-    "pcgs_batch_slab_max": (ctypes.c_int, [ctypes.c_int]),
-    "pcgs_batch_phi_apply": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, _P]),
-    "pcgs_batch_pcg": (ctypes.c_int, [_P, ctypes.c_int, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P,
-                                      _P, _P]),
+    "pcgs_batch_create": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    "pcgs_batch_destroy": (ctypes.c_int, [_P]),
+    "pcgs_batch_info": (ctypes.c_int, [_P, _P]),
+    "pcgs_batch_selftest": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, _P]),
+    "pcgs_batch_phi_apply": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
+    "pcgs_batch_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
     "pcgs_gibbs_scan": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P]),
     "pcgs_gibbs_scan_begin": (ctypes.c_int, [_P, _P, _I32, _P]),
     "pcgs_gibbs_scan_end": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P]),

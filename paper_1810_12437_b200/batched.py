@@ -1,13 +1,15 @@
 """Batched independent chains on one GPU (BASELINE config 4).
 
 R chains with their own omega, prior diagonal and right-hand side share every
-walk over the pattern-only index stream: Phi_c v_c for all c in one SpMM-like
-pass (`pcgs_batch_phi_apply`) and R PCG solves in one persistent kernel
-(`pcgs_batch_pcg`), each chain following the reference loop (cg.py:105-192)
-and masked once it terminates.  Host arrays are chain-major (R, m); the device
-layout is chain-minor (m, R).
+walk over the pattern through the sliced store (csrc/sliced.h): Phi_c v_c
+for all c in one SpMM-like pass (`pcgs_batch_phi_apply`) and R PCG solves in
+one persistent kernel (`pcgs_batch_pcg`), each chain following the reference
+loop (cg.py:105-192) and masked once it terminates.  Host arrays are
+chain-major (R, m); the device layout is chain-minor (m, R).
 """
 from __future__ import annotations
+
+import ctypes
 
 import numpy as np
 
@@ -15,6 +17,47 @@ from . import _lib
 from .cg import CGConfig, CGReport, _n_betas, _raise_status
 
 SUPPORTED = (2, 4, 8)
+
+
+class BatchStore:
+    """Owner of one libpcgs sliced-store handle (R chains, one CUDA device)."""
+
+    KEYS = ["n", "p", "p_total", "nnz", "csr_slabs", "csc_slabs", "csr_vectors", "csc_vectors",
+            "csr_pieces", "csc_pieces", "nchains", "grid", "device", "index_bytes", "slab_max",
+            "bank_conflict_ppm"]
+
+    def __init__(self, n, p, row_ptr, col_idx, intercept, nchains, device=None, slab_max=0, grid=0):
+        if nchains not in SUPPORTED:
+            raise ValueError(f"batch size must be one of {SUPPORTED}")
+        L = _lib.lib()
+        self.device = _lib.cuda_device(device)
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        h = ctypes.c_void_p()
+        _lib.check(L.pcgs_batch_create(int(n), int(p), rp.ctypes.data, ci.ctypes.data, int(bool(intercept)),
+                                       int(nchains), int(slab_max), int(self.device.index), int(grid),
+                                       ctypes.byref(h)))
+        self._h = h
+        info = np.zeros(16, dtype=np.int64)
+        _lib.check(L.pcgs_batch_info(h, info.ctypes.data))
+        self.info = info
+        self.R = int(nchains)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def describe(self) -> dict:
+        return {k: int(v) for k, v in zip(self.KEYS, self.info)}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                _lib.lib().pcgs_batch_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self._h = None
 
 
 def _to_dev_cm(a, dev):
@@ -40,7 +83,7 @@ class BatchedPrecisionOperator:
         if not np.all(np.isfinite(dg)) or np.any(dg < 0):
             raise ValueError("prior precision must be finite and nonnegative")
         self.X, self.R = X, R
-        self.store = X.device_store(device, batch=R)
+        self.store = X.batch_store(R, device)
         self.dev = self.store.device
         self.omega = _to_dev_cm(om, self.dev)
         self.diag = _to_dev_cm(dg, self.dev)
@@ -58,7 +101,7 @@ class BatchedPrecisionOperator:
         vd = _to_dev_cm(V, self.dev)
         out = t.empty_like(vd)
         self.apply_count += 1
-        _lib.check(_lib.lib().pcgs_batch_phi_apply(self.store.handle, self.R, _lib.ptr(self.omega),
+        _lib.check(_lib.lib().pcgs_batch_phi_apply(self.store.handle, _lib.ptr(self.omega),
                                                    _lib.ptr(self.diag), _lib.ptr(vd), _lib.ptr(out),
                                                    _lib.stream_ptr(self.dev)))
         res = out.t().contiguous()
@@ -75,7 +118,7 @@ def batched_pcg_device(op, B_cm, minv_cm, scale_cm, X0_cm=None, max_iter=None, r
     alphas = t.empty((R, max_iter), dtype=t.float64, device=dev)
     betas = t.empty((R, max_iter), dtype=t.float64, device=dev)
     result = t.zeros((R, 4), dtype=t.int32, device=dev)
-    _lib.check(_lib.lib().pcgs_batch_pcg(op.store.handle, R, _lib.ptr(op.omega), _lib.ptr(op.diag),
+    _lib.check(_lib.lib().pcgs_batch_pcg(op.store.handle, _lib.ptr(op.omega), _lib.ptr(op.diag),
                                          _lib.ptr(minv_cm), _lib.ptr(scale_cm), _lib.ptr(B_cm),
                                          _lib.ptr(x), max_iter, float(rtol), _lib.ptr(trace),
                                          _lib.ptr(alphas), _lib.ptr(betas), _lib.ptr(result),

@@ -280,14 +280,12 @@ void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G, bool csc) {
 
 }  // namespace
 
-std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
-                         int intercept, int slab_max, int G, DesignHost& D) {
+std::string validate_csr(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx) {
   if (n < 1) return "design must have at least one row";
   if (p < 0) return "negative column count";
   if (row_ptr[0] != 0) return "row_ptr endpoints must be 0 and nnz";
   for (int64_t i = 0; i < n; ++i)
     if (row_ptr[i + 1] < row_ptr[i]) return "row_ptr must be nondecreasing";
-  const int64_t nnz = row_ptr[n];
   for (int64_t i = 0; i < n; ++i) {
     for (int64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) {
       if (col_idx[k] < 0 || col_idx[k] >= p) return "col_idx entry out of range";
@@ -295,6 +293,16 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
         return "col_idx must be strictly increasing within each row";
     }
   }
+  return "";
+}
+
+std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
+                         int intercept, int slab_max, int G, DesignHost& D) {
+  {
+    std::string err = validate_csr(n, p, row_ptr, col_idx);
+    if (!err.empty()) return err;
+  }
+  const int64_t nnz = row_ptr[n];
   const int64_t hard_max = 22528 - 16;  // doubles per slab (+ sentinel): 176 KB, leaves room for PCG state
   int64_t smax = slab_max > 0 ? std::min<int64_t>(slab_max, hard_max) : hard_max;
   if (smax < 16) smax = 16;

@@ -65,6 +65,10 @@ struct DesignHost {
   PassHost csr, csc;
 };
 
+// The CSR invariants of SparseDesignMatrix._validate (sparse.py:94-117);
+// empty string when they hold.
+std::string validate_csr(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx);
+
 // Validates the CSR (sparse.py:94-117 invariants) and builds both passes for a
 // grid of G CTAs.  Returns an empty string on success, else an error message.
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,

@@ -289,23 +289,30 @@ class SparseDesignMatrix:
     def has_intercept(self):
         return self.pattern()[2]
 
-    def device_store(self, device=None, batch=1, grid=0) -> DesignStore:
-        """The pattern-only store on `device`; `batch` > 1 builds the variant
-        whose slabs leave room for `batch` chain-minor vectors (batched chains);
-        `grid` > 0 plans it for that many CTAs (row-split shards sharing a GPU)."""
+    def device_store(self, device=None, grid=0) -> DesignStore:
+        """The pattern-only store on `device`; `grid` > 0 plans it for that
+        many CTAs (row-split shards or chains side by side sharing a GPU)."""
         dev = _lib.cuda_device(device)
-        key = (dev.index, int(batch), int(grid))
+        key = (dev.index, 1, int(grid))
         st = self._stores.get(key)
         if st is None:
             rp, ci, icpt = self.pattern()
-            slab_max = self.slab_max
-            if batch > 1:
-                cap = _lib.lib().pcgs_batch_slab_max(int(batch))
-                if cap <= 0:
-                    _lib.check(cap)
-                slab_max = min(slab_max, cap) if slab_max else cap
             st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0), rp, ci, icpt,
-                             device=dev, slab_max=slab_max, grid=grid)
+                             device=dev, slab_max=self.slab_max, grid=grid)
+            self._stores[key] = st
+        return st
+
+    def batch_store(self, nchains, device=None, grid=0):
+        """The sliced store of R = `nchains` batched chains on `device`
+        (batched.BatchStore; built once per (device, R, grid))."""
+        from .batched import BatchStore
+        dev = _lib.cuda_device(device)
+        key = (dev.index, "batch", int(nchains), int(grid))
+        st = self._stores.get(key)
+        if st is None:
+            rp, ci, icpt = self.pattern()
+            st = BatchStore(self.n_rows, self.n_cols - (1 if icpt else 0), rp, ci, icpt, int(nchains),
+                            device=dev, slab_max=self.slab_max, grid=grid)
             self._stores[key] = st
         return st
 

@@ -102,3 +102,59 @@ def test_store_config1_layout_and_bank_balance():
     assert st[6] / (16 * st[5]) < 0.1      # < 10 % of shared-memory picks conflict
     # index bytes: 2 B per index, padded to 8 per segment
     assert st[7] < 2 * 2 * (d.nnz + d.n) * 1.6
+
+
+# ------------------------------------------------------------ sliced (batched) store
+def _bselftest(n, p, rp, ci, intercept, R, slab_max=0, grid=148):
+    L = _lib.lib()
+    st = np.zeros(9, dtype=np.int64)
+    rp = np.ascontiguousarray(rp, dtype=np.int64)
+    ci = np.ascontiguousarray(ci, dtype=np.int32)
+    rc = L.pcgs_batch_selftest(n, p, rp.ctypes.data, ci.ctypes.data, int(intercept), R, slab_max, grid,
+                               st.ctypes.data)
+    return rc, L.pcgs_last_error().decode(), st
+
+
+@pytest.mark.parametrize("R", [2, 4, 8])
+@pytest.mark.parametrize("slab_max", [0, 16, 48])
+def test_sliced_store_roundtrip_random(R, slab_max):
+    """The sliced store (csrc/sliced.h) walks every CSR entry exactly once in
+    both passes, for random patterns, multi-slab cuts and grids of 1..148."""
+    rng = np.random.default_rng(10 * R + slab_max)
+    for _ in range(8):
+        n, p = (int(v) for v in rng.integers(1, 300, size=2))
+        rp, ci = random_pattern(rng, n, p, float(rng.uniform(0, 0.6)))
+        for icpt in (True, False):
+            for grid in (1, 5, 148):
+                rc, msg, _ = _bselftest(n, p, rp, ci, icpt, R, slab_max, grid)
+                assert rc == 0, msg
+
+
+def test_sliced_store_edge_cases_and_validation():
+    cases = [
+        (5, 4, np.zeros(6, dtype=np.int64), np.zeros(0, dtype=np.int32)),
+        (1, 3, np.array([0, 2]), np.array([0, 2], dtype=np.int32)),
+        (3, 2000, np.array([0, 2000, 2000, 2001]),
+         np.concatenate([np.arange(2000), [1999]]).astype(np.int32)),
+    ]
+    for n, p, rp, ci in cases:
+        for R in (2, 8):
+            for icpt in (True, False):
+                rc, msg, _ = _bselftest(n, p, rp, ci, icpt, R)
+                assert rc == 0, msg
+    rc, _, _ = _bselftest(1, 3, np.array([0, 2]), np.array([1, 1], dtype=np.int32), True, 8)
+    assert rc == _lib.PCGS_EINVAL
+    rc, _, _ = _bselftest(1, 3, np.array([0, 1]), np.array([0], dtype=np.int32), True, 3)
+    assert rc == _lib.PCGS_EINVAL          # batch size must be 2, 4 or 8
+
+
+def test_sliced_store_config1_bank_balance_and_padding():
+    # short pieces (config 1: ~10 entries per row) leave the builder few
+    # choices when many slots share a half-warp (R = 2: 8 slots per half)
+    d = synth.config_design(1, seed=0)
+    for R, cap in ((2, 0.5), (4, 0.25), (8, 0.12)):
+        rc, msg, st = _bselftest(d.n, d.p, d.row_ptr, d.col_idx, True, R)
+        assert rc == 0, msg
+        vectors = st[2] + st[3]
+        assert st[7] / st[6] < cap          # extra shared-memory wavefronts per half-warp load
+        assert st[8] / vectors < 0.15       # slot padding (sentinel vectors) < 15 % of the stream

@@ -1,5 +1,6 @@
-"""Batched independent chains: R right-hand sides share one walk over the
-index stream; every chain must equal its own single-chain oracle solve."""
+"""Batched independent chains (csrc/sliced.cu): R right-hand sides share one
+walk over the sliced index stream; every chain must equal its own
+single-chain oracle solve."""
 import numpy as np
 import pytest
 
@@ -22,10 +23,12 @@ def chains(d, R, seed, easy=None):
     return om, diag, minv
 
 
-@pytest.mark.parametrize("R", [2, 4])
-def test_batched_phi_matches_oracle_per_chain(R):
+@pytest.mark.parametrize("R", [2, 4, 8])
+@pytest.mark.parametrize("slab_max", [0, 64])
+def test_batched_phi_matches_oracle_per_chain(R, slab_max):
     d = synth.binary_design(1500, 300, 1e-3, 0.3, seed=2)
     X = d.matrix()
+    X.slab_max = slab_max          # 64: many slabs each way, pieces from every slab
     Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
     om, diag, _ = chains(d, R, 1)
     V = np.random.default_rng(3).standard_normal((R, d.p + 1))
@@ -36,7 +39,7 @@ def test_batched_phi_matches_oracle_per_chain(R):
         assert np.linalg.norm(out[c] - ref) <= 1e-12 * np.linalg.norm(ref)
 
 
-@pytest.mark.parametrize("R", [2, 4])
+@pytest.mark.parametrize("R", [2, 4, 8])
 def test_batched_pcg_matches_single_chain(R):
     d = synth.binary_design(2000, 400, 1e-3, 0.25, seed=5)
     X = d.matrix()
@@ -62,23 +65,47 @@ def test_batched_pcg_matches_single_chain(R):
 def test_batched_config2_phi_vs_single():
     d = synth.config_design(2, seed=0)
     X = d.matrix()
-    om, diag, _ = chains(d, 4, 11)
-    V = np.random.default_rng(1).standard_normal((4, d.p + 1))
+    om, diag, _ = chains(d, 8, 11)
+    V = np.random.default_rng(1).standard_normal((8, d.p + 1))
     out = batched.BatchedPrecisionOperator(X, om, diag).apply(V)
-    for c in range(4):
+    for c in range(8):
         ref = pk.PrecisionOperator(X, om[c], diag[c]).apply(V[c])
         assert np.linalg.norm(out[c] - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_batched_config2_pcg_eight_chains():
+    """Config-2 size, 8 chains (config 4's batch): every chain's solution
+    within 1e-8 relative L2 of the single-chain device solve at RMS 1e-10,
+    deterministic, and the per-chain counts at RMS 1e-6 in the band of the
+    single-chain kernel +- the float64 ordering floor of these systems."""
+    d = synth.config_design(2, seed=0)
+    X = d.matrix()
+    # config-2 conditioning (tau = 1e-3, half-Cauchy lambda), one draw per chain
+    conds = [synth.config2_conditioning(d, seed=s, pg_sampler=port.pg_batch) for s in range(8)]
+    om = np.stack([c["omega"] for c in conds])
+    diag = np.stack([c["prior_diag"] for c in conds])
+    minv = np.stack([c["minv"] for c in conds])
+    rng = np.random.default_rng(13)
+    B = rng.standard_normal((8, d.p + 1)) * 10
+    op = batched.BatchedPrecisionOperator(X, om, diag)
+    sc = np.stack([c["scale"] for c in conds])
+    reps = batched.batched_pcg_solve(op, B, minv, sc, config=pk.CGConfig(rtol=1e-10))
+    again = batched.batched_pcg_solve(op, B, minv, sc, config=pk.CGConfig(rtol=1e-10))
+    r6 = batched.batched_pcg_solve(op, B, minv, sc, config=pk.CGConfig(rtol=1e-6))
+    for c in range(8):
+        assert np.array_equal(reps[c].solution, again[c].solution)
+        M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv[c])
+        phi = pk.PrecisionOperator(X, om[c], diag[c])
+        single = pk.pcg_solve(phi, B[c], M, config=pk.CGConfig(rtol=1e-10), residual_scale=sc[c])
+        rel = np.linalg.norm(reps[c].solution - single.solution) / np.linalg.norm(single.solution)
+        s6 = pk.pcg_solve(phi, B[c], M, config=pk.CGConfig(rtol=1e-6), residual_scale=sc[c])
+        print(f"chain {c}: rel L2 vs single {rel:.2e}; RMS-1e-6 iterations batched {r6[c].iterations}, "
+              f"single {s6.iterations}")
+        assert rel < 1e-8, (c, rel)
+        assert abs(r6[c].iterations - s6.iterations) <= max(2, int(0.05 * s6.iterations)), c
 
 
 def test_batch_size_validation():
     d = synth.binary_design(100, 20, 0.01, 0.3, seed=1)
     with pytest.raises(ValueError):
         batched.BatchedPrecisionOperator(d.matrix(), np.ones((3, 100)), np.ones((3, 21)))
-
-
-def test_batch_of_eight_reports_unsupported_pcg_cleanly():
-    d = synth.config_design(2, seed=0)
-    om, diag, minv = chains(d, 8, 1)
-    op = batched.BatchedPrecisionOperator(d.matrix(), om, diag)
-    with pytest.raises(NotImplementedError):
-        batched.batched_pcg_solve(op, np.ones((8, d.p + 1)), minv, np.sqrt(minv))
