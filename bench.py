@@ -54,9 +54,10 @@ def parse():
     ap.add_argument("--no-full-run", action="store_true",
                     help="skip extra.full_run (BASELINE config 3's whole 1,000-scan chain)")
     ap.add_argument("--workload", default="config3", choices=["config3", "config4", "config5"],
-                    help="config4: 8 independent chains per GPU side by side (weak scaling); "
+                    help="config4: 8 independent chains per GPU as one batch (weak scaling); "
                          "config5: the row-split run (rows of X over the N ranks, strong scaling)")
-    ap.add_argument("--concurrent", type=int, default=4, help="config4: chains side by side per wave")
+    ap.add_argument("--concurrent", type=int, default=1,
+                    help="config4: 1 = the 8 chains as one batch (batched PCG); k > 1 = k slots side by side")
     return ap.parse_args()
 
 
@@ -544,10 +545,12 @@ def rowsplit_line(args, K, W):
 
 def run_config4(args):
     """BASELINE config 4: independent chains on the config-2/3 design, 8 per
-    GPU (chain c seeded chain_seed(0, c)), on --concurrent slots side by side
-    (one stream each, the store planned for SMs/concurrent CTAs, a slot's
-    chains one after another).  Step = one scan of every chain of the rank;
-    value = chain-iterations per second over all ranks."""
+    GPU (chain c seeded chain_seed(0, c)).  Default: the rank's 8 chains as ONE
+    batch whose beta solves share one batched PCG per scan
+    (gibbs.BatchedChains, the sliced store); --concurrent k > 1 instead runs
+    them on k slots side by side (one stream each, the store planned for
+    SMs/k CTAs, a slot's chains one after another).  Step = one scan of every
+    chain of the rank; value = chain-iterations per second over all ranks."""
     import torch
     import torch.distributed as dist
     from paper_1810_12437_b200 import gibbs, parallel
@@ -561,64 +564,82 @@ def run_config4(args):
     X = d.matrix()
     K, W, R = args.steps, args.warmup, max(1, args.concurrent)
     per_gpu = 8
+    batched = R == 1
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid = 0 if R == 1 else sms // R
     chains_idx = parallel.chain_assignment(per_gpu * world, world, rank)
-    # R slots (streams); chain i of the rank runs on slot i % R after the
-    # slot's previous chain, with no barrier between rounds.  Warm-up: every
-    # chain's first W scans, issued slot-ordered before the timed region; the
-    # timed region covers the K further scans of every chain.
-    slots = [torch.cuda.Stream(dev) for _ in range(R)]
-    chains = []
+    seeds = [parallel.chain_seed(SEED, c) for c in chains_idx]
+    cgc = gibbs.CGConfig(rtol=RTOL)
     with ClockSampler(local) as clk:
-        for i, c in enumerate(chains_idx):
-            with torch.cuda.stream(slots[i % R]):
-                chains.append((gibbs.DeviceChain(X, y, cfg, W + K, burn_in=W, seed=parallel.chain_seed(SEED, c),
-                                                 cg_config=gibbs.CGConfig(rtol=RTOL), device=dev, grid=grid),
-                               slots[i % R]))
-        for t in range(1, W + 1):
-            for ch, s in chains:
-                with torch.cuda.stream(s):
-                    ch.scan(t)
+        if batched:
+            B = gibbs.BatchedChains(X, y, cfg, W + K, seeds, device=dev, burn_in=W, cg_config=cgc)
+            all_chains = B.chains
+            for t in range(1, W + 1):
+                B.scan(t)
+        else:
+            # R slots (streams); chain i of the rank runs on slot i % R after
+            # the slot's previous chain, with no barrier between rounds
+            slots = [torch.cuda.Stream(dev) for _ in range(R)]
+            chains = []
+            for i, sd in enumerate(seeds):
+                with torch.cuda.stream(slots[i % R]):
+                    chains.append((gibbs.DeviceChain(X, y, cfg, W + K, burn_in=W, seed=sd, cg_config=cgc,
+                                                     device=dev, grid=grid), slots[i % R]))
+            all_chains = [ch for ch, _ in chains]
+            for t in range(1, W + 1):
+                for ch, s in chains:
+                    with torch.cuda.stream(s):
+                        ch.scan(t)
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
         cur = torch.cuda.current_stream(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(cur)
-        for s in slots:
-            s.wait_stream(cur)
-        for r0 in range(0, len(chains), R):       # round by round: a slot's chains in order
+        if batched:
             for t in range(W + 1, W + K + 1):
-                for ch, s in chains[r0:r0 + R]:
-                    with torch.cuda.stream(s):
-                        ch.scan(t)
-        for s in slots:
-            cur.wait_stream(s)
+                B.scan(t)
+        else:
+            for s in slots:
+                s.wait_stream(cur)
+            for r0 in range(0, len(chains), R):       # round by round: a slot's chains in order
+                for t in range(W + 1, W + K + 1):
+                    for ch, s in chains[r0:r0 + R]:
+                        with torch.cuda.stream(s):
+                            ch.scan(t)
+            for s in slots:
+                cur.wait_stream(s)
         e1.record(cur)
         torch.cuda.synchronize(dev)
         total_ms = e0.elapsed_time(e1)
     cg = []
-    for ch, _ in chains:
+    for ch in all_chains:
         ch.check(1, W + K)
         cg += ch.results.view(-1, 8).cpu().numpy()[W:W + K, 0].astype(int).tolist()
+    cg_max = np.max(np.asarray(cg).reshape(len(all_chains), K), axis=0)
     ms_t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
         dist.barrier()
     ms_max = float(ms_t.item())
     if rank == 0:
+        mode = ("one batch: the beta solves of all 8 chains in one batched PCG per scan (sliced store)"
+                if batched else f"{R} slots side by side")
         line = {
             "metric": "gibbs_iter_per_s", "value": world * per_gpu * K / (ms_max * 1e-3), "unit": "chain-iter/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; BASELINE config 4 recipe; no public dataset)",
             "config": {"workload": f"config 4: {per_gpu} independent {args.prior} chains per GPU on the "
-                                   f"n={d.n:,} p={d.p:,} design (nnz {d.nnz:,}), {R} slots side by side",
-                       "chains_per_gpu": per_gpu, "concurrent": R, "grid_per_chain": grid or sms,
+                                   f"n={d.n:,} p={d.p:,} design (nnz {d.nnz:,}), {mode}",
+                       "chains_per_gpu": per_gpu, "mode": "batched" if batched else "slots",
+                       "concurrent": R, "grid_per_chain": grid or sms,
                        "parallelism": f"chain-parallel x{world}", "seed": SEED},
             "clocks": clk.summary(),
-            "extra": {"cg_iters_mean": float(np.mean(cg)), "chain_iterations_timed": per_gpu * K},
+            "extra": {"cg_iters_mean": float(np.mean(cg)), "chain_iterations_timed": per_gpu * K,
+                      "batch_cg_iters_mean": float(np.mean(cg_max)) if batched else None,
+                      "note": ("a batched solve runs until its slowest chain converges: per scan the "
+                               "batch pays the max of the 8 chains' CG counts") if batched else None},
         }
         print(json.dumps(line))
     if world > 1:

@@ -377,6 +377,9 @@ int pcgs_batch_info(pcgs_batch_t b, int64_t* info);
 int pcgs_batch_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h,
                         const int32_t* col_idx_h, int intercept, int nchains,
                         int slab_max, int grid, int64_t* stats);
+/* Debug: device buffer of 8 * 64 uint64 that pcgs_batch_pcg fills with
+ * %globaltimer stamps of the phases of its first 64 iterations (NULL: off). */
+int pcgs_batch_debug_profile(void* buf);
 /* out_c = X'(Omega_c X v_c) + D_c v_c for every chain c. */
 int pcgs_batch_phi_apply(pcgs_batch_t b, const double* omega, const double* prior_diag,
                          const double* v, double* out, pcgs_stream_t stream);
@@ -387,6 +390,17 @@ int pcgs_batch_pcg(pcgs_batch_t b, const double* omega, const double* prior_diag
                    const double* minv, const double* scale, const double* rhs, double* x,
                    int32_t max_iter, double rtol, double* trace, double* alphas,
                    double* betas, int32_t* result, pcgs_stream_t stream);
+
+/* One Gibbs scan t of R = nchains batched chains (BASELINE config 4): every
+ * chain's own omega, tau, lambda and RHS (as pcgs_gibbs_scan), the R beta
+ * solves in one batched PCG on `b` (pcgs_batch_pcg), then every chain's
+ * X beta, statistics and log density.  gs[c] are the chains' states on design
+ * `d` (same pattern as `b`), sharing max_iter and rtol; counts[c] / slots[c]
+ * as in pcgs_gibbs_scan.  Replaces R calls of the reference's scan
+ * (gibbs.py:300-369). */
+int pcgs_batch_gibbs_scan(pcgs_design_t d, pcgs_batch_t b, pcgs_gibbs_t* const* gs,
+                          int32_t nchains, int32_t t, const int32_t* counts,
+                          const int32_t* slots, pcgs_stream_t stream);
 
 #ifdef __cplusplus
 }

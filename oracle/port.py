@@ -158,8 +158,10 @@ class PcgResult:
     applies: int
 
 
-def pcg(apply, b, minv, scale, x0=None, max_iter=None, rtol=1e-6) -> PcgResult:
-    """Hestenes-Stiefel PCG with the RMS scaled-residual stop (cg.py:105-192)."""
+def pcg(apply, b, minv, scale, x0=None, max_iter=None, rtol=1e-6, callback=None) -> PcgResult:
+    """Hestenes-Stiefel PCG with the RMS scaled-residual stop (cg.py:105-192).
+    `callback(x)` sees every iterate (x0 first), as trace_level="full" records
+    them (cg.py:160-170)."""
     b = np.asarray(b, dtype=np.float64)
     p = b.shape[0]
     max_iter = 2 * p if max_iter is None else max_iter
@@ -171,6 +173,8 @@ def pcg(apply, b, minv, scale, x0=None, max_iter=None, rtol=1e-6) -> PcgResult:
     if not np.isfinite(rms):
         raise Breakdown(0)
     trace, alphas, betas = [rms], [], []
+    if callback is not None:
+        callback(x.copy())
     k = 0
     if rms > rtol:
         z = minv * r
@@ -187,6 +191,8 @@ def pcg(apply, b, minv, scale, x0=None, max_iter=None, rtol=1e-6) -> PcgResult:
             alphas.append(alpha)
             x += alpha * d
             r -= alpha * Ad
+            if callback is not None:
+                callback(x.copy())
             t = scale * r
             rms = math.sqrt(float(np.dot(t, t)) / p)
             trace.append(rms)

@@ -91,6 +91,8 @@ SIGNATURES = {
     "pcgs_batch_info": (ctypes.c_int, [_P, _P]),
     "pcgs_batch_selftest": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, _P]),
+    "pcgs_batch_debug_profile": (ctypes.c_int, [_P]),
+    "pcgs_batch_gibbs_scan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _P, _P, _P]),
     "pcgs_batch_phi_apply": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "pcgs_batch_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
     "pcgs_gibbs_scan": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P]),

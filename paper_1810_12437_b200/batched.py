@@ -16,7 +16,7 @@ import numpy as np
 from . import _lib
 from .cg import CGConfig, CGReport, _n_betas, _raise_status
 
-SUPPORTED = (2, 4, 8)
+SUPPORTED = (1, 2, 4, 8)
 
 
 class BatchStore:

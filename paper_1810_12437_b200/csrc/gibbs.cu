@@ -363,36 +363,151 @@ int pcgs_gibbs_scan_begin(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, pcgs_stre
   return PCGS_OK;
 }
 
-int pcgs_gibbs_scan_end(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, int32_t slot,
-                        pcgs_stream_t stream) {
-  if (!d || !g || t < 1) return fail(PCGS_EINVAL, "bad argument");
+}  // extern "C"
+
+// The halves of scan_end around the beta solve (shared by the single-chain
+// and the batched scans).
+static int scan_prep(pcgs_design* d, pcgs_gibbs_t* g, int32_t t, int32_t count, cudaStream_t s) {
   const DesignDev& D = d->dev;
-  cudaStream_t s = (cudaStream_t)stream;
   const long long pt = D.pt;
   const int eblocks = (int)std::min<long long>((pt + 255) / 256, 4 * D.G);
-  const int sblocks = D.G;  // k_stats grid: one partial line per CTA
   int rc;
   // lambda | beta, tau; prior diagonal, M^-1, metric scale, x0
   k_local<<<eblocks, 256, 0, s>>>(*g, pt, t, count);
   if (g->precond == 2) {
-    if ((rc = pcgs_phi_diagonal(d, g->omega, g->prior_diag, g->b, stream))) return rc;
+    if ((rc = pcgs_phi_diagonal(d, g->omega, g->prior_diag, g->b, s))) return rc;
     k_precond<<<eblocks, 256, 0, s>>>(*g, pt, g->b);
   } else if (g->precond == 1) {
     k_precond<<<eblocks, 256, 0, s>>>(*g, pt, nullptr);
   }
   CUDA_TRY(cudaGetLastError());
-  // randomised right-hand side (one fused X' pass) and the PCG solve
-  if ((rc = pcgs_rhs(d, g->kappa, g->omega, g->prior_diag, nullptr, nullptr, nullptr, g->seed, (uint64_t)t, g->b,
-                     stream)))
-    return rc;
+  // randomised right-hand side (one fused X' pass)
+  return pcgs_rhs(d, g->kappa, g->omega, g->prior_diag, nullptr, nullptr, nullptr, g->seed, (uint64_t)t, g->b, s);
+}
+
+static int scan_post(pcgs_design* d, pcgs_gibbs_t* g, int32_t t, int32_t count, int32_t slot, cudaStream_t s) {
+  const DesignDev& D = d->dev;
+  int rc;
+  // z = X beta with the log-likelihood, statistics, stored draw, log density
+  if ((rc = launch_logit(d, g, s))) return rc;
+  k_stats<<<D.G, 256, 0, s>>>(*g, D.pt, count + 1, slot);
+  k_post<<<1, 32, 0, s>>>(*g, D.pt, t, D.G, D.G);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+// Chain-minor packing of the R chains' solve inputs / unpacking of the
+// solutions and reports (batched scan).
+struct PackArgs {
+  const double* src[8];
+  double* dst;
+};
+__global__ void k_pack(PackArgs A, int R, long long m) {
+  const long long nr = m * R;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nr; e += (long long)gridDim.x * blockDim.x)
+    A.dst[e] = A.src[e % R][e / R];
+}
+struct UnpackArgs {
+  double* dst[8];
+  const double* src;
+};
+__global__ void k_unpack(UnpackArgs A, int R, long long m) {
+  const long long nr = m * R;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nr; e += (long long)gridDim.x * blockDim.x)
+    A.dst[e % R][e / R] = A.src[e];
+}
+struct ResultArgs {
+  int* dst[8];
+};
+__global__ void k_results(ResultArgs A, const int* res, int R) {
+  const int i = threadIdx.x;
+  if (i < 4 * R) A.dst[i / 4][i % 4] = res[i];
+}
+
+extern "C" {
+
+int pcgs_gibbs_scan_end(pcgs_design_t d, pcgs_gibbs_t* g, int32_t t, int32_t count, int32_t slot,
+                        pcgs_stream_t stream) {
+  if (!d || !g || t < 1) return fail(PCGS_EINVAL, "bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  if ((rc = scan_prep(d, g, t, count, s))) return rc;
   if ((rc = pcgs_pcg(d, g->omega, g->prior_diag, g->minv, g->scale, g->b, g->beta, g->max_iter, g->rtol, g->trace,
                      g->alphas, g->betas, g->results + 8 * (t - 1), stream)))
     return rc;
-  // z = X beta with the log-likelihood, statistics, stored draw, log density
-  if ((rc = launch_logit(d, g, s))) return rc;
-  k_stats<<<sblocks, 256, 0, s>>>(*g, pt, count + 1, slot);
-  k_post<<<1, 32, 0, s>>>(*g, pt, t, D.G, sblocks);
-  CUDA_TRY(cudaGetLastError());
+  return scan_post(d, g, t, count, slot, s);
+}
+
+int pcgs_batch_gibbs_scan(pcgs_design_t d, pcgs_batch_t bt, pcgs_gibbs_t* const* gs, int32_t nchains, int32_t t,
+                          const int32_t* counts, const int32_t* slots, pcgs_stream_t stream) {
+  if (!d || !bt || !gs || !counts || !slots || t < 1) return fail(PCGS_EINVAL, "bad argument");
+  int64_t info[16];
+  int rc;
+  if ((rc = pcgs_batch_info(bt, info))) return rc;
+  const int R = (int)info[10];
+  if (nchains != R) return fail(PCGS_EINVAL, "nchains must equal the batch store's chain count");
+  const DesignDev& D = d->dev;
+  if (info[0] != D.n || info[2] != D.pt) return fail(PCGS_EINVAL, "batch store and design differ in shape");
+  for (int c = 0; c < R; ++c) {
+    if (!gs[c]) return fail(PCGS_EINVAL, "null chain");
+    if (gs[c]->max_iter != gs[0]->max_iter || gs[c]->rtol != gs[0]->rtol)
+      return fail(PCGS_EINVAL, "batched chains must share max_iter and rtol");
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // each chain's own omega, tau, lambda, prior diagonal, M^-1, scale, x0, RHS
+  for (int c = 0; c < R; ++c) {
+    if ((rc = pcgs_gibbs_scan_begin(d, gs[c], t, stream))) return rc;
+    if ((rc = scan_prep(d, gs[c], t, counts[c], s))) return rc;
+  }
+  // R solves in one batched kernel on chain-minor copies
+  const long long n = D.n, pt = D.pt;
+  const int mi = gs[0]->max_iter;
+  Scratch S(s);
+  double* om = S.get<double>((size_t)n * R);
+  double* vec = S.get<double>((size_t)pt * R * 5);
+  double* tr = S.get<double>((size_t)R * (mi + 1) * 3);
+  int* res = S.get<int>((size_t)R * 4);
+  if (!om || !vec || !tr || !res) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  double *dg = vec, *mv = vec + pt * R, *sc = vec + 2 * pt * R, *bb = vec + 3 * pt * R, *xx = vec + 4 * pt * R;
+  const int blocks = 4 * D.G;
+  {
+    PackArgs P;
+    for (int c = 0; c < R; ++c) P.src[c] = gs[c]->omega;
+    P.dst = om;
+    k_pack<<<blocks, 256, 0, s>>>(P, R, n);
+    for (int f = 0; f < 5; ++f) {
+      for (int c = 0; c < R; ++c) {
+        pcgs_gibbs_t* g = gs[c];
+        P.src[c] = f == 0 ? g->prior_diag : f == 1 ? g->minv : f == 2 ? g->scale : f == 3 ? g->b : g->beta;
+      }
+      P.dst = vec + (long long)f * pt * R;
+      k_pack<<<blocks, 256, 0, s>>>(P, R, pt);
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  double *trace = tr, *alphas = tr + (size_t)R * (mi + 1), *betas = alphas + (size_t)R * (mi + 1);
+  if ((rc = pcgs_batch_pcg(bt, om, dg, mv, sc, bb, xx, mi, gs[0]->rtol, trace, alphas, betas, res, stream)))
+    return rc;
+  {
+    UnpackArgs U;
+    for (int c = 0; c < R; ++c) U.dst[c] = gs[c]->beta;
+    U.src = xx;
+    k_unpack<<<blocks, 256, 0, s>>>(U, R, pt);
+    ResultArgs RA;
+    for (int c = 0; c < R; ++c) RA.dst[c] = gs[c]->results + 8 * (t - 1);
+    k_results<<<1, 32, 0, s>>>(RA, res, R);
+    CUDA_TRY(cudaGetLastError());
+    for (int c = 0; c < R; ++c) {
+      CUDA_TRY(cudaMemcpyAsync(gs[c]->trace, trace + (size_t)c * (mi + 1), sizeof(double) * (mi + 1),
+                               cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(gs[c]->alphas, alphas + (size_t)c * mi, sizeof(double) * mi,
+                               cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(gs[c]->betas, betas + (size_t)c * mi, sizeof(double) * mi,
+                               cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  for (int c = 0; c < R; ++c)
+    if ((rc = scan_post(d, gs[c], t, counts[c], slots[c], s))) return rc;
   return PCGS_OK;
 }
 

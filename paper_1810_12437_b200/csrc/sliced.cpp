@@ -36,7 +36,7 @@ struct SlabPieces {
 
 // Indices of one piece still to be placed, bucketed by bank group (index mod H).
 struct Pool {
-  std::array<std::vector<uint16_t>, 8> b;
+  std::array<std::vector<uint16_t>, 16> b;
   int H = 1;
   uint32_t remaining = 0;
   void load(const uint16_t* d, uint32_t len, int h) {
@@ -63,7 +63,7 @@ struct Pool {
 // extra wavefronts of one half-warp LDS.64: the largest number of distinct
 // indices sharing a bank group (index mod H), minus one
 int half_extra(const int* ix, int n, int H) {
-  int mult[8] = {};
+  int mult[16] = {};
   int worst = 0;
   for (int i = 0; i < n; ++i) {
     bool seen = false;
@@ -100,7 +100,7 @@ void emit_slices(SPassHost& P, SlabPieces& S, const std::vector<uint32_t>& sl_fi
     for (uint32_t t = 0; t < L; ++t) {
       for (int k = 0; k < kVecIdx; ++k) {
         for (int h = 0; h < 2; ++h) {
-          int mult[8] = {};
+          int mult[16] = {};
           int g[16];
           int ng = 0;
           bool pad_seen = false, any = false;
@@ -274,7 +274,7 @@ void build_pass(SPassHost& P, int64_t n_out, int64_t n_in, int64_t smax, int R, 
 
 std::string build_sliced(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx, int intercept,
                          int R, int slab_max, int G, SlicedHost& H) {
-  if (R != 2 && R != 4 && R != 8) return "nchains must be 2, 4 or 8";
+  if (R != 1 && R != 2 && R != 4 && R != 8) return "nchains must be 1, 2, 4 or 8";
   {
     std::string err = validate_csr(n, p, row_ptr, col_idx);
     if (!err.empty()) return err;

@@ -90,10 +90,14 @@ int upload_spass(pcgs_batch* B, const SPassHost& H, SPassDev& P) {
 }
 
 // ------------------------------------------------------------------ streaming
-// steps per load batch (all loads of a batch issued together)
-constexpr int kStepBatch = 4;
 // sliding L2 prefetch distance ahead of the loads, bytes of the warp's stream
 constexpr unsigned kSPrefetch = 4096;
+
+__device__ __forceinline__ unsigned long long stimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int R>
 __device__ __forceinline__ unsigned row_addr(unsigned sb, unsigned idx) {
@@ -111,24 +115,36 @@ __device__ __forceinline__ double gather8_lane(uint4 q, unsigned sb) {
 }
 
 // One warp walks its slice range: lane (slot, c) sums chain c of its slot's
-// piece over the slice's steps and emits it.
+// piece over the slice's steps and emits it.  The warp's slices are
+// contiguous in the stream, so the walk is one flat run of steps (slot s of
+// step g at vector first + g * NS + s) with slice boundaries every L steps:
+// the index loads of the next batch are issued before the current batch is
+// consumed (software pipelining across slice boundaries), and the next
+// slice's descriptor is loaded one slice ahead.
+#ifndef PCGS_SLICED_BATCH
+#define PCGS_SLICED_BATCH 4
+#endif
+#ifndef PCGS_SLICED_PIPE
+#define PCGS_SLICED_PIPE 0
+#endif
+#if !PCGS_SLICED_PIPE
+// per-slice batches of U steps, loads of a batch issued together
 template <int R, class Epi>
 __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi) {
   constexpr int NS = 32 / R;
+  constexpr int U = PCGS_SLICED_BATCH;
   const int lane = threadIdx.x & 31, slot = lane / R, c = lane & (R - 1);
   const uint2 ws = __ldg(P.warp_slices + wr);
   if (ws.x >= ws.y) return;
   const unsigned sb = smem_addr(sv) + (unsigned)c * 8u;
   const uint2 first = __ldg(P.slices + ws.x), last = __ldg(P.slices + ws.y - 1);
   const char* stream0 = (const char*)(P.vec + first.x);
-  // the warp's slices are contiguous in the stream: [stream0, stream0 + total)
   const unsigned total = (unsigned)(((size_t)last.x + (size_t)last.y * NS - first.x) * 16u);
-  unsigned next_pf = kSPrefetch;  // bytes of the warp stream prefetched so far (relative)
+  unsigned next_pf = kSPrefetch;
   for (unsigned q = ws.x; q < ws.y; ++q) {
     const uint2 D = __ldg(P.slices + q);
     const unsigned pid = __ldg(P.piece + (size_t)q * NS + slot);
     const uint4* vp = P.vec + D.x + slot;
-    // keep the L2 prefetch window kSPrefetch bytes ahead of this slice's end
     {
       const unsigned end = min(total, (unsigned)((const char*)(P.vec + D.x + (size_t)D.y * NS) - stream0) + kSPrefetch);
       for (; next_pf < end; next_pf += 32u * 128u) {
@@ -138,17 +154,80 @@ __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const dou
     }
     double acc = 0.0;
     unsigned t = 0;
-    for (; t + kStepBatch <= D.y; t += kStepBatch) {
-      uint4 v[kStepBatch];
+    for (; t + U <= D.y; t += U) {
+      uint4 v[U];
 #pragma unroll
-      for (int u = 0; u < kStepBatch; ++u) v[u] = ldg_stream(vp + (size_t)(t + u) * NS);
+      for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + (size_t)(t + u) * NS);
 #pragma unroll
-      for (int u = 0; u < kStepBatch; ++u) acc += gather8_lane<R>(v[u], sb);
+      for (int u = 0; u < U; ++u) acc += gather8_lane<R>(v[u], sb);
     }
     for (; t < D.y; ++t) acc += gather8_lane<R>(ldg_stream(vp + (size_t)t * NS), sb);
     if (pid != 0xffffffffu) epi.emit(pid, c, acc);
   }
 }
+#else
+template <int R, class Epi>
+__device__ __noinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi) {
+  constexpr int NS = 32 / R;
+  constexpr int U = PCGS_SLICED_BATCH;
+  const int lane = threadIdx.x & 31, slot = lane / R, c = lane & (R - 1);
+  const uint2 ws = __ldg(P.warp_slices + wr);
+  if (ws.x >= ws.y) return;
+  const unsigned sb = smem_addr(sv) + (unsigned)c * 8u;
+  const uint2 first = __ldg(P.slices + ws.x), last = __ldg(P.slices + ws.y - 1);
+  const char* stream0 = (const char*)(P.vec + first.x);
+  const unsigned T = (unsigned)(((size_t)last.x - first.x) / NS + last.y);  // steps of the warp
+  const unsigned total = T * NS * 16u;                                      // bytes of the warp stream
+  const uint4* base = P.vec + first.x + slot;
+  unsigned q = ws.x;
+  unsigned bnd = first.y;  // step at which slice q ends
+  unsigned pid = __ldg(P.piece + (size_t)q * NS + slot);
+  uint2 nD = q + 1 < ws.y ? __ldg(P.slices + q + 1) : make_uint2(0u, 0u);
+  unsigned npid = q + 1 < ws.y ? __ldg(P.piece + (size_t)(q + 1) * NS + slot) : 0xffffffffu;
+  unsigned next_pf = kSPrefetch;  // bytes of the warp stream prefetched so far
+  double acc = 0.0;
+  uint4 cur[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if ((unsigned)u < T) cur[u] = ldg_stream(base + (size_t)u * NS);
+  for (unsigned g0 = 0; g0 < T; g0 += U) {
+    // sliding L2 prefetch kSPrefetch bytes ahead of the loads
+    {
+      const unsigned end = min(total, (g0 + 2 * U) * NS * 16u + kSPrefetch);
+      if (next_pf < end) {
+        const unsigned off = next_pf + (unsigned)lane * 128u;
+        if (off < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(stream0 + off));
+        next_pf += 32u * 128u;
+      }
+    }
+    uint4 nxt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (g0 + U + u < T) nxt[u] = ldg_stream(base + (size_t)(g0 + U + u) * NS);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned g = g0 + u;
+      if (g < T) {
+        if (g == bnd) {  // slice q done: emit, advance to q + 1 (pieces are never empty)
+          if (pid != 0xffffffffu) epi.emit(pid, c, acc);
+          acc = 0.0;
+          ++q;
+          bnd += nD.y;
+          pid = npid;
+          if (q + 1 < ws.y) {
+            nD = __ldg(P.slices + q + 1);
+            npid = __ldg(P.piece + (size_t)(q + 1) * NS + slot);
+          }
+        }
+        acc += gather8_lane<R>(cur[u], sb);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+  }
+  if (pid != 0xffffffffu) epi.emit(pid, c, acc);
+}
+#endif
 
 // TMA copy of elements [lo, lo+len) of a chain-minor R-column vector into the
 // slab; the sentinel row (R doubles at element len) is zeroed.
@@ -289,6 +368,7 @@ struct PcgArgsS {
   double *trace, *alphas, *betas;  // [c][max_iter+1], [c][max_iter]
   int* result;                     // [c][4]
   double *zpiece, *w, *pieces, *dg, *own, *part;
+  unsigned long long* prof;  // debug: [8 a + k] phase stamps of iterations a < 64 (pcgs_batch_debug_profile)
 };
 
 template <int R>
@@ -342,7 +422,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
   // dAd prior part of the first application is not used (a = 0 has no alpha)
   cg::this_grid().sync();
 
+  const bool prof_cta = A.prof && blockIdx.x == 0 && tid == 0;
+  auto stamp = [&](int a, int k) {
+    if (prof_cta && a < 64) A.prof[8 * a + k] = stimer();
+  };
   for (int a = 0;; ++a) {
+    stamp(a, 0);
     // ---------------- phase A: CSR pass, pieces of X d ----------------
     if (tid < R) v0s[tid] = D.icpt ? __ldcg(A.dg + D.p * R + tid) : 0.0;
     {
@@ -351,6 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
       run_spass<R>(D.csr, sv, f, e);
     }
     cg::this_grid().sync();
+    stamp(a, 1);
     // ---------------- row combine: w = omega z, z' Omega z per chain ----------------
     double wz = 0.0;
     {
@@ -371,6 +457,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
       if (tid < R) A.part[(long long)blockIdx.x * PS + tid] += t;  // + the D d^2 part written with d
     }
     cg::this_grid().sync();
+    stamp(a, 2);
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
     {
       FillRows<R> f{A.w, &bf};
@@ -378,6 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
       run_spass<R>(D.csc, sv, f, e);
     }
     cg::this_grid().sync();
+    stamp(a, 3);
     if (tid == 0) ++st_applies;
 
     // ---------------- phase C: per-chain step on the own columns ----------------
@@ -437,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
       }
     }
     cg::this_grid().sync();
+    stamp(a, 4);
 
     // ---------------- convergence test, beta, new direction ----------------
     reduce_parts(A.part, PS, R, 2 * R, sred);
@@ -496,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
       if (tid < R) A.part[(long long)blockIdx.x * PS + tid] = t;
     }
     cg::this_grid().sync();
+    stamp(a, 5);
   }
 
   __syncthreads();
@@ -512,6 +602,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
 }
 
 size_t slab_bytes(const BatchDev& D) { return (size_t)D.smem_doubles * 8; }
+
+unsigned long long* g_bprof = nullptr;  // pcgs_batch_debug_profile
 
 template <int R>
 int raise_all_s() {
@@ -546,6 +638,7 @@ int pcg_s(const BatchDev& D, PcgArgsS& A, cudaStream_t s) {
   if ((rc = raise_all_s<R>())) return rc;
   Scratch S(s);
   A.D = D;
+  A.prof = g_bprof;
   A.zpiece = S.get<double>((size_t)D.csr.npiece * R);
   A.w = S.get<double>((size_t)D.n * R);
   A.pieces = S.get<double>((size_t)D.csc.npiece * R);
@@ -568,7 +661,8 @@ int pcgs_batch_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int3
                       int nchains, int slab_max, int device, int grid, pcgs_batch_t* out) {
   if (!out || !row_ptr_h || (!col_idx_h && row_ptr_h[n] > 0)) return fail(PCGS_EINVAL, "null argument");
   *out = nullptr;
-  if (nchains != 2 && nchains != 4 && nchains != 8) return fail(PCGS_EINVAL, "nchains must be 2, 4 or 8");
+  if (nchains != 1 && nchains != 2 && nchains != 4 && nchains != 8)
+    return fail(PCGS_EINVAL, "nchains must be 1, 2, 4 or 8");
   CUDA_TRY(cudaSetDevice(device));
   cudaDeviceProp prop;
   CUDA_TRY(cudaGetDeviceProperties(&prop, device));
@@ -653,12 +747,18 @@ int pcgs_batch_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h, const in
   return PCGS_OK;
 }
 
+int pcgs_batch_debug_profile(void* buf) {
+  g_bprof = (unsigned long long*)buf;
+  return PCGS_OK;
+}
+
 int pcgs_batch_phi_apply(pcgs_batch_t bt, const double* omega, const double* prior_diag, const double* v,
                          double* out, pcgs_stream_t stream) {
   if (!bt || !omega || !v || !out) return fail(PCGS_EINVAL, "null argument");
   const BatchDev& D = bt->dev;
   cudaStream_t s = (cudaStream_t)stream;
   switch (D.R) {
+    case 1: return phi_apply_s<1>(D, omega, prior_diag, v, out, s);
     case 2: return phi_apply_s<2>(D, omega, prior_diag, v, out, s);
     case 4: return phi_apply_s<4>(D, omega, prior_diag, v, out, s);
     case 8: return phi_apply_s<8>(D, omega, prior_diag, v, out, s);
@@ -687,6 +787,7 @@ int pcgs_batch_pcg(pcgs_batch_t bt, const double* omega, const double* prior_dia
   A.result = result;
   cudaStream_t s = (cudaStream_t)stream;
   switch (bt->dev.R) {
+    case 1: return pcg_s<1>(bt->dev, A, s);
     case 2: return pcg_s<2>(bt->dev, A, s);
     case 4: return pcg_s<4>(bt->dev, A, s);
     case 8: return pcg_s<8>(bt->dev, A, s);

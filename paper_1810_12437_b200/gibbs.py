@@ -313,13 +313,17 @@ class DeviceChain:
         _lib.check(_lib.lib().pcgs_gibbs_init(self.store.handle, ctypes.byref(self.args),
                                               _lib.stream_ptr(self.dev)))
 
+    def next_slot(self, t):
+        """Row of `draws` that scan t stores into (advancing the count), or -1."""
+        if t > self.burn_in and (t - self.burn_in - 1) % self.thin == 0:
+            self.stored += 1
+            return self.stored - 1
+        return -1
+
     def scan(self, t, local_scale_sampler=None, rng=None):
         """Issue scan t (1-based) on the current stream; no synchronisation
         unless a host `local_scale_sampler` has to see beta and tau."""
-        slot = -1
-        if t > self.burn_in and (t - self.burn_in - 1) % self.thin == 0:
-            slot = self.stored
-            self.stored += 1
+        slot = self.next_slot(t)
         L = _lib.lib()
         s = _lib.stream_ptr(self.dev)
         if local_scale_sampler is None:
@@ -525,6 +529,73 @@ def gibbs_run_concurrent(X, y, cfg, n_iter, seeds, concurrent=4, burn_in=0, thin
     for k in sorted(busy):
         finish(k)
     return outs
+
+
+class BatchedChains:
+    """R = len(seeds) chains (R in {2, 4, 8}) whose beta solves run as ONE
+    batched PCG per scan (`pcgs_batch_gibbs_scan`, the sliced store of
+    csrc/sliced.h): every chain keeps its own state, RNG keys and outputs
+    (DeviceChain); `scan(t)` issues scan t of every chain.  A chain's
+    trajectory depends on its seed and R only (each chain's sums run in the
+    same order whatever the other chains hold)."""
+
+    def __init__(self, X, y, cfg, n_iter, seeds, device=None, **kw):
+        seeds = list(seeds)
+        R = len(seeds)
+        if R not in (2, 4, 8):
+            raise ValueError("batched chains come in batches of 2, 4 or 8")
+        self.chains = [DeviceChain(X, y, cfg, n_iter, seed=sd, device=device, **kw) for sd in seeds]
+        mi = {ch.max_iter for ch in self.chains}
+        if len(mi) != 1:
+            raise ValueError("batched chains must share max_iter")
+        self.R = R
+        self.dev = self.chains[0].dev
+        self.store = self.chains[0].store
+        self.bstore = X.batch_store(R, self.dev)
+        self._ptrs = (ctypes.c_void_p * R)(*[ctypes.addressof(ch.args) for ch in self.chains])
+        self._counts = np.zeros(R, dtype=np.int32)
+        self._slots = np.zeros(R, dtype=np.int32)
+
+    def scan(self, t):
+        for c, ch in enumerate(self.chains):
+            self._counts[c] = ch.count
+            self._slots[c] = ch.next_slot(t)
+        _lib.check(_lib.lib().pcgs_batch_gibbs_scan(
+            self.store.handle, self.bstore.handle, ctypes.cast(self._ptrs, ctypes.c_void_p), self.R, int(t),
+            self._counts.ctypes.data, self._slots.ctypes.data, _lib.stream_ptr(self.dev)))
+        for ch in self.chains:
+            ch.count += 1
+
+    def check(self, t_lo, t_hi, allow_max_iter=False):
+        for ch in self.chains:
+            ch.check(t_lo, t_hi, allow_max_iter)
+
+    def outputs(self):
+        return [ch.output() for ch in self.chains]
+
+
+def gibbs_run_batched(X, y, cfg, n_iter, seeds, burn_in=0, sampler="cg", thin=1, preconditioner="prior",
+                      cg_config=None, burn_in_sampler=None, init_state=None, gamma_scale=1.0,
+                      allow_max_iter=False, fixed_omega=None, fixed_tau=None, fixed_lam=None, device=None,
+                      sync_every=64) -> list:
+    """gibbs_run (gibbs.py:260-379) for R = len(seeds) independent chains
+    (R in {2, 4, 8}) whose beta draws share one batched PCG per scan; chain c
+    is the chain of seed seeds[c].  Returns one ChainOutput per seed."""
+    y = _check_run_args(X, y, cfg, n_iter, burn_in, thin, sampler, burn_in_sampler, preconditioner,
+                        fixed_lam, None)
+    B = BatchedChains(X, y, cfg, n_iter, seeds, device=device, burn_in=burn_in, thin=thin,
+                      preconditioner=preconditioner, cg_config=cg_config, init_state=init_state,
+                      gamma_scale=gamma_scale, fixed_omega=fixed_omega, fixed_tau=fixed_tau,
+                      fixed_lam=fixed_lam)
+    checked = 0
+    for t in range(1, n_iter + 1):
+        B.scan(t)
+        if sync_every and t - checked >= sync_every:
+            B.check(checked + 1, t, allow_max_iter)
+            checked = t
+    if checked < n_iter:
+        B.check(checked + 1, n_iter, allow_max_iter)
+    return B.outputs()
 
 
 def scale_draws(prior, mode, count, b_or_acc, tau=1.0, lam_old=1.0, p=1, a0=1.0, b0=1.0, alpha=1.0,

@@ -472,19 +472,26 @@ def chain_assignment(n_chains, world, rank):
 
 
 def run_chains(X, y, cfg, n_iter, n_chains, seed=0, group=None, gather=True, runner=None, concurrent=None,
-               **kwargs):
+               batch=None, **kwargs):
     """Run `n_chains` independent Gibbs chains, sharded over the ranks of
     `group` (default: the initialised torch.distributed world, else one
-    process).  Chain c uses `chain_seed(seed, c)`.  Each rank runs its block
-    of chains on its GPU on `concurrent` slots side by side (one CUDA stream
-    each, the store planned for SMs // concurrent CTAs;
-    `gibbs.gibbs_run_concurrent`; default 4, independent of how many chains
-    the rank holds, so a chain's floating-point trajectory depends on its
-    seed only, never on the world size), or one after another with
-    `concurrent=1` / a custom `runner`.  There is no
-    collective while sampling; with `gather` the outputs are all-gathered at
-    the end (object collective) and every rank returns all chains in index
-    order, otherwise only its own (as {chain: ChainOutput})."""
+    process).  Chain c uses `chain_seed(seed, c)`.  How a rank runs its
+    block of chains:
+
+    * default: in batches of `batch` = 8 chains whose beta solves share one
+      batched PCG per scan (`gibbs.gibbs_run_batched`; BASELINE config 4's
+      8 chains per GPU); a short last batch is padded with extra chains
+      (seeds beyond n_chains, outputs dropped) so every chain runs in a batch
+      of the same size and its trajectory depends on its seed only, never on
+      the world size;
+    * `concurrent` = k > 1: k slots side by side (one CUDA stream each, the
+      store planned for SMs // k CTAs; `gibbs.gibbs_run_concurrent`);
+    * `concurrent=1`, a custom `runner`, or host hooks (local_scale_sampler,
+      on_progress): one after another through gibbs_run.
+
+    There is no collective while sampling; with `gather` the outputs are
+    all-gathered at the end (object collective) and every rank returns all
+    chains in index order, otherwise only its own (as {chain: ChainOutput})."""
     import torch.distributed as dist
     if group is None and dist.is_available() and dist.is_initialized():
         group = dist.group.WORLD
@@ -492,9 +499,20 @@ def run_chains(X, y, cfg, n_iter, n_chains, seed=0, group=None, gather=True, run
     rank = dist.get_rank(group) if group is not None else 0
     block = chain_assignment(n_chains, world, rank)
     host_hooks = kwargs.get("local_scale_sampler") is not None or kwargs.get("on_progress") is not None
-    if concurrent is None:
-        concurrent = 1 if (runner is not None or host_hooks) else 4
-    if concurrent > 1 and runner is None and not host_hooks:
+    if batch is None and concurrent is None and runner is None and not host_hooks:
+        batch = 8
+    if batch:
+        from .gibbs import gibbs_run_batched
+        if batch not in (2, 4, 8):
+            raise ValueError("batch must be 2, 4 or 8")
+        seeds = [chain_seed(seed, c) for c in block]
+        outs = []
+        for i in range(0, len(seeds), batch):
+            grp = seeds[i:i + batch]
+            pad = [chain_seed(seed, n_chains + k) for k in range(batch - len(grp))]
+            outs += gibbs_run_batched(X, y, cfg, n_iter, grp + pad, **kwargs)[:len(grp)]
+        mine = dict(zip(block, outs))
+    elif concurrent is not None and concurrent > 1 and runner is None and not host_hooks:
         from .gibbs import gibbs_run_concurrent
         kw = {k: v for k, v in kwargs.items() if k != "sync_every"}
         outs = gibbs_run_concurrent(X, y, cfg, n_iter, [chain_seed(seed, c) for c in block],

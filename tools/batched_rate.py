@@ -19,6 +19,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--iters", type=int, default=100)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--R", default="1,2,4,8")
+ap.add_argument("--profile", action="store_true", help="phase stamps of the batched kernel")
+ap.add_argument("--sliced1", action="store_true", help="R = 1 through the sliced batched kernel")
 a = ap.parse_args()
 
 d = synth.config_design(2, seed=0)
@@ -47,7 +49,7 @@ for R in (int(v) for v in a.R.split(",")):
     minv = 1.0 / np.maximum(diag, 1e-2)
     B = rng.standard_normal((max(R, 1), d.p + 1))
     cfg = pk.CGConfig(rtol=1e-300, max_iter=a.iters)
-    if R == 1:
+    if R == 1 and not a.sliced1:
         phi = pk.PrecisionOperator(X, om[0], diag[0])
         M = pk.Preconditioner(pk.PreconditionerKind.AUGMENTED_PRIOR, minv[0])
         bt = torch.from_numpy(B[0]).cuda()
@@ -61,6 +63,19 @@ for R in (int(v) for v in a.R.split(",")):
         Sc = batched._to_dev_cm(np.sqrt(minv), dev)
         ms = timed(lambda: batched.batched_pcg_device(op, Bc, Mc, Sc, max_iter=a.iters, rtol=1e-300))
         info = op.store.describe()
+        if a.profile:
+            from paper_1810_12437_b200 import _lib
+            buf = torch.zeros(8 * 64, dtype=torch.int64, device=dev)
+            _lib.lib().pcgs_batch_debug_profile(buf.data_ptr())
+            batched.batched_pcg_device(op, Bc, Mc, Sc, max_iter=a.iters, rtol=1e-300)
+            torch.cuda.synchronize()
+            _lib.lib().pcgs_batch_debug_profile(None)
+            st = buf.cpu().numpy().reshape(64, 8).astype(np.float64)
+            rows = st[2:min(a.iters, 60)]
+            ph = {name: float(np.mean(rows[:, k + 1] - rows[:, k])) / 1e3
+                  for k, name in enumerate(["csr", "combine", "csc", "step", "direction"])}
+            ph["iteration"] = float(np.mean(rows[1:, 0] - rows[:-1, 0])) / 1e3
+            info["phases_us"] = ph
     per_apply = ms * 1e3 / (a.iters + 1)
     print(json.dumps({"R": R, "iters": a.iters, "ms_per_solve": ms, "us_per_apply": per_apply,
                       "us_per_chain_iteration": per_apply / R, "store": info}), flush=True)
