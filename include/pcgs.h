@@ -70,6 +70,22 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h,
 int pcgs_design_create_ex(int64_t n, int64_t p, const int64_t* row_ptr_h,
                           const int32_t* col_idx_h, int intercept, int slab_max,
                           int device, int grid, pcgs_design_t* out);
+
+/* A design with affine terms: `q_dense` dense real columns
+ * (hstack_dense_columns of a real block, sparse.py:314-341) in reference
+ * columns intercept .. intercept + q_dense - 1, ahead of the pattern columns
+ * (q_dense > 0 needs intercept = 0: a leading ones column is one of the
+ * dense columns).  Their values and any standardisation (sparse.py:250-297)
+ * are attached with pcgs_design_set_affine. */
+int pcgs_design_create_affine(int64_t n, int64_t p, const int64_t* row_ptr_h,
+                              const int32_t* col_idx_h, int intercept, int q_dense,
+                              int slab_max, int device, int grid, pcgs_design_t* out);
+/* Device arrays of the affine terms (owned by the caller, kept alive while the
+ * design is used): dense n x q_dense row-major, column means `mu` and scales
+ * `sc` in the reference layout (NULL: none).  Every product then applies
+ * X_eff = ([P | Dn] - 1 mu') diag(1/sc). */
+int pcgs_design_set_affine(pcgs_design_t d, const double* dense, const double* mu,
+                           const double* sc);
 int pcgs_design_destroy(pcgs_design_t d);
 /* Bench/test utility: native synthetic binary design (log-uniform column
  * rates, Binomial row counts; BASELINE config 5 scale).  Call once with

@@ -88,29 +88,43 @@ def phi_apply(X: Csr, omega, prior_diag, v):
     return out
 
 
-def phi_apply_exact_ld(X: Csr, omega, prior_diag, v):
-    """Phi v with every sum accumulated in x87 long double (64-bit mantissa),
-    returned in long double; rounded once to float64 (phi_apply_exact) it is
-    to within an ulp the correctly rounded Phi v
-    of sampler.py:53-58 (binary, unstandardised designs).  Used to measure the
-    TRUE residual b - Phi x of a solution, independent of any fp64 summation
-    order (tests/test_gpu_parity_config2.py)."""
-    L = np.longdouble
+def _csc_cache(X: Csr):
     if not hasattr(X, "_csc_perm"):
         X._csc_perm = np.argsort(X.col_idx, kind="stable")
         X._csc_rows = X.row_of[X._csc_perm]
+        X._csc_vals = X.values[X._csc_perm]
         cnt = np.bincount(X.col_idx, minlength=X.p)
         X._csc_start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
         X._csc_nonempty = cnt > 0
-    v = np.asarray(v, dtype=np.float64)
+
+
+def _phi_ld_core(X: Csr, omega, prior_diag, vL):
+    """Phi v (sampler.py:53-58) of the standardised value-carrying CSR
+    (sparse.py:178-203) with every sum accumulated in long double."""
+    L = np.longdouble
+    _csc_cache(X)
+    sc, mu = np.asarray(X.col_scales).astype(L), np.asarray(X.col_means).astype(L)
+    u = vL / sc
     z = np.zeros(X.n, dtype=L)
     if X.nonempty.size:
-        z[X.nonempty] = np.add.reduceat(v.astype(L)[X.col_idx], X.row_ptr[X.nonempty])
+        z[X.nonempty] = np.add.reduceat(np.asarray(X.values).astype(L) * u[X.col_idx], X.row_ptr[X.nonempty])
+    z -= np.dot(mu, u)
     w = np.asarray(omega, dtype=np.float64).astype(L) * z
     g = np.zeros(X.p, dtype=L)
     ne = X._csc_nonempty
-    g[ne] = np.add.reduceat(w[X._csc_rows], X._csc_start[ne])
-    return g + np.asarray(prior_diag).astype(L) * v.astype(L)
+    g[ne] = np.add.reduceat(X._csc_vals.astype(L) * w[X._csc_rows], X._csc_start[ne])
+    g = (g - mu * w.sum()) / sc
+    return g + np.asarray(prior_diag).astype(L) * vL
+
+
+def phi_apply_exact_ld(X: Csr, omega, prior_diag, v):
+    """Phi v with every sum accumulated in x87 long double (64-bit mantissa),
+    returned in long double; rounded once to float64 (phi_apply_exact) it is
+    to within an ulp the correctly rounded Phi v of sampler.py:53-58 (for
+    binary unstandardised designs every value / shift / scale is exact).  Used
+    to measure the TRUE residual b - Phi x of a solution, independent of any
+    fp64 summation order (tests/test_gpu_parity_config2.py)."""
+    return _phi_ld_core(X, omega, prior_diag, np.asarray(v, dtype=np.float64).astype(np.longdouble))
 
 
 def phi_apply_exact(X: Csr, omega, prior_diag, v):
@@ -220,7 +234,7 @@ def _reordered(X: Csr) -> Csr:
         rp = np.zeros(n + 1, dtype=np.int64)
         np.cumsum(cnt, out=rp[1:])
         ci = X.col_idx[::-1].copy()            # rows reversed AND columns reversed within rows
-        X._rev = Csr(n, X.p, rp, ci, np.ones(len(ci)))
+        X._rev = Csr(n, X.p, rp, ci, X.values[::-1].copy(), X.col_means, X.col_scales)
     return X._rev
 
 
@@ -284,16 +298,7 @@ def pcg_long_double(X: Csr, omega, prior_diag, b, minv, scale, x0=None, rtol=1e-
 
 def _phi_ld_vec(X: Csr, omega, prior_diag, v):
     """phi_apply_exact_ld for a long-double input vector (no rounding to float64)."""
-    L = np.longdouble
-    phi_apply_exact_ld(X, omega, prior_diag, np.zeros(X.p))      # builds the CSC caches
-    z = np.zeros(X.n, dtype=L)
-    if X.nonempty.size:
-        z[X.nonempty] = np.add.reduceat(v[X.col_idx], X.row_ptr[X.nonempty])
-    w = np.asarray(omega, dtype=np.float64).astype(L) * z
-    g = np.zeros(X.p, dtype=L)
-    ne = X._csc_nonempty
-    g[ne] = np.add.reduceat(w[X._csc_rows], X._csc_start[ne])
-    return g + np.asarray(prior_diag).astype(L) * v
+    return _phi_ld_core(X, omega, prior_diag, v)
 
 
 def iteration_band(X: Csr, omega, prior_diag, b, minv, scale, rtol=1e-6, max_iter=None):

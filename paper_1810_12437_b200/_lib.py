@@ -47,6 +47,9 @@ SIGNATURES = {
                                           ctypes.c_int, ctypes.POINTER(_P)]),
     "pcgs_design_create_ex": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    "pcgs_design_create_affine": (ctypes.c_int, [_I64, _I64, _P, _P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                 ctypes.c_int, ctypes.c_int, ctypes.POINTER(_P)]),
+    "pcgs_design_set_affine": (ctypes.c_int, [_P, _P, _P, _P]),
     "pcgs_design_destroy": (ctypes.c_int, [_P]),
     "pcgs_synth_design": (ctypes.c_int, [_I64, _I64, _D, _D, _U64, _P, _P, _I64, _P]),
     "pcgs_mtx_load": (ctypes.c_int, [ctypes.c_char_p, _P, _P]),

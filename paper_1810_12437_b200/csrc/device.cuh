@@ -21,8 +21,24 @@ struct PassDev {
   long long nseg;
 };
 
+// Affine terms of a design beyond its binary pattern:
+// X_eff = ([P | 1? | Dn] - 1 mu') diag(1/s), i.e. a dense real block Dn of q
+// columns next to the pattern P (and the intercept), and column centring /
+// scaling.  The reference layout is [intercept? | dense q | pattern p]
+// (hstack_dense_columns prepends, sparse.py:314-341); the internal layout is
+// [pattern p | intercept? | dense q].  Every pass gathers u = v / s and adds
+// the scalar c0 = u_icpt - mu'u plus the row term (Dn u_D)_i to each row sum;
+// the transposes map raw column sums g to (g_j - mu_j W) / s_j, W = sum w.
+struct AffineDev {
+  int on;              // any affine term present
+  int q;               // dense columns
+  const double* dense; // n x q row-major (reference columns icpt .. icpt+q-1)
+  const double* mu;    // reference layout, length pt (null: no centring)
+  const double* sc;    // reference layout, length pt (null: no scaling)
+};
+
 struct DesignDev {
-  long long n, p, pt;  // rows, shrunk columns, p + intercept
+  long long n, p, pt;  // rows, shrunk columns, p + intercept + dense columns
   int icpt;
   int G;               // CTAs the static plan was built for
   int smem_doubles;    // dynamic shared memory per CTA, in doubles
@@ -32,6 +48,8 @@ struct DesignDev {
                        // (very wide designs): it lives in global memory instead
   double* own_global;  // that buffer (8 x chunk per CTA); allocated per solve, never per
                        // design, so solves on one design from several streams stay apart
+  AffineDev aff;
+  __host__ __device__ int lead() const { return icpt + aff.q; }  // reference offset of pattern column 0
 };
 
 // ------------------------------------------------------------------ utilities
@@ -465,9 +483,10 @@ __device__ __forceinline__ double column_sum(const PassDev& csc, const double* p
   return s;
 }
 
-// internal column j (shrunk 0..p-1, intercept p) -> reference coordinate
-__device__ __forceinline__ long long ref_index(long long j, long long p, int icpt) {
-  return j < p ? j + icpt : 0;
+// internal column j (pattern 0..p-1, then the `lead` intercept / dense
+// columns) -> reference coordinate; lead = intercept + dense columns
+__host__ __device__ __forceinline__ long long ref_index(long long j, long long p, int lead) {
+  return j < p ? j + lead : j - p;
 }
 
 // ------------------------------------------------------------------ Philox4x32-10

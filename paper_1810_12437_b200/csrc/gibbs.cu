@@ -16,18 +16,19 @@
 namespace {
 
 // ---------------------------------------------------------------- CSR with log-likelihood
-struct EpiLogit {  // z_i = v0 + s; acc += y_i z_i - log(1 + e^{z_i})
+struct EpiLogit {  // z_i = v0 + s (+ dense row term); acc += y_i z_i - log(1 + e^{z_i})
   double* z;
   const double* y;
   double v0;
   double acc;
   bool multi;
+  AffRow ar;
   __device__ void emit(long long seg, double s) {
     if (multi) {
       z[seg] = s;
       return;
     }
-    const double zi = v0 + s;
+    const double zi = v0 + s + (ar.q ? ar(seg) : 0.0);
     z[seg] = zi;
     const double yi = __ldg(y + seg);
     acc += yi * zi - (fmax(zi, 0.0) + log1p(exp(-fabs(zi))));
@@ -35,12 +36,12 @@ struct EpiLogit {  // z_i = v0 + s; acc += y_i z_i - log(1 + e^{z_i})
 };
 
 __global__ void __launch_bounds__(kThreads, 1) k_csr_logit(DesignDev D, const double* beta, const double* y,
-                                                           double* z_or_part, double* part) {
+                                                           double* z_or_part, double* part, const double* cbuf) {
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[64];
-  FillVecRef f{beta, D.icpt, 0};
-  const double v0 = D.icpt ? __ldg(beta) : 0.0;
-  EpiLogit e{z_or_part, y, v0, 0.0, D.csr.nslab > 1};
+  FillVecRef f{beta, D.lead(), 0, D.aff.sc};
+  const double v0 = row_const(D, beta, cbuf);
+  EpiLogit e{z_or_part, y, v0, 0.0, D.csr.nslab > 1, aff_row(D, cbuf)};
   run_pass(D.csr, sv, f, e);
   const double t = block_sum(e.acc, red);
   if (threadIdx.x == 0) part[blockIdx.x * kPartStride] = t;
@@ -48,14 +49,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_csr_logit(DesignDev D, const do
 
 // multi column slab: z_i = v0 + sum_s zpart, log-likelihood partials per CTA
 __global__ void __launch_bounds__(kThreads) k_rows_logit(DesignDev D, const double* zpart, const double* beta,
-                                                         const double* y, double* z, double* part) {
+                                                         const double* y, double* z, double* part,
+                                                         const double* cbuf) {
   __shared__ double red[64];
-  const double v0 = D.icpt ? __ldg(beta) : 0.0;
+  const double v0 = row_const(D, beta, cbuf);
+  const AffRow ar = aff_row(D, cbuf);
   double acc = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < D.n; i += (long long)gridDim.x * blockDim.x) {
     double zi = 0.0;
     for (int s = 0; s < D.csr.nslab; ++s) zi += zpart[(long long)s * D.n + i];
     zi += v0;
+    if (ar.q) zi += ar(i);
     z[i] = zi;
     const double yi = __ldg(y + i);
     acc += yi * zi - (fmax(zi, 0.0) + log1p(exp(-fabs(zi))));
@@ -309,14 +313,17 @@ __global__ void __launch_bounds__(256) k_stats(pcgs_gibbs_t G, long long pt, int
 
 int launch_logit(pcgs_design* d, pcgs_gibbs_t* g, cudaStream_t s) {
   const DesignDev& D = d->dev;
+  Scratch S(s);
+  double* cbuf;
+  int rc;
+  if ((rc = aff_pre(d, g->beta, S, s, &cbuf))) return rc;
   if (D.csr.nslab == 1) {
-    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, g->z, g->part);
+    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, g->z, g->part, cbuf);
   } else {
-    Scratch S(s);
     double* zp = S.get<double>((size_t)D.csr.nslab * D.n);
     if (!zp) return fail(PCGS_ENOMEM, "scratch allocation failed");
-    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, zp, g->part);
-    k_rows_logit<<<D.G, kThreads, 0, s>>>(D, zp, g->beta, g->y, g->z, g->part);
+    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, zp, g->part, cbuf);
+    k_rows_logit<<<D.G, kThreads, 0, s>>>(D, zp, g->beta, g->y, g->z, g->part, cbuf);
   }
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;

@@ -91,11 +91,16 @@ struct Scratch {
 // =====================================================================
 // fills and epilogues
 // =====================================================================
-struct FillVecRef {  // CSR slab of a reference-layout p_total vector
+struct FillVecRef {  // CSR slab of a reference-layout p_total vector (u = v / s when scaled)
   const double* v;
-  int icpt;
+  int lead;           // reference offset of pattern column 0
   long long lo;
-  __device__ double operator()(int j) const { return __ldcg(v + icpt + lo + j); }
+  const double* sc;   // affine column scales (reference layout) or null
+  __device__ double operator()(int j) const {
+    const long long r = lead + lo + j;
+    const double x = __ldcg(v + r);
+    return sc ? x / __ldg(sc + r) : x;
+  }
   __device__ void operator()(double* sv, long long l, int len) {
     lo = l;
     fill_smem(sv, len, *this);
@@ -143,19 +148,42 @@ struct EpiStore {  // out[seg] = s
   __device__ void emit(long long seg, double s) { out[seg] = s; }
 };
 
-struct EpiZ {  // matvec, single column slab: out[i] = v0 + s
-  double* out;
-  double v0;
-  __device__ void emit(long long seg, double s) { out[seg] = v0 + s; }
+// Row term of the dense block: (Dn u_D)_i = sum_k Dn[i, k] u_k (q = 0: none).
+struct AffRow {
+  const double* dense;  // n x q
+  const double* u;      // q values of u_D
+  int q;
+  __device__ __forceinline__ double operator()(long long i) const {
+    double t = 0.0;
+    for (int k = 0; k < q; ++k) t += __ldg(dense + i * q + k) * __ldcg(u + k);
+    return t;
+  }
 };
 
-struct EpiW {  // Phi apply, single column slab: w_i = omega_i (v0 + s); acc += w_i z_i
+// The CSR row constant: u_icpt - mu'u for affine designs (cbuf[0], k_aff_pre),
+// else the intercept value v[0] (or 0).
+__device__ __forceinline__ double row_const(const DesignDev& D, const double* v, const double* cbuf) {
+  return cbuf ? __ldcg(cbuf) : (D.icpt ? __ldg(v) : 0.0);
+}
+__device__ __forceinline__ AffRow aff_row(const DesignDev& D, const double* cbuf) {
+  return AffRow{D.aff.dense, cbuf ? cbuf + 1 : nullptr, cbuf ? D.aff.q : 0};
+}
+
+struct EpiZ {  // matvec, single column slab: out[i] = v0 + s (+ dense row term)
+  double* out;
+  double v0;
+  AffRow ar;
+  __device__ void emit(long long seg, double s) { out[seg] = v0 + s + (ar.q ? ar(seg) : 0.0); }
+};
+
+struct EpiW {  // Phi apply, single column slab: w_i = omega_i z_i, z_i = v0 + s (+ row term); acc += w_i z_i
   double* w;
   const double* omega;
   double v0;
   double acc;
+  AffRow ar;
   __device__ void emit(long long seg, double s) {
-    const double z = v0 + s;
+    const double z = v0 + s + (ar.q ? ar(seg) : 0.0);
     const double wi = __ldg(omega + seg) * z;
     w[seg] = wi;
     acc += wi * z;
@@ -180,6 +208,29 @@ struct EpiCsr {  // runtime choice: multi column slab -> partial store, else Epi
   }
 };
 
+
+struct EpiCsrA {  // EpiCsr with the affine row term (dense block) for the affine PCG kernel
+  double* out;
+  const double* omega;
+  double v0;
+  double acc;
+  bool multi;
+  AffRow ar;
+  __device__ void emit(long long seg, double s) {
+    if (multi) {
+      out[seg] = s;
+    } else {
+      const double z = v0 + s + (ar.q ? ar(seg) : 0.0);
+      const double wi = __ldg(omega + seg) * z;
+      out[seg] = wi;
+      acc += wi * z;
+    }
+  }
+};
+
+// Affine designs: launches k_aff_pre for the CSR row constants of v (cbuf is
+// null for pattern-only designs).
+int aff_pre(pcgs_design* d, const double* v, Scratch& S, cudaStream_t s, double** cbuf);
 
 inline size_t smem_bytes(const DesignDev& D) { return (size_t)D.smem_doubles * sizeof(double); }
 

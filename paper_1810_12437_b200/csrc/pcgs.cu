@@ -36,12 +36,13 @@ void set_last_error(const std::string& msg) { g_err = msg; }
 // =====================================================================
 // standalone kernels (one pass each; launched with the plan's G CTAs)
 // =====================================================================
-__global__ void __launch_bounds__(kThreads, 1) k_csr_matvec(DesignDev D, const double* v, double* out) {
+__global__ void __launch_bounds__(kThreads, 1) k_csr_matvec(DesignDev D, const double* v, double* out,
+                                                            const double* cbuf) {
   extern __shared__ __align__(128) double sv[];
-  FillVecRef f{v, D.icpt, 0};
-  const double v0 = D.icpt ? __ldg(v) : 0.0;
+  FillVecRef f{v, D.lead(), 0, D.aff.sc};
+  const double v0 = row_const(D, v, cbuf);
   if (D.csr.nslab == 1) {
-    EpiZ e{out, v0};
+    EpiZ e{out, v0, aff_row(D, cbuf)};
     run_pass(D.csr, sv, f, e, D.dbg);
   } else {
     EpiStore e{out};  // out is the (nslab x n) partial buffer
@@ -49,12 +50,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_csr_matvec(DesignDev D, const d
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_csr_phi(DesignDev D, const double* v, const double* omega, double* w) {
+__global__ void __launch_bounds__(kThreads, 1) k_csr_phi(DesignDev D, const double* v, const double* omega, double* w,
+                                                         const double* cbuf) {
   extern __shared__ __align__(128) double sv[];
-  FillVecRef f{v, D.icpt, 0};
-  const double v0 = D.icpt ? __ldg(v) : 0.0;
+  FillVecRef f{v, D.lead(), 0, D.aff.sc};
+  const double v0 = row_const(D, v, cbuf);
   if (D.csr.nslab == 1) {
-    EpiW e{w, omega, v0, 0.0};
+    EpiW e{w, omega, v0, 0.0, aff_row(D, cbuf)};
     run_pass(D.csr, sv, f, e);
   } else {
     EpiStore e{w};
@@ -62,15 +64,90 @@ __global__ void __launch_bounds__(kThreads, 1) k_csr_phi(DesignDev D, const doub
   }
 }
 
-// multi column slab: z_i = v0 + sum_s part[s*n+i]; out = scale ? scale*z : z
-__global__ void k_rows_combine(DesignDev D, const double* part, const double* v, const double* scale, double* out) {
-  const double v0 = D.icpt ? __ldg(v) : 0.0;
+// multi column slab: z_i = v0 + sum_s part[s*n+i] (+ row term); out = scale ? scale*z : z
+__global__ void k_rows_combine(DesignDev D, const double* part, const double* v, const double* scale, double* out,
+                               const double* cbuf) {
+  const double v0 = row_const(D, v, cbuf);
+  const AffRow ar = aff_row(D, cbuf);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < D.n; i += (long long)gridDim.x * blockDim.x) {
     double z = 0.0;
     for (int s = 0; s < D.csr.nslab; ++s) z += part[(long long)s * D.n + i];
     z += v0;
+    if (ar.q) z += ar(i);
     out[i] = scale ? __ldg(scale + i) * z : z;
   }
+}
+
+// Affine designs, CSR side: cbuf[0] = u_icpt - mu'u, cbuf[1 + k] = u of dense
+// column k (u = v / s); one CTA, fixed-order sum.
+__global__ void __launch_bounds__(kThreads) k_aff_pre(DesignDev D, const double* v, double* cbuf) {
+  __shared__ double red[64];
+  const AffineDev& F = D.aff;
+  double acc = 0.0;
+  for (long long r = threadIdx.x; r < D.pt; r += kThreads) {
+    const double u = F.sc ? v[r] / F.sc[r] : v[r];
+    if (F.mu) acc += F.mu[r] * u;
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) cbuf[0] = (D.icpt ? (F.sc ? v[0] / F.sc[0] : v[0]) : 0.0) - acc;
+  for (int k = threadIdx.x; k < F.q; k += kThreads) {
+    const long long r = D.icpt + k;
+    cbuf[1 + k] = F.sc ? v[r] / F.sc[r] : v[r];
+  }
+}
+
+// Affine designs, transpose side: per-CTA partials of W = sum_i w_i,
+// G_k = sum_i Dn[i,k] w_i and (squares) G2_k = sum_i Dn[i,k]^2 w_i, in line
+// c * (1 + 2q); then k_aff_tw_fin sums the lines in CTA order into gbuf.
+constexpr int kAffMaxQ = 32;
+__global__ void __launch_bounds__(256) k_aff_tw_part(DesignDev D, const double* w, int squares, double* part) {
+  __shared__ double red[64];
+  const int q = D.aff.q, S = 1 + 2 * q;
+  double accW = 0.0, accG[kAffMaxQ], accG2[kAffMaxQ];
+  for (int k = 0; k < q; ++k) accG[k] = accG2[k] = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < D.n; i += (long long)gridDim.x * blockDim.x) {
+    const double wi = __ldcg(w + i);
+    accW += wi;
+    for (int k = 0; k < q; ++k) {
+      const double x = __ldg(D.aff.dense + i * q + k);
+      accG[k] += x * wi;
+      if (squares) accG2[k] += x * x * wi;
+    }
+  }
+  const double tW = block_sum(accW, red);
+  if (threadIdx.x == 0) part[(long long)blockIdx.x * S] = tW;
+  for (int k = 0; k < q; ++k) {
+    const double t = block_sum(accG[k], red);
+    if (threadIdx.x == 0) part[(long long)blockIdx.x * S + 1 + k] = t;
+    if (squares) {
+      const double t2 = block_sum(accG2[k], red);
+      if (threadIdx.x == 0) part[(long long)blockIdx.x * S + 1 + q + k] = t2;
+    }
+  }
+}
+__global__ void k_aff_tw_fin(const double* part, int ncta, int S, double* gbuf) {
+  for (int k = threadIdx.x; k < S; k += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < ncta; ++c) s += part[(long long)c * S + k];
+    gbuf[k] = s;
+  }
+}
+
+// raw column sum of internal column j -> X_eff' w entry: (g - mu W) / s, with
+// g the pattern sum (pieces) or the dense partial G_k; mode 3 (diag(X'Omega X)
+// with w = omega) uses the squared form (g (1 - 2 mu) + mu^2 W) / s^2 for
+// binary columns and (G2 - 2 mu G + mu^2 W) / s^2 for dense ones.
+__device__ __forceinline__ double aff_col(const DesignDev& D, long long j, long long r, double raw,
+                                          const double* gbuf, int mode) {
+  const AffineDev& F = D.aff;
+  const double W = gbuf[0];
+  const double mu = F.mu ? __ldg(F.mu + r) : 0.0, s = F.sc ? __ldg(F.sc + r) : 1.0;
+  const long long k = j - D.p - D.icpt;  // dense column index (k >= 0)
+  if (mode == 3) {
+    if (k >= 0) return (gbuf[1 + F.q + k] - 2.0 * mu * raw + mu * mu * W) / (s * s);
+    return (raw * (1.0 - 2.0 * mu) + mu * mu * W) / (s * s);
+  }
+  return (raw - mu * W) / s;
 }
 
 // u_i = kappa_i + sqrt(omega_i) eta_i for every row (the RHS pass's input)
@@ -93,10 +170,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_csc_vec(DesignDev D, const doub
 //               + sqrt(diag_j) * delta_j           (mode 2: RHS noise)
 __global__ void k_assemble(DesignDev D, const double* pieces, const double* diag, const double* v,
                            const double* delta, unsigned long long seed, unsigned long long stream, int mode,
-                           double* out, const double* linear = nullptr) {
+                           double* out, const double* linear = nullptr, const double* gbuf = nullptr) {
   for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < D.pt; j += (long long)gridDim.x * blockDim.x) {
-    const long long r = ref_index(j, D.p, D.icpt);
-    double s = column_sum(D.csc, pieces, D.pt, j);
+    const long long r = ref_index(j, D.p, D.lead());
+    double s;
+    if (gbuf) {
+      const long long k = j - D.p - D.icpt;
+      const double raw = k >= 0 ? gbuf[1 + k] : column_sum(D.csc, pieces, D.pt, j);
+      s = aff_col(D, j, r, raw, gbuf, mode);
+    } else {
+      s = column_sum(D.csc, pieces, D.pt, j);
+    }
     if (mode == 1) {
       s += __ldg(diag + r) * __ldg(v + r);
     } else if (mode == 2) {
@@ -142,6 +226,7 @@ struct PcgArgs {
   double* part;    // 4 * G partial sums: dAd, rms, rz, spare
   unsigned long long* prof;  // optional: CTA-0 phase timestamps (ns), 4 per apply
   double* iterates;  // optional (trace_level "full"): [max_iter+1][p_total], reference layout
+  double* apart;     // affine designs: per-CTA lines of W and the dense sums G_k (1 + q each)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -337,6 +422,17 @@ __device__ __forceinline__ void trace_stamp(const PcgArgs& A, int a, int k) {
     g_sync_times[16 * blockIdx.x + 8 + k] = gtimer();
 }
 
+// Affine designs: u = v / s of reference column r (the gathered quantity).
+__device__ __forceinline__ double aff_u(const DesignDev& D, long long r, double v) {
+  return D.aff.sc ? v / __ldg(D.aff.sc + r) : v;
+}
+// CTA partial of mu' u over the CTA's own columns -> part slot 3 (call with the whole CTA)
+__device__ __forceinline__ void aff_mu_partial(const PcgArgs& A, double acc, double* red) {
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) A.part[blockIdx.x * kPartStride + 3] = t;
+}
+
+template <bool AFF>
 __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
   // Loop state lives in shared memory so that the inlined streaming passes
   // get the whole register budget (1024 threads -> 64 registers).
@@ -346,6 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
   __shared__ double st_rz;
   __shared__ int st_status, st_iter, st_fail, st_applies;
   __shared__ unsigned long long mbar;
+  __shared__ double affg[AFF ? 1 + kAffMaxQ : 1];  // affine designs: W, G_k
   BulkFill bf;
   bulk_init(bf, &mbar);
   const int tid = threadIdx.x;
@@ -361,13 +458,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       const long long j = j0 + t;
       double xv = 0, m = 0, sc = 0, dg = 0, bv = 0;
       if (j < pt) {
-        const long long rj = ref_index(j, A.D.p, A.D.icpt);
+        const long long rj = ref_index(j, A.D.p, A.D.lead());
         xv = A.x[rj];
         m = __ldg(A.minv + rj);
         sc = __ldg(A.scale + rj);
         dg = __ldg(A.diag + rj);
         bv = __ldg(A.b + rj);
-        A.dvg[dvs + j] = xv;  // v = x0 for the first application
+        A.dvg[dvs + j] = AFF ? aff_u(A.D, rj, xv) : xv;  // v = x0 for the first application
         if (A.iterates) A.iterates[rj] = xv;
       }
       o.x[t] = xv;
@@ -393,6 +490,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       st_iter = 0;
       st_fail = -1;
       st_applies = 0;
+    }
+    if (AFF) {
+      double mu_u = 0.0;
+      if (A.D.aff.mu)
+        for (int t = tid; t < chunk; t += kThreads) {
+          const long long j = j0 + t;
+          if (j < pt) {
+            const long long rj = ref_index(j, A.D.p, A.D.lead());
+            mu_u += __ldg(A.D.aff.mu + rj) * aff_u(A.D, rj, o.x[t]);
+          }
+        }
+      aff_mu_partial(A, mu_u, red);
     }
   }
   cg::this_grid().sync();
@@ -433,11 +542,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       }
       if (stop) break;
       // new direction d = z + beta d on the owned slice, published for the fill
+      // (affine designs publish u = d / s and the CTA partial of mu'u)
+      double mu_u = 0.0;
       for (int t = tid; t < chunk; t += kThreads) {
         const double dn = a == 1 ? o.z[t] : fma(beta, o.d[t], o.z[t]);
         o.d[t] = dn;
-        if (j0 + t < pt) A.dvg[(a & 1) * dvs + j0 + t] = dn;
+        if (j0 + t < pt) {
+          if (AFF) {
+            const long long rj = ref_index(j0 + t, A.D.p, A.D.lead());
+            const double u = aff_u(A.D, rj, dn);
+            A.dvg[(a & 1) * dvs + j0 + t] = u;
+            if (A.D.aff.mu) mu_u += __ldg(A.D.aff.mu + rj) * u;
+          } else {
+            A.dvg[(a & 1) * dvs + j0 + t] = dn;
+          }
+        }
       }
+      if (AFF) aff_mu_partial(A, mu_u, red);
       traced_sync(A, a, 0);
     }
     if (prof) A.prof[4 * a + 0] = gtimer();
@@ -445,12 +566,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     // ---------------- phase A: CSR pass, w = omega (X v) ----------------
     double acc_dAd = 0.0;
     for (int t = tid; t < chunk; t += kThreads) acc_dAd += o.D[t] * o.d[t] * o.d[t];
-    {
-      const double* vcur = A.dvg + (a == 0 ? dvs : (a & 1) * dvs);
+    const double* vcur = A.dvg + (a == 0 ? dvs : (a & 1) * dvs);
+    if (!AFF) {
       if (tid == 0) bc[2] = A.D.icpt ? __ldcg(vcur + A.D.p) : 0.0;
       __syncthreads();
       const bool multi = A.D.csr.nslab > 1;
       EpiCsr e{multi ? A.zpart : A.w, A.omega, bc[2], 0.0, multi};
+      FillBulk f{vcur, &bf};
+      run_pass(A.D.csr, sv, f, e, A.D.dbg);
+      acc_dAd += e.acc;
+    } else {
+      // row constant u_icpt - mu'u (grid sum of the CTA partials, fixed order);
+      // the dense block's u values are read from the published vector
+      const double mu_u = reduce_partials(A.part + 3, gridDim.x, bc + 3);
+      if (tid == 0) bc[2] = (A.D.icpt ? __ldcg(vcur + A.D.p) : 0.0) - mu_u;
+      __syncthreads();
+      const bool multi = A.D.csr.nslab > 1;
+      EpiCsrA e{multi ? A.zpart : A.w, A.omega, bc[2], 0.0, multi,
+                AffRow{A.D.aff.dense, vcur + A.D.p + A.D.icpt, A.D.aff.q}};
       FillBulk f{vcur, &bf};
       run_pass(A.D.csr, sv, f, e, A.D.dbg);
       acc_dAd += e.acc;
@@ -459,10 +592,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       cg::this_grid().sync();
       const long long n = A.D.n;
       const double v0 = bc[2];
+      const AffRow ar{A.D.aff.dense, vcur + A.D.p + A.D.icpt, AFF ? A.D.aff.q : 0};
       for (long long i = (long long)blockIdx.x * kThreads + tid; i < n; i += (long long)gridDim.x * kThreads) {
         double z = 0.0;
         for (int s = 0; s < A.D.csr.nslab; ++s) z += __ldcg(A.zpart + (long long)s * n + i);
         z += v0;
+        if (AFF && ar.q) z += ar(i);
         const double wi = __ldg(A.omega + i) * z;
         A.w[i] = wi;
         acc_dAd += wi * z;
@@ -474,6 +609,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     }
     if (prof) A.prof[4 * a + 1] = gtimer();
     traced_sync(A, a, 1);
+    if (AFF) {  // W = sum w and G_k = sum Dn[i,k] w_i: CTA partials over a row range
+      const int q = A.D.aff.q, L = 1 + q;
+      const long long n = A.D.n, r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
+      for (int k = 0; k < L; ++k) {
+        double acc = 0.0;
+        for (long long i = r0 + tid; i < r1; i += kThreads) {
+          const double wi = __ldcg(A.w + i);
+          acc += k == 0 ? wi : __ldg(A.D.aff.dense + i * q + (k - 1)) * wi;
+        }
+        const double t = block_sum(acc, red);
+        if (tid == 0) A.apart[(long long)blockIdx.x * L + k] = t;
+      }
+    }
 
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
     {
@@ -515,6 +663,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       if (blockIdx.x == 0 && tid == 0) A.alphas[a - 1] = alpha;
     }
     trace_stamp(A, a, 2);
+    if (AFF) {  // grid totals of W and G_k (warp k sums line slot k over the CTAs, fixed order)
+      const int L = 1 + A.D.aff.q, warp = tid >> 5, lane = tid & 31;
+      if (warp < L) {
+        double acc = 0.0;
+        for (int c = lane; c < (int)gridDim.x; c += 32) acc += __ldcg(A.apart + (long long)c * L + warp);
+        acc = warp_sum(acc);
+        if (lane == 0) affg[warp] = acc;
+      }
+      __syncthreads();
+    }
+    // affine designs: raw column sum -> (g - mu W) / s, dense columns from G_k
+    auto aff_ad = [&](int t, double cs) -> double {
+      if (!AFF) return cs;
+      const long long j = j0 + t, r = ref_index(j, A.D.p, A.D.lead()), k = j - A.D.p - A.D.icpt;
+      const double raw = k >= 0 ? affg[1 + k] : cs;
+      const double mu = A.D.aff.mu ? __ldg(A.D.aff.mu + r) : 0.0, sc = A.D.aff.sc ? __ldg(A.D.aff.sc + r) : 1.0;
+      return (raw - mu * affg[0]) / sc;
+    };
     double t_rms = 0.0, t_rz = 0.0;
     constexpr int GS = 4;  // lanes per column in the flat path (slabs g, g+4)
     for (int t0 = 0; t0 < chunk; t0 += (flat ? kThreads / GS : kThreads)) {
@@ -524,11 +690,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
         t = t0 + tid / GS;
         const double cs = group_column_sum<GS>(o, S, chunk, t, tid & (GS - 1), sv);
         if ((tid & (GS - 1)) != 0 || t >= chunk || j0 + t >= pt) continue;
-        Ad = cs + o.D[t] * o.d[t];
+        Ad = aff_ad(t, cs) + o.D[t] * o.d[t];
       } else {
         t = t0 + tid;
         if (t >= chunk || j0 + t >= pt) continue;
-        Ad = owned_column_sum(o, A.pieces, S, chunk, t, sv, staged) + o.D[t] * o.d[t];
+        Ad = aff_ad(t, owned_column_sum(o, A.pieces, S, chunk, t, sv, staged)) + o.D[t] * o.d[t];
       }
       double rv;
       if (a == 0) {
@@ -536,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       } else {
         o.x[t] = fma(alpha, o.d[t], o.x[t]);
         rv = fma(-alpha, Ad, o.r[t]);
-        if (A.iterates) A.iterates[(long long)a * pt + ref_index(j0 + t, A.D.p, A.D.icpt)] = o.x[t];
+        if (A.iterates) A.iterates[(long long)a * pt + ref_index(j0 + t, A.D.p, A.D.lead())] = o.x[t];
       }
       o.r[t] = rv;
       const double zn = o.m[t] * rv;
@@ -562,7 +728,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     const long long j0 = (long long)blockIdx.x * chunk;
     const OwnState o = own_state(sv, A.D, chunk, j0);
     for (int t = tid; t < chunk; t += kThreads)
-      if (j0 + t < pt) A.x[ref_index(j0 + t, A.D.p, A.D.icpt)] = o.x[t];
+      if (j0 + t < pt) A.x[ref_index(j0 + t, A.D.p, A.D.lead())] = o.x[t];
   }
   if (blockIdx.x == 0 && tid == 0) {
     A.result[0] = st_iter;
@@ -663,7 +829,7 @@ static int set_smem_attrs() {
   int rc;
   if ((rc = raise_smem_limit(k_csr_matvec)) || (rc = raise_smem_limit(k_csr_phi)) ||
       (rc = raise_smem_limit(k_csc_vec)) ||
-      (rc = raise_smem_limit(k_pcg)))
+      (rc = raise_smem_limit(k_pcg<false>)) || (rc = raise_smem_limit(k_pcg<true>)))
     return rc;
   return PCGS_OK;
 }
@@ -675,6 +841,22 @@ int pcgs_design_create(int64_t n, int64_t p, const int64_t* row_ptr_h, const int
 
 int pcgs_design_create_ex(int64_t n, int64_t p, const int64_t* row_ptr_h, const int32_t* col_idx_h, int intercept,
                           int slab_max, int device, int grid, pcgs_design_t* out) {
+  return pcgs_design_create_affine(n, p, row_ptr_h, col_idx_h, intercept, 0, slab_max, device, grid, out);
+}
+
+int pcgs_design_set_affine(pcgs_design_t d, const double* dense, const double* mu, const double* sc) {
+  if (!d) return fail(PCGS_EINVAL, "null design");
+  AffineDev& F = d->dev.aff;
+  if (F.q > 0 && !dense) return fail(PCGS_EINVAL, "the design has dense columns: dense values required");
+  F.dense = F.q > 0 ? dense : nullptr;
+  F.mu = mu;
+  F.sc = sc;
+  F.on = F.q > 0 || mu || sc;
+  return PCGS_OK;
+}
+
+int pcgs_design_create_affine(int64_t n, int64_t p, const int64_t* row_ptr_h, const int32_t* col_idx_h,
+                              int intercept, int q_dense, int slab_max, int device, int grid, pcgs_design_t* out) {
   if (!out || !row_ptr_h || (!col_idx_h && row_ptr_h[n] > 0)) return fail(PCGS_EINVAL, "null argument");
   *out = nullptr;
   CUDA_TRY(cudaSetDevice(device));
@@ -683,10 +865,12 @@ int pcgs_design_create_ex(int64_t n, int64_t p, const int64_t* row_ptr_h, const 
   const int sms = std::min(prop.multiProcessorCount, kMaxGrid);
   if (grid < 0 || grid > sms) return fail(PCGS_EINVAL, "grid must be in [0, SM count]");
   const int G = grid > 0 ? grid : sms;
+  if (q_dense < 0 || q_dense > kAffMaxQ) return fail(PCGS_EINVAL, "dense block: at most 32 columns");
   DesignHost H;
-  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H);
+  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H, q_dense);
   if (!err.empty()) return fail(PCGS_EINVAL, err);
   pcgs_design* D = new pcgs_design();
+  D->dev.aff = AffineDev{0, q_dense, nullptr, nullptr, nullptr};
   D->device = device;
   DesignDev& dd = D->dev;
   dd.n = n;
@@ -861,19 +1045,53 @@ int pcgs_design_info(pcgs_design_t d, int64_t* info_h) {
   return PCGS_OK;
 }
 
+}  // extern "C"
+
+// Affine designs: the CSR row constants (cbuf) of a reference-layout vector v.
+int aff_pre(pcgs_design* d, const double* v, Scratch& S, cudaStream_t s, double** cbuf) {
+  *cbuf = nullptr;
+  const DesignDev& D = d->dev;
+  if (!D.aff.on) return PCGS_OK;
+  *cbuf = S.get<double>(1 + D.aff.q);
+  if (!*cbuf) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  k_aff_pre<<<1, kThreads, 0, s>>>(D, v, *cbuf);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
+extern "C" {
+
+// Affine designs: W and the dense-column sums of w (gbuf, see k_aff_tw_part).
+static int aff_tw(pcgs_design_t d, const double* w, int squares, Scratch& S, cudaStream_t s, double** gbuf) {
+  *gbuf = nullptr;
+  const DesignDev& D = d->dev;
+  if (!D.aff.on) return PCGS_OK;
+  const int Sw = 1 + 2 * D.aff.q;
+  double* part = S.get<double>((size_t)D.G * Sw);
+  *gbuf = S.get<double>(Sw);
+  if (!part || !*gbuf) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  k_aff_tw_part<<<D.G, 256, 0, s>>>(D, w, squares, part);
+  k_aff_tw_fin<<<1, 64, 0, s>>>(part, D.G, Sw, *gbuf);
+  CUDA_TRY(cudaGetLastError());
+  return PCGS_OK;
+}
+
 static int launch_csr(pcgs_design_t d, bool phi, const double* v, const double* omega, double* out, cudaStream_t s,
                       Scratch& S) {
   const DesignDev& D = d->dev;
   const size_t sm = smem_bytes(D);
+  double* cbuf;
+  int rc;
+  if ((rc = aff_pre(d, v, S, s, &cbuf))) return rc;
   if (D.csr.nslab == 1) {
-    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, out);
-    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, out);
+    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, out, cbuf);
+    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, out, cbuf);
   } else {
     double* part = S.get<double>((size_t)D.csr.nslab * D.n);
     if (!part) return fail(PCGS_ENOMEM, "scratch allocation failed");
-    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, part);
-    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, part);
-    k_rows_combine<<<D.G * 4, 256, 0, s>>>(D, part, v, phi ? omega : nullptr, out);
+    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, part, cbuf);
+    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, part, cbuf);
+    k_rows_combine<<<D.G * 4, 256, 0, s>>>(D, part, v, phi ? omega : nullptr, out, cbuf);
   }
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
@@ -895,8 +1113,12 @@ int pcgs_matvec_t(pcgs_design_t d, const double* w, double* out, pcgs_stream_t s
   Scratch S(s);
   double* pieces = S.get<double>(D.csc.nseg);
   if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  double* gbuf;
+  int rc;
+  if ((rc = aff_tw(d, w, 0, S, s, &gbuf))) return rc;
   k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, w, pieces);
-  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, nullptr, nullptr, nullptr, 0, 0, 0, out);
+  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, nullptr, nullptr, nullptr, 0, 0, 0, out, nullptr,
+                                                       gbuf);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
 }
@@ -912,8 +1134,11 @@ int pcgs_phi_apply(pcgs_design_t d, const double* omega, const double* prior_dia
   if (!w || !pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
   int rc = launch_csr(d, true, v, omega, w, s, S);
   if (rc) return rc;
+  double* gbuf;
+  if ((rc = aff_tw(d, w, 0, S, s, &gbuf))) return rc;
   k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, w, pieces);
-  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, v, nullptr, 0, 0, 1, out);
+  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, v, nullptr, 0, 0, 1, out, nullptr,
+                                                       gbuf);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
 }
@@ -926,8 +1151,12 @@ int pcgs_phi_diagonal(pcgs_design_t d, const double* omega, const double* prior_
   Scratch S(s);
   double* pieces = S.get<double>(D.csc.nseg);
   if (!pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  double* gbuf;
+  int rc;
+  if ((rc = aff_tw(d, omega, 1, S, s, &gbuf))) return rc;
   k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, omega, pieces);
-  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, nullptr, 0, 0, 3, out);
+  k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, nullptr, 0, 0, 3, out, nullptr,
+                                                       gbuf);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
 }
@@ -946,9 +1175,12 @@ int pcgs_rhs(pcgs_design_t d, const double* kappa, const double* omega, const do
   // CSC pass TMA-fills its row slabs from u like any X' w
   FillRhs f{kappa, omega, eta, seed, kStreamEta ^ stream_id, 0};
   k_rhs_u<<<(int)std::min<long long>((D.n + 255) / 256, 148 * 8), 256, 0, s>>>(f, D.n, u);
+  double* gbuf;
+  int rc;
+  if ((rc = aff_tw(d, u, 0, S, s, &gbuf))) return rc;
   k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, u, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, delta, seed,
-                                                       kStreamDelta ^ stream_id, 2, b, linear);
+                                                       kStreamDelta ^ stream_id, 2, b, linear, gbuf);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
 }
@@ -999,6 +1231,11 @@ int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag
   }
   if (!A.w || !A.pieces || !A.zv || !A.dvg || !A.part || (D.csr.nslab > 1 && !A.zpart))
     return fail(PCGS_ENOMEM, "scratch allocation failed");
+  A.apart = nullptr;
+  if (D.aff.on) {
+    A.apart = S.get<double>((size_t)D.G * (1 + D.aff.q));
+    if (!A.apart) return fail(PCGS_ENOMEM, "scratch allocation failed");
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(D.G);
   cfg.blockDim = dim3(kThreads);
@@ -1028,7 +1265,8 @@ int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag
   }
   cfg.attrs = attrs;
   cfg.numAttrs = na;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pcg, A));
+  if (D.aff.on) CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pcg<true>, A));
+  else CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pcg<false>, A));
   return PCGS_OK;
 }
 

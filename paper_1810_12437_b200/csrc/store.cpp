@@ -297,7 +297,8 @@ std::string validate_csr(int64_t n, int64_t p, const int64_t* row_ptr, const int
 }
 
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
-                         int intercept, int slab_max, int G, DesignHost& D) {
+                         int intercept, int slab_max, int G, DesignHost& D, int q_dense) {
+  if (q_dense < 0 || (q_dense > 0 && intercept)) return "dense columns replace the intercept flag";
   {
     std::string err = validate_csr(n, p, row_ptr, col_idx);
     if (!err.empty()) return err;
@@ -309,7 +310,8 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
   D.n = n;
   D.p = p;
   D.intercept = intercept ? 1 : 0;
-  D.p_total = p + D.intercept;
+  D.q_dense = q_dense;
+  D.p_total = p + D.intercept + q_dense;
   D.nnz = nnz;
   D.slab_max = (int)smax;
 
@@ -370,9 +372,9 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
           int64_t k = cursor[j];
           while (k < col_ptr[j + 1] && row_idx[k] < hi) tmp.push_back((uint16_t)(row_idx[k++] - lo));
           cursor[j] = k;
-        } else {
+        } else if (j < p + D.intercept) {
           for (int64_t i = lo; i < hi; ++i) tmp.push_back((uint16_t)(i - lo));
-        }
+        }  // dense columns (j >= p + intercept): no pattern pieces
         const int64_t len = (int64_t)tmp.size();
         for (int64_t a = 0; a < len; a += piece_max_vec() * kVecIdx) {
           const int64_t m = std::min<int64_t>(piece_max_vec() * kVecIdx, len - a);

@@ -61,6 +61,7 @@ struct PassHost {
 struct DesignHost {
   int64_t n = 0, p = 0, p_total = 0, nnz = 0;
   int intercept = 0;
+  int q_dense = 0;    // dense real columns after the pattern (and intercept) in the internal layout
   int slab_max = 0;
   PassHost csr, csc;
 };
@@ -72,7 +73,7 @@ std::string validate_csr(int64_t n, int64_t p, const int64_t* row_ptr, const int
 // Validates the CSR (sparse.py:94-117 invariants) and builds both passes for a
 // grid of G CTAs.  Returns an empty string on success, else an error message.
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
-                         int intercept, int slab_max, int G, DesignHost& out);
+                         int intercept, int slab_max, int G, DesignHost& out, int q_dense = 0);
 
 // Native synthetic binary design (bench/test infrastructure): returns nnz.
 int64_t synth_binary_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint64_t seed,

@@ -180,16 +180,16 @@ class _Reparam:
     b~_0 = b_0 - sum_j mu_j b~_j, so the device samples b~ on the raw pattern
     (exactly the same posterior; include/pcgs.h, pcgs_gibbs_t.cscale)."""
 
-    def __init__(self, X, cfg):
-        mu = np.asarray(X.col_means, dtype=np.float64)
-        sc = np.asarray(X.col_scales, dtype=np.float64)
+    @staticmethod
+    def applies(X, cfg):
+        if not X.standardized or X.dense_block is not None:
+            return False
         flat0 = cfg.n_unshrunk >= 1 and not np.isfinite(cfg.unshrunk_prior_sd[0])
-        if not (X.has_intercept and mu[0] == 0.0 and sc[0] == 1.0 and flat0):
-            raise NotImplementedError(
-                "standardised designs run on the device through an exact reparametrisation that "
-                "needs an unstandardised intercept column 0 with a flat prior "
-                "(standardize(exclude=[0]) and unshrunk_prior_sd=(inf, ...))")
-        self.mu, self.s = mu, sc
+        return bool(X.has_intercept and X.col_means[0] == 0.0 and X.col_scales[0] == 1.0 and flat0)
+
+    def __init__(self, X, cfg):
+        self.mu = np.asarray(X.col_means, dtype=np.float64)
+        self.s = np.asarray(X.col_scales, dtype=np.float64)
 
     def to_sampled(self, beta):
         bt = np.asarray(beta, dtype=np.float64) / self.s
@@ -215,6 +215,11 @@ class DeviceChain:
         t = _lib.torch()
         self.X = X
         self._grid_req = int(grid)
+        # standardised pattern-only designs with an unstandardised flat-prior
+        # intercept sample on the raw pattern (_Reparam); every other design
+        # with affine terms (dense block, standardisation) runs on the affine
+        # store directly (model coefficients)
+        self.reparam = _Reparam(X, cfg) if _Reparam.applies(X, cfg) else None
         self._open_device(X, device)
         dev = self.dev
         f64 = t.float64
@@ -225,7 +230,6 @@ class DeviceChain:
         self.horseshoe = isinstance(cfg, HorseshoeConfig)
         self.n_iter, self.burn_in, self.thin = n_iter, burn_in, thin
         self.seed = int(seed)
-        self.reparam = _Reparam(X, cfg) if X.standardized else None
         cgc = cg_config if cg_config is not None else CGConfig()
         if cgc.trace_level == "full":
             raise NotImplementedError("trace_level='full' is not on the device path")
@@ -305,7 +309,7 @@ class DeviceChain:
         self._init_device()
 
     def _open_device(self, X, device):
-        self.store = X.device_store(device, grid=self._grid_req)
+        self.store = X.device_store(device, grid=self._grid_req, raw=self.reparam is not None)
         self.dev = self.store.device
         self.grid = self.store.describe()["grid"]
 

@@ -42,6 +42,8 @@ def row_partition(row_ptr, world, intercept=True):
 
 def local_rows(X: SparseDesignMatrix, lo, hi) -> SparseDesignMatrix:
     """The row block [lo, hi) of a design as its own pattern-only design."""
+    if X.affine:
+        raise NotImplementedError("row split: designs with a dense block or standardisation are not sharded")
     rp, ci, icpt = X.pattern()
     sub_rp = rp[lo:hi + 1] - rp[lo]
     sub_ci = ci[rp[lo]:rp[hi]]
@@ -346,8 +348,9 @@ def _row_split_chain_class():
             super().__init__(X, y, cfg, n_iter, device=device, **kw)
 
         def _open_device(self, X, device):
-            if X.standardized:
-                raise NotImplementedError("row split: standardised designs are not sharded")
+            if X.affine:
+                raise NotImplementedError("row split: designs with a dense block or standardisation are "
+                                          "not sharded")
             shards = [local_rows(X, *self._parts[r]) for r in self._hosted]
             self.rs = RowSplitPCG(shards, device=device, group=self._group, exchange=self._exchange)
             self.store = None

@@ -90,17 +90,11 @@ class PrecisionOperator:
 
     @property
     def _pcgs_device_operator(self):
-        return not self.X.standardized
+        return True
 
     def apply_into(self, v, out):
-        """out = Phi v on CUDA tensors (any design, incl. standardised)."""
-        if not self.X.standardized:
-            return self.store.phi_apply(self.device_omega(), self.device_diag(), v, out)
-        z = self.X.device_matvec(v)
-        z *= self.device_omega()
-        out.copy_(self.X.device_matvec_t(z))
-        out.addcmul_(self.device_diag(), v)
-        return out
+        """out = Phi v on CUDA tensors (any design: affine terms in-kernel)."""
+        return self.store.phi_apply(self.device_omega(), self.device_diag(), v, out)
 
     @property
     def store(self):
@@ -187,15 +181,6 @@ def generate_rhs(target: GaussianTarget, rng) -> np.ndarray:
         eta_d, delta_d = _lib.to_device(eta, dev), _lib.to_device(delta, dev)
         seed, sid = 0, 0
     lin = _lib.to_device(target.linear_term, dev)
-    if phi.X.standardized:   # X_s' = S^-1 (X' - mu 1'): compose on device
-        if eta_d is None:
-            g = t.Generator(device=dev)
-            g.manual_seed((seed ^ sid) & (2 ** 63 - 1))
-            eta_d = t.randn(n, generator=g, dtype=t.float64, device=dev)
-            delta_d = t.randn(p, generator=g, dtype=t.float64, device=dev)
-        b = lin + phi.X.device_matvec_t(phi.device_omega().sqrt() * eta_d)
-        b += phi.device_diag().sqrt() * delta_d
-        return b if _lib.is_tensor(target.linear_term) else b.cpu().numpy()
     b = t.empty(p, dtype=t.float64, device=dev)
     _lib.check(_lib.lib().pcgs_rhs(st.handle, 0, _lib.ptr(phi.device_omega()),
                                    _lib.ptr(phi.device_diag()), _lib.ptr(lin), _lib.ptr(eta_d),

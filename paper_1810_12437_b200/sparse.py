@@ -68,15 +68,17 @@ def _check_csr(n, p, row_ptr, col_idx, nvals):
 class DesignStore:
     """Owner of one libpcgs design handle on one CUDA device."""
 
-    def __init__(self, n, p, row_ptr, col_idx, intercept, device=None, slab_max=0, grid=0):
+    def __init__(self, n, p, row_ptr, col_idx, intercept, device=None, slab_max=0, grid=0, q_dense=0):
         L = _lib.lib()
         self.device = _lib.cuda_device(device)
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col_idx, dtype=np.int32)
         h = ctypes.c_void_p()
-        _lib.check(L.pcgs_design_create_ex(int(n), int(p), rp.ctypes.data, ci.ctypes.data,
-                                           int(bool(intercept)), int(slab_max),
-                                           int(self.device.index), int(grid), ctypes.byref(h)))
+        _lib.check(L.pcgs_design_create_affine(int(n), int(p), rp.ctypes.data, ci.ctypes.data,
+                                               int(bool(intercept)), int(q_dense), int(slab_max),
+                                               int(self.device.index), int(grid), ctypes.byref(h)))
+        self.q_dense = int(q_dense)
+        self._affine = None   # (dense, mu, sc) device tensors kept alive while attached
         self._h = h
         info = np.zeros(16, dtype=np.int64)
         _lib.check(L.pcgs_design_info(h, info.ctypes.data))
@@ -87,6 +89,14 @@ class DesignStore:
     @property
     def handle(self):
         return self._h
+
+    def set_affine(self, dense=None, mu=None, sc=None):
+        """Attach the affine terms (dense block values, column means / scales,
+        reference layout) to the device handle; None detaches one."""
+        self._affine = (dense, mu, sc)
+        _lib.check(_lib.lib().pcgs_design_set_affine(
+            self._h, _lib.ptr(dense) if dense is not None else None, _lib.ptr(mu) if mu is not None else None,
+            _lib.ptr(sc) if sc is not None else None))
 
     def describe(self) -> dict:
         keys = ["n", "p", "p_total", "nnz", "csr_slabs", "csc_slabs", "csr_vectors",
@@ -256,6 +266,8 @@ class SparseDesignMatrix:
 
     @property
     def nnz(self):
+        if self._values is not None:
+            return len(self._values)
         if self._pattern is not None:
             rp, _, icpt = self._pattern
             return int(rp[-1]) + (self.n_rows if icpt else 0)
@@ -267,8 +279,7 @@ class SparseDesignMatrix:
         if self._pattern is not None:
             return self._pattern
         if not np.all(self._values == 1.0):
-            raise NotImplementedError(
-                "the B200 store is pattern-only: every stored value must be 1.0 (binary design)")
+            return self._dense_pattern()
         rp, ci, n = self._row_ptr, self._col_idx, self.n_rows
         counts = np.diff(rp)
         icpt = False
@@ -285,27 +296,89 @@ class SparseDesignMatrix:
         self._pattern = (srp, sci, icpt)
         return self._pattern
 
+    def _dense_pattern(self):
+        """A design [Dn | B] with a leading block of q fully stored real
+        columns (hstack_dense_columns of a real block, sparse.py:314-341) and a
+        binary remainder: the pattern of B plus the dense values (n, q).  The
+        device applies Dn through the affine terms of the store."""
+        rp, ci, vals, n = self._row_ptr, self._col_idx, self._values, self.n_rows
+        counts = np.diff(rp)
+        q = 0
+        while q < self.n_cols and n > 0 and np.all(counts > q) and np.all(ci[rp[:-1] + q] == q):
+            q += 1
+        rest = np.ones(len(ci), dtype=bool)
+        if q:
+            rest[(rp[:-1, None] + np.arange(q)).ravel()] = False
+        if q == 0 or not np.all(vals[rest] == 1.0):
+            raise NotImplementedError(
+                "the B200 store is pattern-only apart from a leading dense block: every value outside "
+                "the leading fully stored columns must be 1.0 (binary design)")
+        if q > 32:
+            raise NotImplementedError("a leading dense block of more than 32 columns is not on the device path")
+        self._dense = np.ascontiguousarray(vals[~rest].reshape(n, q))
+        srp = rp - q * np.arange(n + 1, dtype=np.int64)
+        sci = (ci[rest] - q).astype(np.int32)
+        self._pattern = (srp, sci, False)
+        return self._pattern
+
+    @property
+    def dense_block(self):
+        """Leading dense real columns (n, q) handled by the affine terms, or None."""
+        self.pattern()
+        return getattr(self, "_dense", None)
+
+    @property
+    def affine(self):
+        """True when the device applies affine terms (dense block or standardisation)."""
+        return self.dense_block is not None or self.standardized
+
     @property
     def has_intercept(self):
         return self.pattern()[2]
 
-    def device_store(self, device=None, grid=0) -> DesignStore:
-        """The pattern-only store on `device`; `grid` > 0 plans it for that
-        many CTAs (row-split shards or chains side by side sharing a GPU)."""
+    def device_store(self, device=None, grid=0, raw=False) -> DesignStore:
+        """The store on `device`; `grid` > 0 plans it for that many CTAs
+        (row-split shards or chains side by side sharing a GPU).  The affine
+        terms (dense block, standardisation) are attached to it and follow
+        later standardize() calls; `raw` = the pattern-only view of a
+        pattern-only design (the Gibbs reparametrisation of standardised
+        designs samples on the raw pattern)."""
         dev = _lib.cuda_device(device)
-        key = (dev.index, 1, int(grid))
+        rp, ci, icpt = self.pattern()
+        dense = self.dense_block
+        key = (dev.index, 1, int(grid), bool(raw))
         st = self._stores.get(key)
         if st is None:
-            rp, ci, icpt = self.pattern()
-            st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0), rp, ci, icpt,
-                             device=dev, slab_max=self.slab_max, grid=grid)
+            q = 0 if dense is None else dense.shape[1]
+            st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0) - q, rp, ci, icpt,
+                             device=dev, slab_max=self.slab_max, grid=grid, q_dense=q)
             self._stores[key] = st
+        if raw:
+            if dense is not None:
+                raise ValueError("a design with a dense block has no raw pattern view")
+            return st
+        std = self.standardized
+        src = (self.col_means if std else None, self.col_scales if std else None)
+        cur = getattr(st, "_affine_src", None)
+        if dense is None and not std:
+            if st._affine is not None:
+                st.set_affine(None, None, None)
+                st._affine, st._affine_src = None, None
+        elif cur is None or cur[0] is not src[0] or cur[1] is not src[1]:
+            dd = _lib.to_device(dense, dev) if dense is not None else None
+            mu = _lib.to_device(src[0], dev) if std else None
+            sc = _lib.to_device(src[1], dev) if std else None
+            st.set_affine(dd, mu, sc)
+            st._affine_src = src
         return st
 
     def batch_store(self, nchains, device=None, grid=0):
         """The sliced store of R = `nchains` batched chains on `device`
         (batched.BatchStore; built once per (device, R, grid))."""
         from .batched import BatchStore
+        if self.affine:
+            raise NotImplementedError("batched chains: designs with a dense block or standardisation are "
+                                      "not on the batched path")
         dev = _lib.cuda_device(device)
         key = (dev.index, "batch", int(nchains), int(grid))
         st = self._stores.get(key)
@@ -346,35 +419,14 @@ class SparseDesignMatrix:
     def standardized(self):
         return bool(np.any(self.col_means != 0.0) or np.any(self.col_scales != 1.0))
 
-    def _std_tensors(self, dev):
-        key = ("std", dev.index)
-        cache = self._stores.get(key)
-        if cache is None or cache[0] is not self.col_means or cache[1] is not self.col_scales:
-            cache = (self.col_means, self.col_scales, _lib.to_device(self.col_means, dev),
-                     _lib.to_device(self.col_scales, dev))
-            self._stores[key] = cache
-        return cache[2], cache[3]
-
     def device_matvec(self, v):
-        """X v on a CUDA tensor: raw pattern pass (+ the rank-one shift of
-        sparse.py:188-193 when standardised)."""
-        st = self.device_store(v.device)
-        if not self.standardized:
-            return st.matvec(v)
-        mu, sc = self._std_tensors(st.device)
-        u = v / sc
-        out = st.matvec(u)
-        out -= (mu * u).sum()
-        return out
+        """X v on a CUDA tensor: one pattern pass, the affine terms (dense
+        block, the shift/scale of sparse.py:188-193) applied in the same kernel."""
+        return self.device_store(v.device).matvec(v)
 
     def device_matvec_t(self, w):
-        """X' w on a CUDA tensor (+ the correction of sparse.py:203)."""
-        st = self.device_store(w.device)
-        raw = st.matvec_t(w)
-        if not self.standardized:
-            return raw
-        mu, sc = self._std_tensors(st.device)
-        return (raw - w.sum() * mu) / sc
+        """X' w on a CUDA tensor (+ the correction of sparse.py:203, in-kernel)."""
+        return self.device_store(w.device).matvec_t(w)
 
     def standardize(self, exclude=None):
         """Centre and scale columns in place (sparse.py:250-297); returns self.
@@ -420,10 +472,7 @@ class SparseDesignMatrix:
         t = _lib.torch()
         zero = t.zeros(st.p_total, dtype=t.float64, device=st.device)
         om = _lib.to_device(omega, st.device)
-        out = st.phi_diagonal(om, zero)   # binary: sum_i omega_i x_ij^2 = sum_i omega_i x_ij
-        if self.standardized:
-            mu, sc = self._std_tensors(st.device)
-            out = (out - 2.0 * mu * out + om.sum() * mu * mu) / (sc * sc)
+        out = st.phi_diagonal(om, zero)   # sum_i omega_i x_ij^2, affine terms in-kernel
         return out if as_tensor else out.cpu().numpy()
 
     # ------------------------------------------------------------ host views (tests)

@@ -228,7 +228,37 @@ def test_hstack_binary_block_stays_pattern_only():
     v = rng.standard_normal(18)
     np.testing.assert_allclose(port.matvec(port.Csr(80, 18, F.row_ptr, F.col_idx, F.values), v),
                                np.column_stack([block, X.to_dense_raw()]) @ v, rtol=1e-12)
-    # a real-valued block keeps the reference layout (explicit entries)
+    # a real-valued block keeps the reference layout (explicit entries); the
+    # store splits it into a leading dense block and the pattern
     G = pk.hstack_dense_columns(np.column_stack([np.ones(80), rng.standard_normal(80)]), X)
-    with pytest.raises(NotImplementedError):
-        G.pattern()
+    rp, ci, icpt = G.pattern()
+    assert not icpt and G.dense_block.shape == (80, 2)
+
+
+class TestDenseBlock:
+    """Real-valued dense blocks (hstack_dense_columns of a real block,
+    sparse.py:314-341): the design splits into a leading dense block, handled
+    by the store's affine terms, and a binary pattern."""
+
+    def test_hstack_real_block_splits_into_dense_and_pattern(self):
+        d = synth.binary_design(50, 12, 0.05, 0.4, seed=3)
+        X0 = pk.SparseDesignMatrix.from_pattern(d.n, d.p, d.row_ptr, d.col_idx, intercept=True)
+        rng = np.random.default_rng(1)
+        cols = rng.standard_normal((d.n, 2))
+        X = pk.hstack_dense_columns(cols, X0)
+        rp, ci, icpt = X.pattern()
+        dense = X.dense_block
+        # the leading block is the real columns plus X0's intercept column
+        assert dense.shape == (d.n, 3) and not icpt and X.affine
+        np.testing.assert_array_equal(dense[:, :2], cols)
+        np.testing.assert_array_equal(dense[:, 2], np.ones(d.n))
+        np.testing.assert_array_equal(rp, d.row_ptr)
+        np.testing.assert_array_equal(ci, d.col_idx)
+        assert X.n_cols == d.p + 3 and X.nnz == d.nnz + 3 * d.n
+        full = X.to_dense()
+        np.testing.assert_array_equal(full[:, :2], cols)
+
+    def test_values_outside_a_leading_block_are_refused(self):
+        X = pk.SparseDesignMatrix.from_dense(np.array([[1.5, 1.0, 0.0], [0.5, 0.0, 2.0]]))
+        with pytest.raises(NotImplementedError):
+            X.pattern()
