@@ -52,6 +52,37 @@ struct DesignDev {
   __host__ __device__ int lead() const { return icpt + aff.q; }  // reference offset of pattern column 0
 };
 
+// ------------------------------------------------------------------ checked builds
+// PCGS_CHECKED=1 (tools/build_variant.py checked -DPCGS_CHECKED=1) compiles
+// bounds checks into the streaming loops and epilogues -- every gathered
+// index within its slab (sentinel included), every emitted segment / piece
+// id within its output -- trapping on a violation.  compute-sanitizer is
+// closed on this GPU pool; the GPU suite run against the checked library is
+// the substitute (profiles/sanitizer_r02.txt).
+#ifndef PCGS_CHECKED
+#define PCGS_CHECKED 0
+#endif
+#if PCGS_CHECKED
+#define PCGS_CHECK(cond)                                                                        \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("pcgs check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,  \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define PCGS_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+__device__ __forceinline__ void check_vec(uint4 q, int len) {
+  PCGS_CHECK((q.x & 0xffffu) <= (unsigned)len && (q.x >> 16) <= (unsigned)len);
+  PCGS_CHECK((q.y & 0xffffu) <= (unsigned)len && (q.y >> 16) <= (unsigned)len);
+  PCGS_CHECK((q.z & 0xffffu) <= (unsigned)len && (q.z >> 16) <= (unsigned)len);
+  PCGS_CHECK((q.w & 0xffffu) <= (unsigned)len && (q.w >> 16) <= (unsigned)len);
+}
+
 // ------------------------------------------------------------------ utilities
 __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   uint4 r;
@@ -363,7 +394,8 @@ __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int d
 }
 
 template <class Epi>
-__device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const double* sv, Epi& epi, int dbg = 0) {
+__device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const double* sv, Epi& epi, int dbg = 0,
+                                             int slab_len = 0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint4 R = __ldg(P.warps + warp0 + warp);
   const int nvec = (int)R.y;
@@ -419,6 +451,7 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
         double s;
         if (kDebugModes && (dbg & 1)) s = live ? (double)(q[u].x ^ q[u].y ^ q[u].z ^ q[u].w) : 0.0;
         else s = live ? (PCGS_LDS_ASM ? gather8s(q[u], sb) : gather8(q[u], sv)) : 0.0;
+        if (PCGS_CHECKED && live) check_vec(q[u], slab_len);
         if (kDebugModes && (dbg & 2)) acc += s + (double)M;
         else block_reduce(M, dl.x, u, s, lane, acc, open_id, have_open, epi);
       }
@@ -460,7 +493,7 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
       g_cta_times[3 * c + 0] = t_start;
       g_cta_times[3 * c + 1] = t;
     }
-    process_warp(P, T.y, sv, epi, dbg);
+    process_warp(P, T.y, sv, epi, dbg, (int)(hi - lo));
   }
   if (dbg & 64) {
     __syncthreads();

@@ -145,7 +145,11 @@ struct FillRhs {  // u_i = kappa_i + sqrt(omega_i) * eta_i
 
 struct EpiStore {  // out[seg] = s
   double* out;
-  __device__ void emit(long long seg, double s) { out[seg] = s; }
+  long long cap = -1;  // checked builds: number of output slots (-1: unchecked)
+  __device__ void emit(long long seg, double s) {
+    PCGS_CHECK(seg >= 0 && (cap < 0 || seg < cap));
+    out[seg] = s;
+  }
 };
 
 // Row term of the dense block: (Dn u_D)_i = sum_k Dn[i, k] u_k (q = 0: none).

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_csr_matvec(DesignDev D, const d
     EpiZ e{out, v0, aff_row(D, cbuf)};
     run_pass(D.csr, sv, f, e, D.dbg);
   } else {
-    EpiStore e{out};  // out is the (nslab x n) partial buffer
+    EpiStore e{out, (long long)D.csr.nslab * D.n};  // out is the (nslab x n) partial buffer
     run_pass(D.csr, sv, f, e, D.dbg);
   }
 }
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_csr_phi(DesignDev D, const doub
     EpiW e{w, omega, v0, 0.0, aff_row(D, cbuf)};
     run_pass(D.csr, sv, f, e);
   } else {
-    EpiStore e{w};
+    EpiStore e{w, (long long)D.csr.nslab * D.n};
     run_pass(D.csr, sv, f, e);
   }
 }
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_csc_vec(DesignDev D, const doub
   BulkFill bf;
   bulk_init(bf, &mbar);
   FillVecN f{w, &bf};
-  EpiStore e{pieces};
+  EpiStore e{pieces, D.csc.nseg};
   run_pass(D.csc, sv, f, e, D.dbg);
 }
 
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
     {
       FillVecN f{A.w, &bf};
-      EpiStore e{A.pieces};
+      EpiStore e{A.pieces, A.D.csc.nseg};
       run_pass(A.D.csc, sv, f, e, A.D.dbg);
     }
     if (prof) A.prof[4 * a + 2] = gtimer();

@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
   if (A.rhs) {
     {
       FillRhs f{A.kappa[gi], omega, nullptr, A.seed, kStreamEta ^ A.stream_id, 0, A.peers[G.rank].row0};
-      EpiStore e{G.pieces};
+      EpiStore e{G.pieces, G.D.csc.nseg};
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
     rank_sync(A, gi);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg_rs(RsArgs A) {
     // ---------------- B: CSC pass, local column sums g_r = X_r' w_r ----------------
     {
       FillVecN f{G.w, &bf};
-      EpiStore e{G.pieces};
+      EpiStore e{G.pieces, G.D.csc.nseg};
       run_pass(G.D.csc, sv, f, e, 0, cta);
     }
     rank_sync(A, gi);

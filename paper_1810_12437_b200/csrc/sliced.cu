@@ -130,7 +130,8 @@ __device__ __forceinline__ double gather8_lane(uint4 q, unsigned sb) {
 #if !PCGS_SLICED_PIPE
 // per-slice batches of U steps, loads of a batch issued together
 template <int R, class Epi>
-__device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi) {
+__device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi,
+                                            int slab_len = 0) {
   constexpr int NS = 32 / R;
   constexpr int U = PCGS_SLICED_BATCH;
   const int lane = threadIdx.x & 31, slot = lane / R, c = lane & (R - 1);
@@ -159,15 +160,23 @@ __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const dou
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + (size_t)(t + u) * NS);
 #pragma unroll
-      for (int u = 0; u < U; ++u) acc += gather8_lane<R>(v[u], sb);
+      for (int u = 0; u < U; ++u) {
+        if (PCGS_CHECKED) check_vec(v[u], slab_len);
+        acc += gather8_lane<R>(v[u], sb);
+      }
     }
-    for (; t < D.y; ++t) acc += gather8_lane<R>(ldg_stream(vp + (size_t)t * NS), sb);
+    for (; t < D.y; ++t) {
+      const uint4 v = ldg_stream(vp + (size_t)t * NS);
+      if (PCGS_CHECKED) check_vec(v, slab_len);
+      acc += gather8_lane<R>(v, sb);
+    }
+    PCGS_CHECK(pid == 0xffffffffu || (long long)pid < P.npiece);
     if (pid != 0xffffffffu) epi.emit(pid, c, acc);
   }
 }
 #else
 template <int R, class Epi>
-__device__ __noinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi) {
+__device__ __noinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi, int slab_len = 0) {
   constexpr int NS = 32 / R;
   constexpr int U = PCGS_SLICED_BATCH;
   const int lane = threadIdx.x & 31, slot = lane / R, c = lane & (R - 1);
@@ -267,7 +276,7 @@ __device__ __forceinline__ void run_spass(const SPassDev& P, double* sv, Fill& f
     }
     __syncthreads();
     fill(sv, lo, (int)(hi - lo));
-    walk_slices<R>(P, T.y + warp, sv, epi);
+    walk_slices<R>(P, T.y + warp, sv, epi, (int)(hi - lo));
   }
 }
 
