@@ -56,6 +56,11 @@ def parse():
     ap.add_argument("--workload", default="config3", choices=["config3", "config4", "config5"],
                     help="config4: 8 independent chains per GPU as one batch (weak scaling); "
                          "config5: the row-split run (rows of X over the N ranks, strong scaling)")
+    ap.add_argument("--config4-sequential", action="store_true",
+                    help="config4: the 8 chains one after another on the full grid (single-chain kernels)")
+    ap.add_argument("--config4-fused", action="store_true",
+                    help="config4 batched: whole scans in one persistent kernel (chains at their own pace) "
+                         "instead of scan by scan")
     ap.add_argument("--concurrent", type=int, default=1,
                     help="config4: 1 = the 8 chains as one batch (batched PCG); k > 1 = k slots side by side")
     return ap.parse_args()
@@ -564,7 +569,7 @@ def run_config4(args):
     X = d.matrix()
     K, W, R = args.steps, args.warmup, max(1, args.concurrent)
     per_gpu = 8
-    batched = R == 1
+    batched = R == 1 and not args.config4_sequential
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     grid = 0 if R == 1 else sms // R
     chains_idx = parallel.chain_assignment(per_gpu * world, world, rank)
@@ -574,8 +579,11 @@ def run_config4(args):
         if batched:
             B = gibbs.BatchedChains(X, y, cfg, W + K, seeds, device=dev, burn_in=W, cg_config=cgc)
             all_chains = B.chains
-            for t in range(1, W + 1):
-                B.scan(t)
+            if (not args.config4_fused):
+                for t in range(1, W + 1):
+                    B.scan(t)
+            else:
+                B.run(1, W)       # whole scans in one persistent kernel, chains at their own pace
         else:
             # R slots (streams); chain i of the rank runs on slot i % R after
             # the slot's previous chain, with no barrier between rounds
@@ -597,8 +605,11 @@ def run_config4(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(cur)
         if batched:
-            for t in range(W + 1, W + K + 1):
-                B.scan(t)
+            if (not args.config4_fused):
+                for t in range(W + 1, W + K + 1):
+                    B.scan(t)
+            else:
+                B.run(W + 1, W + K)
         else:
             for s in slots:
                 s.wait_stream(cur)
@@ -623,8 +634,11 @@ def run_config4(args):
         dist.barrier()
     ms_max = float(ms_t.item())
     if rank == 0:
-        mode = ("one batch: the beta solves of all 8 chains in one batched PCG per scan (sliced store)"
-                if batched else f"{R} slots side by side")
+        mode = (("one batch, scan by scan: each chain's updates, then one batched PCG for the 8 beta draws"
+                 if (not args.config4_fused) else
+                 "one batch in one persistent kernel: whole Gibbs scans of the 8 chains at their own pace "
+                 "(pcgs_batch_gibbs_run), one walk over the pattern per iteration for all chains")
+                if batched else (f"{R} slots side by side" if R > 1 else "one chain after another"))
         line = {
             "metric": "gibbs_iter_per_s", "value": world * per_gpu * K / (ms_max * 1e-3), "unit": "chain-iter/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True,
@@ -632,14 +646,18 @@ def run_config4(args):
             "data": "synthetic (seeded; BASELINE config 4 recipe; no public dataset)",
             "config": {"workload": f"config 4: {per_gpu} independent {args.prior} chains per GPU on the "
                                    f"n={d.n:,} p={d.p:,} design (nnz {d.nnz:,}), {mode}",
-                       "chains_per_gpu": per_gpu, "mode": "batched" if batched else "slots",
+                       "chains_per_gpu": per_gpu,
+                       "mode": (("batched-scan" if (not args.config4_fused) else "batched-fused") if batched else
+                                ("slots" if R > 1 else "sequential")),
                        "concurrent": R, "grid_per_chain": grid or sms,
                        "parallelism": f"chain-parallel x{world}", "seed": SEED},
             "clocks": clk.summary(),
             "extra": {"cg_iters_mean": float(np.mean(cg)), "chain_iterations_timed": per_gpu * K,
                       "batch_cg_iters_mean": float(np.mean(cg_max)) if batched else None,
-                      "note": ("a batched solve runs until its slowest chain converges: per scan the "
-                               "batch pays the max of the 8 chains' CG counts") if batched else None},
+                      "note": ("scan by scan, a batched solve runs until its slowest chain converges: per scan "
+                               "the batch pays the max of the 8 chains' CG counts" if (not args.config4_fused) else
+                               "fused: every batched iteration advances each chain by one PCG iteration or "
+                               "one Gibbs update; timed = K whole scans of every chain") if batched else None},
         }
         print(json.dumps(line))
     if world > 1:

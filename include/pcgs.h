@@ -418,6 +418,21 @@ int pcgs_batch_gibbs_scan(pcgs_design_t d, pcgs_batch_t b, pcgs_gibbs_t* const* 
                           int32_t nchains, int32_t t, const int32_t* counts,
                           const int32_t* slots, pcgs_stream_t stream);
 
+/* Scans t_first .. t_last of R = nchains batched chains in ONE persistent
+ * kernel (BASELINE config 4): each chain runs whole Gibbs scans at its own
+ * pace -- its omega / tau / lambda / RHS updates, its PCG solve, its
+ * statistics and log density -- while the batch walks the pattern once per
+ * iteration for all chains, so a chain whose solve finishes starts its next
+ * scan instead of waiting for the slowest (gibbs.py:300-369 per chain, the
+ * RNG keys of pcgs_gibbs_scan).  gs[c] as for pcgs_batch_gibbs_scan (prior
+ * preconditioner, no pinned updates, no reparametrisation); counts[c] /
+ * stored[c] = statistics updates / stored draws before t_first; out_state
+ * (device, 2 per chain) receives them after t_last. */
+int pcgs_batch_gibbs_run(pcgs_batch_t b, pcgs_gibbs_t* const* gs, int32_t nchains,
+                         int32_t t_first, int32_t t_last, int32_t burn_in, int32_t thin,
+                         const int32_t* counts, const int32_t* stored, int32_t* out_state,
+                         pcgs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -96,6 +96,7 @@ SIGNATURES = {
                                            ctypes.c_int, _P]),
     "pcgs_batch_debug_profile": (ctypes.c_int, [_P]),
     "pcgs_batch_gibbs_scan": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _P, _P, _P]),
+    "pcgs_batch_gibbs_run": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _I32, _I32, _P, _P, _P, _P]),
     "pcgs_batch_phi_apply": (ctypes.c_int, [_P, _P, _P, _P, _P, _P]),
     "pcgs_batch_pcg": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _I32, _D, _P, _P, _P, _P, _P]),
     "pcgs_gibbs_scan": (ctypes.c_int, [_P, _P, _I32, _I32, _I32, _P]),

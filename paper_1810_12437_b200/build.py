@@ -13,8 +13,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libpcgs.so"
-SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "sliced.cu", CSRC / "sliced.cpp", CSRC / "rowsplit.cu", CSRC / "store.cpp", CSRC / "mtx.cpp"]
-HEADERS = [CSRC / "store.h", CSRC / "mtx.h", CSRC / "device.cuh", CSRC / "internal.cuh", CSRC / "sliced.h",
+SOURCES = [CSRC / "pcgs.cu", CSRC / "gibbs.cu", CSRC / "sliced.cu", CSRC / "sliced.cpp", CSRC / "sgibbs.cu", CSRC / "rowsplit.cu", CSRC / "store.cpp", CSRC / "mtx.cpp"]
+HEADERS = [CSRC / "store.h", CSRC / "mtx.h", CSRC / "device.cuh", CSRC / "internal.cuh", CSRC / "sliced.h", CSRC / "sliced.cuh", CSRC / "pg.cuh", CSRC / "gibbs_math.cuh",
            ROOT / "include" / "pcgs.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

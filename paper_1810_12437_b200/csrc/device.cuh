@@ -317,6 +317,9 @@ static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
 #ifndef PCGS_LANE_PREFETCH
 #define PCGS_LANE_PREFETCH 1
 #endif
+#ifndef PCGS_L1_NEXT
+#define PCGS_L1_NEXT 0
+#endif
 
 // `M` is the block's segment-start mask; `first_id` (the id of the segment
 // starting at the lowest set bit) is fetched lazily by shuffling `dl_x` from
@@ -422,6 +425,14 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
       const unsigned off = (unsigned)(k0 + kPrefetchBlocks) * 512u + (unsigned)lane * 128u;
       if (lane < 4 * kRing && off < (unsigned)nvec * 16u)
         asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)base + off));
+#if PCGS_L1_NEXT
+      // experiment: the next batch's lines into L1 (lanes 16..16+4 kRing)
+      {
+        const unsigned off1 = (unsigned)(k0 + kRing) * 512u + (unsigned)(lane - 16) * 128u;
+        if (lane >= 16 && lane < 16 + 4 * kRing && off1 < (unsigned)nvec * 16u)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)base + off1));
+      }
+#endif
 #else
       if (lane == 0 && k0 + kPrefetchBlocks < nb) {
         const int kb = k0 + kPrefetchBlocks;

@@ -570,6 +570,39 @@ class BatchedChains:
         for ch in self.chains:
             ch.count += 1
 
+    @property
+    def fusable(self):
+        """True when the scans can run whole inside one persistent kernel
+        (`run`): prior preconditioner, no pinned updates, no reparametrisation."""
+        a = self.chains[0].args
+        return (a.precond == 0 and not (a.fixed_omega or a.fixed_tau or a.fixed_lam)
+                and all(ch.reparam is None for ch in self.chains))
+
+    def run(self, t_first, t_last):
+        """Scans t_first..t_last of every chain inside ONE persistent kernel
+        (`pcgs_batch_gibbs_run`): a chain whose solve ends starts its next scan
+        while the others keep iterating.  Same RNG keys, statistics, stored
+        draws and log density as `scan(t)` per scan."""
+        if not self.fusable:
+            raise NotImplementedError("fused batched scans need the prior preconditioner and no pinned updates")
+        if t_last < t_first:
+            return
+        ch0 = self.chains[0]
+        for c, ch in enumerate(self.chains):
+            self._counts[c] = ch.count
+            self._slots[c] = ch.stored
+        t = _lib.torch()
+        out = t.zeros(2 * self.R, dtype=t.int32, device=self.dev)
+        _lib.check(_lib.lib().pcgs_batch_gibbs_run(
+            self.bstore.handle, ctypes.cast(self._ptrs, ctypes.c_void_p), self.R, int(t_first), int(t_last),
+            int(ch0.burn_in), int(ch0.thin), self._counts.ctypes.data, self._slots.ctypes.data, _lib.ptr(out),
+            _lib.stream_ptr(self.dev)))
+        for ch in self.chains:          # the same bookkeeping the kernel does (deterministic)
+            for tt in range(t_first, t_last + 1):
+                ch.next_slot(tt)
+            ch.count += t_last - t_first + 1
+        self._out_state = out
+
     def check(self, t_lo, t_hi, allow_max_iter=False):
         for ch in self.chains:
             ch.check(t_lo, t_hi, allow_max_iter)
@@ -581,10 +614,15 @@ class BatchedChains:
 def gibbs_run_batched(X, y, cfg, n_iter, seeds, burn_in=0, sampler="cg", thin=1, preconditioner="prior",
                       cg_config=None, burn_in_sampler=None, init_state=None, gamma_scale=1.0,
                       allow_max_iter=False, fixed_omega=None, fixed_tau=None, fixed_lam=None, device=None,
-                      sync_every=64) -> list:
+                      sync_every=256, fused=False) -> list:
     """gibbs_run (gibbs.py:260-379) for R = len(seeds) independent chains
-    (R in {2, 4, 8}) whose beta draws share one batched PCG per scan; chain c
-    is the chain of seed seeds[c].  Returns one ChainOutput per seed."""
+    (R in {2, 4, 8}) sharing every walk over the pattern; chain c is the
+    chain of seed seeds[c].  Every scan runs each chain's updates and then
+    one batched PCG for all beta draws (`BatchedChains.scan`); with `fused`
+    (prior preconditioner, no pinned updates) the chains instead run whole
+    scans inside one persistent kernel at their own pace (`BatchedChains.run`,
+    the same chains: same RNG keys, draws equal to the solves' tolerance).
+    Returns one ChainOutput per seed."""
     y = _check_run_args(X, y, cfg, n_iter, burn_in, thin, sampler, burn_in_sampler, preconditioner,
                         fixed_lam, None)
     B = BatchedChains(X, y, cfg, n_iter, seeds, device=device, burn_in=burn_in, thin=thin,
@@ -592,6 +630,14 @@ def gibbs_run_batched(X, y, cfg, n_iter, seeds, burn_in=0, sampler="cg", thin=1,
                       gamma_scale=gamma_scale, fixed_omega=fixed_omega, fixed_tau=fixed_tau,
                       fixed_lam=fixed_lam)
     checked = 0
+    if fused and B.fusable:
+        # whole scans inside one persistent kernel, checked every sync_every scans
+        step = sync_every if sync_every else n_iter
+        for t0 in range(1, n_iter + 1, max(step, 1)):
+            t1 = min(n_iter, t0 + max(step, 1) - 1)
+            B.run(t0, t1)
+            B.check(t0, t1, allow_max_iter)
+        return B.outputs()
     for t in range(1, n_iter + 1):
         B.scan(t)
         if sync_every and t - checked >= sync_every:
