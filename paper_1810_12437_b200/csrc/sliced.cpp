@@ -75,7 +75,7 @@ int half_extra(const int* ix, int n, int H) {
 
 // Lays out slices [a, b) of a slab (pieces already sorted) into the pass.
 void emit_slices(SPassHost& P, SlabPieces& S, const std::vector<uint32_t>& sl_first, size_t a, size_t b, int R) {
-  const int NS = 32 / R, H = 16 / R;
+  const int NS = sliced_slots(R), H = 16 / R, NG = sliced_groups(R);
   std::vector<Pool> pools(NS);
   for (size_t q = a; q < b; ++q) {
     const uint32_t p0 = sl_first[q], p1 = sl_first[q + 1];
@@ -99,7 +99,7 @@ void emit_slices(SPassHost& P, SlabPieces& S, const std::vector<uint32_t>& sl_fi
     uint16_t* out = P.idx.data() + (size_t)D.v0 * kVecIdx;
     for (uint32_t t = 0; t < L; ++t) {
       for (int k = 0; k < kVecIdx; ++k) {
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NG; ++h) {
           int mult[16] = {};
           int g[16];
           int ng = 0;
@@ -146,7 +146,7 @@ void cut_ranges(const std::vector<uint64_t>& pre, size_t a, size_t b, int parts,
 
 // Builds one pass from its per-slab pieces: sort, slice, plan over G CTAs, place.
 void plan_pass(SPassHost& P, std::vector<SlabPieces>& slabs, int R, int G) {
-  const int NS = 32 / R;
+  const int NS = sliced_slots(R);
   const int ns = (int)slabs.size();
   // cost of a slice: its vectors plus a per-piece epilogue charge (in vectors)
   constexpr uint64_t kEpi = 2;
@@ -316,7 +316,7 @@ std::string build_sliced(int64_t n, int64_t p, const int64_t* row_ptr, const int
 }
 
 std::string verify_sliced(const SlicedHost& H, const int64_t* row_ptr, const int32_t* col_idx) {
-  const int NS = 32 / H.R;
+  const int NS = sliced_slots(H.R);
   auto walk = [&](const SPassHost& P, int64_t n_out, std::vector<std::vector<int32_t>>& got) -> std::string {
     std::vector<int32_t> owner((size_t)P.npiece, -1);
     for (int64_t o = 0; o < n_out; ++o)

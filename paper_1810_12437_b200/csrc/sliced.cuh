@@ -63,30 +63,41 @@ __device__ __forceinline__ double gather8_lane(uint4 q, unsigned sb) {
   return (a + b) + (c + d);
 }
 
-// One warp walks its slice range: lane (slot, c) sums chain c of its slot's
-// piece over the slice's steps and emits it.  The warp's slices are
-// contiguous in the stream, so the walk is one flat run of steps (slot s of
-// step g at vector first + g * NS + s) with slice boundaries every L steps:
-// the index loads of the next batch are issued before the current batch is
-// consumed (software pipelining across slice boundaries), and the next
-// slice's descriptor is loaded one slice ahead.
+// Pair mapping: chains 2k, 2k+1 of the 8 indices of one vector (sb includes k * 16).
+__device__ __forceinline__ double2 lds128(unsigned a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+template <int R>
+__device__ __forceinline__ double2 gather8_pair(uint4 q, unsigned sb) {
+  const double2 a0 = lds128(row_addr<R>(sb, lo16(q.x))), a1 = lds128(row_addr<R>(sb, hi16(q.x)));
+  const double2 b0 = lds128(row_addr<R>(sb, lo16(q.y))), b1 = lds128(row_addr<R>(sb, hi16(q.y)));
+  const double2 c0 = lds128(row_addr<R>(sb, lo16(q.z))), c1 = lds128(row_addr<R>(sb, hi16(q.z)));
+  const double2 d0 = lds128(row_addr<R>(sb, lo16(q.w))), d1 = lds128(row_addr<R>(sb, hi16(q.w)));
+  double2 r;
+  r.x = ((a0.x + a1.x) + (b0.x + b1.x)) + ((c0.x + c1.x) + (d0.x + d1.x));
+  r.y = ((a0.y + a1.y) + (b0.y + b1.y)) + ((c0.y + c1.y) + (d0.y + d1.y));
+  return r;
+}
+
+// One warp walks its slice range: each slot walks one piece per slice, lane
+// (slot, k) summing its chains (pair mapping: chains 2k, 2k+1; single
+// mapping: chain k) over the slice's steps and emitting the sums, batches of
+// U steps with all loads of a batch issued together.
 #ifndef PCGS_SLICED_BATCH
 #define PCGS_SLICED_BATCH 4
 #endif
-#ifndef PCGS_SLICED_PIPE
-#define PCGS_SLICED_PIPE 0
-#endif
-#if !PCGS_SLICED_PIPE
-// per-slice batches of U steps, loads of a batch issued together
 template <int R, class Epi>
 __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi,
                                             int slab_len = 0) {
-  constexpr int NS = 32 / R;
+  constexpr int NS = sliced_slots(R), LS = sliced_lanes_per_slot(R);
+  constexpr bool PAIR = sliced_pair(R);
   constexpr int U = PCGS_SLICED_BATCH;
-  const int lane = threadIdx.x & 31, slot = lane / R, c = lane & (R - 1);
+  const int lane = threadIdx.x & 31, slot = lane / LS, k = lane & (LS - 1);
   const uint2 ws = __ldg(P.warp_slices + wr);
   if (ws.x >= ws.y) return;
-  const unsigned sb = smem_addr(sv) + (unsigned)c * 8u;
+  const unsigned sb = smem_addr(sv) + (unsigned)k * (PAIR ? 16u : 8u);
   const uint2 first = __ldg(P.slices + ws.x), last = __ldg(P.slices + ws.y - 1);
   const char* stream0 = (const char*)(P.vec + first.x);
   const unsigned total = (unsigned)(((size_t)last.x + (size_t)last.y * NS - first.x) * 16u);
@@ -102,90 +113,33 @@ __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const dou
         if (off < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(stream0 + off));
       }
     }
-    double acc = 0.0;
+    double acc = 0.0, acc2 = 0.0;
+    auto step = [&](uint4 v) {
+      if (PCGS_CHECKED) check_vec(v, slab_len);
+      if (PAIR) {
+        const double2 g = gather8_pair<R>(v, sb);
+        acc += g.x;
+        acc2 += g.y;
+      } else {
+        acc += gather8_lane<R>(v, sb);
+      }
+    };
     unsigned t = 0;
     for (; t + U <= D.y; t += U) {
       uint4 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = ldg_stream(vp + (size_t)(t + u) * NS);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (PCGS_CHECKED) check_vec(v[u], slab_len);
-        acc += gather8_lane<R>(v[u], sb);
-      }
+      for (int u = 0; u < U; ++u) step(v[u]);
     }
-    for (; t < D.y; ++t) {
-      const uint4 v = ldg_stream(vp + (size_t)t * NS);
-      if (PCGS_CHECKED) check_vec(v, slab_len);
-      acc += gather8_lane<R>(v, sb);
-    }
+    for (; t < D.y; ++t) step(ldg_stream(vp + (size_t)t * NS));
     PCGS_CHECK(pid == 0xffffffffu || (long long)pid < P.npiece);
-    if (pid != 0xffffffffu) epi.emit(pid, c, acc);
+    if (pid != 0xffffffffu) {
+      if (PAIR) epi.emit2(pid, 2 * k, acc, acc2);
+      else epi.emit(pid, k, acc);
+    }
   }
 }
-#else
-template <int R, class Epi>
-__device__ __noinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi, int slab_len = 0) {
-  constexpr int NS = 32 / R;
-  constexpr int U = PCGS_SLICED_BATCH;
-  const int lane = threadIdx.x & 31, slot = lane / R, c = lane & (R - 1);
-  const uint2 ws = __ldg(P.warp_slices + wr);
-  if (ws.x >= ws.y) return;
-  const unsigned sb = smem_addr(sv) + (unsigned)c * 8u;
-  const uint2 first = __ldg(P.slices + ws.x), last = __ldg(P.slices + ws.y - 1);
-  const char* stream0 = (const char*)(P.vec + first.x);
-  const unsigned T = (unsigned)(((size_t)last.x - first.x) / NS + last.y);  // steps of the warp
-  const unsigned total = T * NS * 16u;                                      // bytes of the warp stream
-  const uint4* base = P.vec + first.x + slot;
-  unsigned q = ws.x;
-  unsigned bnd = first.y;  // step at which slice q ends
-  unsigned pid = __ldg(P.piece + (size_t)q * NS + slot);
-  uint2 nD = q + 1 < ws.y ? __ldg(P.slices + q + 1) : make_uint2(0u, 0u);
-  unsigned npid = q + 1 < ws.y ? __ldg(P.piece + (size_t)(q + 1) * NS + slot) : 0xffffffffu;
-  unsigned next_pf = kSPrefetch;  // bytes of the warp stream prefetched so far
-  double acc = 0.0;
-  uint4 cur[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u)
-    if ((unsigned)u < T) cur[u] = ldg_stream(base + (size_t)u * NS);
-  for (unsigned g0 = 0; g0 < T; g0 += U) {
-    // sliding L2 prefetch kSPrefetch bytes ahead of the loads
-    {
-      const unsigned end = min(total, (g0 + 2 * U) * NS * 16u + kSPrefetch);
-      if (next_pf < end) {
-        const unsigned off = next_pf + (unsigned)lane * 128u;
-        if (off < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(stream0 + off));
-        next_pf += 32u * 128u;
-      }
-    }
-    uint4 nxt[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (g0 + U + u < T) nxt[u] = ldg_stream(base + (size_t)(g0 + U + u) * NS);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const unsigned g = g0 + u;
-      if (g < T) {
-        if (g == bnd) {  // slice q done: emit, advance to q + 1 (pieces are never empty)
-          if (pid != 0xffffffffu) epi.emit(pid, c, acc);
-          acc = 0.0;
-          ++q;
-          bnd += nD.y;
-          pid = npid;
-          if (q + 1 < ws.y) {
-            nD = __ldg(P.slices + q + 1);
-            npid = __ldg(P.piece + (size_t)(q + 1) * NS + slot);
-          }
-        }
-        acc += gather8_lane<R>(cur[u], sb);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) cur[u] = nxt[u];
-  }
-  if (pid != 0xffffffffu) epi.emit(pid, c, acc);
-}
-#endif
 
 // TMA copy of elements [lo, lo+len) of a chain-minor R-column vector into the
 // slab; the sentinel row (R doubles at element len) is zeroed.
@@ -203,6 +157,9 @@ struct EpiPiece {  // out[piece * R + c] = s
   double* out;
   int R;
   __device__ __forceinline__ void emit(unsigned pid, int c, double s) { out[(size_t)pid * R + c] = s; }
+  __device__ __forceinline__ void emit2(unsigned pid, int c, double s0, double s1) {
+    *reinterpret_cast<double2*>(out + (size_t)pid * R + c) = make_double2(s0, s1);
+  }
 };
 
 template <int R, class Fill, class Epi>
@@ -218,7 +175,7 @@ __device__ __forceinline__ void run_spass(const SPassDev& P, double* sv, Fill& f
       const uint2 ws = __ldg(P.warp_slices + T.y + warp);
       if (ws.x < ws.y) {
         const uint2 f = __ldg(P.slices + ws.x), l = __ldg(P.slices + ws.y - 1);
-        const unsigned total = (unsigned)(((size_t)l.x + (size_t)l.y * (32 / R) - f.x) * 16u);
+        const unsigned total = (unsigned)(((size_t)l.x + (size_t)l.y * sliced_slots(R) - f.x) * 16u);
         const unsigned off = (threadIdx.x & 31) * 128u;
         if (off < total) asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(P.vec + f.x) + off));
       }
@@ -231,36 +188,6 @@ __device__ __forceinline__ void run_spass(const SPassDev& P, double* sv, Fill& f
 
 // debug: the stamp buffer set by pcgs_batch_debug_profile (batched kernels)
 unsigned long long* batch_profile_buffer();
-
-// run_spass with the walk out of line: inside a persistent kernel with much
-// live state (the fused Gibbs kernel) the caller's registers are saved once per
-// pass and the streaming loop keeps the whole register budget.
-template <int R, class Epi>
-__device__ __noinline__ void walk_slices_ni(const SPassDev& P, int wr, const double* sv, Epi& epi, int slab_len) {
-  walk_slices<R>(P, wr, sv, epi, slab_len);
-}
-template <int R, class Fill, class Epi>
-__device__ __forceinline__ void run_spass_ni(const SPassDev& P, double* sv, Fill& fill, Epi& epi) {
-  const int c = blockIdx.x;
-  const int t0 = P.cta_task_ptr[c], t1 = P.cta_task_ptr[c + 1];
-  const int warp = threadIdx.x >> 5;
-  for (int t = t0; t < t1; ++t) {
-    const int2 T = __ldg(P.task + t);
-    const long long lo = P.slab_lo[T.x], hi = P.slab_lo[T.x + 1];
-    {
-      const uint2 ws = __ldg(P.warp_slices + T.y + warp);
-      if (ws.x < ws.y) {
-        const uint2 f = __ldg(P.slices + ws.x), l = __ldg(P.slices + ws.y - 1);
-        const unsigned total = (unsigned)(((size_t)l.x + (size_t)l.y * (32 / R) - f.x) * 16u);
-        const unsigned off = (threadIdx.x & 31) * 128u;
-        if (off < total) asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(P.vec + f.x) + off));
-      }
-    }
-    __syncthreads();
-    fill(sv, lo, (int)(hi - lo));
-    walk_slices_ni<R>(P, T.y + warp, sv, epi, (int)(hi - lo));
-  }
-}
 
 // Per-chain block sums: thread holds a value of chain (tid & (R-1)); returns,
 // in threads c < R, the CTA total of chain c (fixed order).

@@ -32,6 +32,28 @@ namespace pcgs {
 
 constexpr int kSlicedPieceMax = 32;  // vectors per piece
 
+// Lane mapping.  Pair mapping (default, R >= 2): a slot is R/2 lanes, lane k
+// of the slot sums chains 2k and 2k+1 with one LDS.128 per index, so a warp
+// walks 64/R pieces at once and the slot's index vector reaches R/2 lanes
+// (half the register writeback of the index stream of the single mapping);
+// a 128-bit shared load is one wavefront per quarter-warp, i.e. per 16/R
+// slots.  Single mapping (PCGS_SLICED_PAIR=0, and R = 1): a slot is R lanes
+// with one chain and one LDS.64 each, 32/R pieces per warp, one wavefront per
+// half-warp = 16/R slots.  Either way the slots of one wavefront group read
+// distinct bank groups iff their indices differ mod 16/R.
+#ifndef PCGS_SLICED_PAIR
+#define PCGS_SLICED_PAIR 1
+#endif
+#ifdef __CUDACC__
+#define PCGS_HD __host__ __device__
+#else
+#define PCGS_HD
+#endif
+PCGS_HD constexpr bool sliced_pair(int R) { return PCGS_SLICED_PAIR != 0 && R >= 2; }
+PCGS_HD constexpr int sliced_lanes_per_slot(int R) { return sliced_pair(R) ? R / 2 : R; }
+PCGS_HD constexpr int sliced_slots(int R) { return 32 / sliced_lanes_per_slot(R); }
+PCGS_HD constexpr int sliced_groups(int R) { return sliced_pair(R) ? 4 : 2; }  // wavefront groups per warp
+
 struct SliceDesc {  // 8 bytes, device-readable as uint2
   uint32_t v0;      // first vector of the slice
   uint32_t len;     // steps (vectors per slot)
