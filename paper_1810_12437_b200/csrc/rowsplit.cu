@@ -125,6 +125,28 @@ struct RsSumArgs {               // sum of a per-CTA partial over every rank's C
 
 __device__ __forceinline__ double ld_peer(const double* p, bool remote) { return remote ? __ldcv(p) : __ldcg(p); }
 
+// Watchdog of the cross-rank waits: a peer that never arrives (a rank that
+// died or never launched) traps after kRsWaitNs instead of hanging the GPU;
+// the host sees a launch failure.
+constexpr unsigned long long kRsWaitNs = 30ull * 1000ull * 1000ull * 1000ull;
+__device__ __forceinline__ unsigned long long rs_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void rs_wait_sys(const unsigned long long* flag, unsigned long long e) {
+  const unsigned long long t0 = rs_now();
+  unsigned long long v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= e) return;
+    if (rs_now() - t0 > kRsWaitNs) {
+      printf("pcgs row split: a peer rank did not arrive within %llu s (epoch %llu)\n", kRsWaitNs / 1000000000ull, e);
+      __trap();
+    }
+  }
+}
+
 // Barrier over the CTAs of one rank: the grid barrier, or in the flag
 // validation mode a barrier over the rank's own group of Gr CTAs (thread 0 of
 // every CTA arrives on a monotonic counter with a release fence and spins
@@ -163,10 +185,7 @@ __device__ void rs_exchange(const RsArgs& A, int gi, int cta, int my_rank, unsig
     const RsPeer& q = A.peers[threadIdx.x];
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(q.inbox + my_rank), "l"(e) : "memory");
     const RsPeer& me = A.peers[my_rank];
-    unsigned long long v;
-    do {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(me.inbox + threadIdx.x) : "memory");
-    } while (v < e);
+    rs_wait_sys(me.inbox + threadIdx.x, e);
   }
   rank_sync(A, gi);
 }
@@ -556,10 +575,7 @@ __global__ void __launch_bounds__(32) k_rs_sum(RsSumArgs A) {
     for (int q = lane; q < A.nranks; q += 32) {
       if (q == r) continue;
       asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(A.peers[q].inbox + r), "l"(e) : "memory");
-      unsigned long long f;
-      do {
-        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(me.inbox + q) : "memory");
-      } while (f < e);
+      rs_wait_sys(me.inbox + q, e);
     }
     __syncwarp();
     if (lane == 0 && r == 0) {  // every peer has signalled, so every block has read the epoch
@@ -592,10 +608,7 @@ __global__ void __launch_bounds__(32) k_rs_sum(RsSumArgs A) {
   for (int q = lane; q < A.nranks; q += 32) {
     if (q == A.my_rank) continue;
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(A.peers[q].inbox + A.my_rank), "l"(e) : "memory");
-    unsigned long long f;
-    do {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(f) : "l"(me.inbox + q) : "memory");
-    } while (f < e);
+    rs_wait_sys(me.inbox + q, e);
   }
   __syncwarp();
   if (lane == 0) {
