@@ -281,13 +281,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
       const double tau = st_tau[c_t];
       const unsigned long long t_next = (unsigned long long)st_t[c_t];
       const bool prep = mode == kModeGibbs && st_t[c_t] <= C.t_last;
+      const long long Q0 = stage_own_pieces<R>(A.pieces, D.csc.out_ptr, e0 / R, e1 / R, sv, D.smem_doubles);
+      auto colsum = [&](long long j) {
+        double g = 0.0;
+        const long long q1 = D.csc.out_ptr[j + 1];
+        if (Q0 >= 0) {
+          for (long long qq = D.csc.out_ptr[j]; qq < q1; ++qq) g += sv[(qq - Q0) * R + c_t];
+        } else {
+          for (long long qq = D.csc.out_ptr[j]; qq < q1; ++qq) g += __ldcg(A.pieces + qq * R + c_t);
+        }
+        return g;
+      };
       for (long long e = e0 + tid; e < e1; e += kThreads) {
         const long long j = e / R;
         const long long r = ref_index(j, p, lead);
         if (mode == kModeSolve || mode == kModeInit) {
-          double Ad = 0.0;
-          const long long q1 = D.csc.out_ptr[j + 1];
-          for (long long qq = D.csc.out_ptr[j]; qq < q1; ++qq) Ad += __ldcg(A.pieces + qq * R + c_t);
+          double Ad = colsum(j);
           const double dv = A.d[e];
           Ad += A.diag[e] * (mode == kModeInit ? A.x[e] : dv);
           double rv;
@@ -332,9 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
             sc = tl;
             x0 = count > 0 ? tl * C.mean[r] : 0.0;
           }
-          double g = 0.0;
-          const long long q1 = D.csc.out_ptr[j + 1];
-          for (long long qq = D.csc.out_ptr[j]; qq < q1; ++qq) g += __ldcg(A.pieces + qq * R + c_t);
+          const double g = colsum(j);
           Philox Rd(C.seed, kStreamDelta ^ t_next, (unsigned)r);
           A.b[e] = g + sqrt(dg_) * Rd.normal();
           A.diag[e] = dg_;

@@ -251,11 +251,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
     {
       const bool live = st_active[c_t] && st_alpha[c_t] != 0.0;
       const double alpha = st_alpha[c_t];
-      for (long long e = e0 + tid; e < e1; e += kThreads) {
+      // own columns in NH rounds whose pieces fit the idle slab (staged; else global loads)
+      const long long jb0 = e0 / R, jb1 = e1 / R;
+      const int NH = stage_rounds<R>(D.csc.out_ptr, jb0, jb1, D.smem_doubles);
+      for (int h = 0; h < NH; ++h) {
+      const long long ja = jb0 + (jb1 - jb0) * h / NH, jz = jb0 + (jb1 - jb0) * (h + 1) / NH;
+      if (h > 0) __syncthreads();
+      const long long Q0 = stage_own_pieces<R>(A.pieces, D.csc.out_ptr, ja, jz, sv, D.smem_doubles);
+      for (long long e = ja * R + tid; e < jz * R; e += kThreads) {
         const long long j = e / R;
         double Ad = 0.0;
         const long long q1 = D.csc.out_ptr[j + 1];
-        for (long long q = D.csc.out_ptr[j]; q < q1; ++q) Ad += __ldcg(A.pieces + q * R + c_t);
+        if (Q0 >= 0) {
+          for (long long q = D.csc.out_ptr[j]; q < q1; ++q) Ad += sv[(q - Q0) * R + c_t];
+        } else {
+          for (long long q = D.csc.out_ptr[j]; q < q1; ++q) Ad += __ldcg(A.pieces + q * R + c_t);
+        }
         const long long r = ref_index(j, D.p, D.icpt) * R + c_t;
         const double dv = od[e];
         Ad += __ldg(A.diag + r) * dv;
@@ -272,6 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
         const double tj = __ldg(A.scale + r) * rv;
         trms += tj * tj;
         trz += rv * zn;
+      }
       }
     }
     {

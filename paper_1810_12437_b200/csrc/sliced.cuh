@@ -186,6 +186,35 @@ __device__ __forceinline__ void run_spass(const SPassDev& P, double* sv, Fill& f
   }
 }
 
+// Step phase: the pieces of the CTA's own columns [j0, jend) are contiguous
+// (output-major numbering); stage them into the idle slab with coalesced
+// 16-byte loads so every column sum reads shared memory.  Returns the first
+// staged piece, or -1 (same in every thread) when they do not fit.
+template <int R>
+__device__ __forceinline__ long long stage_own_pieces(const double* pieces, const long long* out_ptr, long long j0,
+                                                      long long jend, double* sv, long long cap) {
+  if (j0 >= jend) return -1;
+  const long long Q0 = __ldg(out_ptr + j0), Q1 = __ldg(out_ptr + jend);
+  const long long len = (Q1 - Q0) * R;
+  if (len > cap) return -1;
+  const double2* src = reinterpret_cast<const double2*>(pieces + Q0 * R);
+  double2* dst = reinterpret_cast<double2*>(sv);
+  for (long long i = threadIdx.x; i < len / 2; i += kThreads) dst[i] = __ldcg(src + i);
+  __syncthreads();
+  return Q0;
+}
+
+// Rounds (1 or 2; 1 if neither fits) in which the own columns' pieces are staged.
+template <int R>
+__device__ __forceinline__ int stage_rounds(const long long* out_ptr, long long j0, long long jend, long long cap) {
+  if (j0 >= jend) return 1;
+  const long long Q0 = __ldg(out_ptr + j0), Q1 = __ldg(out_ptr + jend);
+  if ((Q1 - Q0) * R <= cap) return 1;
+  const long long jm = j0 + (jend - j0) / 2;
+  const long long Qm = __ldg(out_ptr + jm);
+  return ((Qm - Q0) * R <= cap && (Q1 - Qm) * R <= cap) ? 2 : 1;
+}
+
 // debug: the stamp buffer set by pcgs_batch_debug_profile (batched kernels)
 unsigned long long* batch_profile_buffer();
 
