@@ -73,9 +73,31 @@ int half_extra(const int* ix, int n, int H) {
   return worst > 0 ? worst - 1 : 0;
 }
 
+// The slots of each shared-memory wavefront group (see sliced.h): slots whose
+// lanes read the same chunk of their rows at one instruction.
+std::vector<std::vector<int>> slot_groups(int R) {
+  const int C = sliced_cpl(R), LS = sliced_lanes_per_slot(R), NS = sliced_slots(R);
+  std::vector<std::vector<int>> g;
+  if (C == 1) {  // 64-bit loads: half-warps of 16 / R consecutive slots
+    for (int h = 0; h < 2; ++h) {
+      g.emplace_back();
+      for (int s = h * NS / 2; s < (h + 1) * NS / 2; ++s) g.back().push_back(s);
+    }
+    return g;
+  }
+  const int spq = 8 / LS, classes = C / 2;  // slots per quarter-warp, chunk classes
+  for (int q = 0; q < 4; ++q)
+    for (int b = 0; b < classes; ++b) {
+      g.emplace_back();
+      for (int m = b; m < spq; m += classes) g.back().push_back(q * spq + m);
+    }
+  return g;
+}
+
 // Lays out slices [a, b) of a slab (pieces already sorted) into the pass.
 void emit_slices(SPassHost& P, SlabPieces& S, const std::vector<uint32_t>& sl_first, size_t a, size_t b, int R) {
-  const int NS = sliced_slots(R), H = 16 / R, NG = sliced_groups(R);
+  const int NS = sliced_slots(R), H = 16 / R;
+  const std::vector<std::vector<int>> groups = slot_groups(R);
   std::vector<Pool> pools(NS);
   for (size_t q = a; q < b; ++q) {
     const uint32_t p0 = sl_first[q], p1 = sl_first[q + 1];
@@ -99,12 +121,12 @@ void emit_slices(SPassHost& P, SlabPieces& S, const std::vector<uint32_t>& sl_fi
     uint16_t* out = P.idx.data() + (size_t)D.v0 * kVecIdx;
     for (uint32_t t = 0; t < L; ++t) {
       for (int k = 0; k < kVecIdx; ++k) {
-        for (int h = 0; h < NG; ++h) {
+        for (const auto& grp : groups) {
           int mult[16] = {};
           int g[16];
           int ng = 0;
           bool pad_seen = false, any = false;
-          for (int s = h * H; s < h * H + H; ++s) {
+          for (const int s : grp) {
             const int ix = pools[s].pick(mult);
             if (ix < 0) {  // the sentinel is in place (one broadcast address)
               if (!pad_seen) {

@@ -88,16 +88,27 @@ __device__ __forceinline__ double2 gather8_pair(uint4 q, unsigned sb) {
 #ifndef PCGS_SLICED_BATCH
 #define PCGS_SLICED_BATCH 4
 #endif
+// Quad mapping: 4 chains of the 8 indices of one vector; the lane reads its
+// two 16-byte chunks in slot-rotated order (sb0 / sb1 hold the rotation),
+// sums per instruction are un-rotated by the caller.
+template <int R>
+__device__ __forceinline__ void gather8_quad(uint4 q, unsigned sb0, unsigned sb1, double2& s0, double2& s1) {
+  s0 = gather8_pair<R>(q, sb0);
+  s1 = gather8_pair<R>(q, sb1);
+}
+
 template <int R, class Epi>
 __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const double* sv, Epi& epi,
                                             int slab_len = 0) {
-  constexpr int NS = sliced_slots(R), LS = sliced_lanes_per_slot(R);
-  constexpr bool PAIR = sliced_pair(R);
+  constexpr int NS = sliced_slots(R), LS = sliced_lanes_per_slot(R), C = sliced_cpl(R);
   constexpr int U = PCGS_SLICED_BATCH;
   const int lane = threadIdx.x & 31, slot = lane / LS, k = lane & (LS - 1);
   const uint2 ws = __ldg(P.warp_slices + wr);
   if (ws.x >= ws.y) return;
-  const unsigned sb = smem_addr(sv) + (unsigned)k * (PAIR ? 16u : 8u);
+  // chunk c of a row = chains 2c, 2c+1; lane k owns chunks [k C/2, (k+1) C/2)
+  const int rot = C == 4 ? (slot & 1) : 0;
+  const unsigned sb = smem_addr(sv) + (unsigned)k * (unsigned)(8 * C);
+  const unsigned sb0 = sb + 16u * (unsigned)rot, sb1 = sb + 16u * (unsigned)(1 - rot);
   const uint2 first = __ldg(P.slices + ws.x), last = __ldg(P.slices + ws.y - 1);
   const char* stream0 = (const char*)(P.vec + first.x);
   const unsigned total = (unsigned)(((size_t)last.x + (size_t)last.y * NS - first.x) * 16u);
@@ -113,10 +124,17 @@ __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const dou
         if (off < end) asm volatile("prefetch.global.L2 [%0];" ::"l"(stream0 + off));
       }
     }
-    double acc = 0.0, acc2 = 0.0;
+    double acc = 0.0, acc2 = 0.0, acc3 = 0.0, acc4 = 0.0;
     auto step = [&](uint4 v) {
       if (PCGS_CHECKED) check_vec(v, slab_len);
-      if (PAIR) {
+      if (C == 4) {
+        double2 g0, g1;
+        gather8_quad<R>(v, sb0, sb1, g0, g1);
+        acc += g0.x;
+        acc2 += g0.y;
+        acc3 += g1.x;
+        acc4 += g1.y;
+      } else if (C == 2) {
         const double2 g = gather8_pair<R>(v, sb);
         acc += g.x;
         acc2 += g.y;
@@ -135,8 +153,19 @@ __device__ __forceinline__ void walk_slices(const SPassDev& P, int wr, const dou
     for (; t < D.y; ++t) step(ldg_stream(vp + (size_t)t * NS));
     PCGS_CHECK(pid == 0xffffffffu || (long long)pid < P.npiece);
     if (pid != 0xffffffffu) {
-      if (PAIR) epi.emit2(pid, 2 * k, acc, acc2);
-      else epi.emit(pid, k, acc);
+      if (C == 4) {  // un-rotate: instruction 0 read chunk 2k + rot
+        if (rot) {
+          epi.emit2(pid, 4 * k, acc3, acc4);
+          epi.emit2(pid, 4 * k + 2, acc, acc2);
+        } else {
+          epi.emit2(pid, 4 * k, acc, acc2);
+          epi.emit2(pid, 4 * k + 2, acc3, acc4);
+        }
+      } else if (C == 2) {
+        epi.emit2(pid, 2 * k, acc, acc2);
+      } else {
+        epi.emit(pid, k, acc);
+      }
     }
   }
 }

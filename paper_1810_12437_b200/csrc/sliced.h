@@ -32,27 +32,33 @@ namespace pcgs {
 
 constexpr int kSlicedPieceMax = 32;  // vectors per piece
 
-// Lane mapping.  Pair mapping (default, R >= 2): a slot is R/2 lanes, lane k
-// of the slot sums chains 2k and 2k+1 with one LDS.128 per index, so a warp
-// walks 64/R pieces at once and the slot's index vector reaches R/2 lanes
-// (half the register writeback of the index stream of the single mapping);
-// a 128-bit shared load is one wavefront per quarter-warp, i.e. per 16/R
-// slots.  Single mapping (PCGS_SLICED_PAIR=0, and R = 1): a slot is R lanes
-// with one chain and one LDS.64 each, 32/R pieces per warp, one wavefront per
-// half-warp = 16/R slots.  Either way the slots of one wavefront group read
-// distinct bank groups iff their indices differ mod 16/R.
-#ifndef PCGS_SLICED_PAIR
-#define PCGS_SLICED_PAIR 1
+// Lane mapping: a slot (one piece per slice) is R/C lanes, each lane summing
+// C consecutive chains of the slot's piece with C/2 LDS.128 per index
+// (C = 1: one LDS.64).  The slot's 16-byte index vector reaches every lane of
+// the slot, so more chains per lane means less register writeback of the
+// index stream (1/(2C) of the gather wavefronts).  Bank groups: a 128-bit
+// shared load is one wavefront per quarter-warp (64-bit: half-warp); the
+// quarter's slots fall into C/2 classes (slot mod C/2) whose lanes read
+// different 16-byte chunks of a row at every instruction (the quad mapping
+// reads a lane's two chunks in slot-rotated order), so within a class H =
+// 16/R slots share the bank groups and must have indices distinct mod H.
+//   quad   (C = 4, R >= 4; default)  R/4 lanes per slot
+//   pair   (C = 2, R >= 2)            R/2 lanes per slot
+//   single (C = 1)                    R lanes per slot
+// PCGS_SLICED_CPL caps C (1, 2 or 4) for A/B builds.
+#ifndef PCGS_SLICED_CPL
+#define PCGS_SLICED_CPL 4
 #endif
 #ifdef __CUDACC__
 #define PCGS_HD __host__ __device__
 #else
 #define PCGS_HD
 #endif
-PCGS_HD constexpr bool sliced_pair(int R) { return PCGS_SLICED_PAIR != 0 && R >= 2; }
-PCGS_HD constexpr int sliced_lanes_per_slot(int R) { return sliced_pair(R) ? R / 2 : R; }
+PCGS_HD constexpr int sliced_cpl(int R) {  // chains per lane
+  return (PCGS_SLICED_CPL >= 4 && R >= 4) ? 4 : (PCGS_SLICED_CPL >= 2 && R >= 2) ? 2 : 1;
+}
+PCGS_HD constexpr int sliced_lanes_per_slot(int R) { return R / sliced_cpl(R); }
 PCGS_HD constexpr int sliced_slots(int R) { return 32 / sliced_lanes_per_slot(R); }
-PCGS_HD constexpr int sliced_groups(int R) { return sliced_pair(R) ? 4 : 2; }  // wavefront groups per warp
 
 struct SliceDesc {  // 8 bytes, device-readable as uint2
   uint32_t v0;      // first vector of the slice

@@ -8,3 +8,7 @@ timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench_r02.json 2>
 python -c "import json; d=json.load(open('gpurun_out/bench_r02.json')); print(d['value'], d['e2e']['value'], d['roofline']['us_per_apply'], d['roofline']['frac'], d['extra']['full_run']['iter_per_s'], d['clocks'])"
 timeout 900 python bench.py --workload config4 --steps 10 --warmup 3 > gpurun_out/bench_c4_r02.json 2> gpurun_out/bench_c4_r02.err; echo "c4 rc $?"
 python -c "import json; d=json.load(open('gpurun_out/bench_c4_r02.json')); print(d['value'], d['ms_per_step'], d['extra'])"
+bash tools/gpu_c4modes.sh 20 > gpurun_out/c4modes.txt 2>&1; cat gpurun_out/c4modes.txt
+timeout 1200 python bench.py --workload config5 --steps 3 --warmup 1 > gpurun_out/bench_c5_r02.json 2> gpurun_out/bench_c5_r02.err; echo "c5 rc $?"
+python -c "import json; d=json.load(open('gpurun_out/bench_c5_r02.json')); print(d['value'], d['ms_per_step'], d.get('roofline'))" 2>&1 | cut -c1-300
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_r02.json 2> gpurun_out/bench_ref_r02.err; echo "ref rc $?"; cut -c1-400 gpurun_out/bench_ref_r02.json
