@@ -42,12 +42,15 @@ constexpr int kSlicedPieceMax = 32;  // vectors per piece
 // different 16-byte chunks of a row at every instruction (the quad mapping
 // reads a lane's two chunks in slot-rotated order), so within a class H =
 // 16/R slots share the bank groups and must have indices distinct mod H.
-//   quad   (C = 4, R >= 4; default)  R/4 lanes per slot
-//   pair   (C = 2, R >= 2)            R/2 lanes per slot
+//   pair   (C = 2, R >= 2; default)  R/2 lanes per slot
+//   quad   (C = 4, R >= 4)            R/4 lanes per slot
 //   single (C = 1)                    R lanes per slot
-// PCGS_SLICED_CPL caps C (1, 2 or 4) for A/B builds.
+// PCGS_SLICED_CPL caps C (1, 2 or 4).  Measured at config 2 (per 8-chain
+// iteration): single 372 us, pair 340, quad 341 (R = 4: pair 186, quad 197):
+// past the pair mapping the index writeback no longer limits and the quad's
+// extra instructions cost.
 #ifndef PCGS_SLICED_CPL
-#define PCGS_SLICED_CPL 4
+#define PCGS_SLICED_CPL 2
 #endif
 #ifdef __CUDACC__
 #define PCGS_HD __host__ __device__
