@@ -119,3 +119,27 @@ def test_batch_size_validation():
     d = synth.binary_design(100, 20, 0.01, 0.3, seed=1)
     with pytest.raises(ValueError):
         batched.BatchedPrecisionOperator(d.matrix(), np.ones((3, 100)), np.ones((3, 21)))
+
+
+@pytest.mark.parametrize("R", [2, 8])
+def test_batched_edge_cases_empty_rows_columns_no_intercept(R):
+    """Empty rows and columns, no intercept, tiny slabs (many slabs, pieces
+    split across slabs): every chain's Phi v equals the oracle's."""
+    rng = np.random.default_rng(40 + R)
+    n, p = 300, 70
+    mask = rng.random((n, p)) < 0.08
+    mask[::7] = False            # empty rows
+    mask[:, ::5] = False         # empty columns
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(mask.sum(1), out=rp[1:])
+    ci = np.nonzero(mask)[1].astype(np.int32)
+    X = pk.SparseDesignMatrix.from_pattern(n, p, rp, ci, intercept=False)
+    X.slab_max = 16
+    Xo = port.design_from_pattern(n, p, rp, ci, intercept=False)
+    om = rng.uniform(0.05, 0.4, (R, n))
+    diag = rng.uniform(0.5, 2.0, (R, p))
+    V = rng.standard_normal((R, p))
+    out = batched.BatchedPrecisionOperator(X, om, diag).apply(V)
+    for c in range(R):
+        ref = port.phi_apply(Xo, om[c], diag[c], V[c])
+        assert np.linalg.norm(out[c] - ref) <= 1e-12 * np.linalg.norm(ref)
