@@ -54,13 +54,14 @@ def test_products_match_oracle(standardize, slab_max):
     np.testing.assert_allclose(X.matvec(v), full @ v, rtol=1e-10, atol=1e-10)
 
 
-@pytest.mark.parametrize("standardize", [False, True])
-def test_fused_pcg_and_rhs_on_affine_design(standardize):
+@pytest.mark.parametrize("standardize,slab_max", [(False, 0), (True, 0), (True, 40)])
+def test_fused_pcg_and_rhs_on_affine_design(standardize, slab_max):
     """The persistent PCG kernel with the affine terms (k_pcg<true>): relative
     L2 < 1e-8 vs the oracle at RMS 1e-10 and the iteration count inside the
     oracle's band of summation orders; the RHS equals the reference formula
     with shared noise."""
     d, X, Xo = dense_design(seed=5, standardize=standardize)
+    X.slab_max = slab_max            # 40: multi-slab CSR (the row combine of k_pcg<true>)
     rng = np.random.default_rng(2)
     om = rng.uniform(0.05, 0.3, d.n)
     lam = np.abs(rng.standard_cauchy(d.p)) + 0.05
@@ -132,3 +133,31 @@ def test_affine_designs_refused_on_sharded_and_batched_paths():
         parallel.local_rows(X, 0, 100)
     with pytest.raises(NotImplementedError):
         batched.BatchedPrecisionOperator(X, np.ones((2, d.n)), np.ones((2, X.n_cols)))
+
+
+def test_standardised_design_without_intercept():
+    """A standardised pattern-only design with no intercept column (no
+    reparametrisation possible): products, the fused PCG and a Gibbs chain
+    run on the affine store; pinned scales give the exact Gaussian."""
+    d = synth.binary_design(500, 50, 5e-3, 0.3, seed=12)
+    X = d.matrix(intercept=False).standardize()
+    Xo = port.Csr(X.n_rows, X.n_cols, X.row_ptr, X.col_idx, X.values, X.col_means.copy(), X.col_scales.copy())
+    rng = np.random.default_rng(3)
+    om = rng.uniform(0.1, 0.3, d.n)
+    lam = rng.uniform(0.5, 2.0, d.p)
+    tau = 0.4
+    diag = (tau * lam) ** -2.0
+    v = rng.standard_normal(d.p)
+    ref = port.phi_apply(Xo, om, diag, v)
+    assert np.linalg.norm(pk.PrecisionOperator(X, om, diag).apply(v) - ref) <= 1e-12 * np.linalg.norm(ref)
+    y, _ = synth.simulate_outcomes(d, seed=2, n_signal=4, intercept=False)
+    cfg = gibbs.BridgeConfig()
+    out = gibbs.gibbs_run(X, y, cfg, 3000, seed=2, fixed_omega=om, fixed_tau=tau, fixed_lam=lam,
+                          cg_config=gibbs.CGConfig(rtol=1e-10))
+    full = X.to_dense()
+    P = full.T @ (om[:, None] * full) + np.diag(diag)
+    cov = np.linalg.inv(P)
+    mean = cov @ (full.T @ (y - 0.5))
+    z = (out.draws.mean(0) - mean) / np.sqrt(np.diag(cov) / len(out.draws))
+    assert np.mean(np.abs(z) > 4) < 0.02
+    assert np.median(np.var(out.draws, axis=0) / np.diag(cov)) == pytest.approx(1.0, abs=0.1)
