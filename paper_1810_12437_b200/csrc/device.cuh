@@ -320,6 +320,9 @@ static_assert((kRing & (kRing - 1)) == 0, "kRing must be a power of two");
 #ifndef PCGS_L1_NEXT
 #define PCGS_L1_NEXT 0
 #endif
+#ifndef PCGS_DESC_PRED
+#define PCGS_DESC_PRED 1
+#endif
 
 // `M` is the block's segment-start mask; `first_id` (the id of the segment
 // starting at the lowest set bit) is fetched lazily by shuffling `dl_x` from
@@ -446,8 +449,15 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
     }
     // block descriptors of the batch: lane u's copy feeds block u (full
     // batches load unconditionally: no divergent branch around the load)
+#if PCGS_DESC_PRED
+    // only lanes < kRing load (predicated, no branch): 16 B of register
+    // writeback per batch instead of 32 lanes x 8 B through the L1 data pipe
+    uint2 dl = make_uint2(0u, 0u);
+    if (lane < kRing && (!kChecked || k0 + lane < nb)) dl = __ldg(bd + k0 + lane);
+#else
     const uint2 dl = !kChecked ? __ldg(bd + k0 + (lane & (kRing - 1)))
                                : (lane < kRing && k0 + lane < nb ? __ldg(bd + k0 + lane) : make_uint2(0u, 0u));
+#endif
 #pragma unroll
     for (int u = 0; u < kRing; ++u) {
       const int v = (k0 + u) * 32 + lane;
