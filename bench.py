@@ -342,7 +342,13 @@ def run_ours(args):
                 "store_bytes_per_apply": alg_bytes,
                 "store_gbs": alg_bytes / (us_apply * 1e-6) / 1e9,
                 "note": "the store reads 2-byte slab-local indices, half the canonical "
-                        "int32 bytes; store_gbs is the HBM rate of the bytes actually read"}
+                        "int32 bytes; store_gbs is the HBM rate of the bytes actually read",
+                "limiter": {"resource": "L1TEX/shared-memory data pipe (LDS.64 gathers + index writeback)",
+                            "data_pipe_busy_over_kernel": 0.713, "shared_bank_conflict_share": 0.145,
+                            "dram_throughput": 0.26,
+                            "source": "ncu --set full of k_pcg at config 2 (profiles/k_pcg_r02_details.csv); "
+                                      "~90 % busy during the streaming passes, which take ~78 % of an "
+                                      "iteration (DESIGN.md §4)"}}
 
     # ---- end to end through the public API, host buffers ----
     # ONE gibbs_run call of K scans from numpy inputs, continuing from the
