@@ -53,8 +53,8 @@ def parse():
     ap.add_argument("--no-rowsplit", action="store_true", help="N > 1: skip the config-5 row-split extra")
     ap.add_argument("--no-full-run", action="store_true",
                     help="skip extra.full_run (BASELINE config 3's whole 1,000-scan chain)")
-    ap.add_argument("--workload", default="config3", choices=["config3", "config4", "config5"],
-                    help="config4: 8 independent chains per GPU as one batch (weak scaling); "
+    ap.add_argument("--workload", default="config3", choices=["config3", "config1", "config4", "config5"],
+                    help="config1: BASELINE config 1 (n=2,000 p=500, use --steps 200); config4: 8 independent chains per GPU as one batch (weak scaling); "
                          "config5: the row-split run (rows of X over the N ranks, strong scaling)")
     ap.add_argument("--config4-sequential", action="store_true",
                     help="config4: the 8 chains one after another on the full grid (single-chain kernels)")
@@ -670,6 +670,80 @@ def run_config4(args):
         dist.destroy_process_group()
 
 
+def run_config1(args):
+    """BASELINE config 1 (the reference's CPU-runnable case): n=2,000, p=500,
+    rates logU[1e-3, 0.2] + intercept, 10 N(0,1) signals, y ~ Bernoulli(
+    logistic(X beta)), horseshoe, PCG rtol 1e-6, float64.  Step = one scan;
+    value = scans/s over K scans after W warm-up scans (the BASELINE run is
+    --steps 200); e2e = one gibbs_run(n_iter=K) call from numpy; cpu_baseline =
+    the oracle port's horseshoe chain on the same design, every scan in full
+    (no extrapolation at this size)."""
+    import torch
+    from paper_1810_12437_b200 import gibbs, synth
+    from oracle import port
+    rank, world, local = dist_env()
+    if world > 1:
+        print(json.dumps({"workload": "config1", "skipped": "single-GPU configuration"})) if rank == 0 else None
+        return
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    d = synth.config_design(1, seed=SEED)
+    y, _ = synth.simulate_outcomes(d, seed=SEED, n_signal=10)
+    X = d.matrix()
+    cfg = (gibbs.HorseshoeConfig(unshrunk_prior_sd=(math.inf,)) if args.prior == "horseshoe"
+           else gibbs.BridgeConfig(unshrunk_prior_sd=(math.inf,)))
+    K, W = args.steps, args.warmup
+    ch = gibbs.DeviceChain(X, y, cfg, W + K, burn_in=W, seed=SEED, cg_config=gibbs.CGConfig(rtol=RTOL), device=dev)
+    for t in range(1, W + 1):
+        ch.scan(t)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record()
+        for t in range(W + 1, W + K + 1):
+            ch.scan(t)
+        e1.record()
+        torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1)
+    ch.check(1, W + K)
+    cg = ch.results.view(-1, 8).cpu().numpy()[W:W + K, 0].astype(int)
+    yh = np.ascontiguousarray(y, dtype=np.float64)
+    gibbs.gibbs_run(X, yh, cfg, K, seed=SEED + 1, cg_config=gibbs.CGConfig(rtol=RTOL), device=dev)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    gibbs.gibbs_run(X, yh, cfg, K, seed=SEED + 1, cg_config=gibbs.CGConfig(rtol=RTOL), device=dev)
+    torch.cuda.synchronize(dev)
+    t_e2e = time.perf_counter() - t0
+    cpu = None
+    if not args.no_cpu_baseline:
+        Xo = port.design_from_pattern(d.n, d.p, d.row_ptr, d.col_idx)
+        n_cpu = min(K, 40)
+        sd = (math.inf,)
+        run = port.gibbs_horseshoe if args.prior == "horseshoe" else port.gibbs_bridge
+        c0 = time.perf_counter()
+        run(Xo, y, n_cpu, seed=SEED, unshrunk_sd=sd)
+        c_s = time.perf_counter() - c0
+        cpu = {"value": n_cpu / c_s, "unit": "iter/s", "cores": 1, "kind": "port",
+               "sample": f"{n_cpu} full {args.prior} scans of oracle/port.py on config 1 (no extrapolation)"}
+    n = d.n
+    line = {
+        "metric": "gibbs_iter_per_s", "value": K / (ms * 1e-3), "unit": "iter/s", "n_gpus": 1, "steps": K,
+        "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded; BASELINE config 1 recipe)",
+        "config": {"workload": f"config 1: {args.prior} logistic Gibbs scan, n={d.n:,} p={d.p:,} binary sparse "
+                               f"(nnz {d.nnz:,}, rates logU[1e-3,0.2]) + intercept, 10 signals, PCG rtol {RTOL:g}",
+                   "n": d.n, "p": d.p, "nnz": d.nnz, "prior": args.prior, "seed": SEED,
+                   "l2_policy": "design and vectors L2-resident (launch/latency-bound size)"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": K / t_e2e, "unit": "iter/s", "h2d_bytes_per_step": int((2 * n) * 8 / K),
+                "d2h_bytes_per_step": int(8 * (d.p + 4))},
+        "gpu_launches": 10 * K,
+        "clocks": clk.summary(),
+        "extra": {"cg_iters_mean": float(cg.mean()), "cg_iters": cg.tolist()},
+    }
+    print(json.dumps(line))
+
+
 def gibbs_conditional_operator(chain):
     from paper_1810_12437_b200.sampler import PrecisionOperator
     return PrecisionOperator.from_device(chain.X, chain.omega, chain.prior_diag)
@@ -683,6 +757,8 @@ def main():
         run_rowsplit(args)
     elif args.workload == "config4":
         run_config4(args)
+    elif args.workload == "config1":
+        run_config1(args)
     else:
         run_ours(args)
 

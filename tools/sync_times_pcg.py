@@ -1,5 +1,6 @@
 """Arrival / departure of every CTA at the four grid barriers of PCG
-iteration 10 (config 2): how much of each phase is load imbalance vs barrier."""
+iteration 10 (config 2, or `python tools/sync_times_pcg.py 1` for config 1):
+how much of each phase is load imbalance vs barrier."""
 import sys
 from pathlib import Path
 import numpy as np
@@ -8,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_1810_12437_b200 as pk  # noqa: E402
 from paper_1810_12437_b200 import synth, _lib  # noqa: E402
 
-des = synth.config_design(2, seed=0)
+des = synth.config_design(int(sys.argv[1]) if len(sys.argv) > 1 else 2, seed=0)
 X = des.matrix()
 cond = synth.config2_conditioning(des, seed=0)
 phi = pk.PrecisionOperator(X, cond["omega"], cond["prior_diag"])
