@@ -257,7 +257,14 @@ __device__ __forceinline__ void bulk_init(BulkFill& B, unsigned long long* mbar)
   __syncthreads();
 }
 
-__device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double* src, int len) {
+struct NoHook {
+  __device__ void operator()() const {}
+};
+
+// `hook` runs on every thread between the copy's issue and the wait, so
+// independent latency-bound work (e.g. a grid-partial reduction) overlaps it.
+template <class Hook = NoHook>
+__device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double* src, int len, Hook hook = Hook{}) {
   const int n2 = len & ~1;
   if (threadIdx.x == 0) {
     const unsigned bytes = (unsigned)n2 * 8u;
@@ -279,6 +286,7 @@ __device__ __forceinline__ void bulk_fill(BulkFill& B, double* sv, const double*
     }
   }
   if ((len & 1) && threadIdx.x == 32) sv[len - 1] = __ldcg(src + len - 1);
+  hook();
   asm volatile(
       "{\n.reg .pred P;\nWAIT_%=:\n"
       "mbarrier.try_wait.parity.shared.b64 P, [%0], %1;\n"

@@ -410,6 +410,33 @@ __device__ __forceinline__ double group_column_sum(const OwnState& o, int S, int
   return sum;
 }
 
+// CSC slab fill whose TMA wait carries the grid sum of the CSR pass's dAd
+// partials (complete since the CSR barrier): warp 1 reduces them while the
+// first slab is in flight, so the step phase finds d'Ad in *out (`done`
+// records it; a CTA with no CSC work leaves the sum to the step phase).
+#ifndef PCGS_DAD_IN_FILL
+#define PCGS_DAD_IN_FILL 1
+#endif
+struct FillVecNDad {
+  const double* w;
+  BulkFill* bf;
+  const double* part;
+  int G;
+  double* out;
+  bool pending, done;
+  __device__ void operator()(double* sv, long long l, int len) {
+    const bool go = pending;
+    done = done || go;
+    bulk_fill(*bf, sv, w + l, len, [&] {
+      if (go && threadIdx.x >= 32 && threadIdx.x < 64) {
+        const double s = warp_sum(lane_partials(part, G, threadIdx.x & 31));
+        if (threadIdx.x == 32) *out = s;
+      }
+    });
+    pending = false;
+  }
+};
+
 __device__ __forceinline__ void traced_sync(const PcgArgs& A, int a, int k) {
   const bool tr = (A.D.dbg & 128) && a == kSyncTraceIter && threadIdx.x == 0 && g_sync_times;
   if (tr) g_sync_times[16 * blockIdx.x + 2 * k] = gtimer();
@@ -624,10 +651,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     }
 
     // ---------------- phase B: CSC pass, pieces of X' w ----------------
+    bool dad_pending;
     {
-      FillVecN f{A.w, &bf};
+      FillVecNDad f{A.w, &bf, A.part, (int)gridDim.x, bc, PCGS_DAD_IN_FILL && a > 0, false};
       EpiStore e{A.pieces, A.D.csc.nseg};
       run_pass(A.D.csc, sv, f, e, A.D.dbg);
+      dad_pending = a > 0 && !f.done;
     }
     if (prof) A.prof[4 * a + 2] = gtimer();
     traced_sync(A, a, 2);
@@ -638,18 +667,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     double alpha = 0.0;
     const int S = A.D.csc.nslab;
     trace_stamp(A, a, 0);
-    // warp 0's loads of the dAd partials overlap the piece staging round trip
+    // (CTAs without CSC work: warp 0's loads of the dAd partials overlap the
+    // piece staging round trip)
     double dpart = 0.0;
-    if (a > 0 && tid < 32) dpart = lane_partials(A.part, gridDim.x, tid);
+    if (dad_pending && tid < 32) dpart = lane_partials(A.part, gridDim.x, tid);
     const bool flat = PCGS_FLAT_STEP && S <= kFlatSlabs && stage_pieces_flat(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
     const bool staged = flat || stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
     trace_stamp(A, a, 1);
     if (a > 0) {
-      if (tid < 32) {
-        dpart = warp_sum(dpart);
-        if (tid == 0) bc[0] = dpart;
+      if (dad_pending) {
+        if (tid < 32) {
+          dpart = warp_sum(dpart);
+          if (tid == 0) bc[0] = dpart;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       const double dAd = bc[0];
       if (!(dAd > 0.0)) {
         if (tid == 0) {
