@@ -11,7 +11,10 @@ namespace pcgs {
 
 struct PassDev {
   const uint4* vec;          // uint16 index vectors (8 per uint4)
-  const uint2* blocks;       // BlockDesc {first_id, mask} per 32-vector block
+  const uint2* blocks;       // BlockDesc {first_id, mask} per 32-vector block;
+                             // grouped layout: per slice {ids offset, steps | log2 W << 24}
+  const unsigned* ids;       // grouped layout: segment ids of the slices' lane groups
+  int grouped;
   const uint4* warps;        // WarpRange {v0, nvec, blk0, pad}
   const int2* task;          // Task {slab, warp0}
   const int* cta_task_ptr;   // G+1
@@ -403,7 +406,7 @@ __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int d
   }
   const uint2* bd = P.blocks + R.z;
   const unsigned long long d0 = (unsigned long long)bd & ~15ull;
-  const unsigned long long d1 = ((unsigned long long)(bd + nb) + 15ull) & ~15ull;
+  const unsigned long long d1 = ((unsigned long long)(bd + (P.grouped ? (int)R.w : nb)) + 15ull) & ~15ull;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d0), "r"((unsigned)(d1 - d0)) : "memory");
 }
 
@@ -492,6 +495,83 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
   if (have_open && lane == 0) epi.emit((long long)open_id, c);
 }
 
+
+// ---------------------------------------------------------------------------
+// Grouped layout (store.h): every lane sums its own vectors into a private
+// accumulator; when a slice ends (a warp-uniform block count) the W lanes of
+// each group add their accumulators by log2 W butterfly steps and the group's
+// first lane emits the segment.  No per-block masks, no segmented scan: the
+// cross-lane traffic is 2 log2 W shuffles per slice.
+// ---------------------------------------------------------------------------
+#ifndef PCGS_GRING
+#define PCGS_GRING 2
+#endif
+constexpr int kGRing = PCGS_GRING;
+
+template <class Epi>
+__device__ __forceinline__ void process_warp_grouped(const PassDev& P, int warp0, const double* sv, Epi& epi,
+                                                     int slab_len = 0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint4 R = __ldg(P.warps + warp0 + warp);
+  const int nvec = (int)R.y;
+  if (nvec == 0) return;
+  const int nb = nvec >> 5;
+  const uint4* base = P.vec + R.x;
+  const uint2* sd = P.blocks + R.z;
+  const int nsl = (int)R.w;
+  const unsigned sb = smem_addr(sv);
+  // slice state: `end` = block count at which the current slice closes
+  uint2 dn = __ldg(sd);
+  int s = 0, end = 0;
+  unsigned lw = 0, id = 0xffffffffu;
+  auto advance = [&]() {
+    if (s < nsl) {
+      end += (int)(dn.y & 0xffffffu);
+      lw = dn.y >> 24;
+      id = __ldg(P.ids + dn.x + ((unsigned)lane >> lw));
+      ++s;
+      if (s < nsl) dn = __ldg(sd + s);
+    } else {
+      end = -1;
+    }
+  };
+  advance();
+  double acc = 0.0;
+  const int nfull = nb / kGRing * kGRing;
+  auto batch = [&](int k0, auto checked) {
+    constexpr bool kChecked = decltype(checked)::value;
+    uint4 q[kGRing];
+    {
+      const unsigned off = (unsigned)(k0 + kPrefetchBlocks) * 512u + (unsigned)lane * 128u;
+      if (lane < 4 * kGRing && off < (unsigned)nvec * 16u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)base + off));
+    }
+#pragma unroll
+    for (int u = 0; u < kGRing; ++u)
+      if (!kChecked || k0 + u < nb) q[u] = ldg_stream(base + (k0 + u) * 32 + lane);
+#pragma unroll
+    for (int u = 0; u < kGRing; ++u) {
+      if (!kChecked || k0 + u < nb) {
+        if (PCGS_CHECKED) check_vec(q[u], slab_len);
+        acc += gather8s(q[u], sb);
+        if (k0 + u + 1 == end) {
+          double t = acc;
+          if (lw > 0) t += __shfl_xor_sync(0xffffffffu, t, 1);
+          if (lw > 1) t += __shfl_xor_sync(0xffffffffu, t, 2);
+          if (lw > 2) t += __shfl_xor_sync(0xffffffffu, t, 4);
+          if (lw > 3) t += __shfl_xor_sync(0xffffffffu, t, 8);
+          if (lw > 4) t += __shfl_xor_sync(0xffffffffu, t, 16);
+          if ((lane & ((1 << lw) - 1)) == 0 && id != 0xffffffffu) epi.emit((long long)id, t);
+          acc = 0.0;
+          advance();
+        }
+      }
+    }
+  };
+  for (int k0 = 0; k0 < nfull; k0 += kGRing) batch(k0, std::false_type());
+  if (nfull < nb) batch(nfull, std::true_type());
+}
+
 // Runs every task of this CTA: fill the slab vector into shared memory, then
 // walk the warp's bundle range.  `fill(sv, lo, len)` must end with a barrier.
 // Not inlined: inside the persistent PCG kernel the caller's live state is
@@ -522,7 +602,8 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
       g_cta_times[3 * c + 0] = t_start;
       g_cta_times[3 * c + 1] = t;
     }
-    process_warp(P, T.y, sv, epi, dbg, (int)(hi - lo));
+    if (P.grouped) process_warp_grouped(P, T.y, sv, epi, (int)(hi - lo));
+    else process_warp(P, T.y, sv, epi, dbg, (int)(hi - lo));
   }
   if (dbg & 64) {
     __syncthreads();

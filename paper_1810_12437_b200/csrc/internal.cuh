@@ -55,6 +55,8 @@ inline int upload_pass(pcgs_design* D, const PassHost& H, PassDev& P) {
   const BlockDesc* b;
   if ((rc = upload(D, H.blocks, &b))) return rc;
   P.blocks = (const uint2*)b;
+  if ((rc = upload(D, H.ids, &P.ids))) return rc;
+  P.grouped = H.grouped;
   const WarpRange* w;
   if ((rc = upload(D, H.warps, &w))) return rc;
   P.warps = (const uint4*)w;

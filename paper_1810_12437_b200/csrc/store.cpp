@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -16,13 +17,17 @@ namespace pcgs {
 
 namespace {
 
+// Layout of the pass streams: grouped (default) or the flat stream with
+// per-block segment masks (PCGS_LAYOUT=flat), see store.h.
+bool layout_grouped() {
+  const char* e = getenv("PCGS_LAYOUT");
+  return !(e && std::string(e) == "flat");
+}
+
 // CSC pieces: at most this many vectors (load balance); PCGS_PIECE_MAX overrides (tuning)
 int64_t piece_max_vec() {
-  static const int64_t v = [] {
-    const char* e = getenv("PCGS_PIECE_MAX");
-    return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)256;
-  }();
-  return v;
+  const char* e = getenv("PCGS_PIECE_MAX");
+  return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)(layout_grouped() ? 128 : 256);
 }
 
 std::vector<int64_t> make_slabs(int64_t len, int64_t slab_max) {
@@ -177,6 +182,158 @@ void emit_warp(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std::vector
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Grouped layout (store.h): width classes, slices, warp dealing, placement.
+// ---------------------------------------------------------------------------
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+// log2 of the lane-group width of a segment of nv vectors: wide groups for
+// long segments (the round-up to W vectors stays a few percent), one lane for
+// the shortest ones.
+int width_log(uint32_t nv) {
+  static const int w8 = env_int("PCGS_GW8", 80), w4 = env_int("PCGS_GW4", 40), w2 = env_int("PCGS_GW2", 12);
+  return nv >= (uint32_t)w8 ? 3 : nv >= (uint32_t)w4 ? 2 : nv >= (uint32_t)w2 ? 1 : 0;
+}
+
+// vector slots a segment occupies in its slice, in 1/16 vector units, plus its
+// share of the slice close
+uint64_t group_cost16(uint32_t nv) {
+  static const int close = env_int("PCGS_G_CLOSE16", 16);
+  const uint32_t W = 1u << width_log(nv);
+  return 16ull * ((nv + W - 1) / W * W) + (uint64_t)close;
+}
+
+struct Slice {
+  uint32_t first, count;  // items [first, first + count)
+  uint32_t T;             // steps
+  uint8_t lw;
+};
+
+// Lays out segments [s0, s1) of slab S as one CTA task: kWarps warp ranges.
+void emit_task_grouped(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std::vector<Pool>& pools) {
+  struct Item {
+    uint32_t seg, nv;
+    uint8_t lw;
+  };
+  std::vector<Item> items;
+  items.reserve(s1 - s0);
+  for (size_t s = s0; s < s1; ++s) items.push_back(Item{(uint32_t)s, S.segs[s].nv, (uint8_t)width_log(S.segs[s].nv)});
+  // a task with fewer slices than warps (small designs, many CTAs) widens its
+  // groups, up to the whole warp, while a segment still fills its lanes
+  for (int round = 0; round < 5; ++round) {
+    size_t nslices = 0;
+    uint32_t cnt[6] = {};
+    for (const Item& it : items) ++cnt[it.lw];
+    for (int lw = 0; lw < 6; ++lw) nslices += (cnt[lw] + (32u >> lw) - 1) / (32u >> lw);
+    if (nslices >= (size_t)kWarps) break;
+    bool any = false;
+    for (Item& it : items)
+      if (it.lw < 5 && (2u << it.lw) <= it.nv) {
+        ++it.lw;
+        any = true;
+      }
+    if (!any) break;
+  }
+  std::stable_sort(items.begin(), items.end(), [](const Item& a, const Item& b) {
+    return a.lw != b.lw ? a.lw > b.lw : a.nv > b.nv;
+  });
+  std::vector<Slice> slices;
+  for (size_t i = 0; i < items.size();) {
+    const uint8_t lw = items[i].lw;
+    const uint32_t NG = 32u >> lw, W = 1u << lw;
+    size_t j = i;
+    while (j < items.size() && items[j].lw == lw && j - i < NG) ++j;
+    slices.push_back(Slice{(uint32_t)i, (uint32_t)(j - i), (items[i].nv + W - 1) / W, lw});
+    i = j;
+  }
+  // deal slices to warps, longest first, each to the least loaded warp
+  std::vector<uint32_t> order(slices.size());
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return slices[a].T > slices[b].T; });
+  std::vector<std::vector<uint32_t>> mine(kWarps);
+  {
+    static const int close = env_int("PCGS_G_SLICE_COST", 1);
+    uint64_t load[kWarps] = {};
+    for (uint32_t q : order) {
+      int w = 0;
+      for (int c = 1; c < kWarps; ++c)
+        if (load[c] < load[w]) w = c;
+      mine[w].push_back(q);
+      load[w] += slices[q].T + (uint64_t)close;
+    }
+  }
+  for (int w = 0; w < kWarps; ++w) {
+    WarpRange R{};
+    R.v0 = (uint32_t)(P.idx.size() / kVecIdx);
+    R.blk0 = (uint32_t)P.blocks.size();
+    R.pad = (uint32_t)mine[w].size();
+    uint64_t nvec = 0;
+    for (uint32_t q : mine[w]) nvec += 32ull * slices[q].T;
+    R.nvec = (uint32_t)nvec;
+    P.warps.push_back(R);
+    if (nvec == 0) continue;
+    P.idx.resize(P.idx.size() + nvec * kVecIdx, S.sentinel);
+    uint16_t* out = P.idx.data() + (size_t)R.v0 * kVecIdx;
+    for (uint32_t q : mine[w]) {
+      const Slice& L = slices[q];
+      const uint32_t NG = 32u >> L.lw, W = 1u << L.lw;
+      P.blocks.push_back(BlockDesc{(uint32_t)P.ids.size(), L.T | ((uint32_t)L.lw << 24)});
+      uint64_t real_vec = 0;
+      for (uint32_t g = 0; g < NG; ++g) {
+        if (g < L.count) {
+          const Seg& sg = S.segs[items[L.first + g].seg];
+          P.ids.push_back(sg.id);
+          pools[g].load(S.buf.data() + sg.off, sg.len);
+          real_vec += sg.nv;
+        } else {
+          P.ids.push_back(0xffffffffu);
+          pools[g].load(nullptr, 0);
+        }
+      }
+      P.pad_vectors += 32ll * L.T - (int64_t)real_vec;
+      // bank-balanced placement: one LDS.64 per (step, slot); group = half-warp
+      for (uint32_t t = 0; t < L.T; ++t) {
+        for (int slot = 0; slot < kVecIdx; ++slot) {
+          for (int h = 0; h < 2; ++h) {
+            uint16_t g16[16];
+            int ng = 0;
+            uint8_t mult[16] = {};
+            bool pad_seen = false;
+            // the half-warp's groups pick in turn (one lane of each per
+            // round, the starting group rotating), so no group is left the
+            // residues the others did not want
+            const int ngh = L.lw >= 4 ? 1 : 16 >> L.lw;  // groups per half-warp
+            const int rot = (int)((t * kVecIdx + slot) % ngh);
+            for (int r = 0; r < 16; ++r) {
+              const int gi = (r + rot) % ngh, ki = r / ngh;
+              const int l = 16 * h + (L.lw >= 4 ? r : gi * (int)W + ki);
+              const int ix = pools[l >> L.lw].pick(mult);
+              if (ix < 0) {  // the sentinel is already in place (one broadcast address)
+                if (!pad_seen) {
+                  pad_seen = true;
+                  ++mult[S.sentinel & 15];
+                  g16[ng++] = S.sentinel;
+                }
+                continue;
+              }
+              ++mult[ix & 15];
+              out[((size_t)t * 32 + l) * kVecIdx + slot] = (uint16_t)ix;
+              g16[ng++] = (uint16_t)ix;
+            }
+            ++P.lds_groups;
+            P.lds_conflict_excess += group_extra(g16, ng);
+          }
+        }
+      }
+      out += (size_t)L.T * 32 * kVecIdx;
+    }
+  }
+}
+
 // Balanced cut of segments [a, b) into `parts` ranges by vector count.
 void cut(const std::vector<uint64_t>& pre, size_t a, size_t b, int parts, std::vector<size_t>& outv) {
   outv.clear();
@@ -220,6 +377,8 @@ void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G, bool csc) {
   const int ns = (int)slabs.size();
   P.cta_task_ptr.assign(G + 1, 0);
   std::vector<Pool> pools(40);
+  const bool grouped = layout_grouped();
+  P.grouped = grouped ? 1 : 0;
   std::vector<std::vector<uint64_t>> pre(ns);
   std::vector<uint64_t> sw(ns);
   uint64_t W = 0;
@@ -229,15 +388,20 @@ void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G, bool csc) {
     // cost model for balancing: a vector plus a per-segment charge (segment
     // closes: reductions, epilogue), in 1/16 vector units
     for (size_t q = 0; q < slabs[s].segs.size(); ++q)
-      pr[q + 1] = pr[q] + 16u * slabs[s].segs[q].nv + seg_charge16(slabs[s].segs[q].nv, csc);
+      pr[q + 1] = pr[q] + (grouped ? group_cost16(slabs[s].segs[q].nv)
+                                   : 16u * slabs[s].segs[q].nv + seg_charge16(slabs[s].segs[q].nv, csc));
     sw[s] = pr.back();
     W += sw[s];
   }
   auto emit_task = [&](int s, size_t a, size_t b) {
     Task t{s, (int32_t)P.warps.size()};
-    std::vector<size_t> wc;
-    cut(pre[s], a, b, kWarps, wc);
-    for (int w = 0; w < kWarps; ++w) emit_warp(P, slabs[s], wc[w], wc[w + 1], pools);
+    if (grouped) {
+      emit_task_grouped(P, slabs[s], a, b, pools);
+    } else {
+      std::vector<size_t> wc;
+      cut(pre[s], a, b, kWarps, wc);
+      for (int w = 0; w < kWarps; ++w) emit_warp(P, slabs[s], wc[w], wc[w + 1], pools);
+    }
     P.tasks.push_back(t);
   };
   if (ns <= G) {
@@ -386,6 +550,12 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
     P.nseg = piece;
     plan_and_emit(P, slabs, G, true);
   }
+  if (getenv("PCGS_STORE_STATS"))
+    for (const PassHost* P : {&D.csr, &D.csc})
+      fprintf(stderr, "pcgs store: %s vectors %zu pad %lld slices/blocks %zu half-warp gathers %lld excess %lld (%.3f)\n",
+              P == &D.csr ? "csr" : "csc", P->idx.size() / kVecIdx, (long long)P->pad_vectors, P->blocks.size(),
+              (long long)P->lds_groups, (long long)P->lds_conflict_excess,
+              (double)P->lds_conflict_excess / (double)std::max<int64_t>(1, P->lds_groups));
   return "";
 }
 
@@ -402,6 +572,28 @@ std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int
       for (int w = 0; w < kWarps; ++w) {
         const WarpRange& R = P.warps[T.warp0 + w];
         if (R.nvec == 0) continue;
+        if (P.grouped) {
+          if (R.nvec % 32) return std::string("grouped range is not whole blocks");
+          uint64_t v = R.v0;
+          for (uint32_t q = 0; q < R.pad; ++q) {
+            const BlockDesc& B = P.blocks[R.blk0 + q];
+            const uint32_t steps = B.mask & 0xffffffu, lw = B.mask >> 24;
+            if (lw > 5 || steps == 0) return std::string("bad slice descriptor");
+            for (uint32_t t = 0; t < steps; ++t)
+              for (int l = 0; l < 32; ++l, ++v) {
+                const uint32_t id = P.ids[B.first_id + (l >> lw)];
+                for (int e = 0; e < kVecIdx; ++e) {
+                  const uint16_t ix = P.idx[v * kVecIdx + e];
+                  if (ix == sent) continue;
+                  if (ix > sent) return std::string("index beyond slab");
+                  if (id == 0xffffffffu) return std::string("index in an empty group");
+                  f(T.slab, (int64_t)id, lo + ix);
+                }
+              }
+          }
+          if (v != (uint64_t)R.v0 + R.nvec) return std::string("slices do not cover the warp range");
+          continue;
+        }
         const uint32_t nb = (R.nvec + 31) / 32;
         int64_t seg = -1;
         for (uint32_t k = 0; k < nb; ++k) {
@@ -427,6 +619,18 @@ std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int
     }
     return std::string();
   };
+  // grouped layout: every segment id is emitted by exactly one slice group
+  for (const PassHost* P : {&D.csr, &D.csc}) {
+    if (!P->grouped) continue;
+    std::vector<uint8_t> seen((size_t)P->nseg, 0);
+    for (uint32_t id : P->ids) {
+      if (id == 0xffffffffu) continue;
+      if ((int64_t)id >= P->nseg || seen[id]) return std::string("segment id emitted twice or out of range");
+      seen[id] = 1;
+    }
+    for (uint8_t b : seen)
+      if (!b) return std::string("segment never emitted");
+  }
   // CSR: segment (s, i) -> column set of row i within slab s
   std::vector<std::vector<int32_t>> got_rows(n);
   std::string err = walk(D.csr, [&](int s, int64_t seg, int64_t col) {

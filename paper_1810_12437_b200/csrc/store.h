@@ -16,6 +16,20 @@
 //   * inside a segment the index order is free (the sum is order-independent
 //     in exact arithmetic), so the builder places indices so that each 16-lane
 //     half-warp LDS.64 of a block touches distinct shared-memory bank pairs.
+//
+// GROUPED layout (PassHost::grouped, the default; PCGS_LAYOUT=flat selects
+// the flat stream above): a segment is summed inside a fixed GROUP of
+// W = 1, 2, 4, ... 32 adjacent lanes (W grows with the segment's length), so a
+// block needs no segmented warp reduction -- the cross-lane work is log2 W
+// butterfly steps when a SLICE ends.  A slice is 32/W segments of one width
+// class and similar length walked in lockstep for T = ceil(max nv / W) steps;
+// step t is one 32-vector block (lane g*W + k holds vector t*W + k of the
+// slice's g-th segment, sentinel-padded).  A CTA's segments are sorted by
+// length before slicing (padding stays small), its slices are dealt to the 32
+// warps longest first (each to the least loaded warp), and a warp's slices
+// are contiguous in the stream.  `blocks` then holds one descriptor per slice
+// {offset into `ids`, T | log2 W << 24} and `ids` the 32/W segment ids of
+// each slice (0xffffffff: empty group); WarpRange.pad counts the slices.
 #pragma once
 #include <cstdint>
 #include <string>
@@ -31,7 +45,7 @@ struct WarpRange {    // 16 bytes, device-readable as uint4
   uint32_t v0;        // first vector of the range in the pass stream
   uint32_t nvec;      // vectors in the range
   uint32_t blk0;      // first block descriptor
-  uint32_t pad;
+  uint32_t pad;       // grouped layout: slices in the range
 };
 
 struct BlockDesc {    // 8 bytes, device-readable as uint2
@@ -49,6 +63,9 @@ struct PassHost {
   std::vector<int64_t> slab_lo;        // nslab+1 boundaries in gathered-vector coords
   std::vector<uint16_t> idx;           // nvec * 8 indices
   std::vector<BlockDesc> blocks;
+  std::vector<uint32_t> ids;           // grouped layout: segment ids per slice group
+  int grouped = 0;
+  int64_t pad_vectors = 0;             // grouped layout: all-sentinel vector slots
   std::vector<WarpRange> warps;
   std::vector<Task> tasks;
   std::vector<int32_t> cta_task_ptr;   // G+1
