@@ -15,6 +15,8 @@ struct PassDev {
                              // grouped layout: per slice {ids offset, steps | log2 W << 24}
   const unsigned* ids;       // grouped layout: segment ids of the slices' lane groups
   int grouped;
+  const int* rep_ptr;             // nslab+1 offsets into rep_src (null: no replicas)
+  const unsigned short* rep_src;  // replica k of slab s copies slab entry rep_src[rep_ptr[s] + k]
   const uint4* warps;        // WarpRange {v0, nvec, blk0, pad}
   const int2* task;          // Task {slab, warp0}
   const int* cta_task_ptr;   // G+1
@@ -506,6 +508,7 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 #ifndef PCGS_GRING
 #define PCGS_GRING 2
 #endif
+
 constexpr int kGRing = PCGS_GRING;
 
 template <class Epi>
@@ -537,6 +540,52 @@ __device__ __forceinline__ void process_warp_grouped(const PassDev& P, int warp0
   };
   advance();
   double acc = 0.0;
+  // closes the current slice when block `k` was its last
+  auto close_if_end = [&](int k) {
+    if (k + 1 == end) {
+      double t = acc;
+      if (lw > 0) t += __shfl_xor_sync(0xffffffffu, t, 1);
+      if (lw > 1) t += __shfl_xor_sync(0xffffffffu, t, 2);
+      if (lw > 2) t += __shfl_xor_sync(0xffffffffu, t, 4);
+      if (lw > 3) t += __shfl_xor_sync(0xffffffffu, t, 8);
+      if (lw > 4) t += __shfl_xor_sync(0xffffffffu, t, 16);
+      if ((lane & ((1 << lw) - 1)) == 0 && id != 0xffffffffu) epi.emit((long long)id, t);
+      acc = 0.0;
+      advance();
+    }
+  };
+#if PCGS_GPIPE
+  // two register batches of kGRing blocks: the loads of one batch are in
+  // flight while the other is consumed (the index loads' latency is what the
+  // 8 warps per scheduler cannot hide on their own)
+  auto load = [&](uint4(&q)[kGRing], int k0) {
+#pragma unroll
+    for (int u = 0; u < kGRing; ++u)
+      if (k0 + u < nb) q[u] = ldg_stream(base + (k0 + u) * 32 + lane);
+  };
+  auto consume = [&](uint4(&q)[kGRing], int k0) {
+#pragma unroll
+    for (int u = 0; u < kGRing; ++u)
+      if (k0 + u < nb) {
+        if (PCGS_CHECKED) check_vec(q[u], slab_len);
+        acc += gather8s(q[u], sb);
+        close_if_end(k0 + u);
+      }
+  };
+  uint4 qa[kGRing], qb[kGRing];
+  load(qa, 0);
+  for (int k0 = 0; k0 < nb; k0 += 2 * kGRing) {
+    load(qb, k0 + kGRing);
+    {
+      const unsigned off = (unsigned)(k0 + kGPrefetch) * 512u + (unsigned)lane * 128u;
+      if (lane < 8 * kGRing && off < (unsigned)nvec * 16u)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)base + off));
+    }
+    consume(qa, k0);
+    load(qa, k0 + 2 * kGRing);
+    consume(qb, k0 + kGRing);
+  }
+#else
   const int nfull = nb / kGRing * kGRing;
   auto batch = [&](int k0, auto checked) {
     constexpr bool kChecked = decltype(checked)::value;
@@ -554,22 +603,13 @@ __device__ __forceinline__ void process_warp_grouped(const PassDev& P, int warp0
       if (!kChecked || k0 + u < nb) {
         if (PCGS_CHECKED) check_vec(q[u], slab_len);
         acc += gather8s(q[u], sb);
-        if (k0 + u + 1 == end) {
-          double t = acc;
-          if (lw > 0) t += __shfl_xor_sync(0xffffffffu, t, 1);
-          if (lw > 1) t += __shfl_xor_sync(0xffffffffu, t, 2);
-          if (lw > 2) t += __shfl_xor_sync(0xffffffffu, t, 4);
-          if (lw > 3) t += __shfl_xor_sync(0xffffffffu, t, 8);
-          if (lw > 4) t += __shfl_xor_sync(0xffffffffu, t, 16);
-          if ((lane & ((1 << lw) - 1)) == 0 && id != 0xffffffffu) epi.emit((long long)id, t);
-          acc = 0.0;
-          advance();
-        }
+        close_if_end(k0 + u);
       }
     }
   };
   for (int k0 = 0; k0 < nfull; k0 += kGRing) batch(k0, std::false_type());
   if (nfull < nb) batch(nfull, std::true_type());
+#endif
 }
 
 // Runs every task of this CTA: fill the slab vector into shared memory, then
@@ -596,14 +636,29 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
     } else {
       fill(sv, lo, (int)(hi - lo));
     }
+    // replicas (store.h): second copies of the slab's most gathered entries
+    // behind the sentinel, at other bank pairs (the fill ended with a barrier)
+    int nrep = 0;
+    if (P.rep_ptr) {
+      const int r0 = P.rep_ptr[T.x];
+      nrep = P.rep_ptr[T.x + 1] - r0;
+      if (nrep > 0) {
+        double* rp = sv + (hi - lo) + 1;
+        for (int k = threadIdx.x; k < nrep; k += kThreads) rp[k] = sv[__ldg(P.rep_src + r0 + k)];
+        __syncthreads();
+      }
+    }
     if ((dbg & 64) && threadIdx.x == 0 && g_cta_times) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
       g_cta_times[3 * c + 0] = t_start;
       g_cta_times[3 * c + 1] = t;
     }
-    if (P.grouped) process_warp_grouped(P, T.y, sv, epi, (int)(hi - lo));
-    else process_warp(P, T.y, sv, epi, dbg, (int)(hi - lo));
+#if PCGS_FLAT_WALK
+    if (!P.grouped) process_warp(P, T.y, sv, epi, dbg, (int)(hi - lo));
+    else
+#endif
+      process_warp_grouped(P, T.y, sv, epi, (int)(hi - lo) + nrep);
   }
   if (dbg & 64) {
     __syncthreads();

@@ -57,6 +57,14 @@ inline int upload_pass(pcgs_design* D, const PassHost& H, PassDev& P) {
   P.blocks = (const uint2*)b;
   if ((rc = upload(D, H.ids, &P.ids))) return rc;
   P.grouped = H.grouped;
+  P.rep_ptr = nullptr;
+  P.rep_src = nullptr;
+  if (!H.rep_src.empty()) {
+    if ((rc = upload(D, H.rep_ptr, &P.rep_ptr))) return rc;
+    const uint16_t* rs;
+    if ((rc = upload(D, H.rep_src, &rs))) return rc;
+    P.rep_src = (const unsigned short*)rs;
+  }
   const WarpRange* w;
   if ((rc = upload(D, H.warps, &w))) return rc;
   P.warps = (const uint4*)w;

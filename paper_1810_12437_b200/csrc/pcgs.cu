@@ -845,7 +845,7 @@ int pcgs_design_create_affine(int64_t n, int64_t p, const int64_t* row_ptr_h, co
   int64_t maxlen = 0;
   for (const PassHost* P : {&H.csr, &H.csc})
     for (int q = 0; q < P->nslab; ++q) maxlen = std::max<int64_t>(maxlen, P->slab_lo[q + 1] - P->slab_lo[q]);
-  dd.smem_doubles = (int)((maxlen + 1 + 15) / 16 * 16);
+  dd.smem_doubles = std::max((int)((maxlen + 1 + 15) / 16 * 16), H.slab_area);  // slab + sentinel + replicas
   dd.own_global = nullptr;
   int rc;
   {

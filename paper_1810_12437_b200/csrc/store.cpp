@@ -20,14 +20,18 @@ namespace {
 // Layout of the pass streams: grouped (default) or the flat stream with
 // per-block segment masks (PCGS_LAYOUT=flat), see store.h.
 bool layout_grouped() {
+#if PCGS_FLAT_WALK
   const char* e = getenv("PCGS_LAYOUT");
   return !(e && std::string(e) == "flat");
+#else
+  return true;
+#endif
 }
 
 // CSC pieces: at most this many vectors (load balance); PCGS_PIECE_MAX overrides (tuning)
 int64_t piece_max_vec() {
   const char* e = getenv("PCGS_PIECE_MAX");
-  return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)(layout_grouped() ? 128 : 256);
+  return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)256;
 }
 
 std::vector<int64_t> make_slabs(int64_t len, int64_t slab_max) {
@@ -52,6 +56,7 @@ struct SlabSegs {
   std::vector<uint16_t> buf;
   std::vector<Seg> segs;
   uint16_t sentinel = 0;
+  std::vector<uint16_t> rep_of;  // slab index -> its replica's index (0xffff: none), grouped layout
   void add(uint32_t id, const uint16_t* d, uint32_t len) {
     Seg s{id, buf.size(), len, len == 0 ? 1u : (len + kVecIdx - 1) / kVecIdx};
     buf.insert(buf.end(), d, d + len);
@@ -68,28 +73,70 @@ struct SlabSegs {
 // holds max_b c_b indices but each group takes it once, so max_b c_b - groups
 // extra wavefronts are unavoidable (~20 % for an 800-index row).
 struct Pool {
-  std::array<std::vector<uint16_t>, 16> b;
+  std::array<std::vector<uint16_t>, 16> b;  // entries with one address, by bank pair
+  // entries with a replica: two addresses (store.h, REPLICAS); each id sits in
+  // the lists of both its bank pairs and is removed lazily
+  std::vector<std::array<uint16_t, 2>> flex;
+  std::vector<uint8_t> taken;
+  std::array<std::vector<uint32_t>, 16> fl;
+  std::array<uint32_t, 16> nfl{};
   uint32_t remaining = 0;
-  void load(const uint16_t* d, uint32_t len) {
+  void load(const uint16_t* d, uint32_t len, const std::vector<uint16_t>* rep_of = nullptr) {
     for (auto& v : b) v.clear();
-    for (uint32_t t = 0; t < len; ++t) b[d[t] & 15].push_back(d[t]);
+    for (auto& v : fl) v.clear();
+    flex.clear();
+    taken.clear();
+    nfl.fill(0);
+    for (uint32_t t = 0; t < len; ++t) {
+      const uint16_t ix = d[t];
+      const uint16_t rp = rep_of && !rep_of->empty() ? (*rep_of)[ix] : (uint16_t)0xffff;
+      if (rp == 0xffff || ((rp ^ ix) & 15) == 0) {
+        b[ix & 15].push_back(ix);
+      } else {
+        const uint32_t id = (uint32_t)flex.size();
+        flex.push_back({ix, rp});
+        taken.push_back(0);
+        fl[ix & 15].push_back(id);
+        fl[rp & 15].push_back(id);
+        ++nfl[ix & 15];
+        ++nfl[rp & 15];
+      }
+    }
     remaining = len;
   }
   int take(int k) {
-    const int v = b[k].back();
-    b[k].pop_back();
     --remaining;
-    return v;
+    if (!b[k].empty()) {
+      const int v = b[k].back();
+      b[k].pop_back();
+      return v;
+    }
+    auto& L = fl[k];
+    while (taken[L.back()]) L.pop_back();
+    const uint32_t id = L.back();
+    L.pop_back();
+    taken[id] = 1;
+    --nfl[flex[id][0] & 15];
+    --nfl[flex[id][1] & 15];
+    return (flex[id][0] & 15) == k ? flex[id][0] : flex[id][1];
   }
-  // an index whose bank pair has the lowest multiplicity in the group so far
-  // (largest bucket among those); -1 when empty
+  // an index whose bank pair has the lowest multiplicity in the group so far;
+  // among those a single-address entry (largest bucket) before a two-address
+  // one (they stay free to fill the gaps later); -1 when empty
   int pick(const uint8_t* mult) {
     if (remaining == 0) return -1;
     int best = -1;
+    uint64_t best_key = 0;
     for (int k = 0; k < 16; ++k) {
-      if (b[k].empty()) continue;
-      if (best < 0 || mult[k] < mult[best] || (mult[k] == mult[best] && b[k].size() > b[best].size()))
+      const bool fixed = !b[k].empty();
+      if (!fixed && nfl[k] == 0) continue;
+      // smaller is better: multiplicity, then fixed before flexible, then the fuller bucket
+      const uint64_t key = ((uint64_t)mult[k] << 40) | ((uint64_t)(fixed ? 0 : 1) << 32) |
+                           (uint64_t)(0xffffffffu - (fixed ? (uint32_t)b[k].size() : nfl[k]));
+      if (best < 0 || key < best_key) {
         best = k;
+        best_key = key;
+      }
     }
     return take(best);
   }
@@ -195,7 +242,9 @@ int env_int(const char* name, int dflt) {
 // long segments (the round-up to W vectors stays a few percent), one lane for
 // the shortest ones.
 int width_log(uint32_t nv) {
-  static const int w8 = env_int("PCGS_GW8", 80), w4 = env_int("PCGS_GW4", 40), w2 = env_int("PCGS_GW2", 12);
+  // swept on the config-2 PCG iteration (tools/gpu_sweep_group*.sh): 80/40/12
+  // with 128-vector pieces 73.3 us, 128/64/16 71.5, with 256-vector pieces 70.8
+  static const int w8 = env_int("PCGS_GW8", 128), w4 = env_int("PCGS_GW4", 64), w2 = env_int("PCGS_GW2", 16);
   return nv >= (uint32_t)w8 ? 3 : nv >= (uint32_t)w4 ? 2 : nv >= (uint32_t)w2 ? 1 : 0;
 }
 
@@ -206,6 +255,9 @@ uint64_t group_cost16(uint32_t nv) {
   const uint32_t W = 1u << width_log(nv);
   return 16ull * ((nv + W - 1) / W * W) + (uint64_t)close;
 }
+
+long long g_hist[6 * 20];
+long long* g_dbg_hist = nullptr;  // PCGS_STORE_STATS: [lw][decile of the slice]{gathers, excess}
 
 struct Slice {
   uint32_t first, count;  // items [first, first + count)
@@ -287,7 +339,7 @@ void emit_task_grouped(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std
         if (g < L.count) {
           const Seg& sg = S.segs[items[L.first + g].seg];
           P.ids.push_back(sg.id);
-          pools[g].load(S.buf.data() + sg.off, sg.len);
+          pools[g].load(S.buf.data() + sg.off, sg.len, &S.rep_of);
           real_vec += sg.nv;
         } else {
           P.ids.push_back(0xffffffffu);
@@ -325,12 +377,71 @@ void emit_task_grouped(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std
               g16[ng++] = (uint16_t)ix;
             }
             ++P.lds_groups;
-            P.lds_conflict_excess += group_extra(g16, ng);
+            const int ex = group_extra(g16, ng);
+            P.lds_conflict_excess += ex;
+            if (g_dbg_hist) {
+              const int dec = (int)((t * kVecIdx + slot) * 10 / (L.T * kVecIdx));
+              g_dbg_hist[L.lw * 20 + dec * 2] += 1;
+              g_dbg_hist[L.lw * 20 + dec * 2 + 1] += ex;
+            }
           }
         }
       }
       out += (size_t)L.T * 32 * kVecIdx;
     }
+  }
+}
+
+
+// REPLICAS (store.h): the shared-memory area behind a slab's sentinel holds
+// second copies of the slab's most gathered entries at a different bank pair,
+// so the placement below can move an occurrence off an over-subscribed bank
+// pair.  Fills `rep_of` of every slab and the pass's rep_ptr / rep_src.
+void choose_replicas(PassHost& P, std::vector<SlabSegs>& slabs, int64_t area, bool grouped) {
+  P.rep_ptr.assign(1, 0);
+  // off by default: measured at config 2 the replicas cut the predicted (and
+  // ncu-counted) bank conflicts from 16 % to 2 % of the gather wavefronts and
+  // the PCG iteration not at all (71.3 vs 71.0 us) -- the passes are bound by
+  // the LSU's 16 lanes per cycle, not by the data banks
+  const int on = env_int("PCGS_REPLICAS", 0);
+  for (SlabSegs& S : slabs) {
+    const int64_t len = S.sentinel;
+    int64_t K = std::min<int64_t>(area - (len + 1), 65535 - (len + 1));
+    K = std::min<int64_t>(K, len);
+    if (!grouped || !on || K < 16) {
+      P.rep_ptr.push_back((int32_t)P.rep_src.size());
+      continue;
+    }
+    std::vector<uint32_t> cnt((size_t)len, 0);
+    for (uint16_t ix : S.buf) ++cnt[ix];
+    std::vector<uint32_t> order((size_t)len);
+    std::iota(order.begin(), order.end(), 0u);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cnt[a] > cnt[b]; });
+    std::array<std::vector<uint32_t>, 16> free_;
+    for (int64_t k = K - 1; k >= 0; --k) free_[(len + 1 + k) & 15].push_back((uint32_t)k);
+    S.rep_of.assign((size_t)len, (uint16_t)0xffff);
+    std::vector<uint16_t> src((size_t)K, (uint16_t)len);  // unused slots copy the sentinel's zero
+    int64_t placed = 0;
+    for (int64_t q = 0; q < len && placed < K; ++q) {
+      const uint32_t j = order[q];
+      if (cnt[j] == 0) break;
+      // the replica's bank pair: a pseudo-random offset from the original's, so
+      // the two-address entries link all 16 pairs (a fixed offset would only
+      // trade occurrences inside 8 rigid pair classes)
+      const uint32_t h = (j * 2654435761u) >> 16;
+      for (int d = 0; d < 16; ++d) {
+        const int r = (int)((j + 1 + h % 15 + d) & 15);
+        if (r == (int)(j & 15) || free_[r].empty()) continue;
+        const uint32_t slot = free_[r].back();
+        free_[r].pop_back();
+        S.rep_of[j] = (uint16_t)(len + 1 + slot);
+        src[slot] = (uint16_t)j;
+        ++placed;
+        break;
+      }
+    }
+    P.rep_src.insert(P.rep_src.end(), src.begin(), src.end());
+    P.rep_ptr.push_back((int32_t)P.rep_src.size());
   }
 }
 
@@ -373,12 +484,13 @@ uint64_t seg_charge16(uint32_t nv, bool csc) {
   return (uint64_t)((emit + (csc ? block_csc : block) * frac) * 16.0 + 0.5);
 }
 
-void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G, bool csc) {
+void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G, bool csc, int64_t area) {
   const int ns = (int)slabs.size();
   P.cta_task_ptr.assign(G + 1, 0);
   std::vector<Pool> pools(40);
   const bool grouped = layout_grouped();
   P.grouped = grouped ? 1 : 0;
+  choose_replicas(P, slabs, area, grouped);
   std::vector<std::vector<uint64_t>> pre(ns);
   std::vector<uint64_t> sw(ns);
   uint64_t W = 0;
@@ -463,6 +575,8 @@ std::string validate_csr(int64_t n, int64_t p, const int64_t* row_ptr, const int
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
                          int intercept, int slab_max, int G, DesignHost& D, int q_dense) {
   if (q_dense < 0 || (q_dense > 0 && intercept)) return "dense columns replace the intercept flag";
+  g_dbg_hist = getenv("PCGS_STORE_STATS") ? g_hist : nullptr;
+  if (g_dbg_hist) memset(g_hist, 0, sizeof(g_hist));
   {
     std::string err = validate_csr(n, p, row_ptr, col_idx);
     if (!err.empty()) return err;
@@ -478,6 +592,22 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
   D.p_total = p + D.intercept + q_dense;
   D.nnz = nnz;
   D.slab_max = (int)smax;
+  {
+    // shared-memory area of the slab vector: the longest slab plus its
+    // sentinel, grown by the replica region to what one CTA has left next to
+    // the persistent kernels' own-slice state and piece pointers
+    const char* cs = getenv("PCGS_CSC_SLAB_MAX");
+    const int64_t csc_max = cs ? std::max<int64_t>(16, std::min<int64_t>(smax, atoll(cs))) : smax;
+    const std::vector<int64_t> a = make_slabs(p, smax), b = make_slabs(n, csc_max);
+    int64_t maxlen = 0;
+    for (size_t q = 0; q + 1 < a.size(); ++q) maxlen = std::max(maxlen, a[q + 1] - a[q]);
+    for (size_t q = 0; q + 1 < b.size(); ++q) maxlen = std::max(maxlen, b[q + 1] - b[q]);
+    const int64_t base = (maxlen + 1 + 15) / 16 * 16;
+    const int64_t chunk = (D.p_total + G - 1) / G;
+    const int64_t budget =
+        (227 * 1024 - 4096 - chunk * 64 - (int64_t)(b.size() - 1) * (chunk + 1) * 4) / 8 / 16 * 16;
+    D.slab_area = (int)(env_int("PCGS_REPLICAS", 0) ? std::max(base, std::min<int64_t>(budget, 65520)) : base);
+  }
 
   // ---------------- CSR pass: segments = (column slab, row) ----------------
   {
@@ -500,7 +630,7 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
         S.add((uint32_t)(s * n + i), tmp.data(), (uint32_t)tmp.size());
       }
     }
-    plan_and_emit(P, slabs, G, false);
+    plan_and_emit(P, slabs, G, false, D.slab_area);
   }
 
   // ------------- CSC pass: segments = pieces of (row slab, column) -------------
@@ -548,12 +678,25 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
       P.piece_ptr[(size_t)s * (pt + 1) + pt] = (int32_t)piece;
     }
     P.nseg = piece;
-    plan_and_emit(P, slabs, G, true);
+    plan_and_emit(P, slabs, G, true, D.slab_area);
+  }
+  const long long* hist = g_hist;
+  if (getenv("PCGS_STORE_STATS")) {
+    for (int lw = 0; lw < 6; ++lw) {
+      long long tot = 0;
+      for (int d = 0; d < 10; ++d) tot += hist[lw * 20 + 2 * d];
+      if (!tot) continue;
+      fprintf(stderr, "  W=%d excess per gather by slice decile:", 1 << lw);
+      for (int d = 0; d < 10; ++d)
+        fprintf(stderr, " %.2f", (double)hist[lw * 20 + 2 * d + 1] / (double)std::max(1ll, hist[lw * 20 + 2 * d]));
+      fprintf(stderr, "  (%lld gathers)\n", tot);
+    }
   }
   if (getenv("PCGS_STORE_STATS"))
     for (const PassHost* P : {&D.csr, &D.csc})
-      fprintf(stderr, "pcgs store: %s vectors %zu pad %lld slices/blocks %zu half-warp gathers %lld excess %lld (%.3f)\n",
+      fprintf(stderr, "pcgs store: %s vectors %zu pad %lld slices/blocks %zu replicas %zu half-warp gathers %lld excess %lld (%.3f)\n",
               P == &D.csr ? "csr" : "csc", P->idx.size() / kVecIdx, (long long)P->pad_vectors, P->blocks.size(),
+              P->rep_src.size(),
               (long long)P->lds_groups, (long long)P->lds_conflict_excess,
               (double)P->lds_conflict_excess / (double)std::max<int64_t>(1, P->lds_groups));
   return "";
@@ -583,9 +726,14 @@ std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int
               for (int l = 0; l < 32; ++l, ++v) {
                 const uint32_t id = P.ids[B.first_id + (l >> lw)];
                 for (int e = 0; e < kVecIdx; ++e) {
-                  const uint16_t ix = P.idx[v * kVecIdx + e];
+                  uint16_t ix = P.idx[v * kVecIdx + e];
                   if (ix == sent) continue;
-                  if (ix > sent) return std::string("index beyond slab");
+                  if (ix > sent) {  // a replica: back to the entry it copies
+                    const int64_t k = (int64_t)ix - sent - 1, r0 = P.rep_ptr[T.slab], r1 = P.rep_ptr[T.slab + 1];
+                    if (k >= r1 - r0) return std::string("index beyond slab and replicas");
+                    ix = P.rep_src[r0 + k];
+                    if (ix >= sent) return std::string("replica of nothing gathered");
+                  }
                   if (id == 0xffffffffu) return std::string("index in an empty group");
                   f(T.slab, (int64_t)id, lo + ix);
                 }

@@ -18,7 +18,7 @@
 //     half-warp LDS.64 of a block touches distinct shared-memory bank pairs.
 //
 // GROUPED layout (PassHost::grouped, the default; PCGS_LAYOUT=flat selects
-// the flat stream above): a segment is summed inside a fixed GROUP of
+// the flat stream above in builds with -DPCGS_FLAT_WALK=1): a segment is summed inside a fixed GROUP of
 // W = 1, 2, 4, ... 32 adjacent lanes (W grows with the segment's length), so a
 // block needs no segmented warp reduction -- the cross-lane work is log2 W
 // butterfly steps when a SLICE ends.  A slice is 32/W segments of one width
@@ -30,10 +30,25 @@
 // are contiguous in the stream.  `blocks` then holds one descriptor per slice
 // {offset into `ids`, T | log2 W << 24} and `ids` the 32/W segment ids of
 // each slice (0xffffffff: empty group); WarpRange.pad counts the slices.
+//
+// REPLICAS (grouped layout): shared memory left behind the longest slab holds
+// second copies of a slab's most gathered entries, each at a bank pair other
+// than its original's (replica k of slab s sits at index len + 1 + k and
+// copies entry rep_src[rep_ptr[s] + k]; the kernels copy them after every
+// slab fill).  An occurrence of a replicated entry may use either address, so
+// the placement can balance the bank pairs of a half-warp gather beyond what
+// one segment's own index set allows.
 #pragma once
 #include <cstdint>
 #include <string>
 #include <vector>
+
+// The flat-stream layout and its walk (PCGS_LAYOUT=flat) are compiled in only
+// on request (tools/build_variant.py flat -DPCGS_FLAT_WALK=1): next to the
+// grouped walk the flat one costs the persistent kernels registers.
+#ifndef PCGS_FLAT_WALK
+#define PCGS_FLAT_WALK 0
+#endif
 
 namespace pcgs {
 
@@ -65,6 +80,8 @@ struct PassHost {
   std::vector<BlockDesc> blocks;
   std::vector<uint32_t> ids;           // grouped layout: segment ids per slice group
   int grouped = 0;
+  std::vector<int32_t> rep_ptr;        // grouped layout: nslab+1 offsets into rep_src
+  std::vector<uint16_t> rep_src;       // replica k of slab s copies slab entry rep_src[rep_ptr[s] + k]
   int64_t pad_vectors = 0;             // grouped layout: all-sentinel vector slots
   std::vector<WarpRange> warps;
   std::vector<Task> tasks;
@@ -80,6 +97,7 @@ struct DesignHost {
   int intercept = 0;
   int q_dense = 0;    // dense real columns after the pattern (and intercept) in the internal layout
   int slab_max = 0;
+  int slab_area = 0;  // doubles of shared memory for a slab, its sentinel and its replicas
   PassHost csr, csc;
 };
 
