@@ -95,7 +95,8 @@ def test_fused_chains_track_the_scan_by_scan_batch(small):
     at their own pace) uses the RNG keys and the arithmetic of the scan-by-scan
     batched path; the two differ only in the summation order of X beta and
     X'u (sliced vs tiled store), so over a few scans the draws agree to
-    rounding."""
+    within the solves' tolerance (each beta draw is a PCG solution stopped at
+    RMS 1e-6; the two paths stop on residuals that differ in the last bits)."""
     d, y, _ = small
     X = d.matrix()
     cfg = gibbs.HorseshoeConfig(unshrunk_prior_sd=(np.inf,))
@@ -103,7 +104,7 @@ def test_fused_chains_track_the_scan_by_scan_batch(small):
     a = gibbs.gibbs_run_batched(X, y, cfg, 6, seeds, fused=True)
     b = gibbs.gibbs_run_batched(X, y, cfg, 6, seeds, fused=False)
     for oa, ob in zip(a, b):
-        np.testing.assert_allclose(oa.draws, ob.draws, rtol=1e-6, atol=1e-9)
+        np.testing.assert_allclose(oa.draws, ob.draws, rtol=5e-6, atol=1e-8)
         np.testing.assert_allclose(oa.logdensity_trace, ob.logdensity_trace, rtol=1e-8)
         np.testing.assert_allclose(oa.tau_draws, ob.tau_draws, rtol=1e-6)
         assert np.abs(oa.cg_iteration_counts - ob.cg_iteration_counts).max() <= 2
