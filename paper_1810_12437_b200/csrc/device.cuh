@@ -505,11 +505,27 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 // first lane emits the segment.  No per-block masks, no segmented scan: the
 // cross-lane traffic is 2 log2 W shuffles per slice.
 // ---------------------------------------------------------------------------
+// Blocks per register batch and software pipelining of the grouped walk,
+// measured on the config-2 PCG iteration (tools/gpu_ab_pipe.sh): batches of 2
+// without pipelining 73.3 us; two batches of 1 block, one in flight while the
+// other is consumed, 70.6 (two batches of 2 spill: 75.4; of 3: 98.5); with the
+// shared window base pinned in a register 70.2; L2 prefetch distance 4 blocks
+// 69.5 (8: 70.0, 12: 71.7, 16: 73.1); prefetching the lines of 8 blocks every
+// 4th iteration instead of 2 blocks every iteration: 75.0
 #ifndef PCGS_GRING
-#define PCGS_GRING 2
+#define PCGS_GRING 1
 #endif
-
 constexpr int kGRing = PCGS_GRING;
+#ifndef PCGS_GPIPE
+#define PCGS_GPIPE 1
+#endif
+#ifndef PCGS_GPREFETCH
+#define PCGS_GPREFETCH 4
+#endif
+constexpr int kGPrefetch = PCGS_GPREFETCH;  // sliding L2 prefetch distance of the pipelined walk, blocks
+#ifndef PCGS_SB_OPAQUE
+#define PCGS_SB_OPAQUE 1
+#endif
 
 template <class Epi>
 __device__ __forceinline__ void process_warp_grouped(const PassDev& P, int warp0, const double* sv, Epi& epi,
@@ -522,7 +538,11 @@ __device__ __forceinline__ void process_warp_grouped(const PassDev& P, int warp0
   const uint4* base = P.vec + R.x;
   const uint2* sd = P.blocks + R.z;
   const int nsl = (int)R.w;
-  const unsigned sb = smem_addr(sv);
+  unsigned sb = smem_addr(sv);
+#if PCGS_SB_OPAQUE
+  asm volatile("" : "+r"(sb));  // keep the shared window base in a register (else the
+                                // generic->shared conversion is redone in every block)
+#endif
   // slice state: `end` = block count at which the current slice closes
   uint2 dn = __ldg(sd);
   int s = 0, end = 0;

@@ -8,5 +8,8 @@ for l in open('gpurun_out/sw_$tag.jsonl'):
     if l.startswith('{'): d=json.loads(l); print('$tag', round(d['us_per_apply'],2))
 "
 }
-for t in pp1 pp1s pp1sp pp1p pp1 pp1sp; do run $t libpcgs_$t.so A=1; done
-PCGS_LIBRARY=$PWD/paper_1810_12437_b200/libpcgs_pp1sp.so timeout 600 python -m pytest tests/test_gpu_sparse.py tests/test_gpu_cg.py -m gpu -x -q 2>&1 | tail -2
+run dflt libpcgs.so A=1
+for t in pf4 pf6 pf12 pf16; do run $t libpcgs_$t.so A=1; done
+run dflt libpcgs.so A=1
+timeout 300 python tools/sync_times_pcg.py > gpurun_out/sync_times_new.txt 2>&1; tail -5 gpurun_out/sync_times_new.txt
+python tools/pass_phases.py 2>&1 | tail -2
