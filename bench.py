@@ -87,7 +87,7 @@ def config_block(d, prior, world, chains_per_gpu=1):
                      f"PCG rtol {RTOL:g}"),
         "n": d.n, "p": d.p, "nnz": d.nnz, "prior": prior, "chains_per_gpu": chains_per_gpu,
         "parallelism": f"chain-parallel x{world}" if world > 1 else "single chain",
-        "l2_policy": "no flush: the index store (241 MB) exceeds the 126 MB L2 every pass",
+        "l2_policy": "no flush: the index store (249 MB) exceeds the 126 MB L2 every pass",
         "seed": SEED,
     }
 
@@ -343,12 +343,14 @@ def run_ours(args):
                 "store_gbs": alg_bytes / (us_apply * 1e-6) / 1e9,
                 "note": "the store reads 2-byte slab-local indices, half the canonical "
                         "int32 bytes; store_gbs is the HBM rate of the bytes actually read",
-                "limiter": {"resource": "L1TEX/shared-memory data pipe (LDS.64 gathers + index writeback)",
-                            "data_pipe_busy_over_kernel": 0.713, "shared_bank_conflict_share": 0.145,
-                            "dram_throughput": 0.26,
-                            "source": "ncu --set full of k_pcg at config 2 (profiles/k_pcg_r02_details.csv); "
-                                      "~90 % busy during the streaming passes, which take ~78 % of an "
-                                      "iteration (DESIGN.md §4)"}}
+                "limiter": {"resource": "L1TEX/LSU data pipe (LDS.64 gathers + the index vectors' writeback)",
+                            "data_pipe_busy_over_kernel": 0.675, "shared_bank_conflict_share": 0.141,
+                            "dram_throughput": 0.31,
+                            "source": "ncu --set full of k_pcg at config 2 (profiles/k_pcg_r02b_details.csv, "
+                                      "ncu_summary_r02.txt); the streaming passes take ~65 % of an iteration "
+                                      "and keep the pipe ~89 % busy: per 32-vector block 16 gather wavefronts "
+                                      "+ 2.6 conflicts + 4 index writeback + ~2.7 other against 28.5 cycles "
+                                      "measured (DESIGN.md §4)"}}
 
     # ---- end to end through the public API, host buffers ----
     # ONE gibbs_run call of K scans from numpy inputs, continuing from the
