@@ -122,7 +122,7 @@ int pcgs_store_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h,
                         const int32_t* col_idx_h, int intercept, int slab_max,
                         int grid, int64_t* stats_h);
 /* info_h[16]: n, p, p_total, nnz, csr_slabs, csc_slabs, csr_vectors,
- * csc_vectors, csr_bundles, csc_bundles, csc_pieces, grid, device,
+ * csc_vectors, csr_slices, csc_slices, csc_pieces, grid, device,
  * index_bytes (both directions), reserved, reserved */
 int pcgs_design_info(pcgs_design_t d, int64_t* info_h);
 

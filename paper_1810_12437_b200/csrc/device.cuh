@@ -506,7 +506,7 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 // cross-lane traffic is 2 log2 W shuffles per slice.
 // ---------------------------------------------------------------------------
 // Blocks per register batch and software pipelining of the grouped walk,
-// measured on the config-2 PCG iteration (tools/gpu_ab_pipe.sh): batches of 2
+// measured on the config-2 PCG iteration (tools/gpu_ab_grouped.sh): batches of 2
 // without pipelining 73.3 us; two batches of 1 block, one in flight while the
 // other is consumed, 70.6 (two batches of 2 spill: 75.4; of 3: 98.5); with the
 // shared window base pinned in a register 70.2; L2 prefetch distance 4 blocks

@@ -242,7 +242,7 @@ int env_int(const char* name, int dflt) {
 // long segments (the round-up to W vectors stays a few percent), one lane for
 // the shortest ones.
 int width_log(uint32_t nv) {
-  // swept on the config-2 PCG iteration (tools/gpu_sweep_group*.sh): 80/40/12
+  // swept on the config-2 PCG iteration (tools/gpu_ab_grouped.sh): 80/40/12
   // with 128-vector pieces 73.3 us, 128/64/16 71.5, with 256-vector pieces 70.8
   static const int w8 = env_int("PCGS_GW8", 128), w4 = env_int("PCGS_GW4", 64), w2 = env_int("PCGS_GW2", 16);
   return nv >= (uint32_t)w8 ? 3 : nv >= (uint32_t)w4 ? 2 : nv >= (uint32_t)w2 ? 1 : 0;

@@ -100,7 +100,7 @@ class DesignStore:
 
     def describe(self) -> dict:
         keys = ["n", "p", "p_total", "nnz", "csr_slabs", "csc_slabs", "csr_vectors",
-                "csc_vectors", "csr_bundles", "csc_bundles", "csc_pieces", "grid", "device",
+                "csc_vectors", "csr_slices", "csc_slices", "csc_pieces", "grid", "device",
                 "index_bytes", "slab_max"]
         return {k: int(v) for k, v in zip(keys, self.info)}
 
