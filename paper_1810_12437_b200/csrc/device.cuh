@@ -22,6 +22,8 @@ struct PassDev {
   const int* cta_task_ptr;   // G+1
   const long long* slab_lo;  // nslab+1
   const int* piece_ptr;      // CSC: nslab*(p_total+1)
+  const int* col_piece_ptr;  // CSC: p_total+1 column-major slot ranges (store.h)
+  const unsigned* ids_perm;  // CSC: `ids` mapped through piece_perm (k_pcg's CSC pass walks with these)
   int nslab;
   long long nseg;
 };
@@ -511,9 +513,11 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 // other is consumed, 70.6 (two batches of 2 spill: 75.4; of 3: 98.5); with the
 // shared window base pinned in a register 70.2; L2 prefetch distance 4 blocks
 // 69.5 (8: 70.0, 12: 71.7, 16: 73.1); prefetching the lines of 8 blocks every
-// 4th iteration instead of 2 blocks every iteration: 75.0
+// 4th iteration instead of 2 blocks every iteration: 75.0.  With 16 warps of
+// 128 registers (store.h) the batches hold 2 blocks each (1: 79.0, 2: 70.5,
+// 3: 71.7 us).
 #ifndef PCGS_GRING
-#define PCGS_GRING 1
+#define PCGS_GRING (PCGS_WARPS <= 16 ? 2 : 1)
 #endif
 constexpr int kGRing = PCGS_GRING;
 #ifndef PCGS_GPIPE
@@ -638,6 +642,14 @@ __device__ __forceinline__ void process_warp_grouped(const PassDev& P, int warp0
 // saved once per pass and the streaming loop gets the whole register budget.
 __device__ unsigned long long* g_cta_times = nullptr;  // debug: per-CTA [start, filled, end]
 
+// Fill functors that declare `static constexpr bool kHooked = true` take a
+// fourth argument, a callable run by every thread between the issue of the
+// bulk copy and the wait for it.
+template <class F, class = void>
+struct fill_takes_hook : std::false_type {};
+template <class F>
+struct fill_takes_hook<F, std::void_t<decltype(F::kHooked)>> : std::true_type {};
+
 template <class Fill, class Epi>
 __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi, int dbg = 0,
                                          int cta = -1) {
@@ -648,13 +660,21 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
   for (int t = t0; t < t1; ++t) {
     const int2 T = __ldg(P.task + t);
     const long long lo = P.slab_lo[T.x], hi = P.slab_lo[T.x + 1];
-    prefetch_warp(P, T.y, dbg);
-    __syncthreads();
-    if (dbg & 8) {
-      if (threadIdx.x == 0) sv[hi - lo] = 0.0;
+    if constexpr (fill_takes_hook<Fill>::value) {
+      // bulk fills: the copy is issued first; the warps' L2 prefetch (a
+      // dependent load of the warp range, then the prefetch instructions)
+      // runs while it is in flight
       __syncthreads();
+      fill(sv, lo, (int)(hi - lo), [&] { prefetch_warp(P, T.y, dbg); });
     } else {
-      fill(sv, lo, (int)(hi - lo));
+      prefetch_warp(P, T.y, dbg);
+      __syncthreads();
+      if (dbg & 8) {
+        if (threadIdx.x == 0) sv[hi - lo] = 0.0;
+        __syncthreads();
+      } else {
+        fill(sv, lo, (int)(hi - lo));
+      }
     }
     // replicas (store.h): second copies of the slab's most gathered entries
     // behind the sentinel, at other bank pairs (the fill ended with a barrier)

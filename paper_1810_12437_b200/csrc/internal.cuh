@@ -75,6 +75,14 @@ inline int upload_pass(pcgs_design* D, const PassHost& H, PassDev& P) {
   std::vector<long long> lo(H.slab_lo.begin(), H.slab_lo.end());
   if ((rc = upload(D, lo, &P.slab_lo))) return rc;
   if ((rc = upload(D, H.piece_ptr, &P.piece_ptr))) return rc;
+  if ((rc = upload(D, H.col_piece_ptr, &P.col_piece_ptr))) return rc;
+  P.ids_perm = nullptr;
+  if (!H.piece_perm.empty() && H.grouped) {
+    std::vector<uint32_t> ip(H.ids);
+    for (uint32_t& v : ip)
+      if (v != 0xffffffffu) v = (uint32_t)H.piece_perm[v];
+    if ((rc = upload(D, ip, &P.ids_perm))) return rc;
+  }
   P.nslab = H.nslab;
   P.nseg = H.nseg;
   return PCGS_OK;
@@ -120,13 +128,17 @@ struct FillVecRef {  // CSR slab of a reference-layout p_total vector (u = v / s
 struct FillVecN {  // CSC slab of an n-vector: TMA bulk copy
   const double* w;
   BulkFill* bf;
-  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, w + l, len); }
+  static constexpr bool kHooked = true;
+  template <class Hook>
+  __device__ void operator()(double* sv, long long l, int len, Hook hook) { bulk_fill(*bf, sv, w + l, len, hook); }
 };
 
 struct FillBulk {  // TMA copy of an internal-layout vector slab
   const double* src;
   BulkFill* bf;
-  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, src + l, len); }
+  static constexpr bool kHooked = true;
+  template <class Hook>
+  __device__ void operator()(double* sv, long long l, int len, Hook hook) { bulk_fill(*bf, sv, src + l, len, hook); }
 };
 
 struct FillRhs {  // u_i = kappa_i + sqrt(omega_i) * eta_i

@@ -240,9 +240,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // and stamps inside phase C at [16 * cta + 8 + k]
 __device__ unsigned long long* g_sync_times = nullptr;
 constexpr int kSyncTraceIter = 10;
-#ifndef PCGS_FLAT_STEP
-#define PCGS_FLAT_STEP 1
-#endif
 constexpr int kMaxGrid = 256;  // persistent-kernel grid bound (one CTA per SM; B200: 148)
 
 struct FillDir {  // search direction: first ? a : a + beta * b   (internal layout)
@@ -261,22 +258,39 @@ struct FillDir {  // search direction: first ? a : a + beta * b   (internal layo
   }
 };
 
-// Shared-memory layout of k_pcg: [slab vector | own-slice state | piece pointers]
-// The piece pointers of the owned columns are staged in shared memory when they
-// fit (pp_smem), otherwise read from the design's global piece_ptr array.
+// Shared-memory layout of k_pcg: [slab vector | own-slice state | piece slots]
+// The CSC pass of k_pcg stores piece q at its column-major slot (store.h:
+// piece_perm), so the pieces of a CTA's owned columns are one contiguous run
+// [cp[j0], cp[j0 + chunk]) of the pieces array; their slot offsets relative to
+// the run's start are staged in shared memory when they fit (cp), otherwise
+// read from the design's global col_piece_ptr.
 struct OwnState {
   double *x, *r, *d, *m, *s, *D, *b, *z;
-  const int* pp;   // shared copy [s*(chunk+1) + t] or global [s*(pt+1) + j0 + t]
-  long long pp_stride, pp_off, pp_lim;  // pp_lim: last valid t (columns beyond p_total clamp)
-  __device__ __forceinline__ int ppv(int s, int t) const {
-    return pp[s * pp_stride + pp_off + (t < pp_lim ? t : pp_lim)];
+  const int* cp;   // shared copy [chunk + 1] of relative slot offsets, or null
+};
+
+// The owned run of piece slots, set up where it is used (the step phase).
+struct PieceRun {
+  const int* cp;   // OwnState::cp
+  const int* gcp;  // global col_piece_ptr
+  long long j0, pt;
+  int q_lo;        // first slot of the owned run
+  __device__ __forceinline__ int rel(int t) const {
+    if (cp) return cp[t];
+    const long long j = j0 + t < pt ? j0 + t : pt;
+    return __ldg(gcp + j) - q_lo;
   }
 };
+__device__ __forceinline__ PieceRun piece_run(const OwnState& o, const DesignDev& D, long long j0) {
+  PieceRun r{o.cp, D.csc.col_piece_ptr, j0, D.pt, 0};
+  r.q_lo = __ldg(r.gcp + (j0 < D.pt ? j0 : D.pt));
+  return r;
+}
 
 __host__ __device__ inline bool pp_in_smem(const DesignDev& D) {
   const long long chunk = (D.pt + D.G - 1) / D.G;
   const long long own = D.own_in_global ? 0 : chunk * 8 * 8;
-  const long long bytes = (long long)D.smem_doubles * 8 + own + (long long)D.csc.nslab * (chunk + 1) * 4;
+  const long long bytes = (long long)D.smem_doubles * 8 + own + (chunk + 1) * 4;
   return bytes + 1024 <= 227 * 1024;
 }
 
@@ -292,121 +306,38 @@ __device__ __forceinline__ OwnState own_state(double* sv, const DesignDev& D, in
   o.D = base + 5 * chunk;
   o.b = base + 6 * chunk;
   o.z = base + 7 * chunk;
-  if (pp_in_smem(D)) {
-    o.pp = (const int*)after;
-    o.pp_stride = chunk + 1;
-    o.pp_off = 0;
-    o.pp_lim = chunk;
-  } else {
-    o.pp = D.csc.piece_ptr;
-    o.pp_stride = D.pt + 1;
-    o.pp_off = j0;
-    o.pp_lim = D.pt - j0 < chunk ? (D.pt - j0 > 0 ? D.pt - j0 : 0) : chunk;
-  }
+  o.cp = pp_in_smem(D) ? (const int*)after : nullptr;
   return o;
 }
 
 size_t pcg_smem_bytes(const DesignDev& D) {
   const long long chunk = (D.pt + D.G - 1) / D.G;
   size_t b = (size_t)D.smem_doubles * 8 + (D.own_in_global ? 0 : (size_t)chunk * 8 * 8) + 16;
-  if (pp_in_smem(D)) b += (size_t)D.csc.nslab * (chunk + 1) * 4;
+  if (pp_in_smem(D)) b += (size_t)(chunk + 1) * 4;
   return b;
 }
 
-// Stages the pieces of the CTA's owned columns (contiguous per slab) into the
-// idle slab area of shared memory in one coalesced round; returns false when
-// they do not fit (then owned_column_sum reads global memory).
-__device__ __forceinline__ bool stage_pieces(const OwnState& o, const double* pieces, int nslab, int chunk,
-                                             double* stage, int cap) {
-  int total = 0;
-  for (int s = 0; s < nslab; ++s) total += o.ppv(s, chunk) - o.ppv(s, 0);
+// Stages the pieces of the CTA's owned columns (one contiguous run of the
+// column-major slots) into the idle slab area in one coalesced round; returns
+// false when they do not fit (then the column sums read global memory).
+__device__ __forceinline__ bool stage_pieces(const PieceRun& o, const double* pieces, int chunk, double* stage,
+                                             int cap) {
+  const int total = o.rel(chunk);
   if (total > cap) return false;
-  int off = 0;
-  for (int s = 0; s < nslab; ++s) {
-    const int q0 = o.ppv(s, 0), len = o.ppv(s, chunk) - q0;
-#pragma unroll 4
-    for (int q = threadIdx.x; q < len; q += kThreads) stage[off + q] = __ldcg(pieces + q0 + q);
-    off += len;
-  }
+  for (int q = threadIdx.x; q < total; q += kThreads) stage[q] = __ldcg(pieces + o.q_lo + q);
   __syncthreads();
   return true;
 }
 
-// Sum of the pieces of owned column t, slab-major then piece order (fixed).
-__device__ __forceinline__ double owned_column_sum(const OwnState& o, const double* pieces, int nslab, int chunk,
-                                                   int t, const double* stage, bool staged) {
-  double total = 0.0;
-  int off = 0;
-  for (int s = 0; s < nslab; ++s) {
-    const int q0 = o.ppv(s, t), q1 = o.ppv(s, t + 1), p0 = o.ppv(s, 0);
-    double ts = 0.0;
-    if (staged) {
-      for (int q = q0; q < q1; ++q) ts += stage[off + q - p0];
-      off += o.ppv(s, chunk) - p0;
-    } else {
-      for (int q = q0; q < q1; ++q) ts += __ldcg(pieces + q);
-    }
-    total += ts;
-  }
-  return total;
-}
-
-// Step-phase column sums for up to 8 CSC slabs (the common case): the pieces
-// of the owned columns are staged in ONE round of loads (the slab ranges are
-// concatenated; every thread finds its slab among <= 8 offsets), then each
-// column is summed by a group of G = 4 or 8 lanes, lane g taking slabs
-// g, g+G, ... and the group adding its lane sums by an xor tree (fixed order,
-// so the result is deterministic).  Returns false when the pieces do not fit
-// the idle slab area (then the generic path runs).
-constexpr int kFlatSlabs = 8;
-__device__ __forceinline__ bool stage_pieces_flat(const OwnState& o, const double* pieces, int S, int chunk,
-                                                  double* stage, int cap) {
-  int p0[kFlatSlabs], off[kFlatSlabs + 1];
-  off[0] = 0;
-#pragma unroll
-  for (int s = 0; s < kFlatSlabs; ++s) {
-    p0[s] = s < S ? o.ppv(s, 0) : 0;
-    off[s + 1] = off[s] + (s < S ? o.ppv(s, chunk) - p0[s] : 0);
-  }
-  const int total = off[kFlatSlabs];
-  if (total > cap) return false;
-  for (int i = threadIdx.x; i < total; i += kThreads) {
-    int s = 0;
-#pragma unroll
-    for (int u = 1; u < kFlatSlabs; ++u) s += i >= off[u] ? 1 : 0;
-    int ps = p0[0], os = off[0];
-#pragma unroll
-    for (int u = 1; u < kFlatSlabs; ++u)
-      if (s == u) {
-        ps = p0[u];
-        os = off[u];
-      }
-    stage[i] = __ldcg(pieces + ps + (i - os));
-  }
-  __syncthreads();
-  return true;
-}
-
-// Sum of column t over the staged slabs taken by lane g of a G-lane group,
-// then the group total (every lane of the group receives it).  All lanes of
-// the warp must call it (shuffles).
-template <int G>
-__device__ __forceinline__ double group_column_sum(const OwnState& o, int S, int chunk, int t, int g,
-                                                   const double* stage) {
+// Sum of the pieces of owned column t: slab-major, then piece order (fixed).
+__device__ __forceinline__ double owned_column_sum(const PieceRun& o, const double* pieces, int t,
+                                                   const double* stage, bool staged) {
+  const int q0 = o.rel(t), q1 = o.rel(t + 1);
   double sum = 0.0;
-  if (t < chunk) {
-    int off = 0;
-    for (int s = 0; s < S; ++s) {
-      const int p0 = o.ppv(s, 0);
-      if ((s & (G - 1)) == g) {
-        const int q0 = o.ppv(s, t) - p0, q1 = o.ppv(s, t + 1) - p0;
-        for (int q = q0; q < q1; ++q) sum += stage[off + q];
-      }
-      off += o.ppv(s, chunk) - p0;
-    }
-  }
-#pragma unroll
-  for (int m = 1; m < G; m <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, m);
+  if (staged)
+    for (int q = q0; q < q1; ++q) sum += stage[q];
+  else
+    for (int q = q0; q < q1; ++q) sum += __ldcg(pieces + o.q_lo + q);
   return sum;
 }
 
@@ -424,16 +355,39 @@ struct FillVecNDad {
   int G;
   double* out;
   bool pending, done;
-  __device__ void operator()(double* sv, long long l, int len) {
+  static constexpr bool kHooked = true;
+  template <class Hook>
+  __device__ void operator()(double* sv, long long l, int len, Hook hook) {
     const bool go = pending;
     done = done || go;
     bulk_fill(*bf, sv, w + l, len, [&] {
+      hook();
       if (go && threadIdx.x >= 32 && threadIdx.x < 64) {
         const double s = warp_sum(lane_partials(part, G, threadIdx.x & 31));
         if (threadIdx.x == 32) *out = s;
       }
     });
     pending = false;
+  }
+};
+
+// CSR slab fill of the published direction whose TMA wait also fetches the
+// intercept's entry (one thread, into shared memory): every thread's epilogue
+// constant is set from it after the fill's closing barrier.
+struct FillBulkV0 {
+  const double* src;
+  BulkFill* bf;
+  const double* icpt_src;  // null: no intercept
+  double* slot;            // shared memory
+  double* v0;              // the calling thread's epilogue constant
+  static constexpr bool kHooked = true;
+  template <class Hook>
+  __device__ void operator()(double* sv, long long l, int len, Hook hook) {
+    bulk_fill(*bf, sv, src + l, len, [&] {
+      hook();
+      if (threadIdx.x == 64) *slot = icpt_src ? __ldcg(icpt_src) : 0.0;
+    });
+    *v0 = *slot;
   }
 };
 
@@ -503,13 +457,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       o.b[t] = bv;
       o.z[t] = 0.0;
     }
-    if (pp_in_smem(A.D)) {
-      int* ppw = const_cast<int*>(o.pp);
-      for (int t = tid; t < A.D.csc.nslab * (chunk + 1); t += kThreads) {
-        const int s = t / (chunk + 1), q = t % (chunk + 1);
-        const long long j = min(j0 + q, pt);
-        ppw[t] = A.D.csc.piece_ptr[(long long)s * (pt + 1) + j];
-      }
+    if (o.cp) {
+      int* cpw = const_cast<int*>(o.cp);
+      const int* gcp = A.D.csc.col_piece_ptr;
+      const int q_lo = __ldg(gcp + min(j0, pt));
+      for (int t = tid; t <= chunk; t += kThreads) cpw[t] = __ldg(gcp + min(j0 + t, pt)) - q_lo;
     }
     if (tid == 0) {
       st_rz = 0.0;
@@ -595,11 +547,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     for (int t = tid; t < chunk; t += kThreads) acc_dAd += o.D[t] * o.d[t] * o.d[t];
     const double* vcur = A.dvg + (a == 0 ? dvs : (a & 1) * dvs);
     if (!AFF) {
-      if (tid == 0) bc[2] = A.D.icpt ? __ldcg(vcur + A.D.p) : 0.0;
-      __syncthreads();
       const bool multi = A.D.csr.nslab > 1;
-      EpiCsr e{multi ? A.zpart : A.w, A.omega, bc[2], 0.0, multi};
-      FillBulk f{vcur, &bf};
+      EpiCsr e{multi ? A.zpart : A.w, A.omega, 0.0, 0.0, multi};
+      const double* icpt_src = A.D.icpt ? vcur + A.D.p : nullptr;
+      if (A.D.csr.cta_task_ptr[blockIdx.x] == A.D.csr.cta_task_ptr[blockIdx.x + 1]) {
+        // a CTA without CSR work still needs the row constant (combine loop)
+        if (tid == 0) bc[2] = icpt_src ? __ldcg(icpt_src) : 0.0;
+        __syncthreads();
+      }
+      FillBulkV0 f{vcur, &bf, icpt_src, bc + 2, &e.v0};
       run_pass(A.D.csr, sv, f, e, A.D.dbg);
       acc_dAd += e.acc;
     } else {
@@ -654,7 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     bool dad_pending;
     {
       FillVecNDad f{A.w, &bf, A.part, (int)gridDim.x, bc, PCGS_DAD_IN_FILL && a > 0, false};
-      EpiStore e{A.pieces, A.D.csc.nseg};
+      EpiStore e{A.pieces, A.D.csc.nseg};  // A.D.csc.ids are the column-major piece slots (host: pcgs_pcg_full)
       run_pass(A.D.csc, sv, f, e, A.D.dbg);
       dad_pending = a > 0 && !f.done;
     }
@@ -665,14 +621,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
 
     // ---------------- phase C: assemble, step, residual ----------------
     double alpha = 0.0;
-    const int S = A.D.csc.nslab;
     trace_stamp(A, a, 0);
     // (CTAs without CSC work: warp 0's loads of the dAd partials overlap the
     // piece staging round trip)
     double dpart = 0.0;
     if (dad_pending && tid < 32) dpart = lane_partials(A.part, gridDim.x, tid);
-    const bool flat = PCGS_FLAT_STEP && S <= kFlatSlabs && stage_pieces_flat(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
-    const bool staged = flat || stage_pieces(o, A.pieces, S, chunk, sv, A.D.smem_doubles);
+    const PieceRun pr = piece_run(o, A.D, j0);
+    const bool staged = stage_pieces(pr, A.pieces, chunk, sv, A.D.smem_doubles);
     trace_stamp(A, a, 1);
     if (a > 0) {
       if (dad_pending) {
@@ -714,20 +669,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       return (raw - mu * affg[0]) / sc;
     };
     double t_rms = 0.0, t_rz = 0.0;
-    constexpr int GS = 4;  // lanes per column in the flat path (slabs g, g+4)
-    for (int t0 = 0; t0 < chunk; t0 += (flat ? kThreads / GS : kThreads)) {
-      int t;
-      double Ad;
-      if (flat) {
-        t = t0 + tid / GS;
-        const double cs = group_column_sum<GS>(o, S, chunk, t, tid & (GS - 1), sv);
-        if ((tid & (GS - 1)) != 0 || t >= chunk || j0 + t >= pt) continue;
-        Ad = aff_ad(t, cs) + o.D[t] * o.d[t];
-      } else {
-        t = t0 + tid;
-        if (t >= chunk || j0 + t >= pt) continue;
-        Ad = aff_ad(t, owned_column_sum(o, A.pieces, S, chunk, t, sv, staged)) + o.D[t] * o.d[t];
-      }
+    for (int t = tid; t < chunk; t += kThreads) {
+      if (j0 + t >= pt) continue;
+      const double Ad = aff_ad(t, owned_column_sum(pr, A.pieces, t, sv, staged)) + o.D[t] * o.d[t];
       double rv;
       if (a == 0) {
         rv = o.b[t] - Ad;
@@ -1187,6 +1131,7 @@ int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag
   A.part = S.get<double>((size_t)kPartStride * D.G);
   A.prof = g_prof;
   A.D.dbg = g_dbg;
+  A.D.csc.ids = D.csc.ids_perm;  // k_pcg's CSC pass emits to the column-major piece slots (store.h)
   A.iterates = iterates;
   if (D.own_in_global) {  // per-solve state: concurrent solves on one design must not share it
     const long long chunk = (D.pt + D.G - 1) / D.G;

@@ -96,7 +96,7 @@ __device__ __forceinline__ double tau_term_s(const GibbsCfgS& G, double b, doubl
 }
 
 template <int R>
-__global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
+__global__ void __launch_bounds__(kSThreads, 1) k_sgibbs(FusedArgs A) {
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[32 * R];
   __shared__ double sred[6 * R];
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
   __syncthreads();
   {
     double ts = 0.0;
-    for (long long e = e0 + tid; e < e1; e += kThreads) {
+    for (long long e = e0 + tid; e < e1; e += kSThreads) {
       const long long j = e / R;
       const long long r = ref_index(j, p, lead);
       const ChainDev& C = A.ch[c_t];
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
       const bool draw = mode == kModeGibbs && st_t[c_t] <= C.t_last;
       double wz = 0.0, ll = 0.0;
       const long long nr = n * R;
-      for (long long e = (long long)blockIdx.x * kThreads + tid; e < nr; e += (long long)gridDim.x * kThreads) {
+      for (long long e = (long long)blockIdx.x * kSThreads + tid; e < nr; e += (long long)gridDim.x * kSThreads) {
         const long long i = e / R;
         double wi = 0.0;
         if (mode != kModeDone) {
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
         }
         return g;
       };
-      for (long long e = e0 + tid; e < e1; e += kThreads) {
+      for (long long e = e0 + tid; e < e1; e += kSThreads) {
         const long long j = e / R;
         const long long r = ref_index(j, p, lead);
         if (mode == kModeSolve || mode == kModeInit) {
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
       const int count_new = st_count[c_t] + 1;
       int slot = -1;
       if (fin && t > G.burn_in && (t - G.burn_in - 1) % G.thin == 0) slot = st_stored[c_t];
-      for (long long e = e0 + tid; e < e1; e += kThreads) {
+      for (long long e = e0 + tid; e < e1; e += kSThreads) {
         const long long j = e / R;
         const long long r = ref_index(j, p, lead);
         double dn = 0.0;
@@ -517,13 +517,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_sgibbs(FusedArgs A) {
 
   // ---- write back the final state: beta (last draw), omega, counters
   __syncthreads();
-  for (long long e = e0 + tid; e < e1; e += kThreads) {
+  for (long long e = e0 + tid; e < e1; e += kSThreads) {
     const long long j = e / R;
     A.ch[c_t].beta[ref_index(j, p, lead)] = A.x[e];
   }
   {
     const long long nr = n * R;
-    for (long long e = (long long)blockIdx.x * kThreads + tid; e < nr; e += (long long)gridDim.x * kThreads)
+    for (long long e = (long long)blockIdx.x * kSThreads + tid; e < nr; e += (long long)gridDim.x * kSThreads)
       A.ch[c_t].omega[e / R] = A.om[e];
   }
   if (blockIdx.x == 0 && tid < R) {
@@ -559,7 +559,7 @@ int run_fused(const BatchDev& D, FusedArgs& A, cudaStream_t s) {
   CUDA_TRY(cudaMemsetAsync(own, 0, 8 * pR * sizeof(double), s));
   CUDA_TRY(cudaMemsetAsync(A.om, 0, nR * sizeof(double), s));
   void* args[] = {&A};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_sgibbs<R>, D.G, kThreads, args, (size_t)D.smem_doubles * 8, s));
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_sgibbs<R>, D.G, kSThreads, args, (size_t)D.smem_doubles * 8, s));
   return PCGS_OK;
 }
 

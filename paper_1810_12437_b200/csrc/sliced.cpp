@@ -194,8 +194,8 @@ void plan_pass(SPassHost& P, std::vector<SlabPieces>& slabs, int R, int G) {
   auto emit_task = [&](int s, size_t a, size_t b) {
     Task t{s, (int32_t)(P.warp_slices.size() / 2)};
     std::vector<size_t> wc;
-    cut_ranges(pre[s], a, b, kWarps, wc);
-    for (int w = 0; w < kWarps; ++w) {
+    cut_ranges(pre[s], a, b, kSWarps, wc);
+    for (int w = 0; w < kSWarps; ++w) {
       const uint32_t s0 = (uint32_t)P.slices.size();
       emit_slices(P, slabs[s], first[s], wc[w], wc[w + 1], R);
       P.warp_slices.push_back(s0);
@@ -348,7 +348,7 @@ std::string verify_sliced(const SlicedHost& H, const int64_t* row_ptr, const int
       const Task& T = P.tasks[t];
       const int64_t lo = P.slab_lo[T.slab], hi = P.slab_lo[T.slab + 1];
       const uint16_t sent = (uint16_t)(hi - lo);
-      for (int w = 0; w < kWarps; ++w) {
+      for (int w = 0; w < kSWarps; ++w) {
         const uint32_t s0 = P.warp_slices[2 * (T.warp0 + w)], s1 = P.warp_slices[2 * (T.warp0 + w) + 1];
         for (uint32_t q = s0; q < s1; ++q) {
           const SliceDesc& D = P.slices[q];

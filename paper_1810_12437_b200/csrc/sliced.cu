@@ -62,7 +62,7 @@ int upload_spass(pcgs_batch* B, const SPassHost& H, SPassDev& P) {
 
 // ------------------------------------------------------------------ kernels (single apply)
 template <int R>
-__global__ void __launch_bounds__(kThreads, 1) k_scsr(BatchDev D, const double* v_ref, double* zpiece) {
+__global__ void __launch_bounds__(kSThreads, 1) k_scsr(BatchDev D, const double* v_ref, double* zpiece) {
   extern __shared__ __align__(128) double sv[];
   __shared__ unsigned long long mbar;
   BulkFill bf;
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_scsr(BatchDev D, const double* 
 }
 
 template <int R>
-__global__ void __launch_bounds__(kThreads, 1) k_scsc(BatchDev D, const double* w, double* pieces) {
+__global__ void __launch_bounds__(kSThreads, 1) k_scsc(BatchDev D, const double* w, double* pieces) {
   extern __shared__ __align__(128) double sv[];
   __shared__ unsigned long long mbar;
   BulkFill bf;
@@ -135,7 +135,7 @@ __host__ __device__ constexpr int part_stride_s() {
 }
 
 template <int R>
-__global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
+__global__ void __launch_bounds__(kSThreads, 1) k_spcg(PcgArgsS A) {
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[32 * R];
   __shared__ double sred[3 * R];
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
   double *ox = A.own, *orr = A.own + ptR, *od = A.own + 2 * ptR, *oz = A.own + 3 * ptR;
 
   // own slice: x0, the first direction (v = x0), r, z
-  for (long long e = e0 + tid; e < e1; e += kThreads) {
+  for (long long e = e0 + tid; e < e1; e += kSThreads) {
     const long long j = e / R;
     const long long r = ref_index(j, D.p, D.icpt) * R + c_t;
     const double xv = A.x[r];
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
     double wz = 0.0;
     {
       const long long nr = D.n * R;
-      for (long long e = (long long)blockIdx.x * kThreads + tid; e < nr; e += (long long)gridDim.x * kThreads) {
+      for (long long e = (long long)blockIdx.x * kSThreads + tid; e < nr; e += (long long)gridDim.x * kSThreads) {
         const long long i = e / R;
         double z = 0.0;
         const long long q1 = D.csr.out_ptr[i + 1];
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
       const long long ja = jb0 + (jb1 - jb0) * h / NH, jz = jb0 + (jb1 - jb0) * (h + 1) / NH;
       if (h > 0) __syncthreads();
       const long long Q0 = stage_own_pieces<R>(A.pieces, D.csc.out_ptr, ja, jz, sv, D.smem_doubles);
-      for (long long e = ja * R + tid; e < jz * R; e += kThreads) {
+      for (long long e = ja * R + tid; e < jz * R; e += kSThreads) {
         const long long j = e / R;
         double Ad = 0.0;
         const long long q1 = D.csc.out_ptr[j + 1];
@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
     {
       const bool act = st_active[c_t];
       const double beta = st_beta[c_t];
-      for (long long e = e0 + tid; e < e1; e += kThreads) {
+      for (long long e = e0 + tid; e < e1; e += kSThreads) {
         const double dn = act ? (a == 0 ? oz[e] : fma(beta, od[e], oz[e])) : 0.0;
         od[e] = dn;
         A.dg[e] = dn;
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_spcg(PcgArgsS A) {
   }
 
   __syncthreads();
-  for (long long e = e0 + tid; e < e1; e += kThreads) {
+  for (long long e = e0 + tid; e < e1; e += kSThreads) {
     const long long j = e / R;
     A.x[ref_index(j, D.p, D.icpt) * R + c_t] = ox[e];
   }
@@ -394,9 +394,9 @@ int phi_apply_s(const BatchDev& D, const double* omega, const double* diag, cons
   double* w = S.get<double>((size_t)D.n * R);
   double* pieces = S.get<double>((size_t)D.csc.npiece * R);
   if (!zp || !w || !pieces) return fail(PCGS_ENOMEM, "scratch allocation failed");
-  k_scsr<R><<<D.G, kThreads, slab_bytes(D), s>>>(D, v, zp);
+  k_scsr<R><<<D.G, kSThreads, slab_bytes(D), s>>>(D, v, zp);
   k_scombine<R><<<D.G * 4, 256, 0, s>>>(D, zp, v, omega, w);
-  k_scsc<R><<<D.G, kThreads, slab_bytes(D), s>>>(D, w, pieces);
+  k_scsc<R><<<D.G, kSThreads, slab_bytes(D), s>>>(D, w, pieces);
   k_sassemble<R><<<(int)std::min<long long>((D.pt * R + 255) / 256, 4 * D.G), 256, 0, s>>>(D, pieces, diag, v, out);
   CUDA_TRY(cudaGetLastError());
   return PCGS_OK;
@@ -419,7 +419,7 @@ int pcg_s(const BatchDev& D, PcgArgsS& A, cudaStream_t s) {
     return fail(PCGS_ENOMEM, "scratch allocation failed");
   CUDA_TRY(cudaMemsetAsync(A.part, 0, sizeof(double) * part_stride_s<R>() * D.G, s));
   void* args[] = {&A};
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_spcg<R>, D.G, kThreads, args, slab_bytes(D), s));
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_spcg<R>, D.G, kSThreads, args, slab_bytes(D), s));
   return PCGS_OK;
 }
 

@@ -228,7 +228,7 @@ __device__ __forceinline__ long long stage_own_pieces(const double* pieces, cons
   if (len > cap) return -1;
   const double2* src = reinterpret_cast<const double2*>(pieces + Q0 * R);
   double2* dst = reinterpret_cast<double2*>(sv);
-  for (long long i = threadIdx.x; i < len / 2; i += kThreads) dst[i] = __ldcg(src + i);
+  for (long long i = threadIdx.x; i < len / 2; i += kSThreads) dst[i] = __ldcg(src + i);
   __syncthreads();
   return Q0;
 }

@@ -29,6 +29,13 @@
 #include "store.h"
 
 namespace pcgs {
+// warps per CTA of the batched (sliced-store) kernels; the single-chain tiled
+// store has its own count (store.h: kWarps)
+constexpr int kSWarps = 32;
+constexpr int kSThreads = kSWarps * 32;
+}  // namespace pcgs
+
+namespace pcgs {
 
 constexpr int kSlicedPieceMax = 32;  // vectors per piece
 
@@ -75,7 +82,7 @@ struct SPassHost {
   std::vector<SliceDesc> slices;
   std::vector<uint32_t> piece;       // S per slice: output piece id per slot (0xffffffff: idle slot)
   std::vector<uint32_t> warp_slices; // per warp range: [first slice, end slice) pairs
-  std::vector<Task> tasks;           // {slab, first warp range}, kWarps ranges per task
+  std::vector<Task> tasks;           // {slab, first warp range}, kSWarps ranges per task
   std::vector<int32_t> cta_task_ptr; // G+1
   std::vector<int64_t> out_ptr;      // n_out+1: pieces of output j are [out_ptr[j], out_ptr[j+1])
   int64_t npiece = 0;

@@ -678,6 +678,20 @@ std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int
       P.piece_ptr[(size_t)s * (pt + 1) + pt] = (int32_t)piece;
     }
     P.nseg = piece;
+    {
+      // column-major slots: column j's pieces of slab 0, then slab 1, ...
+      P.col_piece_ptr.assign((size_t)pt + 1, 0);
+      for (int s = 0; s < P.nslab; ++s)
+        for (int64_t j = 0; j < pt; ++j)
+          P.col_piece_ptr[j + 1] += P.piece_ptr[(size_t)s * (pt + 1) + j + 1] - P.piece_ptr[(size_t)s * (pt + 1) + j];
+      for (int64_t j = 0; j < pt; ++j) P.col_piece_ptr[j + 1] += P.col_piece_ptr[j];
+      P.piece_perm.assign((size_t)piece, 0);
+      std::vector<int32_t> next(P.col_piece_ptr.begin(), P.col_piece_ptr.end() - 1);
+      for (int s = 0; s < P.nslab; ++s)
+        for (int64_t j = 0; j < pt; ++j)
+          for (int32_t q = P.piece_ptr[(size_t)s * (pt + 1) + j]; q < P.piece_ptr[(size_t)s * (pt + 1) + j + 1]; ++q)
+            P.piece_perm[q] = next[j]++;
+    }
     plan_and_emit(P, slabs, G, true, D.slab_area);
   }
   const long long* hist = g_hist;
@@ -800,6 +814,17 @@ std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int
     for (int64_t j = 0; j < pt; ++j)
       for (int q = C.piece_ptr[(size_t)s * (pt + 1) + j]; q < C.piece_ptr[(size_t)s * (pt + 1) + j + 1]; ++q)
         piece_col[q] = (int32_t)j;
+  {
+    std::vector<uint8_t> hit((size_t)C.nseg, 0);
+    for (int64_t q = 0; q < C.nseg; ++q) {
+      const int32_t slot = C.piece_perm[q];
+      if (slot < 0 || slot >= C.nseg || hit[slot]) return "csc: piece_perm is not a permutation";
+      hit[slot] = 1;
+      const int32_t j = piece_col[q];
+      if (j < 0 || slot < C.col_piece_ptr[j] || slot >= C.col_piece_ptr[j + 1])
+        return "csc: piece_perm leaves its column's slots";
+    }
+  }
   std::vector<std::vector<int32_t>> got_cols(pt);
   err = walk(C, [&](int, int64_t seg, int64_t row) {
     if (seg >= 0 && seg < C.nseg && piece_col[seg] >= 0) got_cols[piece_col[seg]].push_back((int32_t)row);

@@ -52,7 +52,16 @@
 
 namespace pcgs {
 
-constexpr int kWarps = 32;             // warps per CTA of the pass kernels
+// Warps per CTA of the tiled-store kernels.  16 warps get 128 registers each:
+// with the grouped walk's two-block register batches they keep the LSU pipe as
+// busy as 32 warps at 64 registers did (70.5 vs 69.8 us per PCG iteration at
+// config 2), and the register room pays for the step phase on column-major
+// piece slots and the hooks in the slab fills' TMA wait, which spilled at 64
+// registers (67.8 us).
+#ifndef PCGS_WARPS
+#define PCGS_WARPS 16
+#endif
+constexpr int kWarps = PCGS_WARPS;     // warps per CTA of the pass kernels
 constexpr int kThreads = kWarps * 32;  // 1024
 constexpr int kVecIdx = 8;             // uint16 indices per 16-byte vector
 
@@ -88,6 +97,10 @@ struct PassHost {
   std::vector<int32_t> cta_task_ptr;   // G+1
   int64_t nseg = 0;                    // number of output segments
   std::vector<int32_t> piece_ptr;      // CSC: slab-major piece_ptr[s*(ncols+1) + j]
+  // CSC, column-major view of the same pieces (the persistent PCG kernel's step
+  // phase): piece id q is stored at slot piece_perm[q]; the slots of column j
+  // are [col_piece_ptr[j], col_piece_ptr[j+1]), slab-major inside the column
+  std::vector<int32_t> piece_perm, col_piece_ptr;
   // statistics
   int64_t lds_groups = 0, lds_conflict_excess = 0;
 };
