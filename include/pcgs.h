@@ -211,7 +211,9 @@ int pcgs_copy(void* dst, const void* src, int64_t bytes, int kind);
 int pcgs_debug_profile(void* buf);
 /* Debug/tuning switches: key 1 = debug bits of the pass kernels (64: per-CTA
  * pass timestamps, 128: barrier trace of PCG iteration 10), key 2 = L2
- * persisting window over the CSC index stream in MB (0 = off). */
+ * persisting window over the CSC index stream in MB (0 = off), key 3 = warp
+ * ranges per CTA task of the stores created from now on (0 = the default 16,
+ * the persistent PCG kernel's warp count; the row-split shards use 32). */
 int pcgs_debug_option(int key, int value);
 /* Debug: device buffer (3 uint64 per CTA) for per-CTA pass timestamps when
  * the debug-option key 1 bit 64 is set. */

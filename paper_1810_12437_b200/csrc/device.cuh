@@ -15,6 +15,7 @@ struct PassDev {
                              // grouped layout: per slice {ids offset, steps | log2 W << 24}
   const unsigned* ids;       // grouped layout: segment ids of the slices' lane groups
   int grouped;
+  int nranges;               // warp ranges per task (store.h)
   const int* rep_ptr;             // nslab+1 offsets into rep_src (null: no replicas)
   const unsigned short* rep_src;  // replica k of slab s copies slab entry rep_src[rep_ptr[s] + k]
   const uint4* warps;        // WarpRange {v0, nvec, blk0, pad}
@@ -228,16 +229,17 @@ __device__ __forceinline__ double gather8s(uint4 q, unsigned sb) {
 template <class F>
 __device__ __forceinline__ void fill_smem(double* sv, int len, F& f) {
   constexpr int U = 8;
-  for (int j0 = threadIdx.x; j0 < len; j0 += kThreads * U) {
+  const int nthr = (int)blockDim.x;
+  for (int j0 = threadIdx.x; j0 < len; j0 += nthr * U) {
     double vals[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      int j = j0 + u * kThreads;
+      int j = j0 + u * nthr;
       vals[u] = j < len ? f(j) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      int j = j0 + u * kThreads;
+      int j = j0 + u * nthr;
       if (j < len) sv[j] = vals[u];
     }
   }
@@ -394,10 +396,10 @@ constexpr int kPrefetchBlocks = PCGS_PREFETCH_DIST;  // sliding L2 prefetch dist
 #define PCGS_PREFETCH0 4
 #endif
 constexpr int kPrefetchFirst = PCGS_PREFETCH0;  // blocks prefetched before the slab fill
-__device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int dbg) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void prefetch_range(const PassDev& P, int range, int dbg) {
+  const int lane = threadIdx.x & 31;
   if (lane != 0 || (kDebugModes && (dbg & 4))) return;
-  const uint4 R = __ldg(P.warps + warp0 + warp);
+  const uint4 R = __ldg(P.warps + range);
   const int nvec = (int)R.y;
   if (nvec == 0) return;
   const int nb = (nvec + 31) >> 5;
@@ -412,6 +414,13 @@ __device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int d
   const unsigned long long d0 = (unsigned long long)bd & ~15ull;
   const unsigned long long d1 = ((unsigned long long)(bd + (P.grouped ? (int)R.w : nb)) + 15ull) & ~15ull;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d0), "r"((unsigned)(d1 - d0)) : "memory");
+}
+
+// A CTA of blockDim.x / 32 warps walks the P.nranges ranges of a task: warp w takes
+// ranges w, w + nwarps, ...
+__device__ __forceinline__ void prefetch_warp(const PassDev& P, int warp0, int dbg) {
+  const int nw = (int)(blockDim.x >> 5);
+  for (int r = (int)(threadIdx.x >> 5); r < P.nranges; r += nw) prefetch_range(P, warp0 + r, dbg);
 }
 
 template <class Epi>
@@ -514,12 +523,12 @@ __device__ __forceinline__ void process_warp(const PassDev& P, int warp0, const 
 // shared window base pinned in a register 70.2; L2 prefetch distance 4 blocks
 // 69.5 (8: 70.0, 12: 71.7, 16: 73.1); prefetching the lines of 8 blocks every
 // 4th iteration instead of 2 blocks every iteration: 75.0.  With 16 warps of
-// 128 registers (store.h) the batches hold 2 blocks each (1: 79.0, 2: 70.5,
+// 128 registers (k_pcg) the batches hold 2 blocks each (1: 79.0, 2: 70.5,
 // 3: 71.7 us).
 #ifndef PCGS_GRING
-#define PCGS_GRING (PCGS_WARPS <= 16 ? 2 : 1)
+#define PCGS_GRING 1
 #endif
-constexpr int kGRing = PCGS_GRING;
+constexpr int kGRing = PCGS_GRING;  // 32-warp kernels (64 registers); k_pcg (16 warps) passes 2
 #ifndef PCGS_GPIPE
 #define PCGS_GPIPE 1
 #endif
@@ -531,11 +540,11 @@ constexpr int kGPrefetch = PCGS_GPREFETCH;  // sliding L2 prefetch distance of t
 #define PCGS_SB_OPAQUE 1
 #endif
 
-template <class Epi>
-__device__ __forceinline__ void process_warp_grouped(const PassDev& P, int warp0, const double* sv, Epi& epi,
+template <int kGRing, class Epi>
+__device__ __forceinline__ void process_warp_grouped(const PassDev& P, int range, const double* sv, Epi& epi,
                                                      int slab_len = 0) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint4 R = __ldg(P.warps + warp0 + warp);
+  const int lane = threadIdx.x & 31;
+  const uint4 R = __ldg(P.warps + range);
   const int nvec = (int)R.y;
   if (nvec == 0) return;
   const int nb = nvec >> 5;
@@ -650,7 +659,7 @@ struct fill_takes_hook : std::false_type {};
 template <class F>
 struct fill_takes_hook<F, std::void_t<decltype(F::kHooked)>> : std::true_type {};
 
-template <class Fill, class Epi>
+template <int kRingBlocks = kGRing, class Fill, class Epi>
 __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fill, Epi& epi, int dbg = 0,
                                          int cta = -1) {
   const int c = cta < 0 ? (int)blockIdx.x : cta;  // CTA index within the plan (row-split groups)
@@ -684,7 +693,7 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
       nrep = P.rep_ptr[T.x + 1] - r0;
       if (nrep > 0) {
         double* rp = sv + (hi - lo) + 1;
-        for (int k = threadIdx.x; k < nrep; k += kThreads) rp[k] = sv[__ldg(P.rep_src + r0 + k)];
+        for (int k = threadIdx.x; k < nrep; k += (int)blockDim.x) rp[k] = sv[__ldg(P.rep_src + r0 + k)];
         __syncthreads();
       }
     }
@@ -698,7 +707,11 @@ __device__ __forceinline__ void run_pass(const PassDev& P, double* sv, Fill& fil
     if (!P.grouped) process_warp(P, T.y, sv, epi, dbg, (int)(hi - lo));
     else
 #endif
-      process_warp_grouped(P, T.y, sv, epi, (int)(hi - lo) + nrep);
+    {
+        const int nw = (int)(blockDim.x >> 5);
+        for (int r = (int)(threadIdx.x >> 5); r < P.nranges; r += nw)
+          process_warp_grouped<kRingBlocks>(P, T.y + r, sv, epi, (int)(hi - lo) + nrep);
+      }
   }
   if (dbg & 64) {
     __syncthreads();

@@ -274,11 +274,11 @@ int launch_logit(pcgs_design* d, pcgs_gibbs_t* g, cudaStream_t s) {
   int rc;
   if ((rc = aff_pre(d, g->beta, S, s, &cbuf))) return rc;
   if (D.csr.nslab == 1) {
-    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, g->z, g->part, cbuf);
+    k_csr_logit<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, g->beta, g->y, g->z, g->part, cbuf);
   } else {
     double* zp = S.get<double>((size_t)D.csr.nslab * D.n);
     if (!zp) return fail(PCGS_ENOMEM, "scratch allocation failed");
-    k_csr_logit<<<D.G, kThreads, smem_bytes(D), s>>>(D, g->beta, g->y, zp, g->part, cbuf);
+    k_csr_logit<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, g->beta, g->y, zp, g->part, cbuf);
     k_rows_logit<<<D.G, kThreads, 0, s>>>(D, zp, g->beta, g->y, g->z, g->part, cbuf);
   }
   CUDA_TRY(cudaGetLastError());

@@ -57,6 +57,7 @@ inline int upload_pass(pcgs_design* D, const PassHost& H, PassDev& P) {
   P.blocks = (const uint2*)b;
   if ((rc = upload(D, H.ids, &P.ids))) return rc;
   P.grouped = H.grouped;
+  P.nranges = H.nranges;
   P.rep_ptr = nullptr;
   P.rep_src = nullptr;
   if (!H.rep_src.empty()) {
@@ -128,12 +129,16 @@ struct FillVecRef {  // CSR slab of a reference-layout p_total vector (u = v / s
 struct FillVecN {  // CSC slab of an n-vector: TMA bulk copy
   const double* w;
   BulkFill* bf;
-  static constexpr bool kHooked = true;
-  template <class Hook>
-  __device__ void operator()(double* sv, long long l, int len, Hook hook) { bulk_fill(*bf, sv, w + l, len, hook); }
+  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, w + l, len); }
 };
 
 struct FillBulk {  // TMA copy of an internal-layout vector slab
+  const double* src;
+  BulkFill* bf;
+  __device__ void operator()(double* sv, long long l, int len) { bulk_fill(*bf, sv, src + l, len); }
+};
+
+struct FillBulkH {  // FillBulk taking run_pass's hook (k_pcg: the warps' prefetch runs in the TMA wait)
   const double* src;
   BulkFill* bf;
   static constexpr bool kHooked = true;
@@ -259,6 +264,8 @@ struct EpiCsrA {  // EpiCsr with the affine row term (dense block) for the affin
 int aff_pre(pcgs_design* d, const double* v, Scratch& S, cudaStream_t s, double** cbuf);
 
 inline size_t smem_bytes(const DesignDev& D) { return (size_t)D.smem_doubles * sizeof(double); }
+// threads per CTA of the standalone pass kernels: one warp per range of the store's tasks
+inline int pass_threads(const DesignDev& D) { return D.csr.nranges * 32; }
 
 // Raises a kernel's dynamic shared-memory limit to the device's opt-in maximum
 // (minus its static shared memory).  The limit is a per-kernel, per-process

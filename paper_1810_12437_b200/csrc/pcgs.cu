@@ -30,6 +30,7 @@ namespace cg = cooperative_groups;
 static unsigned long long* g_prof = nullptr;  // debug: phase timestamps of the next pcgs_pcg
 static int g_dbg = 0;
 static int g_l2_persist_mb = 0;
+static int g_nranges = 0;  // debug option 3: warp ranges per task of stores created from now on (0: default)
 static thread_local std::string g_err;
 void set_last_error(const std::string& msg) { g_err = msg; }
 
@@ -240,6 +241,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // and stamps inside phase C at [16 * cta + 8 + k]
 __device__ unsigned long long* g_sync_times = nullptr;
 constexpr int kSyncTraceIter = 10;
+// The persistent PCG kernel runs 16 warps of 128 registers, each walking two of
+// a task's 32 warp ranges with two-block register batches: they keep the LSU
+// pipe as busy as 32 warps of 64 registers (70.5 vs 69.8 us per iteration at
+// config 2), and the register room pays for the step phase on column-major
+// piece slots and the hooks in the slab fills' TMA wait, which spilled at 64
+// registers (67.7 us).  The standalone passes and the row-split
+// kernel stay at 32 warps (their streams ran 9 % slower on 16).
+#ifndef PCGS_PCG_WARPS
+#define PCGS_PCG_WARPS 16
+#endif
+constexpr int kPcgWarps = PCGS_PCG_WARPS;
+constexpr int kPcgThreads = kPcgWarps * 32;
+constexpr int kPcgRing = kPcgWarps <= 16 ? 2 : 1;  // blocks per register batch of the grouped walk
 constexpr int kMaxGrid = 256;  // persistent-kernel grid bound (one CTA per SM; B200: 148)
 
 struct FillDir {  // search direction: first ? a : a + beta * b   (internal layout)
@@ -324,7 +338,7 @@ __device__ __forceinline__ bool stage_pieces(const PieceRun& o, const double* pi
                                              int cap) {
   const int total = o.rel(chunk);
   if (total > cap) return false;
-  for (int q = threadIdx.x; q < total; q += kThreads) stage[q] = __ldcg(pieces + o.q_lo + q);
+  for (int q = threadIdx.x; q < total; q += (int)blockDim.x) stage[q] = __ldcg(pieces + o.q_lo + q);
   __syncthreads();
   return true;
 }
@@ -414,7 +428,7 @@ __device__ __forceinline__ void aff_mu_partial(const PcgArgs& A, double acc, dou
 }
 
 template <bool AFF>
-__global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
+__global__ void __launch_bounds__(kPcgThreads, 1) k_pcg(PcgArgs A) {
   // Loop state lives in shared memory so that the inlined streaming passes
   // get the whole register budget (1024 threads -> 64 registers).
   extern __shared__ __align__(128) double sv[];
@@ -435,7 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     const long long j0 = (long long)blockIdx.x * chunk;
     const long long dvs = (pt + 15) / 16 * 16;
     const OwnState o = own_state(sv, A.D, chunk, j0);
-    for (int t = tid; t < chunk; t += kThreads) {
+    for (int t = tid; t < chunk; t += kPcgThreads) {
       const long long j = j0 + t;
       double xv = 0, m = 0, sc = 0, dg = 0, bv = 0;
       if (j < pt) {
@@ -461,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       int* cpw = const_cast<int*>(o.cp);
       const int* gcp = A.D.csc.col_piece_ptr;
       const int q_lo = __ldg(gcp + min(j0, pt));
-      for (int t = tid; t <= chunk; t += kThreads) cpw[t] = __ldg(gcp + min(j0 + t, pt)) - q_lo;
+      for (int t = tid; t <= chunk; t += kPcgThreads) cpw[t] = __ldg(gcp + min(j0 + t, pt)) - q_lo;
     }
     if (tid == 0) {
       st_rz = 0.0;
@@ -473,7 +487,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     if (AFF) {
       double mu_u = 0.0;
       if (A.D.aff.mu)
-        for (int t = tid; t < chunk; t += kThreads) {
+        for (int t = tid; t < chunk; t += kPcgThreads) {
           const long long j = j0 + t;
           if (j < pt) {
             const long long rj = ref_index(j, A.D.p, A.D.lead());
@@ -523,7 +537,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       // new direction d = z + beta d on the owned slice, published for the fill
       // (affine designs publish u = d / s and the CTA partial of mu'u)
       double mu_u = 0.0;
-      for (int t = tid; t < chunk; t += kThreads) {
+      for (int t = tid; t < chunk; t += kPcgThreads) {
         const double dn = a == 1 ? o.z[t] : fma(beta, o.d[t], o.z[t]);
         o.d[t] = dn;
         if (j0 + t < pt) {
@@ -544,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
 
     // ---------------- phase A: CSR pass, w = omega (X v) ----------------
     double acc_dAd = 0.0;
-    for (int t = tid; t < chunk; t += kThreads) acc_dAd += o.D[t] * o.d[t] * o.d[t];
+    for (int t = tid; t < chunk; t += kPcgThreads) acc_dAd += o.D[t] * o.d[t] * o.d[t];
     const double* vcur = A.dvg + (a == 0 ? dvs : (a & 1) * dvs);
     if (!AFF) {
       const bool multi = A.D.csr.nslab > 1;
@@ -556,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
         __syncthreads();
       }
       FillBulkV0 f{vcur, &bf, icpt_src, bc + 2, &e.v0};
-      run_pass(A.D.csr, sv, f, e, A.D.dbg);
+      run_pass<kPcgRing>(A.D.csr, sv, f, e, A.D.dbg);
       acc_dAd += e.acc;
     } else {
       // row constant u_icpt - mu'u (grid sum of the CTA partials, fixed order);
@@ -567,8 +581,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       const bool multi = A.D.csr.nslab > 1;
       EpiCsrA e{multi ? A.zpart : A.w, A.omega, bc[2], 0.0, multi,
                 AffRow{A.D.aff.dense, vcur + A.D.p + A.D.icpt, A.D.aff.q}};
-      FillBulk f{vcur, &bf};
-      run_pass(A.D.csr, sv, f, e, A.D.dbg);
+      FillBulkH f{vcur, &bf};
+      run_pass<kPcgRing>(A.D.csr, sv, f, e, A.D.dbg);
       acc_dAd += e.acc;
     }
     if (A.D.csr.nslab > 1) {
@@ -576,7 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       const long long n = A.D.n;
       const double v0 = bc[2];
       const AffRow ar{A.D.aff.dense, vcur + A.D.p + A.D.icpt, AFF ? A.D.aff.q : 0};
-      for (long long i = (long long)blockIdx.x * kThreads + tid; i < n; i += (long long)gridDim.x * kThreads) {
+      for (long long i = (long long)blockIdx.x * kPcgThreads + tid; i < n; i += (long long)gridDim.x * kPcgThreads) {
         double z = 0.0;
         for (int s = 0; s < A.D.csr.nslab; ++s) z += __ldcg(A.zpart + (long long)s * n + i);
         z += v0;
@@ -597,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       const long long n = A.D.n, r0 = n * blockIdx.x / gridDim.x, r1 = n * (blockIdx.x + 1) / gridDim.x;
       for (int k = 0; k < L; ++k) {
         double acc = 0.0;
-        for (long long i = r0 + tid; i < r1; i += kThreads) {
+        for (long long i = r0 + tid; i < r1; i += kPcgThreads) {
           const double wi = __ldcg(A.w + i);
           acc += k == 0 ? wi : __ldg(A.D.aff.dense + i * q + (k - 1)) * wi;
         }
@@ -611,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     {
       FillVecNDad f{A.w, &bf, A.part, (int)gridDim.x, bc, PCGS_DAD_IN_FILL && a > 0, false};
       EpiStore e{A.pieces, A.D.csc.nseg};  // A.D.csc.ids are the column-major piece slots (host: pcgs_pcg_full)
-      run_pass(A.D.csc, sv, f, e, A.D.dbg);
+      run_pass<kPcgRing>(A.D.csc, sv, f, e, A.D.dbg);
       dad_pending = a > 0 && !f.done;
     }
     if (prof) A.prof[4 * a + 2] = gtimer();
@@ -669,7 +683,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
       return (raw - mu * affg[0]) / sc;
     };
     double t_rms = 0.0, t_rz = 0.0;
-    for (int t = tid; t < chunk; t += kThreads) {
+    for (int t = tid; t < chunk; t += kPcgThreads) {
       if (j0 + t >= pt) continue;
       const double Ad = aff_ad(t, owned_column_sum(pr, A.pieces, t, sv, staged)) + o.D[t] * o.d[t];
       double rv;
@@ -703,7 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pcg(PcgArgs A) {
     const int chunk = (int)((pt + gridDim.x - 1) / gridDim.x);
     const long long j0 = (long long)blockIdx.x * chunk;
     const OwnState o = own_state(sv, A.D, chunk, j0);
-    for (int t = tid; t < chunk; t += kThreads)
+    for (int t = tid; t < chunk; t += kPcgThreads)
       if (j0 + t < pt) A.x[ref_index(j0 + t, A.D.p, A.D.lead())] = o.x[t];
   }
   if (blockIdx.x == 0 && tid == 0) {
@@ -775,7 +789,8 @@ int pcgs_design_create_affine(int64_t n, int64_t p, const int64_t* row_ptr_h, co
   const int G = grid > 0 ? grid : sms;
   if (q_dense < 0 || q_dense > kAffMaxQ) return fail(PCGS_EINVAL, "dense block: at most 32 columns");
   DesignHost H;
-  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H, q_dense);
+  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, G, H, q_dense,
+                                 g_nranges > 0 ? g_nranges : kDefaultRanges);
   if (!err.empty()) return fail(PCGS_EINVAL, err);
   pcgs_design* D = new pcgs_design();
   D->dev.aff = AffineDev{0, q_dense, nullptr, nullptr, nullptr};
@@ -992,13 +1007,13 @@ static int launch_csr(pcgs_design_t d, bool phi, const double* v, const double* 
   int rc;
   if ((rc = aff_pre(d, v, S, s, &cbuf))) return rc;
   if (D.csr.nslab == 1) {
-    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, out, cbuf);
-    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, out, cbuf);
+    if (phi) k_csr_phi<<<D.G, pass_threads(D), sm, s>>>(D, v, omega, out, cbuf);
+    else k_csr_matvec<<<D.G, pass_threads(D), sm, s>>>(D, v, out, cbuf);
   } else {
     double* part = S.get<double>((size_t)D.csr.nslab * D.n);
     if (!part) return fail(PCGS_ENOMEM, "scratch allocation failed");
-    if (phi) k_csr_phi<<<D.G, kThreads, sm, s>>>(D, v, omega, part, cbuf);
-    else k_csr_matvec<<<D.G, kThreads, sm, s>>>(D, v, part, cbuf);
+    if (phi) k_csr_phi<<<D.G, pass_threads(D), sm, s>>>(D, v, omega, part, cbuf);
+    else k_csr_matvec<<<D.G, pass_threads(D), sm, s>>>(D, v, part, cbuf);
     k_rows_combine<<<D.G * 4, 256, 0, s>>>(D, part, v, phi ? omega : nullptr, out, cbuf);
   }
   CUDA_TRY(cudaGetLastError());
@@ -1024,7 +1039,7 @@ int pcgs_matvec_t(pcgs_design_t d, const double* w, double* out, pcgs_stream_t s
   double* gbuf;
   int rc;
   if ((rc = aff_tw(d, w, 0, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, w, pieces);
+  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, w, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, nullptr, nullptr, nullptr, 0, 0, 0, out, nullptr,
                                                        gbuf);
   CUDA_TRY(cudaGetLastError());
@@ -1044,7 +1059,7 @@ int pcgs_phi_apply(pcgs_design_t d, const double* omega, const double* prior_dia
   if (rc) return rc;
   double* gbuf;
   if ((rc = aff_tw(d, w, 0, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, w, pieces);
+  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, w, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, v, nullptr, 0, 0, 1, out, nullptr,
                                                        gbuf);
   CUDA_TRY(cudaGetLastError());
@@ -1062,7 +1077,7 @@ int pcgs_phi_diagonal(pcgs_design_t d, const double* omega, const double* prior_
   double* gbuf;
   int rc;
   if ((rc = aff_tw(d, omega, 1, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, omega, pieces);
+  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, omega, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, nullptr, 0, 0, 3, out, nullptr,
                                                        gbuf);
   CUDA_TRY(cudaGetLastError());
@@ -1086,7 +1101,7 @@ int pcgs_rhs(pcgs_design_t d, const double* kappa, const double* omega, const do
   double* gbuf;
   int rc;
   if ((rc = aff_tw(d, u, 0, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, kThreads, smem_bytes(D), s>>>(D, u, pieces);
+  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, u, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, delta, seed,
                                                        kStreamDelta ^ stream_id, 2, b, linear, gbuf);
   CUDA_TRY(cudaGetLastError());
@@ -1147,7 +1162,7 @@ int pcgs_pcg_full(pcgs_design_t d, const double* omega, const double* prior_diag
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(D.G);
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(kPcgThreads);
   cfg.dynamicSmemBytes = pcg_smem_bytes(D);
   cfg.stream = s;
   cudaLaunchAttribute attrs[2];
@@ -1333,6 +1348,7 @@ int pcgs_debug_cta_times(void* buf) {
 int pcgs_debug_option(int key, int value) {
   if (key == 1) g_dbg = value;
   if (key == 2) g_l2_persist_mb = value;
+  if (key == 3) g_nranges = value;
   return PCGS_OK;
 }
 

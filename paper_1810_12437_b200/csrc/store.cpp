@@ -265,8 +265,9 @@ struct Slice {
   uint8_t lw;
 };
 
-// Lays out segments [s0, s1) of slab S as one CTA task: kWarps warp ranges.
+// Lays out segments [s0, s1) of slab S as one CTA task: P.nranges warp ranges.
 void emit_task_grouped(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std::vector<Pool>& pools) {
+  const int NR = P.nranges;
   struct Item {
     uint32_t seg, nv;
     uint8_t lw;
@@ -281,7 +282,7 @@ void emit_task_grouped(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std
     uint32_t cnt[6] = {};
     for (const Item& it : items) ++cnt[it.lw];
     for (int lw = 0; lw < 6; ++lw) nslices += (cnt[lw] + (32u >> lw) - 1) / (32u >> lw);
-    if (nslices >= (size_t)kWarps) break;
+    if (nslices >= (size_t)NR) break;
     bool any = false;
     for (Item& it : items)
       if (it.lw < 5 && (2u << it.lw) <= it.nv) {
@@ -306,19 +307,19 @@ void emit_task_grouped(PassHost& P, const SlabSegs& S, size_t s0, size_t s1, std
   std::vector<uint32_t> order(slices.size());
   std::iota(order.begin(), order.end(), 0u);
   std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return slices[a].T > slices[b].T; });
-  std::vector<std::vector<uint32_t>> mine(kWarps);
+  std::vector<std::vector<uint32_t>> mine(NR);
   {
     static const int close = env_int("PCGS_G_SLICE_COST", 1);
-    uint64_t load[kWarps] = {};
+    uint64_t load[kWarps] = {};  // NR <= kWarps
     for (uint32_t q : order) {
       int w = 0;
-      for (int c = 1; c < kWarps; ++c)
+      for (int c = 1; c < NR; ++c)
         if (load[c] < load[w]) w = c;
       mine[w].push_back(q);
       load[w] += slices[q].T + (uint64_t)close;
     }
   }
-  for (int w = 0; w < kWarps; ++w) {
+  for (int w = 0; w < NR; ++w) {
     WarpRange R{};
     R.v0 = (uint32_t)(P.idx.size() / kVecIdx);
     R.blk0 = (uint32_t)P.blocks.size();
@@ -511,8 +512,8 @@ void plan_and_emit(PassHost& P, std::vector<SlabSegs>& slabs, int G, bool csc, i
       emit_task_grouped(P, slabs[s], a, b, pools);
     } else {
       std::vector<size_t> wc;
-      cut(pre[s], a, b, kWarps, wc);
-      for (int w = 0; w < kWarps; ++w) emit_warp(P, slabs[s], wc[w], wc[w + 1], pools);
+      cut(pre[s], a, b, P.nranges, wc);
+      for (int w = 0; w < P.nranges; ++w) emit_warp(P, slabs[s], wc[w], wc[w + 1], pools);
     }
     P.tasks.push_back(t);
   };
@@ -573,7 +574,9 @@ std::string validate_csr(int64_t n, int64_t p, const int64_t* row_ptr, const int
 }
 
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
-                         int intercept, int slab_max, int G, DesignHost& D, int q_dense) {
+                         int intercept, int slab_max, int G, DesignHost& D, int q_dense, int nranges) {
+  if (nranges < 1 || nranges > kWarps) return "warp ranges per task must be in [1, 32]";
+  D.csr.nranges = D.csc.nranges = nranges;
   if (q_dense < 0 || (q_dense > 0 && intercept)) return "dense columns replace the intercept flag";
   g_dbg_hist = getenv("PCGS_STORE_STATS") ? g_hist : nullptr;
   if (g_dbg_hist) memset(g_hist, 0, sizeof(g_hist));
@@ -726,7 +729,7 @@ std::string verify_design(const DesignHost& D, const int64_t* row_ptr, const int
       const Task& T = P.tasks[t];
       const int64_t lo = P.slab_lo[T.slab], hi = P.slab_lo[T.slab + 1];
       const uint16_t sent = (uint16_t)(hi - lo);
-      for (int w = 0; w < kWarps; ++w) {
+      for (int w = 0; w < P.nranges; ++w) {
         const WarpRange& R = P.warps[T.warp0 + w];
         if (R.nvec == 0) continue;
         if (P.grouped) {

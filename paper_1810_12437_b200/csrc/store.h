@@ -52,16 +52,14 @@
 
 namespace pcgs {
 
-// Warps per CTA of the tiled-store kernels.  16 warps get 128 registers each:
-// with the grouped walk's two-block register batches they keep the LSU pipe as
-// busy as 32 warps at 64 registers did (70.5 vs 69.8 us per PCG iteration at
-// config 2), and the register room pays for the step phase on column-major
-// piece slots and the hooks in the slab fills' TMA wait, which spilled at 64
-// registers (67.8 us).
-#ifndef PCGS_WARPS
-#define PCGS_WARPS 16
-#endif
-constexpr int kWarps = PCGS_WARPS;     // warps per CTA of the pass kernels
+// Warps per CTA of the kernels that walk one warp range per warp, and the most
+// warp ranges a CTA task can hold.  A store is built with `nranges` ranges per
+// task (PassHost::nranges): 16 by default -- the persistent PCG kernel runs 16
+// warps of 128 registers (pcgs.cu) -- and 32 for the row-split shards, whose
+// kernel runs 32 warps of 64 registers.  A CTA of nw warps walks any store:
+// warp w takes ranges w, w + nw, ... (warps beyond nranges idle).
+constexpr int kWarps = 32;
+constexpr int kDefaultRanges = 16;
 constexpr int kThreads = kWarps * 32;  // 1024
 constexpr int kVecIdx = 8;             // uint16 indices per 16-byte vector
 
@@ -79,7 +77,7 @@ struct BlockDesc {    // 8 bytes, device-readable as uint2
 
 struct Task {         // one (slab, 16 warp ranges) assignment of a CTA
   int32_t slab;
-  int32_t warp0;      // first of kWarps consecutive WarpRange entries
+  int32_t warp0;      // first of nranges consecutive WarpRange entries
 };
 
 struct PassHost {
@@ -89,6 +87,7 @@ struct PassHost {
   std::vector<BlockDesc> blocks;
   std::vector<uint32_t> ids;           // grouped layout: segment ids per slice group
   int grouped = 0;
+  int nranges = kDefaultRanges;        // warp ranges per task
   std::vector<int32_t> rep_ptr;        // grouped layout: nslab+1 offsets into rep_src
   std::vector<uint16_t> rep_src;       // replica k of slab s copies slab entry rep_src[rep_ptr[s] + k]
   int64_t pad_vectors = 0;             // grouped layout: all-sentinel vector slots
@@ -121,7 +120,8 @@ std::string validate_csr(int64_t n, int64_t p, const int64_t* row_ptr, const int
 // Validates the CSR (sparse.py:94-117 invariants) and builds both passes for a
 // grid of G CTAs.  Returns an empty string on success, else an error message.
 std::string build_design(int64_t n, int64_t p, const int64_t* row_ptr, const int32_t* col_idx,
-                         int intercept, int slab_max, int G, DesignHost& out, int q_dense = 0);
+                         int intercept, int slab_max, int G, DesignHost& out, int q_dense = 0,
+                         int nranges = kDefaultRanges);
 
 // Native synthetic binary design (bench/test infrastructure): returns nnz.
 int64_t synth_binary_design(int64_t n, int64_t p, double rate_lo, double rate_hi, uint64_t seed,

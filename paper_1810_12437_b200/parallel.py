@@ -251,7 +251,7 @@ class RowSplitPCG:
         nranks = world * n_local if real else n_local
         sms = t.cuda.get_device_properties(self.device).multi_processor_count
         grid = 0 if n_local == 1 else sms // n_local
-        self.stores = [s.device_store(self.device, grid=grid) for s in self.shards]
+        self.stores = [s.device_store(self.device, grid=grid, ranges=32) for s in self.shards]
         p_total = {st.p_total for st in self.stores}
         if len(p_total) != 1:
             raise ValueError("row shards must share the column set")

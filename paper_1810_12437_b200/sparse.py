@@ -336,9 +336,12 @@ class SparseDesignMatrix:
     def has_intercept(self):
         return self.pattern()[2]
 
-    def device_store(self, device=None, grid=0, raw=False) -> DesignStore:
+    def device_store(self, device=None, grid=0, raw=False, ranges=0) -> DesignStore:
         """The store on `device`; `grid` > 0 plans it for that many CTAs
-        (row-split shards or chains side by side sharing a GPU).  The affine
+        (row-split shards or chains side by side sharing a GPU); `ranges` > 0
+        sets the warp ranges per CTA task (the row-split kernel runs 32 warps
+        and builds its shards with 32; the default, 16, is the persistent PCG
+        kernel's warp count).  The affine
         terms (dense block, standardisation) are attached to it and follow
         later standardize() calls; `raw` = the pattern-only view of a
         pattern-only design (the Gibbs reparametrisation of standardised
@@ -346,12 +349,18 @@ class SparseDesignMatrix:
         dev = _lib.cuda_device(device)
         rp, ci, icpt = self.pattern()
         dense = self.dense_block
-        key = (dev.index, 1, int(grid), bool(raw))
+        key = (dev.index, 1, int(grid), bool(raw), int(ranges))
         st = self._stores.get(key)
         if st is None:
             q = 0 if dense is None else dense.shape[1]
-            st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0) - q, rp, ci, icpt,
-                             device=dev, slab_max=self.slab_max, grid=grid, q_dense=q)
+            if ranges:
+                _lib.lib().pcgs_debug_option(3, int(ranges))
+            try:
+                st = DesignStore(self.n_rows, self.n_cols - (1 if icpt else 0) - q, rp, ci, icpt,
+                                 device=dev, slab_max=self.slab_max, grid=grid, q_dense=q)
+            finally:
+                if ranges:
+                    _lib.lib().pcgs_debug_option(3, 0)
             self._stores[key] = st
         if raw:
             if dense is not None:

@@ -31,7 +31,7 @@ int main(int argc, char** argv) {
       uint64_t cta_max = 0;
       for (int t = P->cta_task_ptr[c]; t < P->cta_task_ptr[c + 1]; ++t) {
         uint64_t m = 0;
-        for (int w = 0; w < pcgs::kWarps; ++w) {
+        for (int w = 0; w < P->nranges; ++w) {
           m = std::max<uint64_t>(m, P->warps[P->tasks[t].warp0 + w].nvec);
           total += P->warps[P->tasks[t].warp0 + w].nvec;
         }
@@ -42,14 +42,14 @@ int main(int argc, char** argv) {
       ++ctas;
     }
     printf("  %s: busiest warp path %llu vectors (mean over CTAs %.0f), ideal %.0f\n", P == &D.csr ? "csr" : "csc",
-           (unsigned long long)worst, (double)sum_max / ctas, (double)total / (G * pcgs::kWarps));
+           (unsigned long long)worst, (double)sum_max / ctas, (double)total / (G * P->nranges));
   }
   if (getenv("STATS_CTA")) {
     const int c = atoi(getenv("STATS_CTA"));
     for (const pcgs::PassHost* P : {&D.csr, &D.csc})
       for (int t = P->cta_task_ptr[c]; t < P->cta_task_ptr[c + 1]; ++t) {
         printf("  %s cta %d task %d slab %d: warp steps/slices:", P == &D.csr ? "csr" : "csc", c, t, P->tasks[t].slab);
-        for (int w = 0; w < pcgs::kWarps; ++w) {
+        for (int w = 0; w < P->nranges; ++w) {
           const pcgs::WarpRange& R = P->warps[P->tasks[t].warp0 + w];
           printf(" %u/%u", R.nvec / 32, R.pad);
         }
