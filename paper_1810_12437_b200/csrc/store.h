@@ -25,9 +25,9 @@
 // class and similar length walked in lockstep for T = ceil(max nv / W) steps;
 // step t is one 32-vector block (lane g*W + k holds vector t*W + k of the
 // slice's g-th segment, sentinel-padded).  A CTA's segments are sorted by
-// length before slicing (padding stays small), its slices are dealt to the 32
-// warps longest first (each to the least loaded warp), and a warp's slices
-// are contiguous in the stream.  `blocks` then holds one descriptor per slice
+// length before slicing (padding stays small), its slices are dealt to the
+// task's warp ranges (PassHost::nranges, below) longest first, each to the
+// least loaded range, and a range's slices are contiguous in the stream.  `blocks` then holds one descriptor per slice
 // {offset into `ids`, T | log2 W << 24} and `ids` the 32/W segment ids of
 // each slice (0xffffffff: empty group); WarpRange.pad counts the slices.
 //
