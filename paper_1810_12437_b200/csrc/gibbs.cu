@@ -36,14 +36,15 @@ struct EpiLogit {  // z_i = v0 + s (+ dense row term); acc += y_i z_i - log(1 + 
   }
 };
 
-__global__ void __launch_bounds__(kThreads, 1) k_csr_logit(DesignDev D, const double* beta, const double* y,
+template <int kT, int kRingB>
+__global__ void __launch_bounds__(kT, 1) k_csr_logit(DesignDev D, const double* beta, const double* y,
                                                            double* z_or_part, double* part, const double* cbuf) {
   extern __shared__ __align__(128) double sv[];
   __shared__ double red[64];
   FillVecRef f{beta, D.lead(), 0, D.aff.sc};
   const double v0 = row_const(D, beta, cbuf);
   EpiLogit e{z_or_part, y, v0, 0.0, D.csr.nslab > 1, aff_row(D, cbuf)};
-  run_pass(D.csr, sv, f, e);
+  run_pass<kRingB>(D.csr, sv, f, e);
   const double t = block_sum(e.acc, red);
   if (threadIdx.x == 0) part[blockIdx.x * kPartStride] = t;
 }
@@ -274,11 +275,11 @@ int launch_logit(pcgs_design* d, pcgs_gibbs_t* g, cudaStream_t s) {
   int rc;
   if ((rc = aff_pre(d, g->beta, S, s, &cbuf))) return rc;
   if (D.csr.nslab == 1) {
-    k_csr_logit<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, g->beta, g->y, g->z, g->part, cbuf);
+    PASS_LAUNCH(k_csr_logit, D, smem_bytes(D), s, D, g->beta, g->y, g->z, g->part, cbuf);
   } else {
     double* zp = S.get<double>((size_t)D.csr.nslab * D.n);
     if (!zp) return fail(PCGS_ENOMEM, "scratch allocation failed");
-    k_csr_logit<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, g->beta, g->y, zp, g->part, cbuf);
+    PASS_LAUNCH(k_csr_logit, D, smem_bytes(D), s, D, g->beta, g->y, zp, g->part, cbuf);
     k_rows_logit<<<D.G, kThreads, 0, s>>>(D, zp, g->beta, g->y, g->z, g->part, cbuf);
   }
   CUDA_TRY(cudaGetLastError());
@@ -306,7 +307,7 @@ int pcgs_scale_draws(int prior, int mode, int64_t count, double b_or_acc, double
 int pcgs_gibbs_init(pcgs_design_t d, pcgs_gibbs_t* g, pcgs_stream_t stream) {
   if (!d || !g || !g->beta || !g->z || !g->y || !g->part) return fail(PCGS_EINVAL, "null argument");
   int rc0;
-  if ((rc0 = raise_smem_limit(k_csr_logit))) return rc0;
+  if ((rc0 = raise_smem_limit(k_csr_logit<512, 2>)) || (rc0 = raise_smem_limit(k_csr_logit<1024, 1>))) return rc0;
   k_tau_sums<<<d->dev.G, 256, 0, (cudaStream_t)stream>>>(*g, d->dev.pt);
   CUDA_TRY(cudaGetLastError());
   return launch_logit(d, g, (cudaStream_t)stream);
@@ -496,7 +497,7 @@ static int rs_logit(pcgs_rs_t rs, pcgs_gibbs_t* g, const pcgs_rs_rows_t* rows, c
     int64_t row0;
     int rc;
     if ((rc = rs_local(rs, l, &d, &row0))) return rc;
-    if ((rc = raise_smem_limit(k_csr_logit))) return rc;
+    if ((rc = raise_smem_limit(k_csr_logit<512, 2>)) || (rc = raise_smem_limit(k_csr_logit<1024, 1>))) return rc;
     pcgs_gibbs_t gl = *g;
     gl.y = rows[l].y;
     gl.z = rows[l].z;

@@ -266,6 +266,14 @@ int aff_pre(pcgs_design* d, const double* v, Scratch& S, cudaStream_t s, double*
 inline size_t smem_bytes(const DesignDev& D) { return (size_t)D.smem_doubles * sizeof(double); }
 // threads per CTA of the standalone pass kernels: one warp per range of the store's tasks
 inline int pass_threads(const DesignDev& D) { return D.csr.nranges * 32; }
+// The standalone pass kernels come in two builds: 16 warps of 128 registers
+// with two-block register batches (stores with <= 16 ranges per task) and 32
+// warps of 64 registers with one-block batches.
+#define PASS_LAUNCH(kern, D, smem, s, ...)                                            \
+  do {                                                                                \
+    if (pass_threads(D) <= 512) kern<512, 2><<<(D).G, pass_threads(D), smem, s>>>(__VA_ARGS__); \
+    else kern<1024, 1><<<(D).G, pass_threads(D), smem, s>>>(__VA_ARGS__);             \
+  } while (0)
 
 // Raises a kernel's dynamic shared-memory limit to the device's opt-in maximum
 // (minus its static shared memory).  The limit is a per-kernel, per-process

@@ -37,31 +37,33 @@ void set_last_error(const std::string& msg) { g_err = msg; }
 // =====================================================================
 // standalone kernels (one pass each; launched with the plan's G CTAs)
 // =====================================================================
-__global__ void __launch_bounds__(kThreads, 1) k_csr_matvec(DesignDev D, const double* v, double* out,
+template <int kT, int kRingB>
+__global__ void __launch_bounds__(kT, 1) k_csr_matvec(DesignDev D, const double* v, double* out,
                                                             const double* cbuf) {
   extern __shared__ __align__(128) double sv[];
   FillVecRef f{v, D.lead(), 0, D.aff.sc};
   const double v0 = row_const(D, v, cbuf);
   if (D.csr.nslab == 1) {
     EpiZ e{out, v0, aff_row(D, cbuf)};
-    run_pass(D.csr, sv, f, e, D.dbg);
+    run_pass<kRingB>(D.csr, sv, f, e, D.dbg);
   } else {
     EpiStore e{out, (long long)D.csr.nslab * D.n};  // out is the (nslab x n) partial buffer
-    run_pass(D.csr, sv, f, e, D.dbg);
+    run_pass<kRingB>(D.csr, sv, f, e, D.dbg);
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_csr_phi(DesignDev D, const double* v, const double* omega, double* w,
+template <int kT, int kRingB>
+__global__ void __launch_bounds__(kT, 1) k_csr_phi(DesignDev D, const double* v, const double* omega, double* w,
                                                          const double* cbuf) {
   extern __shared__ __align__(128) double sv[];
   FillVecRef f{v, D.lead(), 0, D.aff.sc};
   const double v0 = row_const(D, v, cbuf);
   if (D.csr.nslab == 1) {
     EpiW e{w, omega, v0, 0.0, aff_row(D, cbuf)};
-    run_pass(D.csr, sv, f, e);
+    run_pass<kRingB>(D.csr, sv, f, e);
   } else {
     EpiStore e{w, (long long)D.csr.nslab * D.n};
-    run_pass(D.csr, sv, f, e);
+    run_pass<kRingB>(D.csr, sv, f, e);
   }
 }
 
@@ -157,14 +159,15 @@ __global__ void k_rhs_u(FillRhs f, long long n, double* u) {
     u[i] = f((int)i);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_csc_vec(DesignDev D, const double* w, double* pieces) {
+template <int kT, int kRingB>
+__global__ void __launch_bounds__(kT, 1) k_csc_vec(DesignDev D, const double* w, double* pieces) {
   extern __shared__ __align__(128) double sv[];
   __shared__ unsigned long long mbar;
   BulkFill bf;
   bulk_init(bf, &mbar);
   FillVecN f{w, &bf};
   EpiStore e{pieces, D.csc.nseg};
-  run_pass(D.csc, sv, f, e, D.dbg);
+  run_pass<kRingB>(D.csc, sv, f, e, D.dbg);
 }
 
 // out[ref(j)] = column_sum(j) + diag_j * v[ref(j)]  (diag/v may be null)
@@ -749,8 +752,9 @@ const char* pcgs_last_error(void) { return g_err.c_str(); }
 
 static int set_smem_attrs() {
   int rc;
-  if ((rc = raise_smem_limit(k_csr_matvec)) || (rc = raise_smem_limit(k_csr_phi)) ||
-      (rc = raise_smem_limit(k_csc_vec)) ||
+  if ((rc = raise_smem_limit(k_csr_matvec<512, 2>)) || (rc = raise_smem_limit(k_csr_matvec<1024, 1>)) ||
+      (rc = raise_smem_limit(k_csr_phi<512, 2>)) || (rc = raise_smem_limit(k_csr_phi<1024, 1>)) ||
+      (rc = raise_smem_limit(k_csc_vec<512, 2>)) || (rc = raise_smem_limit(k_csc_vec<1024, 1>)) ||
       (rc = raise_smem_limit(k_pcg<false>)) || (rc = raise_smem_limit(k_pcg<true>)))
     return rc;
   return PCGS_OK;
@@ -1007,13 +1011,13 @@ static int launch_csr(pcgs_design_t d, bool phi, const double* v, const double* 
   int rc;
   if ((rc = aff_pre(d, v, S, s, &cbuf))) return rc;
   if (D.csr.nslab == 1) {
-    if (phi) k_csr_phi<<<D.G, pass_threads(D), sm, s>>>(D, v, omega, out, cbuf);
-    else k_csr_matvec<<<D.G, pass_threads(D), sm, s>>>(D, v, out, cbuf);
+    if (phi) PASS_LAUNCH(k_csr_phi, D, sm, s, D, v, omega, out, cbuf);
+    else PASS_LAUNCH(k_csr_matvec, D, sm, s, D, v, out, cbuf);
   } else {
     double* part = S.get<double>((size_t)D.csr.nslab * D.n);
     if (!part) return fail(PCGS_ENOMEM, "scratch allocation failed");
-    if (phi) k_csr_phi<<<D.G, pass_threads(D), sm, s>>>(D, v, omega, part, cbuf);
-    else k_csr_matvec<<<D.G, pass_threads(D), sm, s>>>(D, v, part, cbuf);
+    if (phi) PASS_LAUNCH(k_csr_phi, D, sm, s, D, v, omega, part, cbuf);
+    else PASS_LAUNCH(k_csr_matvec, D, sm, s, D, v, part, cbuf);
     k_rows_combine<<<D.G * 4, 256, 0, s>>>(D, part, v, phi ? omega : nullptr, out, cbuf);
   }
   CUDA_TRY(cudaGetLastError());
@@ -1039,7 +1043,7 @@ int pcgs_matvec_t(pcgs_design_t d, const double* w, double* out, pcgs_stream_t s
   double* gbuf;
   int rc;
   if ((rc = aff_tw(d, w, 0, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, w, pieces);
+  PASS_LAUNCH(k_csc_vec, D, smem_bytes(D), s, D, w, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, nullptr, nullptr, nullptr, 0, 0, 0, out, nullptr,
                                                        gbuf);
   CUDA_TRY(cudaGetLastError());
@@ -1059,7 +1063,7 @@ int pcgs_phi_apply(pcgs_design_t d, const double* omega, const double* prior_dia
   if (rc) return rc;
   double* gbuf;
   if ((rc = aff_tw(d, w, 0, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, w, pieces);
+  PASS_LAUNCH(k_csc_vec, D, smem_bytes(D), s, D, w, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, v, nullptr, 0, 0, 1, out, nullptr,
                                                        gbuf);
   CUDA_TRY(cudaGetLastError());
@@ -1077,7 +1081,7 @@ int pcgs_phi_diagonal(pcgs_design_t d, const double* omega, const double* prior_
   double* gbuf;
   int rc;
   if ((rc = aff_tw(d, omega, 1, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, omega, pieces);
+  PASS_LAUNCH(k_csc_vec, D, smem_bytes(D), s, D, omega, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, nullptr, 0, 0, 3, out, nullptr,
                                                        gbuf);
   CUDA_TRY(cudaGetLastError());
@@ -1101,7 +1105,7 @@ int pcgs_rhs(pcgs_design_t d, const double* kappa, const double* omega, const do
   double* gbuf;
   int rc;
   if ((rc = aff_tw(d, u, 0, S, s, &gbuf))) return rc;
-  k_csc_vec<<<D.G, pass_threads(D), smem_bytes(D), s>>>(D, u, pieces);
+  PASS_LAUNCH(k_csc_vec, D, smem_bytes(D), s, D, u, pieces);
   k_assemble<<<(int)((D.pt + 255) / 256), 256, 0, s>>>(D, pieces, prior_diag, nullptr, delta, seed,
                                                        kStreamDelta ^ stream_id, 2, b, linear, gbuf);
   CUDA_TRY(cudaGetLastError());
