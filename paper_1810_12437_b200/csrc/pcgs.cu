@@ -863,7 +863,8 @@ int pcgs_store_selftest(int64_t n, int64_t p, const int64_t* row_ptr_h, const in
                         int slab_max, int grid, int64_t* stats_h) {
   if (!row_ptr_h || grid < 1) return fail(PCGS_EINVAL, "null argument");
   DesignHost H;
-  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, grid, H);
+  std::string err = build_design(n, p, row_ptr_h, col_idx_h, intercept, slab_max, grid, H, 0,
+                                 g_nranges > 0 ? g_nranges : kDefaultRanges);
   if (!err.empty()) return fail(PCGS_EINVAL, err);
   err = verify_design(H, row_ptr_h, col_idx_h);
   if (stats_h) {

@@ -139,6 +139,27 @@ def test_store_config1_layout_and_bank_balance(monkeypatch):
             assert rc == 0, msg
 
 
+def test_store_roundtrip_with_32_ranges_per_task():
+    """Debug option 3 sets the warp ranges per CTA task of the stores built
+    from then on (the row-split shards use 32, the default is 16)."""
+    L = _lib.lib()
+    rng = np.random.default_rng(21)
+    try:
+        for ranges in (32, 8, 1):
+            L.pcgs_debug_option(3, ranges)
+            for _ in range(4):
+                n, p = (int(v) for v in rng.integers(1, 500, size=2))
+                rp, ci = random_pattern(rng, n, p, float(rng.uniform(0, 0.6)))
+                for grid, sm in ((2, 0), (148, 0), (148, 32)):
+                    rc, msg, _ = _selftest(n, p, rp, ci, True, sm, grid)
+                    assert rc == 0, msg
+        L.pcgs_debug_option(3, 33)
+        rc, msg, _ = _selftest(3, 3, np.array([0, 1, 2, 3]), np.array([0, 1, 2], dtype=np.int32), True, 0)
+        assert rc == _lib.PCGS_EINVAL
+    finally:
+        L.pcgs_debug_option(3, 0)
+
+
 def test_store_roundtrip_more_grids():
     rng = np.random.default_rng(11)
     for _ in range(10):
