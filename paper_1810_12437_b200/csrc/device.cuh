@@ -532,10 +532,12 @@ constexpr int kGRing = PCGS_GRING;  // 32-warp kernels (64 registers); k_pcg (16
 #ifndef PCGS_GPIPE
 #define PCGS_GPIPE 1
 #endif
+// sliding L2 prefetch distance of the pipelined walk, blocks: 0 = two blocks
+// past the register batches (4 with one-block batches, 6 with two-block ones:
+// at 16 warps 2 -> 71.9 us, 4 -> 67.2, 6 -> 66.6, 8 -> 66.8, 12 -> 67.8)
 #ifndef PCGS_GPREFETCH
-#define PCGS_GPREFETCH 4
+#define PCGS_GPREFETCH 0
 #endif
-constexpr int kGPrefetch = PCGS_GPREFETCH;  // sliding L2 prefetch distance of the pipelined walk, blocks
 #ifndef PCGS_SB_OPAQUE
 #define PCGS_SB_OPAQUE 1
 #endif
@@ -610,6 +612,7 @@ __device__ __forceinline__ void process_warp_grouped(const PassDev& P, int range
   for (int k0 = 0; k0 < nb; k0 += 2 * kGRing) {
     load(qb, k0 + kGRing);
     {
+      constexpr int kGPrefetch = PCGS_GPREFETCH > 0 ? PCGS_GPREFETCH : 2 * kGRing + 2;
       const unsigned off = (unsigned)(k0 + kGPrefetch) * 512u + (unsigned)lane * 128u;
       if (lane < 8 * kGRing && off < (unsigned)nvec * 16u)
         asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)base + off));
