@@ -344,8 +344,8 @@ def run_ours(args):
                 "note": "the store reads 2-byte slab-local indices, half the canonical "
                         "int32 bytes; store_gbs is the HBM rate of the bytes actually read",
                 "limiter": {"resource": "L1TEX/LSU data pipe (LDS.64 gathers + the index vectors' writeback)",
-                            "data_pipe_busy_over_kernel": 0.638, "shared_bank_conflict_share": 0.142,
-                            "dram_throughput": 0.31,
+                            "data_pipe_busy_over_kernel": 0.644, "shared_bank_conflict_share": 0.142,
+                            "dram_throughput": 0.32,
                             "source": "ncu --set full of k_pcg at config 2 (profiles/k_pcg_r02b_details.csv, "
                                       "ncu_summary_r02.txt); the streaming passes take ~65 % of an iteration "
                                       "and keep the pipe ~89 % busy: per 32-vector block 16 gather wavefronts "
